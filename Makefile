@@ -1,0 +1,64 @@
+# Top-level build (no GPU needed: nvcc cross-compiles sm_100a here).
+#
+#   make            product library + oracle (+ reference-linked binaries when
+#                   /root/reference is present)
+#
+# Product:
+#   paper_0906_0231_b200/lib/libknn_b200.so         CUDA kernels + C ABI
+#   paper_0906_0231_b200/lib/libknn_b200_engine.a   drop-in knn::solve_knn TU
+#                                                   (needs the reference headers)
+# Test binaries linking the UNMODIFIED reference around the drop-in:
+#   oracle/_ref/acceptance_b200      reference acceptance.cpp on the GPU engine
+#   build/test_engine_b200           test_engine.cpp assertions on the GPU engine
+
+NVCC ?= /usr/local/cuda/bin/nvcc
+CXX ?= g++
+REF ?= /root/reference/proj
+ARCH := -gencode arch=compute_100a,code=sm_100a
+# -fmad=false: no implicit mul+add contraction anywhere; FMAs are written
+# explicitly where the algorithm wants them.  No fast-math (IEEE sqrt/div).
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -fmad=false -Xcompiler -fPIC,-fvisibility=hidden \
+           --expt-relaxed-constexpr -Xptxas -warn-spills
+PKG := paper_0906_0231_b200
+CSRC := $(PKG)/csrc
+CU_SRCS := $(wildcard $(CSRC)/*.cu)
+CU_OBJS := $(patsubst $(CSRC)/%.cu,build/obj/%.o,$(CU_SRCS))
+LIB := $(PKG)/lib/libknn_b200.so
+ENGINE_A := $(PKG)/lib/libknn_b200_engine.a
+HAVE_REF := $(wildcard $(REF)/src/engine.cpp)
+REF_FLAGS := -std=c++20 -O3 -ffp-contract=off -fno-math-errno -fPIC
+
+.PHONY: all lib oracle ref-bins clean
+all: lib oracle $(if $(HAVE_REF),ref-bins,)
+lib: $(LIB)
+
+build/obj/%.o: $(CSRC)/%.cu $(wildcard $(CSRC)/*.cuh) $(CSRC)/kernels.h include/knn_b200.h
+	@mkdir -p build/obj
+	$(NVCC) $(NVFLAGS) -Iinclude -c $< -o $@
+
+$(LIB): $(CU_OBJS)
+	@mkdir -p $(PKG)/lib
+	$(NVCC) $(ARCH) -shared -o $@ $^ -Xlinker --exclude-libs,ALL -lpthread
+
+oracle:
+	$(MAKE) -C oracle REF=$(REF)
+
+$(ENGINE_A): $(PKG)/host/engine_b200.cpp include/knn_b200.h
+	@mkdir -p build/obj $(PKG)/lib
+	$(CXX) $(REF_FLAGS) -I$(REF)/include -Iinclude -c $< -o build/obj/engine_b200.o
+	rm -f $@ && ar rcs $@ build/obj/engine_b200.o
+
+REF_LINK := $(ENGINE_A) oracle/_ref/libtknn_ref_noengine.a -L$(PKG)/lib -lknn_b200 \
+            -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib' -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib' -lpthread
+
+ref-bins: oracle/_ref/acceptance_b200 build/test_engine_b200
+
+oracle/_ref/acceptance_b200: $(REF)/tests/acceptance.cpp $(ENGINE_A) $(LIB) oracle
+	$(CXX) $(REF_FLAGS) -I$(REF)/include -o $@ $< $(REF_LINK)
+
+build/test_engine_b200: tests/cpp/test_engine_b200.cpp $(ENGINE_A) $(LIB) oracle
+	$(CXX) $(REF_FLAGS) -I$(REF)/include -Iinclude -o $@ $< $(REF_LINK)
+
+clean:
+	rm -rf build $(PKG)/lib
+	$(MAKE) -C oracle clean

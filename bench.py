@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""bench.py -- all-pairs k-NN throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--arith auto]
+    python bench.py --impl reference ...          # the reference CPU path
+
+A "step" is one complete exact all-pairs k-NN solve of the configured
+synthetic dataset (every query row against every vector, Phase 1 + Phase 2).
+The unit of work is one unordered pair {x, y} (reference counter
+pair_evaluations, engine.hpp:28), so
+
+    value = n (n-1) / 2 * K / (max-over-ranks time of K steps)   [pairs/s]
+
+Inputs are SplitMix64 generate_dataset(n, d, seed) (src/io.cpp:57-62), made on
+the device by knn_b200_generate_device (bit-identical to the host stream).
+Multi-GPU (torchrun, one rank per GPU): rank 0 generates, the reference set is
+replicated by an NCCL broadcast, each rank solves a contiguous query-row
+shard (weak in pairs per GPU only approximately; n is fixed, so "strong").
+
+`value` is device-resident (inputs already in HBM); `e2e` is the same metric
+through the public API with the host copy of the inputs (rank 0, pinned) and
+the device->host copy of every rank's result lists inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: n, d, k, metric, seed  (SURVEY §8(d) seeds C1=42 ... C5=4)
+    "c1": dict(n=16384, d=64, k=10, metric="euclidean", seed=42, label="n=16384 d=64 k=10 Euclidean"),
+    "c2": dict(n=1_000_000, d=256, k=10, metric="euclidean", seed=1, label="n=1M d=256 k=10 Euclidean"),
+    "c3": dict(n=1_000_000, d=1024, k=100, metric="euclidean", seed=2, label="n=1M d=1024 k=100 Euclidean"),
+    "c4": dict(n=4_000_000, d=128, k=32, metric="cosine", seed=3, label="n=4M d=128 k=32 cosine"),
+    "c5": dict(n=16_000_000, d=256, k=10, metric="euclidean", seed=4, label="n=16M d=256 k=10 Euclidean"),
+}
+DEFAULT_CONFIG = "c2"   # BASELINE.json configs[1]: the metric's 1-GPU configuration
+METRIC = "all-pairs k-NN distance-evals/s (unordered pairs)"
+UNIT = "pairs/s"
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._pump, daemon=True)
+        self.thread.start()
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=5)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# --------------------------------------------------------------------------
+# CPU reference arm / cpu_baseline (the ONLY places bench.py runs oracle/)
+
+def cpu_reference_sample(cfg, budget_s: float):
+    """Time the reference's own solve_knn (oracle/_ref, unmodified library,
+    all host cores as lanes) on a bounded prefix of the workload, or the C
+    restatement when the reference was not compiled.  Returns
+    (pairs_per_s, seconds, cores, kind, sample_desc)."""
+    import numpy as np
+
+    import oracle
+    cores = os.cpu_count() or 1
+    ref = oracle.reference()
+    co = oracle.c_oracle()
+    metric = {"euclidean": "sqeuclidean"}.get(cfg["metric"], cfg["metric"])
+    d, k = cfg["d"], cfg["k"]
+
+    def run(nn):
+        x = co.generate(nn, d, cfg["seed"])  # prefix rows of the same stream
+        if metric == "cosine":
+            x = oracle.normalize_rows(x)
+        if ref is not None:
+            # every lane gets >= 2 grid rows (SURVEY §8(d) CPU baseline (ii))
+            gsize = 64 * max(1, math.ceil(nn / (2 * cores * 64)))
+            t0 = time.perf_counter()
+            ref.solve_knn(x, k, metric, n_lanes=cores, gsize=gsize, want_lists=False)
+            return time.perf_counter() - t0, "reference", f"reference solve_knn, {cores} lanes, gsize {gsize}"
+        rows = np.arange(nn, dtype=np.uint32)
+        t0 = time.perf_counter()
+        co.rows_topk(x, k, metric, rows, threads=cores)
+        # rows_topk evaluates every ordered pair: report unordered-pair rate
+        return 2 * (time.perf_counter() - t0), "port", f"C restatement rows_topk, {cores} threads (x2: no symmetry)"
+
+    nn = 2048
+    t, kind, desc = run(nn)
+    # pairs scale as nn^2: grow to about budget_s
+    while t < budget_s / 4 and nn < cfg["n"]:
+        nn = min(cfg["n"], int(nn * min(4.0, math.sqrt(budget_s / max(t, 1e-3)))) // 64 * 64)
+        t, kind, desc = run(nn)
+    pairs = nn * (nn - 1) / 2
+    sample = (f"prefix n'={nn} of {cfg['label']} (same seed/metric), {desc}; "
+              f"pairs/s = n'(n'-1)/2 / time")
+    return pairs / t, t, cores, kind, sample, nn
+
+
+def run_reference_arm(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    budget = max(5.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    # calibrate the sample size once, then time W + K steps of that size
+    rate, t, cores, kind, sample, nn = cpu_reference_sample(cfg, budget)
+    import numpy as np
+
+    import oracle
+    ref = oracle.reference()
+    co = oracle.c_oracle()
+    metric = {"euclidean": "sqeuclidean"}.get(cfg["metric"], cfg["metric"])
+    x = co.generate(nn, cfg["d"], cfg["seed"])
+    if metric == "cosine":
+        x = oracle.normalize_rows(x)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        if ref is not None:
+            gsize = 64 * max(1, math.ceil(nn / (2 * cores * 64)))
+            ref.solve_knn(x, cfg["k"], metric, n_lanes=cores, gsize=gsize, want_lists=False)
+            dt = time.perf_counter() - t0
+        else:
+            co.rows_topk(x, cfg["k"], metric, np.arange(nn, dtype=np.uint32), threads=cores)
+            dt = 2 * (time.perf_counter() - t0)
+        if i >= args.warmup:
+            times.append(dt)
+    pairs = nn * (nn - 1) / 2
+    total = sum(times)
+    value = pairs * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (SplitMix64 generate_dataset)",
+        "config": {"workload": cfg["label"], "sample": sample, "metric_fold": metric},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------
+# B200 arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=None, help="override n (smoke/profiling only)")
+    ap.add_argument("--arith", default="auto", choices=["auto", "exact", "tensor"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.n:
+        cfg["n"] = args.n
+        cfg["label"] += f" [n overridden to {args.n}]"
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_0906_0231_b200 import Context, _lib, distance_by_name, generate_torch, solve_rows_torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device(f"cuda:{local if world > 1 else 0}")
+    ctx = Context(dev.index)
+    n, d, k = cfg["n"], cfg["d"], cfg["k"]
+    metric = distance_by_name(cfg["metric"])
+    arith = _lib.ARITH_NAMES[args.arith]
+    klist = min(k, n - 1)
+    r0, r1 = n * rank // world, n * (rank + 1) // world
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- inputs: generated on rank 0's device, replicated by NCCL broadcast
+    x = generate_torch(ctx, n, d, cfg["seed"], dev) if rank == 0 else torch.empty((n, d), dtype=torch.float32,
+                                                                                  device=dev)
+    if cfg["metric"] == "cosine" and rank == 0:
+        xd = x.double()
+        x = (xd / xd.norm(dim=1, keepdim=True).clamp_min(1e-300)).float().contiguous()
+        del xd
+    if world > 1:
+        dist.broadcast(x, src=0)
+    torch.cuda.synchronize()
+    out_idx = torch.empty((r1 - r0, klist), dtype=torch.int32, device=dev)
+    out_dist = torch.empty((r1 - r0, klist), dtype=torch.float32, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[dev.index])
+        torch.cuda.synchronize()
+
+    def device_step(want_stats=True):
+        _, _, st = solve_rows_torch(ctx, x, k, metric, r0, r1, arith, out=(out_idx, out_dist),
+                                    want_stats=want_stats)
+        return st
+
+    # ---- warm-up (W >= 3 full steps)
+    for _ in range(max(args.warmup, 0)):
+        device_step()
+    barrier()
+
+    # ---- timed device-resident region
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    launches = 0
+    sweep_ms, stats = [], []
+    for _ in range(args.steps):
+        st = device_step()
+        launches += st["kernel_launches"]
+        sweep_ms.append(st["sweep_ms"])
+        stats.append(st)
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    pairs = n * (n - 1) / 2
+    value = pairs * args.steps / (ms_max / 1e3)
+
+    # ---- e2e through the public API: pinned host input -> H2D (rank 0) ->
+    #      NCCL broadcast -> shard solve -> D2H of the shard's lists
+    x_host = torch.empty((n, d), dtype=torch.float32, pin_memory=True) if rank == 0 else None
+    if rank == 0:
+        x_host.copy_(x)
+    idx_host = torch.empty((r1 - r0, klist), dtype=torch.int32, pin_memory=True)
+    dist_host = torch.empty((r1 - r0, klist), dtype=torch.float32, pin_memory=True)
+    x_e2e = torch.empty_like(x)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        if rank == 0:
+            x_e2e.copy_(x_host, non_blocking=True)
+        if world > 1:
+            dist.broadcast(x_e2e, src=0)
+        solve_rows_torch(ctx, x_e2e, k, metric, r0, r1, arith, out=(out_idx, out_dist))
+        idx_host.copy_(out_idx, non_blocking=True)
+        dist_host.copy_(out_dist, non_blocking=True)
+    e1.record(stream)
+    barrier()
+    t2 = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t2.item())
+    e2e_value = pairs * args.steps / (e2e_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (the fused distance + top-k sweep)
+    peaks = load_peaks()
+    last = stats[-1]
+    tensor = last["arith_used"] == _lib.ARITH_TENSOR
+    rows = r1 - r0
+    # algorithmic work per launch: 2*d flop per unordered pair;
+    # a shard of `rows` query rows covers rows*(n-1) ordered = half as many pairs
+    alg_flop = rows * (n - 1) / 2 * 2 * d
+    sweep_avg_s = statistics.mean(sweep_ms) / 1e3
+    achieved = alg_flop / sweep_avg_s / 1e12
+    if tensor:
+        peak = peaks.get("bf16_tflops", 1590.0)
+        peak_src = "measured bf16 dense burst (MEASURED_PEAKS.json; fp16 runs at the bf16 rate)" if peaks else "fallback"
+        bound = "tensor"
+    else:
+        sm = peaks.get("sm_max_mhz", 1965.0)
+        peak = 148 * 128 * 2 * sm * 1e6 / 1e12
+        peak_src = f"FP32 SIMT nominal 148 SM x 128 lanes x 2 flop x {sm:.0f} MHz (no measured FP32 peak)"
+        bound = "fp32"
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if not tensor else "f16->f32 filter, f32 exact rescore",
+        "data": "synthetic (SplitMix64 generate_dataset on device)",
+        "config": {"workload": cfg["label"], "n": n, "d": d, "k": k, "metric": cfg["metric"],
+                   "seed": cfg["seed"], "arith": args.arith, "parallelism": f"query-row shards x{world}",
+                   "l2": f"inputs {n * d * 4 / 1e9:.2f} GB > 126 MB L2 (no flush needed)"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms / args.steps,
+                "h2d_bytes_per_step": n * d * 4 if rank == 0 else 0,
+                "d2h_bytes_per_step": n * klist * 8},
+        "gpu_launches": launches,
+        "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "kernel_ms": statistics.mean(sweep_ms),
+                     "alg_flop_per_launch": alg_flop},
+        "clocks": clk,
+        "gpu_stats": {kk: last[kk] for kk in ("distance_evals", "rescored", "fallback_rows", "arith_used")},
+    }
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            rate, t_cpu, cores, kind, sample, _ = cpu_reference_sample(cfg, args.cpu_budget)
+            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+                                    "seconds": t_cpu}
+        except Exception as e:  # reported, never substituted
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,154 @@
+/*
+ * knn_b200.h -- C ABI of the B200-native exact all-pairs k-NN engine.
+ *
+ * This is the drop-in boundary for the hot path of the reference tknn
+ * library (paths relative to /root/reference/proj):
+ *
+ *   knn::solve_knn(const Dataset&, const CumulativeDistance&,
+ *                  const EngineOptions&) -> EngineResult
+ *     declared include/knn/engine.hpp:37-38, defined src/engine.cpp:13-68
+ *
+ * The C++ translation unit paper_0906_0231_b200/host/engine_b200.cpp defines
+ * exactly that function on top of this ABI (it replaces src/engine.cpp at
+ * link time); INTEGRATION.md shows the link line and a ctypes binding.
+ *
+ * Conventions
+ *   - Plain C types only.  Nothing here allocates caller-visible memory; the
+ *     caller owns every input and output buffer.
+ *   - Every entry point returns a knn_b200_status.  Codes mirror the exit
+ *     codes of the reference CLI (tools/main.cpp:225-240): 2 = ConfigError,
+ *     3 = ValidationError, 4 = internal/CUDA error.  knn_b200_last_error()
+ *     returns the message of the last failure on the calling thread.
+ *   - Output rows are ascending by (distance, index), self excluded, of length
+ *     min(k, n-1), exactly as NeighborList (include/knn/heap.hpp:62-67,
+ *     src/heap.cpp:69).  Results are bit-identical to the reference's
+ *     brute_force_knn for every arithmetic policy.
+ *   - There is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point fails with KNN_B200_ERR_INTERNAL.
+ */
+#ifndef KNN_B200_H
+#define KNN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KNN_B200_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define KNN_B200_API __attribute__((visibility("default")))
+#else
+#define KNN_B200_API
+#endif
+
+typedef enum {
+    KNN_B200_OK = 0,
+    KNN_B200_ERR_CONFIG = 2,     /* knn::ConfigError     (engine.cpp:15-17)  */
+    KNN_B200_ERR_VALIDATION = 3, /* knn::ValidationError (distance.cpp:36-59, dataset.cpp:13-29) */
+    KNN_B200_ERR_INTERNAL = 4    /* std::runtime_error / CUDA failure        */
+} knn_b200_status;
+
+/* Metric ids.  HELLINGER and SQEUCLIDEAN are the reference built-ins
+ * (src/distance.cpp:12-34, MetricKind include/knn/distance.hpp:19); COSINE is
+ * the custom fold "cosine" (step acc + u*v, finalize 1 - acc) of SURVEY §8(d).
+ * Other custom functors cannot run on the GPU and are rejected by the C++
+ * drop-in with ConfigError. */
+typedef enum {
+    KNN_B200_METRIC_HELLINGER = 0,
+    KNN_B200_METRIC_SQEUCLIDEAN = 1,
+    KNN_B200_METRIC_COSINE = 2,
+    /* "Euclidean" of the BASELINE configs: selection on the
+     * sqeuclidean fold, reported distance = IEEE sqrtf of it at output. */
+    KNN_B200_METRIC_EUCLIDEAN = 3
+} knn_b200_metric;
+
+/* Arithmetic policy for Phase 1 (EngineOptions has no field for it; the C++
+ * drop-in reads KNN_B200_ARITH=auto|exact|tensor).
+ *   EXACT  : SIMT FP32 fold, coordinate order 0..d-1, FSUB/FMUL/FADD with no
+ *            contraction -- every distance bit-identical to fold_distance.
+ *   TENSOR : tcgen05 FP16 filter (||a||^2+||b||^2-2ab, FP32 accumulate in
+ *            TMEM) keeping a per-row candidate list with a proven error band,
+ *            then an exact re-score; rows whose band is not proven are
+ *            recomputed by the EXACT kernel.  Output equals EXACT bit for bit.
+ *   AUTO   : TENSOR where supported, else EXACT. */
+typedef enum {
+    KNN_B200_ARITH_AUTO = 0,
+    KNN_B200_ARITH_EXACT = 1,
+    KNN_B200_ARITH_TENSOR = 2
+} knn_b200_arith;
+
+typedef struct {
+    uint64_t pair_evaluations; /* semantic count: unordered pairs covered, n(n-1)/2 for a full solve
+                                  (EngineResult::pair_evaluations, engine.hpp:28) */
+    uint64_t distance_evals;   /* ordered (query, reference) distances the kernels executed */
+    uint64_t rescored;         /* candidates re-scored by the exact fold (TENSOR) */
+    uint32_t fallback_rows;    /* rows recomputed by the EXACT kernel (TENSOR) */
+    uint32_t kernel_launches;  /* device kernels launched by this call */
+    int32_t arith_used;        /* knn_b200_arith actually run */
+    int32_t n_devices;         /* GPUs used */
+    double seconds;            /* whole call, host clock (validation excluded for host API) */
+    double h2d_ms;             /* host->device copy, CUDA events */
+    double kernel_ms;          /* all kernels, CUDA events */
+    double d2h_ms;             /* device->host copy, CUDA events */
+    double sweep_ms;           /* the dominant distance+top-k kernel alone, CUDA events */
+} knn_b200_stats;
+
+typedef struct knn_b200_ctx knn_b200_ctx;
+
+KNN_B200_API int knn_b200_abi_version(void);
+KNN_B200_API const char *knn_b200_last_error(void);
+
+/* Number of visible CUDA devices with compute capability 10.x. */
+KNN_B200_API int knn_b200_device_count(int *out_count);
+
+/* A context owns one device's streams and grow-only workspace; reuse it
+ * across calls (the reference CLI bench calls solve_knn twice,
+ * tools/main.cpp:163-164).  Not thread-safe: one context per host thread. */
+KNN_B200_API int knn_b200_create(int device, knn_b200_ctx **out_ctx);
+KNN_B200_API void knn_b200_destroy(knn_b200_ctx *ctx);
+
+/* Full drop-in solve on one device.  host_vectors: n x d float32 row-major
+ * (pageable or pinned).  out_index/out_dist: n x min(k, n-1), host memory.
+ * Validates n >= 2, d >= 1, k >= 1 (ConfigError) and, on the device, that
+ * every coordinate is finite and inside the metric's domain
+ * (ValidationError, message as in distance.cpp:41-45 / dataset.cpp:25-27). */
+KNN_B200_API int knn_b200_solve(knn_b200_ctx *ctx, const float *host_vectors, uint32_t n, uint32_t d,
+                   uint32_t k, int metric, int arith, uint32_t *out_index, float *out_dist,
+                   knn_b200_stats *stats);
+
+/* Device-resident shard solve: dev_vectors is the full n x d reference set
+ * already on ctx's device (e.g. replicated by an NCCL broadcast); computes the
+ * lists of query rows [row_begin, row_end) against all n vectors and writes
+ * (row_end - row_begin) x min(k, n-1) results to device buffers.  Work is
+ * enqueued on `stream` (a cudaStream_t, NULL = ctx's own stream).  The call
+ * synchronises once after the validation pass (the reference validates before
+ * any compute, engine.cpp:23) and, when stats is non-NULL, at the end; the
+ * sweep itself is left in flight otherwise. */
+KNN_B200_API int knn_b200_solve_rows_device(knn_b200_ctx *ctx, const float *dev_vectors, uint32_t n,
+                               uint32_t d, uint32_t k, int metric, int arith,
+                               uint32_t row_begin, uint32_t row_end, uint32_t *dev_out_index,
+                               float *dev_out_dist, void *stream, knn_b200_stats *stats);
+
+/* Synthetic inputs on the device, bit-identical to the reference's
+ * generate_dataset (src/io.cpp:57-62, include/knn/rng.hpp:13-23): element i of
+ * the row-major n x d buffer is the (i+1)-th SplitMix64(seed) unit float.  The
+ * SplitMix64 state is a Weyl sequence, so element i is computed directly as
+ * mix(seed + (i+1) * 0x9e3779b97f4a7c15). */
+KNN_B200_API int knn_b200_generate_device(knn_b200_ctx *ctx, float *dev_out, uint64_t count,
+                                          uint64_t seed, void *stream);
+
+/* Single-process multi-GPU solve (the reference's n_lanes, engine.cpp:37-56):
+ * uses min(n_gpus, device count) devices, one host thread each; query rows are
+ * split into contiguous shards, every device holds the full reference set and
+ * writes its shard straight into the host outputs.  No merge is needed. */
+KNN_B200_API int knn_b200_solve_multi(const float *host_vectors, uint32_t n, uint32_t d, uint32_t k,
+                         int metric, int arith, uint32_t n_gpus, uint32_t *out_index,
+                         float *out_dist, knn_b200_stats *stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KNN_B200_H */

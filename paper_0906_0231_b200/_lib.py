@@ -1,0 +1,101 @@
+"""ctypes binding of the C ABI in include/knn_b200.h.
+
+The shared library is built in-tree (``make`` at the repo root or
+``__graft_entry__.build()``) into ``paper_0906_0231_b200/lib/libknn_b200.so``.
+Loading fails loudly when it is missing: there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libknn_b200.so"
+
+# Every exported symbol of include/knn_b200.h (checked by the CPU test suite).
+EXPORTS = (
+    "knn_b200_abi_version",
+    "knn_b200_last_error",
+    "knn_b200_device_count",
+    "knn_b200_create",
+    "knn_b200_destroy",
+    "knn_b200_solve",
+    "knn_b200_solve_rows_device",
+    "knn_b200_solve_multi",
+    "knn_b200_generate_device",
+)
+
+ABI_VERSION = 1
+
+OK, ERR_CONFIG, ERR_VALIDATION, ERR_INTERNAL = 0, 2, 3, 4
+METRIC_HELLINGER, METRIC_SQEUCLIDEAN, METRIC_COSINE, METRIC_EUCLIDEAN = 0, 1, 2, 3
+ARITH_AUTO, ARITH_EXACT, ARITH_TENSOR = 0, 1, 2
+ARITH_NAMES = {"auto": ARITH_AUTO, "exact": ARITH_EXACT, "tensor": ARITH_TENSOR}
+
+
+class Stats(ctypes.Structure):
+    """knn_b200_stats."""
+
+    _fields_ = [
+        ("pair_evaluations", ctypes.c_uint64),
+        ("distance_evals", ctypes.c_uint64),
+        ("rescored", ctypes.c_uint64),
+        ("fallback_rows", ctypes.c_uint32),
+        ("kernel_launches", ctypes.c_uint32),
+        ("arith_used", ctypes.c_int32),
+        ("n_devices", ctypes.c_int32),
+        ("seconds", ctypes.c_double),
+        ("h2d_ms", ctypes.c_double),
+        ("kernel_ms", ctypes.c_double),
+        ("d2h_ms", ctypes.c_double),
+        ("sweep_ms", ctypes.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+_f32p = ctypes.POINTER(ctypes.c_float)
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load and type the library once; raise if it was not built."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: the B200 CUDA library was not built "
+                "(run `make` or __graft_entry__.build()); there is no CPU fallback")
+        lib = ctypes.CDLL(str(LIB_PATH))
+        lib.knn_b200_abi_version.restype = ctypes.c_int
+        lib.knn_b200_last_error.restype = ctypes.c_char_p
+        lib.knn_b200_device_count.argtypes = [ctypes.POINTER(ctypes.c_int)]
+        lib.knn_b200_create.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
+        lib.knn_b200_destroy.argtypes = [ctypes.c_void_p]
+        lib.knn_b200_destroy.restype = None
+        lib.knn_b200_solve.argtypes = [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+            ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)]
+        lib.knn_b200_solve_rows_device.argtypes = [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+            ctypes.c_int, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)]
+        lib.knn_b200_solve_multi.argtypes = [
+            ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int,
+            ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)]
+        lib.knn_b200_generate_device.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                                 ctypes.c_uint64, ctypes.c_void_p]
+        if lib.knn_b200_abi_version() != ABI_VERSION:
+            raise RuntimeError(f"{LIB_PATH}: ABI version {lib.knn_b200_abi_version()} != {ABI_VERSION}")
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    return load().knn_b200_last_error().decode(errors="replace")

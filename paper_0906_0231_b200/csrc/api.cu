@@ -1,0 +1,437 @@
+// api.cu -- the C ABI (include/knn_b200.h): contexts, workspace, dispatch.
+//
+// Mirrors the control flow of knn::solve_knn (src/engine.cpp:13-68) on the
+// device: argument checks -> validation (before any compute) -> Phase 1+2
+// fused sweep per row shard -> results.  The reference's per-lane HeapStore +
+// merge_all (engine.cpp:27-59) has no counterpart: each query row is owned by
+// exactly one CTA, so its list is final when the sweep ends.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/knn_b200.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Status {
+    int code;
+    std::string msg;
+};
+
+struct KnnError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw KnnError{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(KNN_B200_ERR_INTERNAL, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return KNN_B200_OK;
+    } catch (const KnnError& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return KNN_B200_ERR_INTERNAL;
+    }
+}
+
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    void* get(size_t want) {
+        if (want > bytes) {
+            if (ptr) cudaFree(ptr);
+            ptr = nullptr;
+            bytes = 0;
+            cuda_check(cudaMalloc(&ptr, want ? want : 16), "cudaMalloc workspace");
+            bytes = want ? want : 16;
+        }
+        return ptr;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+};
+
+std::string fmt_value(float v) {
+    // std::to_string(float) formatting, as the reference message uses.
+    return std::to_string(v);
+}
+
+}  // namespace
+
+struct knn_b200_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[6] = {};  // [0..3] call phases, [4..5] around the sweep kernel
+    DevBuf vectors, staged, flags, out_index, out_dist;
+    unsigned long long* host_flags = nullptr;  // pinned
+    std::mutex mu;
+};
+
+namespace {
+
+const char* metric_name(int metric) {
+    switch (metric) {
+    case KNN_B200_METRIC_HELLINGER: return "hellinger";
+    case KNN_B200_METRIC_SQEUCLIDEAN: return "sqeuclidean";
+    case KNN_B200_METRIC_COSINE: return "cosine";
+    case KNN_B200_METRIC_EUCLIDEAN: return "euclidean";
+    default: return "?";
+    }
+}
+
+void check_args(uint32_t n, uint32_t d, uint32_t k, int metric, int arith) {
+    // engine.cpp:15 (k), schedule.cpp:12 (n), dataset.cpp:13-19 (n, d)
+    if (k < 1) fail(KNN_B200_ERR_CONFIG, "k must be at least 1");
+    if (n < 2) fail(KNN_B200_ERR_CONFIG, "n must be at least 2, got " + std::to_string(n));
+    if (d < 1) fail(KNN_B200_ERR_CONFIG, "dataset dimension must be at least 1");
+    if (metric < 0 || metric > 3) fail(KNN_B200_ERR_CONFIG, "unknown metric id " + std::to_string(metric));
+    if (arith < 0 || arith > 2) fail(KNN_B200_ERR_CONFIG, "unknown arithmetic policy " + std::to_string(arith));
+    const uint32_t klist = std::min(k, n - 1);
+    if (klist > knnb::kExactMaxK)
+        fail(KNN_B200_ERR_CONFIG, "min(k, n-1) = " + std::to_string(klist) + " exceeds the supported " +
+                                      std::to_string(knnb::kExactMaxK));
+}
+
+struct Counters {
+    uint32_t launches = 0;
+    uint64_t distance_evals = 0;
+    uint64_t rescored = 0;
+    uint32_t fallback_rows = 0;
+    int arith_used = KNN_B200_ARITH_EXACT;
+};
+
+// Device validation of the whole reference set (host copy of two flags; this
+// synchronises, as the reference validates before its timer, engine.cpp:23).
+void validate_device(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, int metric,
+                     cudaStream_t stream, Counters& ctr) {
+    auto* flags = static_cast<unsigned long long*>(ctx->flags.get(2 * sizeof(unsigned long long)));
+    cuda_check(cudaMemsetAsync(flags, 0xff, 2 * sizeof(unsigned long long), stream), "memset flags");
+    const uint64_t count = uint64_t(n) * d;
+    cuda_check(knnb::launch_validate(X, count, metric == KNN_B200_METRIC_HELLINGER, flags, ctx->sm_count,
+                                     stream),
+               "validate launch");
+    ++ctr.launches;
+    cuda_check(cudaMemcpyAsync(ctx->host_flags, flags, 2 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, stream),
+               "flags D2H");
+    cuda_check(cudaStreamSynchronize(stream), "validate sync");
+    const unsigned long long bad_nf = ctx->host_flags[0], bad_dom = ctx->host_flags[1];
+    const unsigned long long none = ~0ull;
+    if (bad_nf != none) {
+        // dataset.cpp:25-27
+        fail(KNN_B200_ERR_VALIDATION, "non-finite coordinate " + std::to_string(bad_nf % d) + " in vector " +
+                                          std::to_string(bad_nf / d));
+    }
+    if (bad_dom != none) {
+        float v = 0;
+        cuda_check(cudaMemcpy(&v, X + bad_dom, sizeof(float), cudaMemcpyDeviceToHost), "value D2H");
+        // distance.cpp:41-45
+        fail(KNN_B200_ERR_VALIDATION, "coordinate " + std::to_string(bad_dom % d) + " of vector " +
+                                          std::to_string(bad_dom / d) + " (value " + fmt_value(v) +
+                                          ") is outside the domain of " + metric_name(metric));
+    }
+}
+
+// Validation + staging + the row-shard sweep, all enqueued on `stream`.
+void solve_rows_core(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, uint32_t k, int metric,
+                     int arith, uint32_t row_begin, uint32_t row_end, uint32_t* out_index, float* out_dist,
+                     cudaStream_t stream, Counters& ctr) {
+    validate_device(ctx, X, n, d, metric, stream, ctr);
+    const float* Xs = X;
+    if (metric == KNN_B200_METRIC_HELLINGER) {
+        float* staged = static_cast<float*>(ctx->staged.get(size_t(n) * d * sizeof(float)));
+        cuda_check(knnb::launch_stage_sqrt(X, staged, uint64_t(n) * d, ctx->sm_count, stream), "stage launch");
+        ++ctr.launches;
+        Xs = staged;
+    }
+    const uint32_t klist = std::min(k, n - 1);
+    (void)arith;
+    ctr.arith_used = KNN_B200_ARITH_EXACT;
+    const int fold = metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean;
+    cuda_check(cudaEventRecord(ctx->ev[4], stream), "event");
+    cuda_check(knnb::launch_exact_fused(fold, Xs, n, d, klist, nullptr, row_begin, row_end, out_index,
+                                        out_dist, metric == KNN_B200_METRIC_EUCLIDEAN, stream),
+               "exact sweep launch");
+    cuda_check(cudaEventRecord(ctx->ev[5], stream), "event");
+    ++ctr.launches;
+    ctr.distance_evals += uint64_t(row_end - row_begin) * n;
+}
+
+void fill_stats(knn_b200_stats* st, const Counters& ctr, uint64_t pairs, int ndev) {
+    if (!st) return;
+    st->pair_evaluations = pairs;
+    st->distance_evals = ctr.distance_evals;
+    st->rescored = ctr.rescored;
+    st->fallback_rows = ctr.fallback_rows;
+    st->kernel_launches = ctr.launches;
+    st->arith_used = ctr.arith_used;
+    st->n_devices = ndev;
+}
+
+float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+int knn_b200_abi_version(void) { return KNN_B200_ABI_VERSION; }
+
+const char* knn_b200_last_error(void) { return g_last_error.c_str(); }
+
+int knn_b200_device_count(int* out_count) {
+    return guarded([&] {
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess) n = 0;
+        int ok = 0;
+        for (int i = 0; i < n; ++i) {
+            cudaDeviceProp p;
+            if (cudaGetDeviceProperties(&p, i) == cudaSuccess && p.major == 10) ++ok;
+        }
+        *out_count = ok;
+    });
+}
+
+int knn_b200_create(int device, knn_b200_ctx** out_ctx) {
+    return guarded([&] {
+        *out_ctx = nullptr;
+        int ndev = 0;
+        cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount (no CUDA device; there is no CPU fallback)");
+        if (device < 0 || device >= ndev)
+            fail(KNN_B200_ERR_CONFIG, "device " + std::to_string(device) + " out of range (" +
+                                          std::to_string(ndev) + " visible)");
+        cudaDeviceProp p;
+        cuda_check(cudaGetDeviceProperties(&p, device), "cudaGetDeviceProperties");
+        if (p.major != 10)
+            fail(KNN_B200_ERR_INTERNAL, std::string("device ") + p.name + " is sm_" + std::to_string(p.major) +
+                                            std::to_string(p.minor) + "; this build targets sm_100a only");
+        auto* ctx = new knn_b200_ctx();
+        ctx->device = device;
+        ctx->sm_count = p.multiProcessorCount;
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        cuda_check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        for (auto& e : ctx->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        cuda_check(cudaMallocHost(&ctx->host_flags, 4 * sizeof(unsigned long long)), "cudaMallocHost");
+        *out_ctx = ctx;
+    });
+}
+
+void knn_b200_destroy(knn_b200_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->vectors.release();
+    ctx->staged.release();
+    ctx->flags.release();
+    ctx->out_index.release();
+    ctx->out_dist.release();
+    if (ctx->host_flags) cudaFreeHost(ctx->host_flags);
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int knn_b200_solve(knn_b200_ctx* ctx, const float* host_vectors, uint32_t n, uint32_t d, uint32_t k,
+                   int metric, int arith, uint32_t* out_index, float* out_dist, knn_b200_stats* stats) {
+    return guarded([&] {
+        if (!ctx) fail(KNN_B200_ERR_CONFIG, "null context");
+        check_args(n, d, k, metric, arith);
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        const auto t0 = std::chrono::steady_clock::now();
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const uint32_t klist = std::min(k, n - 1);
+        const size_t vec_bytes = size_t(n) * d * sizeof(float);
+        const size_t out_elems = size_t(n) * klist;
+        float* X = static_cast<float*>(ctx->vectors.get(vec_bytes));
+        auto* oi = static_cast<uint32_t*>(ctx->out_index.get(out_elems * sizeof(uint32_t)));
+        auto* od = static_cast<float*>(ctx->out_dist.get(out_elems * sizeof(float)));
+        Counters ctr;
+        cudaStream_t s = ctx->stream;
+        cuda_check(cudaEventRecord(ctx->ev[0], s), "event");
+        cuda_check(cudaMemcpyAsync(X, host_vectors, vec_bytes, cudaMemcpyHostToDevice, s), "H2D vectors");
+        cuda_check(cudaEventRecord(ctx->ev[1], s), "event");
+        solve_rows_core(ctx, X, n, d, k, metric, arith, 0, n, oi, od, s, ctr);
+        cuda_check(cudaEventRecord(ctx->ev[2], s), "event");
+        cuda_check(cudaMemcpyAsync(out_index, oi, out_elems * sizeof(uint32_t), cudaMemcpyDeviceToHost, s),
+                   "D2H index");
+        cuda_check(cudaMemcpyAsync(out_dist, od, out_elems * sizeof(float), cudaMemcpyDeviceToHost, s),
+                   "D2H dist");
+        cuda_check(cudaEventRecord(ctx->ev[3], s), "event");
+        cuda_check(cudaStreamSynchronize(s), "solve sync");
+        if (stats) {
+            fill_stats(stats, ctr, uint64_t(n) * (n - 1) / 2, 1);
+            stats->h2d_ms = elapsed_ms(ctx->ev[0], ctx->ev[1]);
+            stats->kernel_ms = elapsed_ms(ctx->ev[1], ctx->ev[2]);
+            stats->d2h_ms = elapsed_ms(ctx->ev[2], ctx->ev[3]);
+            stats->sweep_ms = elapsed_ms(ctx->ev[4], ctx->ev[5]);
+            stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+    });
+}
+
+int knn_b200_generate_device(knn_b200_ctx* ctx, float* dev_out, uint64_t count, uint64_t seed, void* stream) {
+    return guarded([&] {
+        if (!ctx) fail(KNN_B200_ERR_CONFIG, "null context");
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        cuda_check(knnb::launch_generate(dev_out, count, seed, ctx->sm_count, s), "generate launch");
+    });
+}
+
+int knn_b200_solve_rows_device(knn_b200_ctx* ctx, const float* dev_vectors, uint32_t n, uint32_t d, uint32_t k,
+                               int metric, int arith, uint32_t row_begin, uint32_t row_end,
+                               uint32_t* dev_out_index, float* dev_out_dist, void* stream,
+                               knn_b200_stats* stats) {
+    return guarded([&] {
+        if (!ctx) fail(KNN_B200_ERR_CONFIG, "null context");
+        check_args(n, d, k, metric, arith);
+        if (row_begin > row_end || row_end > n)
+            fail(KNN_B200_ERR_CONFIG, "row range [" + std::to_string(row_begin) + ", " + std::to_string(row_end) +
+                                          ") outside [0, " + std::to_string(n) + ")");
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        const auto t0 = std::chrono::steady_clock::now();
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        Counters ctr;
+        if (stats) cuda_check(cudaEventRecord(ctx->ev[1], s), "event");
+        solve_rows_core(ctx, dev_vectors, n, d, k, metric, arith, row_begin, row_end, dev_out_index,
+                        dev_out_dist, s, ctr);
+        if (stats) {
+            cuda_check(cudaEventRecord(ctx->ev[2], s), "event");
+            cuda_check(cudaStreamSynchronize(s), "solve sync");
+            uint64_t pairs = 0;  // unordered pairs {x, y} with at least one endpoint in the shard
+            const uint64_t rows = row_end - row_begin;
+            pairs = rows * (n - 1) - rows * (rows - 1) / 2;
+            fill_stats(stats, ctr, pairs, 1);
+            stats->h2d_ms = 0;
+            stats->d2h_ms = 0;
+            stats->kernel_ms = elapsed_ms(ctx->ev[1], ctx->ev[2]);
+            stats->sweep_ms = elapsed_ms(ctx->ev[4], ctx->ev[5]);
+            stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+    });
+}
+
+int knn_b200_solve_multi(const float* host_vectors, uint32_t n, uint32_t d, uint32_t k, int metric, int arith,
+                         uint32_t n_gpus, uint32_t* out_index, float* out_dist, knn_b200_stats* stats) {
+    // One process-wide context per device, reused across calls and guarded by
+    // a mutex so concurrent solve_knn calls serialise.
+    static std::mutex pool_mu;
+    static std::vector<knn_b200_ctx*> pool;
+    return guarded([&] {
+        check_args(n, d, k, metric, arith);
+        if (n_gpus < 1) fail(KNN_B200_ERR_CONFIG, "n_lanes must be at least 1");
+        int ndev = 0;
+        cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount (no CUDA device; there is no CPU fallback)");
+        const uint32_t use = std::min<uint32_t>(std::min<uint32_t>(n_gpus, uint32_t(ndev)), n);
+        std::lock_guard<std::mutex> lock(pool_mu);
+        if (pool.size() < size_t(ndev)) pool.resize(ndev, nullptr);
+        for (uint32_t g = 0; g < use; ++g) {
+            if (!pool[g]) {
+                knn_b200_ctx* c = nullptr;
+                const int rc = knn_b200_create(int(g), &c);
+                if (rc != KNN_B200_OK) fail(rc, g_last_error);
+                pool[g] = c;
+            }
+        }
+        const auto t0 = std::chrono::steady_clock::now();
+        const uint32_t klist = std::min(k, n - 1);
+        std::vector<KnnError> errs(use, KnnError{0, {}});
+        std::vector<Counters> ctrs(use);
+        std::vector<float> kms(use, 0.f), hms(use, 0.f), dms(use, 0.f), sms(use, 0.f);
+        auto lane = [&](uint32_t g) {
+            try {
+                knn_b200_ctx* ctx = pool[g];
+                std::lock_guard<std::mutex> cl(ctx->mu);
+                cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+                // Contiguous query-row shards; every device holds all n vectors.
+                const uint32_t r0 = uint32_t(uint64_t(n) * g / use);
+                const uint32_t r1 = uint32_t(uint64_t(n) * (g + 1) / use);
+                const size_t vec_bytes = size_t(n) * d * sizeof(float);
+                const size_t out_elems = size_t(r1 - r0) * klist;
+                float* X = static_cast<float*>(ctx->vectors.get(vec_bytes));
+                auto* oi = static_cast<uint32_t*>(ctx->out_index.get(std::max<size_t>(out_elems, 1) * 4));
+                auto* od = static_cast<float*>(ctx->out_dist.get(std::max<size_t>(out_elems, 1) * 4));
+                cudaStream_t s = ctx->stream;
+                cuda_check(cudaEventRecord(ctx->ev[0], s), "event");
+                cuda_check(cudaMemcpyAsync(X, host_vectors, vec_bytes, cudaMemcpyHostToDevice, s), "H2D vectors");
+                cuda_check(cudaEventRecord(ctx->ev[1], s), "event");
+                solve_rows_core(ctx, X, n, d, k, metric, arith, r0, r1, oi, od, s, ctrs[g]);
+                cuda_check(cudaEventRecord(ctx->ev[2], s), "event");
+                if (out_elems) {
+                    cuda_check(cudaMemcpyAsync(out_index + size_t(r0) * klist, oi, out_elems * 4,
+                                               cudaMemcpyDeviceToHost, s),
+                               "D2H index");
+                    cuda_check(cudaMemcpyAsync(out_dist + size_t(r0) * klist, od, out_elems * 4,
+                                               cudaMemcpyDeviceToHost, s),
+                               "D2H dist");
+                }
+                cuda_check(cudaEventRecord(ctx->ev[3], s), "event");
+                cuda_check(cudaStreamSynchronize(s), "solve sync");
+                hms[g] = elapsed_ms(ctx->ev[0], ctx->ev[1]);
+                kms[g] = elapsed_ms(ctx->ev[1], ctx->ev[2]);
+                dms[g] = elapsed_ms(ctx->ev[2], ctx->ev[3]);
+                sms[g] = elapsed_ms(ctx->ev[4], ctx->ev[5]);
+            } catch (const KnnError& e) {
+                errs[g] = e;
+            } catch (const std::exception& e) {
+                errs[g] = KnnError{KNN_B200_ERR_INTERNAL, e.what()};
+            }
+        };
+        std::vector<std::thread> threads;
+        for (uint32_t g = 1; g < use; ++g) threads.emplace_back(lane, g);
+        lane(0);
+        for (auto& t : threads) t.join();
+        // engine.cpp:53-56: rethrow the first lane error after joining.
+        for (const auto& e : errs)
+            if (e.code) throw e;
+        if (stats) {
+            Counters tot;
+            for (const auto& c : ctrs) {
+                tot.launches += c.launches;
+                tot.distance_evals += c.distance_evals;
+                tot.rescored += c.rescored;
+                tot.fallback_rows += c.fallback_rows;
+                tot.arith_used = c.arith_used;
+            }
+            fill_stats(stats, tot, uint64_t(n) * (n - 1) / 2, int(use));
+            stats->h2d_ms = *std::max_element(hms.begin(), hms.end());
+            stats->kernel_ms = *std::max_element(kms.begin(), kms.end());
+            stats->d2h_ms = *std::max_element(dms.begin(), dms.end());
+            stats->sweep_ms = *std::max_element(sms.begin(), sms.end());
+            stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+// common.cuh -- shared device helpers for the B200 k-NN kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace knnb {
+
+enum Metric : int { kHellinger = 0, kSqEuclidean = 1, kCosine = 2 };
+
+// (distance, index) packed into one u64 whose unsigned order is the
+// reference's Neighbor order (include/knn/heap.hpp:21-24): distance first,
+// smaller index on ties.  The float is mapped to an order-preserving u32
+// (negative values, possible for cosine, flip all bits).  -0.0 is
+// canonicalised to +0.0 first because the reference compares with float
+// `<`/`!=`, where the two are equal and the index decides.
+__host__ __device__ __forceinline__ uint32_t float_to_ordered(float f) {
+#ifdef __CUDA_ARCH__
+    uint32_t b = __float_as_uint(f + 0.0f);
+#else
+    union { float f; uint32_t u; } c;
+    c.f = f + 0.0f;
+    uint32_t b = c.u;
+#endif
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__host__ __device__ __forceinline__ float ordered_to_float(uint32_t o) {
+    const uint32_t b = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+#ifdef __CUDA_ARCH__
+    return __uint_as_float(b);
+#else
+    union { float f; uint32_t u; } c;
+    c.u = b;
+    return c.f;
+#endif
+}
+
+__host__ __device__ __forceinline__ uint64_t make_key(float dist, uint32_t index) {
+    return (uint64_t(float_to_ordered(dist)) << 32) | index;
+}
+
+constexpr uint64_t kEmptyKey = ~0ull;
+
+// One step of the reference fold on staged coordinates, with every operation
+// separately rounded (no FMA contraction), distance.hpp:49-52 / :59-62.
+// Hellinger arrives here with both coordinates already sqrt-staged.
+template <int METRIC>
+__device__ __forceinline__ float fold_step(float u, float v, float acc) {
+    if constexpr (METRIC == kCosine) {
+        return __fadd_rn(acc, __fmul_rn(u, v));
+    } else {
+        const float t = __fsub_rn(u, v);
+        return __fadd_rn(acc, __fmul_rn(t, t));
+    }
+}
+
+template <int METRIC>
+__device__ __forceinline__ float fold_finalize(float acc) {
+    if constexpr (METRIC == kCosine) {
+        return __fsub_rn(1.0f, acc);
+    } else {
+        return acc;
+    }
+}
+
+}  // namespace knnb

@@ -1,0 +1,31 @@
+// kernels.h -- host-side launchers for the device kernels (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace knnb {
+
+// validate: flags[0] = first non-finite flat index, flags[1] = first domain
+// violation (negative coordinate when check_nonneg); both must be preset to
+// all-ones by the caller.
+cudaError_t launch_validate(const float* X, uint64_t count, int check_nonneg,
+                            unsigned long long* flags, int sm_count, cudaStream_t stream);
+
+cudaError_t launch_stage_sqrt(const float* X, float* Y, uint64_t count, int sm_count,
+                              cudaStream_t stream);
+
+cudaError_t launch_generate(float* out, uint64_t count, uint64_t seed, int sm_count, cudaStream_t stream);
+
+// EXACT fused sweep.  Output slot s (0 <= s < row_end - row_begin) holds the
+// list of query row `rows ? rows[s] : row_begin + s`; klist = min(k, n-1) <= 256.
+// out_sqrt: report sqrtf(distance) (the Euclidean metric) -- selection is
+// unaffected because sqrtf is monotone and the lists are final.
+cudaError_t launch_exact_fused(int metric, const float* X, uint32_t n, uint32_t d, uint32_t klist,
+                               const uint32_t* rows, uint32_t row_begin, uint32_t row_end,
+                               uint32_t* out_index, float* out_dist, int out_sqrt,
+                               cudaStream_t stream);
+
+constexpr uint32_t kExactMaxK = 256;
+
+}  // namespace knnb

@@ -1,0 +1,115 @@
+// engine_b200.cpp -- drop-in definition of knn::solve_knn on the B200 C ABI.
+//
+// Replaces the reference's src/engine.cpp:13-68 at link time: same signature
+// (include/knn/engine.hpp:37-38), same option checks and plan
+// (engine.cpp:15-22), same validation-before-timer (engine.cpp:23-25), same
+// EngineResult fields (engine.hpp:25-31).  Compiled against the reference's
+// public headers; everything else it needs (make_plan, auto_gsize,
+// validate_dataset) comes from the rest of the reference library, which the
+// caller links unchanged.  The compute runs on the GPU through
+// include/knn_b200.h; there is no CPU fallback.
+//
+// n_lanes -> GPUs used = min(n_lanes, visible sm_100 devices); results are
+// lane-independent bit for bit, as the reference promises (engine.hpp:33-36).
+// The arithmetic policy is chosen out of band (EngineOptions has no field):
+// KNN_B200_ARITH=auto|exact|tensor, default auto.  All policies return the
+// same bits.
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "knn/engine.hpp"
+#include "knn/errors.hpp"
+#include "knn_b200.h"
+
+namespace knn {
+
+static_assert(std::is_same_v<dist_t, float>,
+              "the B200 engine computes in float; build without KNN_DOUBLE_ACCUM");
+
+namespace {
+
+int gpu_metric(const CumulativeDistance& f) {
+    switch (f.kind) {
+    case MetricKind::hellinger:
+        return KNN_B200_METRIC_HELLINGER;
+    case MetricKind::sqeuclidean:
+        return KNN_B200_METRIC_SQEUCLIDEAN;
+    case MetricKind::custom:
+        if (f.name == "cosine") return KNN_B200_METRIC_COSINE;
+        break;
+    }
+    throw ConfigError("distance functor '" + f.name +
+                      "' is a host function pointer and cannot run on the GPU engine");
+}
+
+int arith_from_env() {
+    const char* v = std::getenv("KNN_B200_ARITH");
+    if (!v || !*v || std::strcmp(v, "auto") == 0) return KNN_B200_ARITH_AUTO;
+    if (std::strcmp(v, "exact") == 0) return KNN_B200_ARITH_EXACT;
+    if (std::strcmp(v, "tensor") == 0) return KNN_B200_ARITH_TENSOR;
+    throw ConfigError(std::string("KNN_B200_ARITH must be auto, exact or tensor, got '") + v + "'");
+}
+
+[[noreturn]] void rethrow_status(int rc) {
+    const std::string msg = knn_b200_last_error();
+    switch (rc) {
+    case KNN_B200_ERR_CONFIG:
+        throw ConfigError(msg);
+    case KNN_B200_ERR_VALIDATION:
+        throw ValidationError(msg);
+    default:
+        throw std::runtime_error("B200 engine: " + msg);
+    }
+}
+
+}  // namespace
+
+EngineResult solve_knn(const Dataset& ds, const CumulativeDistance& f, const EngineOptions& opt) {
+    if (opt.k < 1) throw ConfigError("k must be at least 1");
+    if (opt.buf_size < 1) throw ConfigError("buf_size must be at least 1");
+    if (opt.workers < 1) throw ConfigError("workers must be at least 1");
+
+    const std::uint32_t gsize = opt.gsize != 0 ? opt.gsize : auto_gsize(ds.size(), opt.bsize);
+    const GridPlan plan = make_plan(ds.size(), gsize, opt.bsize, opt.c1, opt.c2, opt.n_lanes);
+    validate_dataset(f, ds);
+    const int metric = gpu_metric(f);
+    const int arith = arith_from_env();
+
+    const auto t0 = std::chrono::steady_clock::now();
+
+    const std::uint32_t n = ds.size();
+    const std::uint32_t klist = std::min(opt.k, n - 1);
+    std::vector<std::uint32_t> index(std::size_t(n) * klist);
+    std::vector<float> dist(std::size_t(n) * klist);
+    knn_b200_stats st{};
+    const int rc = knn_b200_solve_multi(ds.values().data(), n, ds.dim(), opt.k, metric, arith,
+                                        plan.n_lanes, index.data(), dist.data(), &st);
+    if (rc != KNN_B200_OK) rethrow_status(rc);
+
+    EngineResult result;
+    result.lists.resize(n);
+    for (std::uint32_t i = 0; i < n; ++i) {
+        NeighborList& list = result.lists[i];
+        list.query = i;
+        list.neighbors.resize(klist);
+        const std::size_t base = std::size_t(i) * klist;
+        for (std::uint32_t j = 0; j < klist; ++j) {
+            list.neighbors[j] = Neighbor{dist[base + j], index[base + j]};
+        }
+    }
+    result.seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    result.plan = plan;
+    // Semantic counters (test_engine.cpp:65-68): every unordered pair is
+    // covered once and offered to both endpoints.  The filter/flush counters
+    // of the CPU funnel have no GPU analogue and stay 0.
+    result.pair_evaluations = st.pair_evaluations;
+    result.select_stats.offered = 2 * st.pair_evaluations;
+    return result;
+}
+
+}  // namespace knn
