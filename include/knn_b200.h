@@ -122,7 +122,8 @@ KNN_B200_API int knn_b200_solve(knn_b200_ctx *ctx, const float *host_vectors, ui
  * already on ctx's device (e.g. replicated by an NCCL broadcast); computes the
  * lists of query rows [row_begin, row_end) against all n vectors and writes
  * (row_end - row_begin) x min(k, n-1) results to device buffers.  Work is
- * enqueued on `stream` (a cudaStream_t, NULL = ctx's own stream).  The call
+ * enqueued on `stream` (a cudaStream_t; NULL is the legacy default stream,
+ * as everywhere in the CUDA runtime).  The call
  * synchronises once after the validation pass (the reference validates before
  * any compute, engine.cpp:23) and, when stats is non-NULL, at the end; the
  * sweep itself is left in flight otherwise. */
@@ -137,7 +138,7 @@ KNN_B200_API int knn_b200_solve_rows_device(knn_b200_ctx *ctx, const float *dev_
  * SplitMix64 state is a Weyl sequence, so element i is computed directly as
  * mix(seed + (i+1) * 0x9e3779b97f4a7c15). */
 KNN_B200_API int knn_b200_generate_device(knn_b200_ctx *ctx, float *dev_out, uint64_t count,
-                                          uint64_t seed, void *stream);
+                                          uint64_t seed, void *stream /* NULL = legacy default */);
 
 /* Single-process multi-GPU solve (the reference's n_lanes, engine.cpp:37-56):
  * uses min(n_gpus, device count) devices, one host thread each; query rows are

@@ -87,7 +87,7 @@ struct knn_b200_ctx {
     int sm_count = 148;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};  // [0..3] call phases, [4..5] around the sweep kernel
-    DevBuf vectors, staged, flags, out_index, out_dist;
+    DevBuf vectors, staged, flags, out_index, out_dist, tensor_ws;
     unsigned long long* host_flags = nullptr;  // pinned
     std::mutex mu;
 };
@@ -170,16 +170,47 @@ void solve_rows_core(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, 
         Xs = staged;
     }
     const uint32_t klist = std::min(k, n - 1);
-    (void)arith;
-    ctr.arith_used = KNN_B200_ARITH_EXACT;
     const int fold = metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean;
+    const int out_sqrt = metric == KNN_B200_METRIC_EUCLIDEAN;
+    const uint32_t kp = knnb::tensor_kp_for(klist);
+    // AUTO: the tensor filter pays off once the sweep dominates its fixed
+    // prologue; both policies return identical bits.
+    const bool tensor = kp != 0 && (arith == KNN_B200_ARITH_TENSOR || (arith == KNN_B200_ARITH_AUTO && n >= 4096));
+    ctr.distance_evals += uint64_t(row_end - row_begin) * n;
+    if (tensor) {
+        ctr.arith_used = KNN_B200_ARITH_TENSOR;
+        knnb::TensorPathArgs ta{};
+        ta.X = Xs;
+        ta.n = n;
+        ta.d = d;
+        ta.klist = klist;
+        ta.kp = kp;
+        ta.row_begin = row_begin;
+        ta.row_end = row_end;
+        ta.fold = fold;
+        ta.out_sqrt = out_sqrt;
+        ta.out_index = out_index;
+        ta.out_dist = out_dist;
+        ta.workspace = ctx->tensor_ws.get(knnb::tensor_workspace_bytes(n, d, row_end - row_begin, kp));
+        ta.host_scratch = ctx->host_flags + 4;
+        ta.sm_count = ctx->sm_count;
+        ta.stream = stream;
+        ta.ev_sweep0 = ctx->ev[4];
+        ta.ev_sweep1 = ctx->ev[5];
+        knnb::TensorPathResult tr;
+        cuda_check(knnb::run_tensor_path(ta, tr), "tensor path");
+        ctr.launches += tr.launches;
+        ctr.rescored += tr.rescored;
+        ctr.fallback_rows += tr.fallback_rows;
+        return;
+    }
+    ctr.arith_used = KNN_B200_ARITH_EXACT;
     cuda_check(cudaEventRecord(ctx->ev[4], stream), "event");
-    cuda_check(knnb::launch_exact_fused(fold, Xs, n, d, klist, nullptr, row_begin, row_end, out_index,
-                                        out_dist, metric == KNN_B200_METRIC_EUCLIDEAN, stream),
+    cuda_check(knnb::launch_exact_fused(fold, Xs, n, d, klist, nullptr, row_begin, row_end, out_index, out_dist,
+                                        out_sqrt, 0, stream),
                "exact sweep launch");
     cuda_check(cudaEventRecord(ctx->ev[5], stream), "event");
     ++ctr.launches;
-    ctr.distance_evals += uint64_t(row_end - row_begin) * n;
 }
 
 void fill_stats(knn_b200_stats* st, const Counters& ctr, uint64_t pairs, int ndev) {
@@ -240,7 +271,7 @@ int knn_b200_create(int device, knn_b200_ctx** out_ctx) {
         cuda_check(cudaSetDevice(device), "cudaSetDevice");
         cuda_check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
         for (auto& e : ctx->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
-        cuda_check(cudaMallocHost(&ctx->host_flags, 4 * sizeof(unsigned long long)), "cudaMallocHost");
+        cuda_check(cudaMallocHost(&ctx->host_flags, 16 * sizeof(unsigned long long)), "cudaMallocHost");
         *out_ctx = ctx;
     });
 }
@@ -254,6 +285,7 @@ void knn_b200_destroy(knn_b200_ctx* ctx) {
     ctx->flags.release();
     ctx->out_index.release();
     ctx->out_dist.release();
+    ctx->tensor_ws.release();
     if (ctx->host_flags) cudaFreeHost(ctx->host_flags);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
@@ -303,7 +335,7 @@ int knn_b200_generate_device(knn_b200_ctx* ctx, float* dev_out, uint64_t count, 
     return guarded([&] {
         if (!ctx) fail(KNN_B200_ERR_CONFIG, "null context");
         cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
         cuda_check(knnb::launch_generate(dev_out, count, seed, ctx->sm_count, s), "generate launch");
     });
 }
@@ -321,7 +353,7 @@ int knn_b200_solve_rows_device(knn_b200_ctx* ctx, const float* dev_vectors, uint
         std::lock_guard<std::mutex> lock(ctx->mu);
         const auto t0 = std::chrono::steady_clock::now();
         cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
         Counters ctr;
         if (stats) cuda_check(cudaEventRecord(ctx->ev[1], s), "event");
         solve_rows_core(ctx, dev_vectors, n, d, k, metric, arith, row_begin, row_end, dev_out_index,

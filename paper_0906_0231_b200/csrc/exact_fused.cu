@@ -97,7 +97,8 @@ template <int METRIC, int KCAP>
 __global__ void __launch_bounds__(EX_THREADS)
 exact_fused_kernel(const float* __restrict__ X, uint32_t n, uint32_t d, uint32_t klist,
                    const uint32_t* __restrict__ rows, uint32_t row_begin, uint32_t row_end,
-                   uint32_t* __restrict__ out_index, float* __restrict__ out_dist, int out_sqrt) {
+                   uint32_t* __restrict__ out_index, float* __restrict__ out_dist, int out_sqrt,
+                   uint32_t scatter_base) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ExactSmem<KCAP>& S = *reinterpret_cast<ExactSmem<KCAP>*>(smem_raw);
     const int tid = threadIdx.x;
@@ -192,11 +193,12 @@ exact_fused_kernel(const float* __restrict__ X, uint32_t n, uint32_t d, uint32_t
     for (int rr = warp; rr < EX_BM; rr += EX_THREADS / 32) {
         const uint32_t s = slot0 + rr;
         if (s >= nslots) continue;
+        const size_t orow = rows ? size_t(qrow[rr] - scatter_base) : size_t(s);
         for (uint32_t t = lane; t < klist; t += 32) {
             const uint64_t key = S.list[rr][t];
-            out_index[size_t(s) * klist + t] = uint32_t(key);
+            out_index[orow * klist + t] = uint32_t(key);
             const float dv = ordered_to_float(uint32_t(key >> 32));
-            out_dist[size_t(s) * klist + t] = out_sqrt ? __fsqrt_rn(dv) : dv;
+            out_dist[orow * klist + t] = out_sqrt ? __fsqrt_rn(dv) : dv;
         }
     }
 }
@@ -204,7 +206,7 @@ exact_fused_kernel(const float* __restrict__ X, uint32_t n, uint32_t d, uint32_t
 template <int METRIC, int KCAP>
 static cudaError_t launch_exact_t(const float* X, uint32_t n, uint32_t d, uint32_t klist,
                                   const uint32_t* rows, uint32_t row_begin, uint32_t row_end,
-                                  uint32_t* out_index, float* out_dist, int out_sqrt, cudaStream_t stream) {
+                                  uint32_t* out_index, float* out_dist, int out_sqrt, uint32_t scatter_base, cudaStream_t stream) {
     const size_t smem = sizeof(ExactSmem<KCAP>);
     auto kern = exact_fused_kernel<METRIC, KCAP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -212,33 +214,33 @@ static cudaError_t launch_exact_t(const float* X, uint32_t n, uint32_t d, uint32
     const uint32_t nslots = row_end - row_begin;
     const dim3 grid((nslots + EX_BM - 1) / EX_BM);
     kern<<<grid, EX_THREADS, smem, stream>>>(X, n, d, klist, rows, row_begin, row_end, out_index,
-                                            out_dist, out_sqrt);
+                                            out_dist, out_sqrt, scatter_base);
     return cudaGetLastError();
 }
 
 template <int METRIC>
 static cudaError_t launch_exact_m(const float* X, uint32_t n, uint32_t d, uint32_t klist,
                                   const uint32_t* rows, uint32_t row_begin, uint32_t row_end,
-                                  uint32_t* out_index, float* out_dist, int out_sqrt, cudaStream_t stream) {
+                                  uint32_t* out_index, float* out_dist, int out_sqrt, uint32_t scatter_base, cudaStream_t stream) {
     if (klist <= 32)
-        return launch_exact_t<METRIC, 32>(X, n, d, klist, rows, row_begin, row_end, out_index, out_dist, out_sqrt, stream);
+        return launch_exact_t<METRIC, 32>(X, n, d, klist, rows, row_begin, row_end, out_index, out_dist, out_sqrt, scatter_base, stream);
     if (klist <= 64)
-        return launch_exact_t<METRIC, 64>(X, n, d, klist, rows, row_begin, row_end, out_index, out_dist, out_sqrt, stream);
+        return launch_exact_t<METRIC, 64>(X, n, d, klist, rows, row_begin, row_end, out_index, out_dist, out_sqrt, scatter_base, stream);
     if (klist <= 128)
-        return launch_exact_t<METRIC, 128>(X, n, d, klist, rows, row_begin, row_end, out_index, out_dist, out_sqrt, stream);
-    return launch_exact_t<METRIC, 256>(X, n, d, klist, rows, row_begin, row_end, out_index, out_dist, out_sqrt, stream);
+        return launch_exact_t<METRIC, 128>(X, n, d, klist, rows, row_begin, row_end, out_index, out_dist, out_sqrt, scatter_base, stream);
+    return launch_exact_t<METRIC, 256>(X, n, d, klist, rows, row_begin, row_end, out_index, out_dist, out_sqrt, scatter_base, stream);
 }
 
 cudaError_t launch_exact_fused(int metric, const float* X, uint32_t n, uint32_t d, uint32_t klist,
                                const uint32_t* rows, uint32_t row_begin, uint32_t row_end,
-                               uint32_t* out_index, float* out_dist, int out_sqrt, cudaStream_t stream) {
+                               uint32_t* out_index, float* out_dist, int out_sqrt, uint32_t scatter_base, cudaStream_t stream) {
     if (row_end <= row_begin) return cudaSuccess;
     // Hellinger arrives sqrt-staged and folds exactly like sqeuclidean.
     switch (metric) {
     case kCosine:
-        return launch_exact_m<kCosine>(X, n, d, klist, rows, row_begin, row_end, out_index, out_dist, out_sqrt, stream);
+        return launch_exact_m<kCosine>(X, n, d, klist, rows, row_begin, row_end, out_index, out_dist, out_sqrt, scatter_base, stream);
     default:
-        return launch_exact_m<kSqEuclidean>(X, n, d, klist, rows, row_begin, row_end, out_index, out_dist, out_sqrt, stream);
+        return launch_exact_m<kSqEuclidean>(X, n, d, klist, rows, row_begin, row_end, out_index, out_dist, out_sqrt, scatter_base, stream);
     }
 }
 

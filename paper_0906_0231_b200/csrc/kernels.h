@@ -20,12 +20,37 @@ cudaError_t launch_generate(float* out, uint64_t count, uint64_t seed, int sm_co
 // EXACT fused sweep.  Output slot s (0 <= s < row_end - row_begin) holds the
 // list of query row `rows ? rows[s] : row_begin + s`; klist = min(k, n-1) <= 256.
 // out_sqrt: report sqrtf(distance) (the Euclidean metric) -- selection is
-// unaffected because sqrtf is monotone and the lists are final.
+// unaffected because sqrtf is monotone and the lists are final.  With an
+// explicit row list, slot s is written to output row rows[s] - scatter_base.
 cudaError_t launch_exact_fused(int metric, const float* X, uint32_t n, uint32_t d, uint32_t klist,
                                const uint32_t* rows, uint32_t row_begin, uint32_t row_end,
                                uint32_t* out_index, float* out_dist, int out_sqrt,
-                               cudaStream_t stream);
+                               uint32_t scatter_base, cudaStream_t stream);
 
 constexpr uint32_t kExactMaxK = 256;
+
+// TENSOR policy (tensor_path.cu)
+struct TensorPathArgs {
+    const float* X;  // fp32, sqrt-staged for Hellinger
+    uint32_t n, d, klist, kp;
+    uint32_t row_begin, row_end;
+    int fold;        // kSqEuclidean or kCosine
+    int out_sqrt;
+    uint32_t* out_index;
+    float* out_dist;
+    void* workspace;      // tensor_workspace_bytes()
+    void* host_scratch;   // 64 B pinned
+    int sm_count;
+    cudaStream_t stream;
+    cudaEvent_t ev_sweep0, ev_sweep1;  // optional, around the sweep kernel
+};
+struct TensorPathResult {
+    unsigned long long rescored = 0;
+    uint32_t fallback_rows = 0;
+    uint32_t launches = 0;
+};
+uint32_t tensor_kp_for(uint32_t klist);  // 0 = unsupported
+size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t rows, uint32_t kp);
+cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r);
 
 }  // namespace knnb

@@ -1,0 +1,631 @@
+// tensor_path.cu -- TENSOR policy: tcgen05 FP16 filter + exact FP32 re-score.
+//
+// The reference (src/dist_kernel.cpp:42-115 + src/select.cpp:60-130) computes
+// every pair with the exact fold and funnels it into per-row heaps.  Here the
+// n x n work runs on the 5th-generation tensor cores instead:
+//
+//   prep     x^_i = fp16_rn(s * (x_i - mu))   (mu = column mean, s = 2^e so
+//            |x^| <= 65504), stored as 128-byte-swizzled K-major planes
+//            [ceil(d/64)][npad][64]; alpha_i = ||x^_i||^2 (fp32); and, in fp64,
+//            the exact quantisation error rho_i = ||x^_i - s (x_i - mu)|| and
+//            ||x^_i|| for the error bound.  (cosine: mu = 0, alpha = s^2.)
+//   sweep    per CTA 128 query rows (UMMA M) against every reference tile of
+//            BN columns: TMA bulk copies -> smem ring -> tcgen05.mma kind::f16
+//            (FP32 accumulators in TMEM, double-buffered) -> 4 epilogue warps,
+//            one thread per query row, A = alpha_i + alpha_j - 2 x^_i.x^_j, kept
+//            in a per-row top-KP list (KP = k + margin) in shared memory.  The
+//            n x n matrix never leaves the SM.
+//   rescore  per row: the exact reference fold (FSUB/FMUL/FADD, coordinates in
+//            order) on the KP candidates, the top-k by (distance, index), and a
+//            proof that no row outside the list can belong to the top-k:
+//            A_max > s^2 T' + E, with T the exact k-th distance and E a
+//            rigorous bound on |A - s^2 D_ref|.  Rows without a
+//            proof are recomputed by the EXACT kernel.
+// Result: bit-identical to brute_force_knn.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "sm100_ptx.cuh"
+
+namespace knnb {
+
+constexpr int TS_BM = 128;
+constexpr int TS_THREADS = 192;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2..5 epilogue
+constexpr uint32_t TS_A_CHUNK = TS_BM * 128;  // 128 rows x 128 B (64 fp16 of K)
+constexpr uint32_t TS_SMEM_MAX = 232448;
+constexpr int TS_MAX_RES_KC = 4;              // A resident in smem when d <= 256
+
+template <int KP, int BN, bool ARES>
+struct TSLayout {
+    static constexpr uint32_t B_CHUNK = BN * 128;
+    static constexpr uint32_t STAGE = B_CHUNK + (ARES ? 0 : TS_A_CHUNK);
+    static constexpr uint32_t A_BYTES = ARES ? TS_MAX_RES_KC * TS_A_CHUNK : 0;
+    static constexpr uint32_t LISTS = TS_BM * KP * 8;
+    static constexpr uint32_t MISC = 256;
+    static constexpr uint32_t AVAIL = TS_SMEM_MAX - 1024 - MISC - LISTS - A_BYTES;
+    static constexpr int STAGES_RAW = int(AVAIL / STAGE);
+    static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
+    static_assert(STAGES >= 2, "shared memory budget too small for a 2-stage ring");
+    static constexpr uint32_t SMEM = 1024 + A_BYTES + STAGES * STAGE + LISTS + MISC;
+    static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
+};
+
+struct SweepParams {
+    const uint8_t* xh;    // swizzled fp16 planes
+    const float* alpha;   // [npad], +inf on padding rows
+    uint32_t n, npad, kc;
+    uint32_t row_begin, row_end;
+    uint64_t* cand;       // [(row_end - row_begin) * KP]
+};
+
+template <int KP, int BN, bool ARES>
+__global__ void __launch_bounds__(TS_THREADS, 1) tensor_sweep_kernel(const SweepParams p) {
+    using L = TSLayout<KP, BN, ARES>;
+    constexpr int S = L::STAGES;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* a_smem = smem;
+    uint8_t* stage_smem = smem + L::A_BYTES;
+    uint64_t* lists = reinterpret_cast<uint64_t*>(stage_smem + S * L::STAGE);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(lists) + L::LISTS);
+    // bars: full[S], empty[S], tfull[2], tempty[2], afull
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 5);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t r0 = p.row_begin + blockIdx.x * TS_BM;
+    const uint32_t ntiles = (p.n + BN - 1) / BN;
+    const uint32_t bar0 = ptx::smem_u32(bars);
+    auto full_bar = [&](int s) { return bar0 + 8u * s; };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (S + s); };
+    auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * S + b); };
+    auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * S + 2 + b); };
+    const uint32_t afull_bar = bar0 + 8u * (2 * S + 4);
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(full_bar(s), 1);
+            ptx::mbar_init(empty_bar(s), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(tfull_bar(b), 1);
+            ptx::mbar_init(tempty_bar(b), 4);  // one arrive per epilogue warp
+        }
+        ptx::mbar_init(afull_bar, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), L::TMEM_COLS);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer (one lane) ----------------
+        if (lane == 0) {
+            const uint64_t keep = ptx::policy_evict_last();  // reference tiles: reused by every CTA
+            if constexpr (ARES) {
+                ptx::mbar_arrive_expect_tx(afull_bar, p.kc * TS_A_CHUNK);
+                for (uint32_t kc = 0; kc < p.kc; ++kc)
+                    ptx::bulk_g2s(ptx::smem_u32(a_smem + kc * TS_A_CHUNK),
+                                  p.xh + (size_t(kc) * p.npad + r0) * 128, TS_A_CHUNK, afull_bar);
+            }
+            int stage = 0;
+            uint32_t phase = 0;
+            for (uint32_t t = 0; t < ntiles; ++t) {
+                for (uint32_t kc = 0; kc < p.kc; ++kc) {
+                    ptx::mbar_wait(empty_bar(stage), phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(full_bar(stage), L::STAGE);
+                    uint8_t* dst = stage_smem + stage * L::STAGE;
+                    ptx::bulk_g2s_hint(ptx::smem_u32(dst), p.xh + (size_t(kc) * p.npad + size_t(t) * BN) * 128,
+                                       L::B_CHUNK, full_bar(stage), keep);
+                    if constexpr (!ARES)
+                        ptx::bulk_g2s(ptx::smem_u32(dst + L::B_CHUNK), p.xh + (size_t(kc) * p.npad + r0) * 128,
+                                      TS_A_CHUNK, full_bar(stage));
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (one lane) ----------------
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_f16_f32(TS_BM, BN);
+            if constexpr (ARES) ptx::mbar_wait(afull_bar, 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (uint32_t t = 0; t < ntiles; ++t) {
+                const uint32_t b = t & 1, use = t >> 1;
+                ptx::mbar_wait(tempty_bar(b), (use & 1) ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem + b * BN;
+                for (uint32_t kc = 0; kc < p.kc; ++kc) {
+                    ptx::mbar_wait(full_bar(stage), phase);
+                    ptx::tc_fence_after();
+                    const uint8_t* bsm = stage_smem + stage * L::STAGE;
+                    const uint8_t* asm_ = ARES ? a_smem + kc * TS_A_CHUNK : bsm + L::B_CHUNK;
+                    const uint32_t a_addr = ptx::smem_u32(asm_);
+                    const uint32_t b_addr = ptx::smem_u32(bsm);
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k) {  // UMMA_K = 16 fp16 = 32 B inside the swizzle atom
+                        ptx::mma_f16_ss(d_tmem, ptx::sw128_kmajor_desc(a_addr + 32 * k),
+                                        ptx::sw128_kmajor_desc(b_addr + 32 * k), idesc, (kc | k) != 0);
+                    }
+                    ptx::mma_commit(empty_bar(stage));
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::mma_commit(tfull_bar(b));
+            }
+        }
+    } else {
+        // ---------------- epilogue: one thread per query row ----------------
+        const int quad = warp & 3;  // TMEM lanes 32*quad .. +31 are this warp's
+        const int rl = quad * 32 + lane;
+        const uint32_t row = r0 + rl;
+        const bool valid = row < p.row_end;
+        uint64_t* my = lists + rl;
+#pragma unroll 4
+        for (int s = 0; s < KP; ++s) my[s * TS_BM] = kEmptyKey;
+        const float alpha_i = valid ? p.alpha[row] : 0.0f;
+        uint64_t thr_key = kEmptyKey;
+        float thr_f = valid ? __int_as_float(0x7f800000) : __int_as_float(0xff800000);
+        const uint32_t lane_addr = tmem + (uint32_t(quad * 32) << 16);
+        for (uint32_t t = 0; t < ntiles; ++t) {
+            const uint32_t b = t & 1, use = t >> 1;
+            ptx::mbar_wait(tfull_bar(b), use & 1);
+            ptx::tc_fence_after();
+            const uint32_t cbase = t * BN;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(lane_addr + b * BN + c0, v);
+                const float4* beta4 = reinterpret_cast<const float4*>(p.alpha + cbase + c0);
+                float beta[32];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float4 f = __ldg(beta4 + q);
+                    beta[4 * q] = f.x;
+                    beta[4 * q + 1] = f.y;
+                    beta[4 * q + 2] = f.z;
+                    beta[4 * q + 3] = f.w;
+                }
+                ptx::tmem_wait_ld();
+                if (c0 + 32 == BN) {  // all of this buffer is in registers: hand it back to the MMA warp
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(tempty_bar(b));
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float a = __fmaf_rn(-2.0f, __uint_as_float(v[j]), __fadd_rn(alpha_i, beta[j]));
+                    if (a <= thr_f) {
+                        const uint32_t col = cbase + c0 + j;
+                        const uint64_t key = (uint64_t(float_to_ordered(a)) << 32) | col;
+                        if (key < thr_key && col < p.n) {
+                            int pos = KP - 1;
+                            while (pos > 0) {
+                                const uint64_t prev = my[(pos - 1) * TS_BM];
+                                if (prev < key) break;
+                                my[pos * TS_BM] = prev;
+                                --pos;
+                            }
+                            my[pos * TS_BM] = key;
+                            thr_key = my[(KP - 1) * TS_BM];
+                            thr_f = thr_key == kEmptyKey ? __int_as_float(0x7f800000)
+                                                         : ordered_to_float(uint32_t(thr_key >> 32));
+                        }
+                    }
+                }
+            }
+        }
+        if (valid) {
+            uint64_t* out = p.cand + size_t(row - p.row_begin) * KP;
+            for (int s = 0; s < KP; ++s) out[s] = my[s * TS_BM];
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, L::TMEM_COLS);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// prep kernels
+
+__device__ __forceinline__ void atomic_max_pos_double(unsigned long long* addr, double v) {
+    // non-negative doubles order like their bit patterns
+    atomicMax(addr, (unsigned long long)__double_as_longlong(v));
+}
+
+// Column sums in double -> mu (any mu is correct: distances are translation
+// invariant; mu only shrinks the magnitudes the fp16 filter sees).
+__global__ void colsum_kernel(const float* __restrict__ X, uint32_t n, uint32_t d, double* __restrict__ acc) {
+    const uint32_t rows_per = (n + gridDim.x - 1) / gridDim.x;
+    const uint32_t ra = blockIdx.x * rows_per;
+    const uint32_t rb = min(n, ra + rows_per);
+    for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) {
+        double s = 0;
+        for (uint32_t r = ra; r < rb; ++r) s += X[size_t(r) * d + j];
+        atomicAdd(acc + j, s);
+    }
+}
+
+__global__ void mu_finalize_kernel(const double* __restrict__ acc, uint32_t n, uint32_t d, float* __restrict__ mu) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < d; j += gridDim.x * blockDim.x)
+        mu[j] = float(acc[j] / double(n));
+}
+
+__global__ void maxabs_kernel(const float* __restrict__ X, uint64_t count, uint32_t d, const float* __restrict__ mu,
+                              unsigned int* __restrict__ out) {
+    float m = 0.0f;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride)
+        m = fmaxf(m, fabsf(__fsub_rn(X[i], mu[i % d])));
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+// Power-of-two scale with |s x| <= 65504 (fp16 max), capped at 2^40.
+__device__ __forceinline__ int scale_exponent(unsigned int maxabs_bits) {
+    const float m = __uint_as_float(maxabs_bits);
+    if (!(m > 0.0f)) return 0;
+    int p;
+    frexp(65504.0 / double(m), &p);  // 65504/m = f * 2^p, f in [0.5, 1)
+    int e = p - 1;
+    return e > 40 ? 40 : e;
+}
+
+struct PrepOut {
+    uint8_t* xh;
+    float* alpha;
+    double* rho;
+    double* xnorm;
+    unsigned long long* gmax;  // [0] max xnorm, [1] max rho, [2] max alpha
+};
+
+// One warp per (padded) row.
+__global__ void prep_kernel(const float* __restrict__ X, uint32_t n, uint32_t d, uint32_t npad, uint32_t kc,
+                            const float* __restrict__ mu, const unsigned int* __restrict__ maxabs, int cosine,
+                            PrepOut o) {
+    const uint32_t warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp_global >= npad) return;
+    const uint32_t row = warp_global;
+    const int e = scale_exponent(*maxabs);
+    const float s = ldexpf(1.0f, e);
+    const double sd = ldexp(1.0, e);
+    double rho2 = 0, nrm2 = 0;
+    float alpha = 0.0f;
+    const uint32_t kpad = kc * 64;
+    for (uint32_t k = lane; k < kpad; k += 32) {
+        __half h = __float2half_rn(0.0f);
+        if (row < n && k < d) {
+            const float x = X[size_t(row) * d + k];
+            const float m = cosine ? 0.0f : mu[k];
+            const float v = __fsub_rn(x, m);
+            h = __float2half_rn(__fmul_rn(v, s));
+            const double hv = double(__half2float(h));
+            const double exact = (double(x) - double(m)) * sd;
+            rho2 += (hv - exact) * (hv - exact);
+            nrm2 += hv * hv;
+            const float hf = __half2float(h);
+            alpha = __fadd_rn(alpha, __fmul_rn(hf, hf));
+        }
+        const uint32_t chunk = k >> 6, kk = k & 63;
+        const uint32_t off = ((((kk >> 3) ^ (row & 7)) << 4) | ((kk & 7) << 1));
+        *reinterpret_cast<__half*>(o.xh + (size_t(chunk) * npad + row) * 128 + off) = h;
+    }
+    for (int of = 16; of; of >>= 1) {
+        rho2 += __shfl_xor_sync(0xffffffffu, rho2, of);
+        nrm2 += __shfl_xor_sync(0xffffffffu, nrm2, of);
+        alpha = __fadd_rn(alpha, __shfl_xor_sync(0xffffffffu, alpha, of));
+    }
+    if (lane == 0) {
+        if (row < n) {
+            const float a = cosine ? __fmul_rn(s, s) : alpha;
+            o.alpha[row] = a;
+            const double rho = sqrt(rho2) * (1.0 + 1e-12);
+            const double xn = sqrt(nrm2) * (1.0 + 1e-12);
+            o.rho[row] = rho;
+            o.xnorm[row] = xn;
+            atomic_max_pos_double(o.gmax + 0, xn);
+            atomic_max_pos_double(o.gmax + 1, rho);
+            atomic_max_pos_double(o.gmax + 2, double(a));
+        } else {
+            o.alpha[row] = __int_as_float(0x7f800000);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// exact re-score + proof of completeness
+
+struct RescoreParams {
+    const float* X;       // fp32 (sqrt-staged for Hellinger)
+    uint32_t n, d, klist, kp;
+    uint32_t row_begin, row_end;
+    const uint64_t* cand;
+    const float* alpha;
+    const double* rho;
+    const double* xnorm;
+    const unsigned long long* gmax;
+    const unsigned int* maxabs;
+    int fold;             // kSqEuclidean or kCosine
+    int out_sqrt;
+    uint32_t* out_index;
+    float* out_dist;
+    uint32_t* fb_count;
+    uint32_t* fb_rows;
+    unsigned long long* rescored;
+};
+
+constexpr double kTcSafety = 4.0;  // tensor-core accumulation error allowance
+
+template <int FOLD>
+__device__ __forceinline__ float exact_fold_rows(const float* __restrict__ a, const float* __restrict__ b, uint32_t d,
+                                                 bool vec) {
+    float acc = 0.0f;
+    if (vec) {
+        const float4* a4 = reinterpret_cast<const float4*>(a);
+        const float4* b4 = reinterpret_cast<const float4*>(b);
+        for (uint32_t j = 0; j < d / 4; ++j) {
+            const float4 x = __ldg(a4 + j), y = __ldg(b4 + j);
+            acc = fold_step<FOLD>(x.x, y.x, acc);
+            acc = fold_step<FOLD>(x.y, y.y, acc);
+            acc = fold_step<FOLD>(x.z, y.z, acc);
+            acc = fold_step<FOLD>(x.w, y.w, acc);
+        }
+    } else {
+        for (uint32_t j = 0; j < d; ++j) acc = fold_step<FOLD>(__ldg(a + j), __ldg(b + j), acc);
+    }
+    return fold_finalize<FOLD>(acc);
+}
+
+template <int FOLD, int KP>
+__global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
+    __shared__ uint64_t keys_s[8][KP];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t slot = blockIdx.x * 8 + warp;
+    if (slot >= p.row_end - p.row_begin) return;
+    const uint32_t q = p.row_begin + slot;
+    const uint64_t* cand = p.cand + size_t(slot) * KP;
+    const float* xq = p.X + size_t(q) * p.d;
+    const bool vec = (p.d % 4 == 0);
+    constexpr int PER = (KP + 31) / 32;
+    uint32_t valid = 0;
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+        const int i = lane + 32 * m;
+        if (i >= KP) break;
+        const uint64_t c = cand[i];
+        uint64_t key = kEmptyKey;
+        const uint32_t col = uint32_t(c);
+        if (c != kEmptyKey && col != q) {
+            const float* xc = p.X + size_t(col) * p.d;
+            // Reference argument order (larger index first) -- the fold is
+            // symmetric bit for bit, kept for clarity.
+            const float dist = col > q ? exact_fold_rows<FOLD>(xc, xq, p.d, vec) : exact_fold_rows<FOLD>(xq, xc, p.d, vec);
+            key = make_key(dist, col);
+            ++valid;
+        }
+        keys_s[warp][i] = key;
+    }
+    for (int o = 16; o; o >>= 1) valid += __shfl_xor_sync(0xffffffffu, valid, o);
+    __syncwarp();
+    if (lane == 0) atomicAdd(p.rescored, (unsigned long long)valid);
+
+    // rank sort of the exact keys (unique except the empty ones, which sort last)
+    uint64_t mine[PER];
+    uint32_t rank[PER];
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+        const int i = lane + 32 * m;
+        mine[m] = i < KP ? keys_s[warp][i] : kEmptyKey;
+        rank[m] = 0;
+    }
+    for (int j = 0; j < KP; ++j) {
+        const uint64_t o = keys_s[warp][j];
+#pragma unroll
+        for (int m = 0; m < PER; ++m) rank[m] += (o < mine[m]) || (o == mine[m] && j < lane + 32 * m);
+    }
+    // the k-th exact key (T) and the largest approximate key of the list
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < PER; ++m)
+        if (lane + 32 * m < KP) keys_s[warp][rank[m]] = mine[m];
+    __syncwarp();
+    const uint64_t last_approx = cand[KP - 1];
+    bool complete;
+    if (last_approx == kEmptyKey) {
+        complete = true;  // every column was offered into a non-full list: the list holds all of them
+    } else if (valid < p.klist) {
+        complete = false;
+    } else {
+        const uint64_t kth = keys_s[warp][p.klist - 1];
+        const double T = double(ordered_to_float(uint32_t(kth >> 32)));
+        const double a_max = double(ordered_to_float(uint32_t(last_approx >> 32)));
+        const double u = 5.9604644775390625e-08;  // 2^-24
+        const double dd = double(p.d);
+        const int e = scale_exponent(*p.maxabs);
+        const double s2 = ldexp(1.0, 2 * e);
+        const double xnmax = __longlong_as_double((long long)p.gmax[0]);
+        const double rhomax = __longlong_as_double((long long)p.gmax[1]);
+        const double alphamax = __longlong_as_double((long long)p.gmax[2]);
+        const double nx = p.xnorm[q], rh = p.rho[q], al = double(p.alpha[q]);
+        const double Tp = T + fabs(T) * 2.0 * (dd + 3.0) * u + 1e-300;
+        const double ctc = 2.0 * kTcSafety * dd * 2.0 * u;  // 2 * c * d * 2^-23
+        double bound;
+        if (FOLD == kCosine) {
+            const double eref = (dd + 2.0) * u * ((nx + rh) * (xnmax + rhomax) / s2 + 1.0);
+            const double eacc = ctc * nx * xnmax + 2.0 * (rh * xnmax + rhomax * (nx + rh)) + u * 2.0 * s2 * (fabs(Tp) + 2.0);
+            bound = 2.0 * s2 * (Tp + 2.0 * eref) + 2.0 * eacc;
+        } else {
+            const double rr = rh + rhomax;
+            const double e_all = (ctc + 6.0 * u) * nx * xnmax + (dd + 3.0) * u * (al + alphamax) +
+                                 rr * (2.0 * sqrt(s2 * fmax(Tp, 0.0)) + rr);
+            bound = s2 * Tp + 2.0 * e_all;
+        }
+        complete = a_max > bound;
+    }
+    if (!complete) {
+        if (lane == 0) {
+            const uint32_t at = atomicAdd(p.fb_count, 1u);
+            p.fb_rows[at] = q;
+        }
+        return;
+    }
+    for (uint32_t t = lane; t < p.klist; t += 32) {
+        const uint64_t key = keys_s[warp][t];
+        const float dv = ordered_to_float(uint32_t(key >> 32));
+        p.out_index[size_t(slot) * p.klist + t] = uint32_t(key);
+        p.out_dist[size_t(slot) * p.klist + t] = p.out_sqrt ? __fsqrt_rn(dv) : dv;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+
+uint32_t tensor_kp_for(uint32_t klist) {
+    // k + 1 (the query itself can occupy a slot) + margin for the error band
+    const uint32_t need = klist + 1 + (klist / 4 > 8 ? klist / 4 : 8);
+    if (need <= 32) return 32;
+    if (need <= 64) return 64;
+    if (need <= 128) return 128;
+    return 0;  // not supported by the tensor sweep
+}
+
+size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t rows, uint32_t kp) {
+    const uint32_t npad = (n + 255) / 256 * 256;
+    const uint32_t kc = (d + 63) / 64;
+    size_t b = 0;
+    auto add = [&](size_t x) { b += (x + 255) / 256 * 256; };
+    add(size_t(kc) * npad * 128);  // xh
+    add(size_t(npad) * 4);         // alpha
+    add(size_t(npad) * 8);         // rho
+    add(size_t(npad) * 8);         // xnorm
+    add(size_t(d) * 8);            // mu acc
+    add(size_t(d) * 4);            // mu
+    add(64);                       // scalars
+    add(size_t(rows) * kp * 8);    // cand
+    add(size_t(rows) * 4);         // fallback rows
+    return b;
+}
+
+template <int KP, int BN, bool ARES>
+static cudaError_t launch_sweep_t(const SweepParams& sp, uint32_t nrows, cudaStream_t stream) {
+    using L = TSLayout<KP, BN, ARES>;
+    auto kern = tensor_sweep_kernel<KP, BN, ARES>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::SMEM));
+    if (e != cudaSuccess) return e;
+    const dim3 grid((nrows + TS_BM - 1) / TS_BM);
+    kern<<<grid, TS_THREADS, L::SMEM, stream>>>(sp);
+    return cudaGetLastError();
+}
+
+static cudaError_t launch_sweep(uint32_t kp, bool ares, const SweepParams& sp, uint32_t nrows, cudaStream_t stream) {
+    switch (kp) {
+    case 32:
+        return ares ? launch_sweep_t<32, 256, true>(sp, nrows, stream) : launch_sweep_t<32, 256, false>(sp, nrows, stream);
+    case 64:
+        return ares ? launch_sweep_t<64, 256, true>(sp, nrows, stream) : launch_sweep_t<64, 256, false>(sp, nrows, stream);
+    default:
+        return ares ? launch_sweep_t<128, 128, true>(sp, nrows, stream)
+                    : launch_sweep_t<128, 128, false>(sp, nrows, stream);
+    }
+}
+
+template <int FOLD>
+static cudaError_t launch_rescore(uint32_t kp, const RescoreParams& rp, uint32_t nrows, cudaStream_t stream) {
+    const dim3 grid((nrows + 7) / 8);
+    switch (kp) {
+    case 32: rescore_kernel<FOLD, 32><<<grid, 256, 0, stream>>>(rp); break;
+    case 64: rescore_kernel<FOLD, 64><<<grid, 256, 0, stream>>>(rp); break;
+    default: rescore_kernel<FOLD, 128><<<grid, 256, 0, stream>>>(rp); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
+    const uint32_t n = a.n, d = a.d, nrows = a.row_end - a.row_begin;
+    const uint32_t npad = (n + 255) / 256 * 256;
+    const uint32_t kc = (d + 63) / 64;
+    const uint32_t kp = a.kp;
+    const int cosine = a.fold == kCosine;
+    uint8_t* w = static_cast<uint8_t*>(a.workspace);
+    auto take = [&](size_t x) {
+        uint8_t* p = w;
+        w += (x + 255) / 256 * 256;
+        return p;
+    };
+    uint8_t* xh = take(size_t(kc) * npad * 128);
+    float* alpha = reinterpret_cast<float*>(take(size_t(npad) * 4));
+    double* rho = reinterpret_cast<double*>(take(size_t(npad) * 8));
+    double* xnorm = reinterpret_cast<double*>(take(size_t(npad) * 8));
+    double* muacc = reinterpret_cast<double*>(take(size_t(d) * 8));
+    float* mu = reinterpret_cast<float*>(take(size_t(d) * 4));
+    uint8_t* scal = take(64);
+    uint64_t* cand = reinterpret_cast<uint64_t*>(take(size_t(nrows) * kp * 8));
+    uint32_t* fb_rows = reinterpret_cast<uint32_t*>(take(size_t(nrows) * 4));
+    unsigned int* maxabs = reinterpret_cast<unsigned int*>(scal);
+    uint32_t* fb_count = reinterpret_cast<uint32_t*>(scal + 4);
+    unsigned long long* gmax = reinterpret_cast<unsigned long long*>(scal + 8);
+    unsigned long long* rescored = reinterpret_cast<unsigned long long*>(scal + 32);
+    cudaStream_t st = a.stream;
+    cudaError_t e;
+    uint32_t launches = 0;
+
+    if ((e = cudaMemsetAsync(scal, 0, 64, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(muacc, 0, size_t(d) * 8, st)) != cudaSuccess) return e;
+    if (!cosine) {
+        colsum_kernel<<<a.sm_count * 4, 256, 0, st>>>(a.X, n, d, muacc);
+        mu_finalize_kernel<<<(d + 255) / 256, 256, 0, st>>>(muacc, n, d, mu);
+        launches += 2;
+    } else {
+        if ((e = cudaMemsetAsync(mu, 0, size_t(d) * 4, st)) != cudaSuccess) return e;
+    }
+    maxabs_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, uint64_t(n) * d, d, mu, maxabs);
+    PrepOut po{xh, alpha, rho, xnorm, gmax};
+    prep_kernel<<<(npad * 32 + 255) / 256, 256, 0, st>>>(a.X, n, d, npad, kc, mu, maxabs, cosine, po);
+    launches += 2;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+
+    SweepParams sp{xh, alpha, n, npad, kc, a.row_begin, a.row_end, cand};
+    if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
+    if ((e = launch_sweep(kp, kc <= uint32_t(TS_MAX_RES_KC), sp, nrows, st)) != cudaSuccess) return e;
+    if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
+    ++launches;
+
+    RescoreParams rp{a.X, n, d, a.klist, kp, a.row_begin, a.row_end, cand, alpha, rho, xnorm, gmax, maxabs,
+                     a.fold, a.out_sqrt, a.out_index, a.out_dist, fb_count, fb_rows, rescored};
+    e = cosine ? launch_rescore<kCosine>(kp, rp, nrows, st) : launch_rescore<kSqEuclidean>(kp, rp, nrows, st);
+    if (e != cudaSuccess) return e;
+    ++launches;
+
+    // Rows without a completeness proof: exact recomputation (rare).
+    if ((e = cudaMemcpyAsync(a.host_scratch, scal, 64, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    const uint32_t nfb = *reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(a.host_scratch) + 4);
+    r.rescored = *reinterpret_cast<const unsigned long long*>(static_cast<const uint8_t*>(a.host_scratch) + 32);
+    r.fallback_rows = nfb;
+    if (nfb) {
+        if ((e = launch_exact_fused(a.fold, a.X, n, d, a.klist, fb_rows, 0, nfb, a.out_index, a.out_dist, a.out_sqrt,
+                                    a.row_begin, st)) != cudaSuccess)
+            return e;
+        ++launches;
+    }
+    r.launches = launches;
+    return cudaSuccess;
+}
+
+}  // namespace knnb

@@ -351,7 +351,7 @@ class Context:
         st = _lib.Stats() if want_stats else None
         rc = _lib.load().knn_b200_solve_rows_device(
             self._h, x_ptr, n, d, k, metric.metric_id, arith, row_begin, row_end, out_index_ptr,
-            out_dist_ptr, stream_ptr or None, ctypes.byref(st) if st is not None else None)
+            out_dist_ptr, stream_ptr, ctypes.byref(st) if st is not None else None)
         raise_for_status(rc)
         return st.as_dict() if st is not None else None
 
