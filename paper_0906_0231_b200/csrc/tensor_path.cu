@@ -57,10 +57,60 @@ struct TSLayout {
 struct SweepParams {
     const uint8_t* xh;    // swizzled fp16 planes
     const float* alpha;   // [npad], +inf on padding rows
+    const unsigned long long* alpha_max;  // bits of max alpha (double), from prep
     uint32_t n, npad, kc;
     uint32_t row_begin, row_end;
     uint64_t* cand;       // [(row_end - row_begin) * KP]
 };
+
+// Per-row candidate list: KP unsorted (approximate distance, index) entries in
+// shared memory -- a [KP][TS_BM] float array and a [KP][TS_BM] index array,
+// so the 32 lanes of a warp touch consecutive words -- plus its maximum, the
+// admission threshold (the reference's heap root, heap.hpp:86-90).  The list
+// keeps the KP smallest approximate distances with ties broken arbitrarily:
+// the completeness proof only needs "every row outside the list has A >= the
+// list maximum".  Replacing the maximum and rescanning costs KP independent
+// shared loads and runs warp-convergently.
+struct ListMax {
+    float a;
+    uint32_t slot;
+};
+
+constexpr uint32_t kListStride = TS_BM * 4;  // bytes between consecutive entries of one row
+
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+template <int KP>
+__device__ __forceinline__ ListMax list_rescan(uint32_t a_base) {
+    // pass 1: maximum (independent loads, a max tree); pass 2: its slot
+    float m = lds_f32(a_base);
+#pragma unroll
+    for (int i = 1; i < KP; ++i) m = fmaxf(m, lds_f32(a_base + i * kListStride));
+    uint32_t slot = 0;
+#pragma unroll
+    for (int i = KP - 1; i >= 0; --i) slot = (lds_f32(a_base + i * kListStride) == m) ? uint32_t(i) : slot;
+    return ListMax{m, slot};
+}
+
+template <int KP>
+__device__ __noinline__ ListMax list_replace_max(uint32_t a_base, uint32_t i_base, uint32_t slot, float a,
+                                                 uint32_t col) {
+    sts_f32(a_base + slot * kListStride, a);
+    sts_u32(i_base + slot * kListStride, col);
+    return list_rescan<KP>(a_base);
+}
 
 template <int KP, int BN, bool ARES>
 __global__ void __launch_bounds__(TS_THREADS, 1) tensor_sweep_kernel(const SweepParams p) {
@@ -70,8 +120,9 @@ __global__ void __launch_bounds__(TS_THREADS, 1) tensor_sweep_kernel(const Sweep
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* a_smem = smem;
     uint8_t* stage_smem = smem + L::A_BYTES;
-    uint64_t* lists = reinterpret_cast<uint64_t*>(stage_smem + S * L::STAGE);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(lists) + L::LISTS);
+    float* list_a = reinterpret_cast<float*>(stage_smem + S * L::STAGE);   // [KP][TS_BM]
+    uint32_t* list_i = reinterpret_cast<uint32_t*>(list_a + KP * TS_BM);    // [KP][TS_BM]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stage_smem + S * L::STAGE + L::LISTS);
     // bars: full[S], empty[S], tfull[2], tempty[2], afull
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 5);
 
@@ -172,64 +223,100 @@ __global__ void __launch_bounds__(TS_THREADS, 1) tensor_sweep_kernel(const Sweep
         const int rl = quad * 32 + lane;
         const uint32_t row = r0 + rl;
         const bool valid = row < p.row_end;
-        uint64_t* my = lists + rl;
+        float* my_a = list_a + rl;
+        uint32_t* my_i = list_i + rl;
+        const uint32_t a_base = ptx::smem_u32(my_a), i_base = ptx::smem_u32(my_i);
+        const float kInf = __int_as_float(0x7f800000);
 #pragma unroll 4
-        for (int s = 0; s < KP; ++s) my[s * TS_BM] = kEmptyKey;
+        for (int s = 0; s < KP; ++s) {
+            my_a[s * TS_BM] = kInf;
+            my_i[s * TS_BM] = 0xffffffffu;
+        }
         const float alpha_i = valid ? p.alpha[row] : 0.0f;
-        uint64_t thr_key = kEmptyKey;
-        float thr_f = valid ? __int_as_float(0x7f800000) : __int_as_float(0xff800000);
+        const float slack = 1e-6f * (fabsf(alpha_i) + float(__longlong_as_double((long long)*p.alpha_max)));
+        ListMax thr{kInf, 0};
+        // Hot-path test: A = fl(fl(alpha_i + beta_j) - 2 dot) < thr.a is
+        // pre-filtered as fl(beta_j - 2 dot) <= thr.a - alpha_i + slack, which
+        // admits a superset (slack >> the rounding difference);
+        // the exact A is recomputed for the admitted columns only.
+        float thr_pre = -kInf;
+        auto set_thr = [&](ListMax m) {
+            thr = m;
+            thr_pre = !valid ? -kInf : (m.a == kInf ? kInf : __fadd_ru(__fsub_ru(m.a, alpha_i), slack + 1e-6f * fabsf(m.a)));
+        };
         const uint32_t lane_addr = tmem + (uint32_t(quad * 32) << 16);
+        auto process = [&](const uint32_t (&v)[32], uint32_t col0) {
+            const float4* beta4 = reinterpret_cast<const float4*>(p.alpha + col0);
+            float beta[32];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const float4 f = __ldg(beta4 + q);
+                beta[4 * q] = f.x;
+                beta[4 * q + 1] = f.y;
+                beta[4 * q + 2] = f.z;
+                beta[4 * q + 3] = f.w;
+            }
+            if (col0 < uint32_t(KP)) {  // first KP columns: fill the list directly
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t col = col0 + j;
+                    const float a = __fmaf_rn(-2.0f, __uint_as_float(v[j]), __fadd_rn(alpha_i, beta[j]));
+                    my_a[col * TS_BM] = col < p.n ? a : kInf;
+                    my_i[col * TS_BM] = col < p.n ? col : 0xffffffffu;
+                }
+                if (col0 + 32 == uint32_t(KP)) set_thr(list_rescan<KP>(a_base));
+                return;
+            }
+            // 2 instructions per distance: FFMA + FMNMX
+            float y[32];
+            float ymin = kInf;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                y[j] = __fmaf_rn(-2.0f, __uint_as_float(v[j]), beta[j]);
+                ymin = fminf(ymin, y[j]);
+            }
+            if (__any_sync(0xffffffffu, ymin <= thr_pre)) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (y[j] <= thr_pre) {
+                        const uint32_t col = col0 + j;
+                        const float a = __fmaf_rn(-2.0f, __uint_as_float(v[j]), __fadd_rn(alpha_i, beta[j]));
+                        if (a < thr.a && col < p.n) set_thr(list_replace_max<KP>(a_base, i_base, thr.slot, a, col));
+                    }
+                }
+            }
+        };
         for (uint32_t t = 0; t < ntiles; ++t) {
             const uint32_t b = t & 1, use = t >> 1;
             ptx::mbar_wait(tfull_bar(b), use & 1);
             ptx::tc_fence_after();
             const uint32_t cbase = t * BN;
+            const uint32_t taddr = lane_addr + b * BN;
+            uint32_t va[32], vb[32];
+            // software-pipelined TMEM reads: chunk c+1 streams in while chunk c is filtered
+            ptx::tmem_ld_32x32b_x32(taddr, va);
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
-                uint32_t v[32];
-                ptx::tmem_ld_32x32b_x32(lane_addr + b * BN + c0, v);
-                const float4* beta4 = reinterpret_cast<const float4*>(p.alpha + cbase + c0);
-                float beta[32];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const float4 f = __ldg(beta4 + q);
-                    beta[4 * q] = f.x;
-                    beta[4 * q + 1] = f.y;
-                    beta[4 * q + 2] = f.z;
-                    beta[4 * q + 3] = f.w;
-                }
+            for (int c0 = 0; c0 < BN; c0 += 64) {
                 ptx::tmem_wait_ld();
-                if (c0 + 32 == BN) {  // all of this buffer is in registers: hand it back to the MMA warp
+                ptx::tmem_ld_32x32b_x32(taddr + c0 + 32, vb);
+                process(va, cbase + c0);
+                ptx::tmem_wait_ld();
+                if (c0 + 64 < BN) {
+                    ptx::tmem_ld_32x32b_x32(taddr + c0 + 64, va);
+                } else {  // the whole accumulator is in registers: hand it back to the MMA warp
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(tempty_bar(b));
                 }
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float a = __fmaf_rn(-2.0f, __uint_as_float(v[j]), __fadd_rn(alpha_i, beta[j]));
-                    if (a <= thr_f) {
-                        const uint32_t col = cbase + c0 + j;
-                        const uint64_t key = (uint64_t(float_to_ordered(a)) << 32) | col;
-                        if (key < thr_key && col < p.n) {
-                            int pos = KP - 1;
-                            while (pos > 0) {
-                                const uint64_t prev = my[(pos - 1) * TS_BM];
-                                if (prev < key) break;
-                                my[pos * TS_BM] = prev;
-                                --pos;
-                            }
-                            my[pos * TS_BM] = key;
-                            thr_key = my[(KP - 1) * TS_BM];
-                            thr_f = thr_key == kEmptyKey ? __int_as_float(0x7f800000)
-                                                         : ordered_to_float(uint32_t(thr_key >> 32));
-                        }
-                    }
-                }
+                process(vb, cbase + c0 + 32);
             }
         }
         if (valid) {
             uint64_t* out = p.cand + size_t(row - p.row_begin) * KP;
-            for (int s = 0; s < KP; ++s) out[s] = my[s * TS_BM];
+            for (int s = 0; s < KP; ++s) {
+                const uint32_t col = my_i[s * TS_BM];
+                out[s] = col == 0xffffffffu ? kEmptyKey : (uint64_t(float_to_ordered(my_a[s * TS_BM])) << 32) | col;
+            }
         }
     }
     ptx::tc_fence_before();
@@ -445,7 +532,16 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     for (int m = 0; m < PER; ++m)
         if (lane + 32 * m < KP) keys_s[warp][rank[m]] = mine[m];
     __syncwarp();
-    const uint64_t last_approx = cand[KP - 1];
+    // the candidate list is unsorted: its largest key and whether it is full
+    uint64_t amax = 0;
+#pragma unroll
+    for (int m = 0; m < PER; ++m)
+        if (lane + 32 * m < KP) amax = max(amax, cand[lane + 32 * m]);
+    for (int o = 16; o; o >>= 1) {
+        const uint64_t other = __shfl_xor_sync(0xffffffffu, amax, o);
+        amax = other > amax ? other : amax;
+    }
+    const uint64_t last_approx = amax;
     bool complete;
     if (last_approx == kEmptyKey) {
         complete = true;  // every column was offered into a non-full list: the list holds all of them
@@ -600,7 +696,7 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     launches += 2;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
-    SweepParams sp{xh, alpha, n, npad, kc, a.row_begin, a.row_end, cand};
+    SweepParams sp{xh, alpha, gmax + 2, n, npad, kc, a.row_begin, a.row_end, cand};
     if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
     if ((e = launch_sweep(kp, kc <= uint32_t(TS_MAX_RES_KC), sp, nrows, st)) != cudaSuccess) return e;
     if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
