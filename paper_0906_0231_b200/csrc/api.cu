@@ -87,7 +87,7 @@ struct knn_b200_ctx {
     int sm_count = 148;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};  // [0..3] call phases, [4..5] around the sweep kernel
-    DevBuf vectors, staged, flags, out_index, out_dist, tensor_ws;
+    DevBuf vectors, staged, flags, out_index, out_dist, tensor_ws, exact_ws;
     unsigned long long* host_flags = nullptr;  // pinned
     std::mutex mu;
 };
@@ -193,6 +193,8 @@ void solve_rows_core(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, 
         ta.out_dist = out_dist;
         ta.workspace = ctx->tensor_ws.get(knnb::tensor_workspace_bytes(n, d, row_end - row_begin, kp));
         ta.host_scratch = ctx->host_flags + 4;
+        ta.exact_scratch = ctx->exact_ws.get(std::max<size_t>(
+            16, knnb::exact_scratch_bytes(row_end - row_begin, n, klist, ctx->sm_count)));
         ta.sm_count = ctx->sm_count;
         ta.stream = stream;
         ta.ev_sweep0 = ctx->ev[4];
@@ -206,8 +208,10 @@ void solve_rows_core(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, 
     }
     ctr.arith_used = KNN_B200_ARITH_EXACT;
     cuda_check(cudaEventRecord(ctx->ev[4], stream), "event");
+    void* xs = ctx->exact_ws.get(std::max<size_t>(16, knnb::exact_scratch_bytes(row_end - row_begin, n, klist,
+                                                                                   ctx->sm_count)));
     cuda_check(knnb::launch_exact_fused(fold, Xs, n, d, klist, nullptr, row_begin, row_end, out_index, out_dist,
-                                        out_sqrt, 0, stream),
+                                        out_sqrt, 0, xs, ctx->sm_count, stream),
                "exact sweep launch");
     cuda_check(cudaEventRecord(ctx->ev[5], stream), "event");
     ++ctr.launches;
@@ -286,6 +290,7 @@ void knn_b200_destroy(knn_b200_ctx* ctx) {
     ctx->out_index.release();
     ctx->out_dist.release();
     ctx->tensor_ws.release();
+    ctx->exact_ws.release();
     if (ctx->host_flags) cudaFreeHost(ctx->host_flags);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);

@@ -22,10 +22,13 @@ cudaError_t launch_generate(float* out, uint64_t count, uint64_t seed, int sm_co
 // out_sqrt: report sqrtf(distance) (the Euclidean metric) -- selection is
 // unaffected because sqrtf is monotone and the lists are final.  With an
 // explicit row list, slot s is written to output row rows[s] - scatter_base.
+// `scratch` (exact_scratch_bytes) lets few rows spread their columns over
+// every SM; null forces one chunk.
 cudaError_t launch_exact_fused(int metric, const float* X, uint32_t n, uint32_t d, uint32_t klist,
                                const uint32_t* rows, uint32_t row_begin, uint32_t row_end,
                                uint32_t* out_index, float* out_dist, int out_sqrt,
-                               uint32_t scatter_base, cudaStream_t stream);
+                               uint32_t scatter_base, void* scratch, int sm_count, cudaStream_t stream);
+size_t exact_scratch_bytes(uint32_t nslots, uint32_t n, uint32_t klist, int sm_count);
 
 constexpr uint32_t kExactMaxK = 256;
 
@@ -39,6 +42,7 @@ struct TensorPathArgs {
     uint32_t* out_index;
     float* out_dist;
     void* workspace;      // tensor_workspace_bytes()
+    void* exact_scratch;  // exact_scratch_bytes(row_end - row_begin, ...) for fallback rows
     void* host_scratch;   // 64 B pinned
     int sm_count;
     cudaStream_t stream;

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -34,17 +35,22 @@
 namespace knnb {
 
 constexpr int TS_BM = 128;
-constexpr int TS_THREADS = 192;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2..5 epilogue
 constexpr uint32_t TS_A_CHUNK = TS_BM * 128;  // 128 rows x 128 B (64 fp16 of K)
 constexpr uint32_t TS_SMEM_MAX = 232448;
 constexpr int TS_MAX_RES_KC = 4;              // A resident in smem when d <= 256
 
-template <int KP, int BN, bool ARES>
+// EW epilogue warps (4 or 8).  With 8, two warps share each TMEM lane
+// quadrant and split every tile's columns in halves; each half keeps its own
+// list of KPL entries per row (NSEG = 2 list segments per row).
+template <int KPL, int BN, bool ARES, int EW>
 struct TSLayout {
+    static constexpr int NSEG = EW / 4;
+    static constexpr int THREADS = 64 + 32 * EW;  // warp 0 TMA producer, warp 1 MMA issuer, epilogue warps
     static constexpr uint32_t B_CHUNK = BN * 128;
     static constexpr uint32_t STAGE = B_CHUNK + (ARES ? 0 : TS_A_CHUNK);
     static constexpr uint32_t A_BYTES = ARES ? TS_MAX_RES_KC * TS_A_CHUNK : 0;
-    static constexpr uint32_t LISTS = TS_BM * KP * 8;
+    static constexpr uint32_t LIST_ROWS = TS_BM * NSEG;                 // list "columns"
+    static constexpr uint32_t LISTS = LIST_ROWS * KPL * 8;
     static constexpr uint32_t MISC = 256;
     static constexpr uint32_t AVAIL = TS_SMEM_MAX - 1024 - MISC - LISTS - A_BYTES;
     static constexpr int STAGES_RAW = int(AVAIL / STAGE);
@@ -52,31 +58,32 @@ struct TSLayout {
     static_assert(STAGES >= 2, "shared memory budget too small for a 2-stage ring");
     static constexpr uint32_t SMEM = 1024 + A_BYTES + STAGES * STAGE + LISTS + MISC;
     static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
+    static constexpr uint32_t STRIDE = LIST_ROWS * 4;  // bytes between entries of one list
 };
 
 struct SweepParams {
     const uint8_t* xh;    // swizzled fp16 planes
     const float* alpha;   // [npad], +inf on padding rows
-    const unsigned long long* alpha_max;  // bits of max alpha (double), from prep
     uint32_t n, npad, kc;
     uint32_t row_begin, row_end;
-    uint64_t* cand;       // [(row_end - row_begin) * KP]
+    uint32_t group_tiles;  // column tiles per L2-resident column group
+    int debug_mode;        // profiling only: 1 = epilogue loads TMEM but skips the filter, 2 = releases only
+    uint64_t* cand;       // [(row_end - row_begin) * NSEG * KPL], segment-major per row;
+                          // also the list state carried between column groups
 };
 
-// Per-row candidate list: KP unsorted (approximate distance, index) entries in
-// shared memory -- a [KP][TS_BM] float array and a [KP][TS_BM] index array,
-// so the 32 lanes of a warp touch consecutive words -- plus its maximum, the
+// Per-row candidate list: KPL unsorted (y, index) entries in shared memory --
+// a [KPL][LIST_ROWS] float array and a [KPL][LIST_ROWS] index array, so the
+// 32 lanes of a warp touch consecutive words -- plus its maximum, the
 // admission threshold (the reference's heap root, heap.hpp:86-90).  The list
-// keeps the KP smallest approximate distances with ties broken arbitrarily:
-// the completeness proof only needs "every row outside the list has A >= the
-// list maximum".  Replacing the maximum and rescanning costs KP independent
-// shared loads and runs warp-convergently.
+// keeps the KPL smallest y with ties broken arbitrarily: the completeness
+// proof only needs "every column outside the list has y >= the list maximum".
+// Replacing the maximum and rescanning costs KPL independent shared loads and
+// runs warp-convergently: a warp pays once per column any of its rows admits.
 struct ListMax {
     float a;
     uint32_t slot;
 };
-
-constexpr uint32_t kListStride = TS_BM * 4;  // bytes between consecutive entries of one row
 
 __device__ __forceinline__ float lds_f32(uint32_t addr) {
     float v;
@@ -92,50 +99,64 @@ __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
-template <int KP>
+template <int KPL, uint32_t STRIDE>
 __device__ __forceinline__ ListMax list_rescan(uint32_t a_base) {
     // pass 1: maximum (independent loads, a max tree); pass 2: its slot
     float m = lds_f32(a_base);
-#pragma unroll
-    for (int i = 1; i < KP; ++i) m = fmaxf(m, lds_f32(a_base + i * kListStride));
+#pragma unroll 32
+    for (int i = 1; i < KPL; ++i) m = fmaxf(m, lds_f32(a_base + i * STRIDE));
     uint32_t slot = 0;
-#pragma unroll
-    for (int i = KP - 1; i >= 0; --i) slot = (lds_f32(a_base + i * kListStride) == m) ? uint32_t(i) : slot;
+#pragma unroll 32
+    for (int i = KPL - 1; i >= 0; --i) slot = (lds_f32(a_base + i * STRIDE) == m) ? uint32_t(i) : slot;
     return ListMax{m, slot};
 }
 
-template <int KP>
+template <int KPL, uint32_t STRIDE>
 __device__ __noinline__ ListMax list_replace_max(uint32_t a_base, uint32_t i_base, uint32_t slot, float a,
                                                  uint32_t col) {
-    sts_f32(a_base + slot * kListStride, a);
-    sts_u32(i_base + slot * kListStride, col);
-    return list_rescan<KP>(a_base);
+    sts_f32(a_base + slot * STRIDE, a);
+    sts_u32(i_base + slot * STRIDE, col);
+    return list_rescan<KPL, STRIDE>(a_base);
 }
 
-template <int KP, int BN, bool ARES>
-__global__ void __launch_bounds__(TS_THREADS, 1) tensor_sweep_kernel(const SweepParams p) {
-    using L = TSLayout<KP, BN, ARES>;
+// Persistent sweep.  Work item = (column group g, row block rb); every CTA
+// walks g = 0, 1, ... and, inside a group, its row blocks rb = blockIdx.x,
+// blockIdx.x + gridDim.x, ...  All CTAs therefore stream the same column
+// group at the same time and a group's reference tiles (sized to fit in L2)
+// come from HBM once per group instead of once per row block.  The per-row
+// candidate lists are written to `cand` at the end of each item and read
+// back when the row block's next group starts.
+template <int KPL, int BN, bool ARES, int EW>
+__global__ void __launch_bounds__(TSLayout<KPL, BN, ARES, EW>::THREADS, 1)
+tensor_sweep_kernel(const SweepParams p) {
+    using L = TSLayout<KPL, BN, ARES, EW>;
     constexpr int S = L::STAGES;
+    constexpr int NSEG = L::NSEG;
+    constexpr int SEG_COLS = BN / NSEG;  // columns of a tile one epilogue warp filters
+    static_assert(SEG_COLS % 64 == 0 && KPL % 16 == 0 && KPL <= SEG_COLS, "tile / list shape");
+    constexpr bool DIRECT = KPL % 32 == 0;  // fill the first KPL columns without the filter
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* a_smem = smem;
     uint8_t* stage_smem = smem + L::A_BYTES;
-    float* list_a = reinterpret_cast<float*>(stage_smem + S * L::STAGE);   // [KP][TS_BM]
-    uint32_t* list_i = reinterpret_cast<uint32_t*>(list_a + KP * TS_BM);    // [KP][TS_BM]
+    float* list_a = reinterpret_cast<float*>(stage_smem + S * L::STAGE);        // [KPL][LIST_ROWS]
+    uint32_t* list_i = reinterpret_cast<uint32_t*>(list_a + KPL * L::LIST_ROWS);  // [KPL][LIST_ROWS]
     uint64_t* bars = reinterpret_cast<uint64_t*>(stage_smem + S * L::STAGE + L::LISTS);
-    // bars: full[S], empty[S], tfull[2], tempty[2], afull
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 5);
+    // bars: full[S], empty[S], tfull[2], tempty[2], afull, aempty
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 6);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t r0 = p.row_begin + blockIdx.x * TS_BM;
     const uint32_t ntiles = (p.n + BN - 1) / BN;
+    const uint32_t nrb = (p.row_end - p.row_begin + TS_BM - 1) / TS_BM;
+    const uint32_t ngroups = (ntiles + p.group_tiles - 1) / p.group_tiles;
     const uint32_t bar0 = ptx::smem_u32(bars);
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto empty_bar = [&](int s) { return bar0 + 8u * (S + s); };
     auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * S + b); };
     auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * S + 2 + b); };
     const uint32_t afull_bar = bar0 + 8u * (2 * S + 4);
+    const uint32_t aempty_bar = bar0 + 8u * (2 * S + 5);
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < S; ++s) {
@@ -144,9 +165,10 @@ __global__ void __launch_bounds__(TS_THREADS, 1) tensor_sweep_kernel(const Sweep
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(tfull_bar(b), 1);
-            ptx::mbar_init(tempty_bar(b), 4);  // one arrive per epilogue warp
+            ptx::mbar_init(tempty_bar(b), EW);  // one arrive per epilogue warp
         }
         ptx::mbar_init(afull_bar, 1);
+        ptx::mbar_init(aempty_bar, 1);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), L::TMEM_COLS);
@@ -158,28 +180,35 @@ __global__ void __launch_bounds__(TS_THREADS, 1) tensor_sweep_kernel(const Sweep
     if (warp == 0) {
         // ---------------- TMA producer (one lane) ----------------
         if (lane == 0) {
-            const uint64_t keep = ptx::policy_evict_last();  // reference tiles: reused by every CTA
-            if constexpr (ARES) {
-                ptx::mbar_arrive_expect_tx(afull_bar, p.kc * TS_A_CHUNK);
-                for (uint32_t kc = 0; kc < p.kc; ++kc)
-                    ptx::bulk_g2s(ptx::smem_u32(a_smem + kc * TS_A_CHUNK),
-                                  p.xh + (size_t(kc) * p.npad + r0) * 128, TS_A_CHUNK, afull_bar);
-            }
             int stage = 0;
-            uint32_t phase = 0;
-            for (uint32_t t = 0; t < ntiles; ++t) {
-                for (uint32_t kc = 0; kc < p.kc; ++kc) {
-                    ptx::mbar_wait(empty_bar(stage), phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(full_bar(stage), L::STAGE);
-                    uint8_t* dst = stage_smem + stage * L::STAGE;
-                    ptx::bulk_g2s_hint(ptx::smem_u32(dst), p.xh + (size_t(kc) * p.npad + size_t(t) * BN) * 128,
-                                       L::B_CHUNK, full_bar(stage), keep);
-                    if constexpr (!ARES)
-                        ptx::bulk_g2s(ptx::smem_u32(dst + L::B_CHUNK), p.xh + (size_t(kc) * p.npad + r0) * 128,
-                                      TS_A_CHUNK, full_bar(stage));
-                    if (++stage == S) {
-                        stage = 0;
-                        phase ^= 1;
+            uint32_t phase = 0, a_phase = 0;
+            for (uint32_t g = 0; g < ngroups; ++g) {
+                const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
+                for (uint32_t rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
+                    const uint32_t r0 = p.row_begin + rb * TS_BM;
+                    if constexpr (ARES) {  // A stays resident for the item; reload once the MMA released it
+                        ptx::mbar_wait(aempty_bar, a_phase ^ 1);
+                        ptx::mbar_arrive_expect_tx(afull_bar, p.kc * TS_A_CHUNK);
+                        for (uint32_t kc = 0; kc < p.kc; ++kc)
+                            ptx::bulk_g2s(ptx::smem_u32(a_smem + kc * TS_A_CHUNK),
+                                          p.xh + (size_t(kc) * p.npad + r0) * 128, TS_A_CHUNK, afull_bar);
+                        a_phase ^= 1;
+                    }
+                    for (uint32_t t = t0; t < t1; ++t) {
+                        for (uint32_t kc = 0; kc < p.kc; ++kc) {
+                            ptx::mbar_wait(empty_bar(stage), phase ^ 1);
+                            ptx::mbar_arrive_expect_tx(full_bar(stage), L::STAGE);
+                            uint8_t* dst = stage_smem + stage * L::STAGE;
+                            ptx::bulk_g2s(ptx::smem_u32(dst), p.xh + (size_t(kc) * p.npad + size_t(t) * BN) * 128,
+                                          L::B_CHUNK, full_bar(stage));
+                            if constexpr (!ARES)
+                                ptx::bulk_g2s(ptx::smem_u32(dst + L::B_CHUNK),
+                                              p.xh + (size_t(kc) * p.npad + r0) * 128, TS_A_CHUNK, full_bar(stage));
+                            if (++stage == S) {
+                                stage = 0;
+                                phase ^= 1;
+                            }
+                        }
                     }
                 }
             }
@@ -188,134 +217,177 @@ __global__ void __launch_bounds__(TS_THREADS, 1) tensor_sweep_kernel(const Sweep
         // ---------------- MMA issuer (one lane) ----------------
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_f16_f32(TS_BM, BN);
-            if constexpr (ARES) ptx::mbar_wait(afull_bar, 0);
             int stage = 0;
-            uint32_t phase = 0;
-            for (uint32_t t = 0; t < ntiles; ++t) {
-                const uint32_t b = t & 1, use = t >> 1;
-                ptx::mbar_wait(tempty_bar(b), (use & 1) ^ 1);
-                ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem + b * BN;
-                for (uint32_t kc = 0; kc < p.kc; ++kc) {
-                    ptx::mbar_wait(full_bar(stage), phase);
-                    ptx::tc_fence_after();
-                    const uint8_t* bsm = stage_smem + stage * L::STAGE;
-                    const uint8_t* asm_ = ARES ? a_smem + kc * TS_A_CHUNK : bsm + L::B_CHUNK;
-                    const uint32_t a_addr = ptx::smem_u32(asm_);
-                    const uint32_t b_addr = ptx::smem_u32(bsm);
+            uint32_t phase = 0, a_phase = 0, tcount = 0;
+            for (uint32_t g = 0; g < ngroups; ++g) {
+                const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
+                for (uint32_t rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
+                    if constexpr (ARES) {
+                        ptx::mbar_wait(afull_bar, a_phase);
+                        a_phase ^= 1;
+                    }
+                    for (uint32_t t = t0; t < t1; ++t, ++tcount) {
+                        const uint32_t b = tcount & 1, use = tcount >> 1;
+                        ptx::mbar_wait(tempty_bar(b), (use & 1) ^ 1);
+                        ptx::tc_fence_after();
+                        const uint32_t d_tmem = tmem + b * BN;
+                        for (uint32_t kc = 0; kc < p.kc; ++kc) {
+                            ptx::mbar_wait(full_bar(stage), phase);
+                            ptx::tc_fence_after();
+                            const uint8_t* bsm = stage_smem + stage * L::STAGE;
+                            const uint8_t* asm_ = ARES ? a_smem + kc * TS_A_CHUNK : bsm + L::B_CHUNK;
+                            const uint32_t a_addr = ptx::smem_u32(asm_);
+                            const uint32_t b_addr = ptx::smem_u32(bsm);
 #pragma unroll
-                    for (uint32_t k = 0; k < 4; ++k) {  // UMMA_K = 16 fp16 = 32 B inside the swizzle atom
-                        ptx::mma_f16_ss(d_tmem, ptx::sw128_kmajor_desc(a_addr + 32 * k),
-                                        ptx::sw128_kmajor_desc(b_addr + 32 * k), idesc, (kc | k) != 0);
+                            for (uint32_t k = 0; k < 4; ++k) {  // UMMA_K = 16 fp16 = 32 B inside the swizzle atom
+                                ptx::mma_f16_ss(d_tmem, ptx::sw128_kmajor_desc(a_addr + 32 * k),
+                                                ptx::sw128_kmajor_desc(b_addr + 32 * k), idesc, (kc | k) != 0);
+                            }
+                            ptx::mma_commit(empty_bar(stage));
+                            if (++stage == S) {
+                                stage = 0;
+                                phase ^= 1;
+                            }
+                        }
+                        ptx::mma_commit(tfull_bar(b));
                     }
-                    ptx::mma_commit(empty_bar(stage));
-                    if (++stage == S) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                    if constexpr (ARES) ptx::mma_commit(aempty_bar);  // A may be replaced once these MMAs retire
                 }
-                ptx::mma_commit(tfull_bar(b));
             }
         }
     } else {
-        // ---------------- epilogue: one thread per query row ----------------
-        const int quad = warp & 3;  // TMEM lanes 32*quad .. +31 are this warp's
+        // ---------------- epilogue: one thread per (query row, column segment) ----------------
+        const int ew = warp - 2;
+        const int quad = warp & 3;       // TMEM lanes 32*quad .. +31 are this warp's
+        const int seg = ew / 4;          // which column segment of every tile
         const int rl = quad * 32 + lane;
-        const uint32_t row = r0 + rl;
-        const bool valid = row < p.row_end;
-        float* my_a = list_a + rl;
-        uint32_t* my_i = list_i + rl;
+        const int li = seg * TS_BM + rl;  // this thread's list
+        float* my_a = list_a + li;
+        uint32_t* my_i = list_i + li;
         const uint32_t a_base = ptx::smem_u32(my_a), i_base = ptx::smem_u32(my_i);
         const float kInf = __int_as_float(0x7f800000);
-#pragma unroll 4
-        for (int s = 0; s < KP; ++s) {
-            my_a[s * TS_BM] = kInf;
-            my_i[s * TS_BM] = 0xffffffffu;
-        }
-        const float alpha_i = valid ? p.alpha[row] : 0.0f;
-        const float slack = 1e-6f * (fabsf(alpha_i) + float(__longlong_as_double((long long)*p.alpha_max)));
-        ListMax thr{kInf, 0};
-        // Hot-path test: A = fl(fl(alpha_i + beta_j) - 2 dot) < thr.a is
-        // pre-filtered as fl(beta_j - 2 dot) <= thr.a - alpha_i + slack, which
-        // admits a superset (slack >> the rounding difference);
-        // the exact A is recomputed for the admitted columns only.
-        float thr_pre = -kInf;
-        auto set_thr = [&](ListMax m) {
-            thr = m;
-            thr_pre = !valid ? -kInf : (m.a == kInf ? kInf : __fadd_ru(__fsub_ru(m.a, alpha_i), slack + 1e-6f * fabsf(m.a)));
-        };
         const uint32_t lane_addr = tmem + (uint32_t(quad * 32) << 16);
-        auto process = [&](const uint32_t (&v)[32], uint32_t col0) {
+        const uint32_t seg0 = seg * SEG_COLS;
+        auto load_beta = [&](uint32_t col0, float (&bt)[32]) {
             const float4* beta4 = reinterpret_cast<const float4*>(p.alpha + col0);
-            float beta[32];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const float4 f = __ldg(beta4 + q);
-                beta[4 * q] = f.x;
-                beta[4 * q + 1] = f.y;
-                beta[4 * q + 2] = f.z;
-                beta[4 * q + 3] = f.w;
-            }
-            if (col0 < uint32_t(KP)) {  // first KP columns: fill the list directly
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const uint32_t col = col0 + j;
-                    const float a = __fmaf_rn(-2.0f, __uint_as_float(v[j]), __fadd_rn(alpha_i, beta[j]));
-                    my_a[col * TS_BM] = col < p.n ? a : kInf;
-                    my_i[col * TS_BM] = col < p.n ? col : 0xffffffffu;
-                }
-                if (col0 + 32 == uint32_t(KP)) set_thr(list_rescan<KP>(a_base));
-                return;
-            }
-            // 2 instructions per distance: FFMA + FMNMX
-            float y[32];
-            float ymin = kInf;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                y[j] = __fmaf_rn(-2.0f, __uint_as_float(v[j]), beta[j]);
-                ymin = fminf(ymin, y[j]);
-            }
-            if (__any_sync(0xffffffffu, ymin <= thr_pre)) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    if (y[j] <= thr_pre) {
-                        const uint32_t col = col0 + j;
-                        const float a = __fmaf_rn(-2.0f, __uint_as_float(v[j]), __fadd_rn(alpha_i, beta[j]));
-                        if (a < thr.a && col < p.n) set_thr(list_replace_max<KP>(a_base, i_base, thr.slot, a, col));
-                    }
-                }
+                bt[4 * q] = f.x;
+                bt[4 * q + 1] = f.y;
+                bt[4 * q + 2] = f.z;
+                bt[4 * q + 3] = f.w;
             }
         };
-        for (uint32_t t = 0; t < ntiles; ++t) {
-            const uint32_t b = t & 1, use = t >> 1;
-            ptx::mbar_wait(tfull_bar(b), use & 1);
-            ptx::tc_fence_after();
-            const uint32_t cbase = t * BN;
-            const uint32_t taddr = lane_addr + b * BN;
-            uint32_t va[32], vb[32];
-            // software-pipelined TMEM reads: chunk c+1 streams in while chunk c is filtered
-            ptx::tmem_ld_32x32b_x32(taddr, va);
-#pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 64) {
-                ptx::tmem_wait_ld();
-                ptx::tmem_ld_32x32b_x32(taddr + c0 + 32, vb);
-                process(va, cbase + c0);
-                ptx::tmem_wait_ld();
-                if (c0 + 64 < BN) {
-                    ptx::tmem_ld_32x32b_x32(taddr + c0 + 64, va);
-                } else {  // the whole accumulator is in registers: hand it back to the MMA warp
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(tempty_bar(b));
+        uint32_t tcount = 0;
+        for (uint32_t g = 0; g < ngroups; ++g) {
+            const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
+            for (uint32_t rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
+                const uint32_t row = p.row_begin + rb * TS_BM + rl;
+                const bool valid = row < p.row_end;
+                uint64_t* state = p.cand + (size_t(row - p.row_begin) * NSEG + seg) * KPL;
+                // Columns are ranked by y = fl(beta_j - 2 dot): alpha_i is
+                // constant along a row; the rescore forms A = alpha_i + y in fp64.
+                ListMax thr{valid ? kInf : -kInf, 0};
+                if (g == 0 || !valid) {
+#pragma unroll 4
+                    for (int s = 0; s < KPL; ++s) {
+                        my_a[s * L::LIST_ROWS] = kInf;
+                        my_i[s * L::LIST_ROWS] = 0xffffffffu;
+                    }
+                } else {
+                    for (int s = 0; s < KPL; ++s) {
+                        const uint64_t key = state[s];
+                        my_a[s * L::LIST_ROWS] = key == kEmptyKey ? kInf : ordered_to_float(uint32_t(key >> 32));
+                        my_i[s * L::LIST_ROWS] = uint32_t(key);
+                    }
+                    thr = list_rescan<KPL, L::STRIDE>(a_base);
                 }
-                process(vb, cbase + c0 + 32);
-            }
-        }
-        if (valid) {
-            uint64_t* out = p.cand + size_t(row - p.row_begin) * KP;
-            for (int s = 0; s < KP; ++s) {
-                const uint32_t col = my_i[s * TS_BM];
-                out[s] = col == 0xffffffffu ? kEmptyKey : (uint64_t(float_to_ordered(my_a[s * TS_BM])) << 32) | col;
+                // direct: position of this chunk among the first KPL columns
+                // this thread sees (first tile of group 0), or -1
+                auto process = [&](const uint32_t (&v)[32], const float (&bt)[32], uint32_t col0, int direct) {
+                    if (direct >= 0) {  // first KPL columns: fill the list directly
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const uint32_t col = col0 + j;
+                            my_a[(direct + j) * L::LIST_ROWS] =
+                                col < p.n ? __fmaf_rn(-2.0f, __uint_as_float(v[j]), bt[j]) : kInf;
+                            my_i[(direct + j) * L::LIST_ROWS] = col < p.n ? col : 0xffffffffu;
+                        }
+                        if (direct + 32 == KPL && valid) thr = list_rescan<KPL, L::STRIDE>(a_base);
+                        return;
+                    }
+                    // hot path: FFMA + FMNMX per distance, min as a tree
+                    float m[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        m[i] = fminf(__fmaf_rn(-2.0f, __uint_as_float(v[2 * i]), bt[2 * i]),
+                                     __fmaf_rn(-2.0f, __uint_as_float(v[2 * i + 1]), bt[2 * i + 1]));
+#pragma unroll
+                    for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+                        for (int i = 0; i < w; ++i) m[i] = fminf(m[i], m[i + w]);
+                    if (__any_sync(0xffffffffu, m[0] < thr.a)) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const float y = __fmaf_rn(-2.0f, __uint_as_float(v[j]), bt[j]);
+                            const uint32_t col = col0 + j;
+                            if (y < thr.a && col < p.n)
+                                thr = list_replace_max<KPL, L::STRIDE>(a_base, i_base, thr.slot, y, col);
+                        }
+                    }
+                };
+                for (uint32_t t = t0; t < t1; ++t, ++tcount) {
+                    const uint32_t b = tcount & 1, use = tcount >> 1;
+                    ptx::mbar_wait(tfull_bar(b), use & 1);
+                    ptx::tc_fence_after();
+                    const uint32_t cbase = t * BN + seg0;
+                    const uint32_t taddr = lane_addr + b * BN + seg0;
+                    const bool first = DIRECT && g == 0 && t == 0;
+                    if (p.debug_mode) {  // pipeline-ceiling experiments (KNN_B200_DEBUG_SWEEP)
+                        uint32_t vd[32];
+                        if (p.debug_mode == 1)
+                            for (int c0 = 0; c0 < SEG_COLS; c0 += 32) {
+                                ptx::tmem_ld_32x32b_x32(taddr + c0, vd);
+                                ptx::tmem_wait_ld();
+                                if (vd[0] == 0x7fc00001u && vd[31] == 0x7fc00001u) thr.a = 0.0f;  // keep the loads
+                            }
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(tempty_bar(b));
+                        continue;
+                    }
+                    uint32_t va[32], vb[32];
+                    float ba[32], bb[32];
+                    // software pipeline: chunk c+1's TMEM read and beta load are
+                    // in flight while chunk c is filtered
+                    ptx::tmem_ld_32x32b_x32(taddr, va);
+                    load_beta(cbase, ba);
+#pragma unroll 1
+                    for (int c0 = 0; c0 < SEG_COLS; c0 += 64) {
+                        ptx::tmem_wait_ld();
+                        ptx::tmem_ld_32x32b_x32(taddr + c0 + 32, vb);
+                        load_beta(cbase + c0 + 32, bb);
+                        process(va, ba, cbase + c0, (first && c0 < KPL) ? c0 : -1);
+                        ptx::tmem_wait_ld();
+                        if (c0 + 64 < SEG_COLS) {
+                            ptx::tmem_ld_32x32b_x32(taddr + c0 + 64, va);
+                            load_beta(cbase + c0 + 64, ba);
+                        } else {  // this warp's part of the accumulator is in registers: release it
+                            ptx::tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) ptx::mbar_arrive(tempty_bar(b));
+                        }
+                        process(vb, bb, cbase + c0 + 32, (first && c0 + 32 < KPL) ? c0 + 32 : -1);
+                    }
+                }
+                if (valid) {
+                    for (int s = 0; s < KPL; ++s) {
+                        const uint32_t col = my_i[s * L::LIST_ROWS];
+                        state[s] = col == 0xffffffffu ? kEmptyKey
+                                                      : (uint64_t(float_to_ordered(my_a[s * L::LIST_ROWS])) << 32) | col;
+                    }
+                }
             }
         }
     }
@@ -479,8 +551,9 @@ __device__ __forceinline__ float exact_fold_rows(const float* __restrict__ a, co
     return fold_finalize<FOLD>(acc);
 }
 
-template <int FOLD, int KP>
+template <int FOLD, int KP, int NSEG>
 __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
+    constexpr int KPL = KP / NSEG;
     __shared__ uint64_t keys_s[8][KP];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t slot = blockIdx.x * 8 + warp;
@@ -532,25 +605,47 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     for (int m = 0; m < PER; ++m)
         if (lane + 32 * m < KP) keys_s[warp][rank[m]] = mine[m];
     __syncwarp();
-    // the candidate list is unsorted: its largest key and whether it is full
-    uint64_t amax = 0;
+    // Each of the NSEG lists is unsorted; per list its largest key.  A list
+    // holding an empty slot saw (and kept) every column of its segment, so
+    // it excludes nothing; a full list excludes only columns with y >= its
+    // maximum.  The bound for everything excluded is the smallest such
+    // maximum over the full lists.
+    uint64_t segmax[NSEG];
 #pragma unroll
-    for (int m = 0; m < PER; ++m)
-        if (lane + 32 * m < KP) amax = max(amax, cand[lane + 32 * m]);
-    for (int o = 16; o; o >>= 1) {
-        const uint64_t other = __shfl_xor_sync(0xffffffffu, amax, o);
-        amax = other > amax ? other : amax;
+    for (int s = 0; s < NSEG; ++s) segmax[s] = 0;
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+        const int i = lane + 32 * m;
+        if (i < KP) {
+            const uint64_t c = cand[i];
+#pragma unroll
+            for (int s = 0; s < NSEG; ++s)
+                if (i / KPL == s) segmax[s] = c > segmax[s] ? c : segmax[s];
+        }
     }
-    const uint64_t last_approx = amax;
+    bool any_full = false;
+    uint64_t last_approx = kEmptyKey;  // smallest maximum over full lists
+#pragma unroll
+    for (int s = 0; s < NSEG; ++s) {
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t other = __shfl_xor_sync(0xffffffffu, segmax[s], o);
+            segmax[s] = other > segmax[s] ? other : segmax[s];
+        }
+        if (segmax[s] != kEmptyKey) {
+            any_full = true;
+            last_approx = segmax[s] < last_approx ? segmax[s] : last_approx;
+        }
+    }
     bool complete;
-    if (last_approx == kEmptyKey) {
+    if (!any_full) {
         complete = true;  // every column was offered into a non-full list: the list holds all of them
     } else if (valid < p.klist) {
         complete = false;
     } else {
         const uint64_t kth = keys_s[warp][p.klist - 1];
         const double T = double(ordered_to_float(uint32_t(kth >> 32)));
-        const double a_max = double(ordered_to_float(uint32_t(last_approx >> 32)));
+        // the list ranks y = fl(beta - 2 dot); A = alpha_q + y exactly in fp64
+        const double a_max = double(p.alpha[q]) + double(ordered_to_float(uint32_t(last_approx >> 32)));
         const double u = 5.9604644775390625e-08;  // 2^-24
         const double dd = double(p.d);
         const int e = scale_exponent(*p.maxabs);
@@ -592,13 +687,26 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
 // ---------------------------------------------------------------------------
 // host orchestration
 
+// Candidate-list shape per k: KPL entries per list, NSEG lists per row (one
+// per epilogue column segment).  A segment may hold every one of the k
+// nearest, so each list needs k + 1 (the query itself) + a margin for the
+// error band; the margin is where rows fail their proof and fall back.
+struct TensorCfg {
+    uint32_t kpl, nseg;
+};
+
+static TensorCfg tensor_cfg(uint32_t klist) {
+    const uint32_t margin = klist / 4 > 8 ? klist / 4 : 8;
+    if (klist + 1 + 5 <= 16) return {16, 2};
+    if (klist + 1 + margin <= 32) return {32, 2};
+    if (klist + 1 + margin <= 64) return {64, 1};
+    if (klist + 1 + margin <= 128) return {128, 1};
+    return {0, 0};  // not supported by the tensor sweep
+}
+
 uint32_t tensor_kp_for(uint32_t klist) {
-    // k + 1 (the query itself can occupy a slot) + margin for the error band
-    const uint32_t need = klist + 1 + (klist / 4 > 8 ? klist / 4 : 8);
-    if (need <= 32) return 32;
-    if (need <= 64) return 64;
-    if (need <= 128) return 128;
-    return 0;  // not supported by the tensor sweep
+    const TensorCfg c = tensor_cfg(klist);
+    return c.kpl * c.nseg;
 }
 
 size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t rows, uint32_t kp) {
@@ -618,36 +726,47 @@ size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t rows, uint32_t kp
     return b;
 }
 
-template <int KP, int BN, bool ARES>
+template <int KPL, int BN, bool ARES, int EW>
 static cudaError_t launch_sweep_t(const SweepParams& sp, uint32_t nrows, cudaStream_t stream) {
-    using L = TSLayout<KP, BN, ARES>;
-    auto kern = tensor_sweep_kernel<KP, BN, ARES>;
+    using L = TSLayout<KPL, BN, ARES, EW>;
+    auto kern = tensor_sweep_kernel<KPL, BN, ARES, EW>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::SMEM));
     if (e != cudaSuccess) return e;
-    const dim3 grid((nrows + TS_BM - 1) / TS_BM);
-    kern<<<grid, TS_THREADS, L::SMEM, stream>>>(sp);
+    const uint32_t nrb = (nrows + TS_BM - 1) / TS_BM;
+    int sms = 148;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const dim3 grid(nrb < uint32_t(sms) ? nrb : uint32_t(sms));  // persistent: one CTA per SM
+    kern<<<grid, L::THREADS, L::SMEM, stream>>>(sp);
     return cudaGetLastError();
 }
 
-static cudaError_t launch_sweep(uint32_t kp, bool ares, const SweepParams& sp, uint32_t nrows, cudaStream_t stream) {
-    switch (kp) {
+static cudaError_t launch_sweep(TensorCfg c, bool ares, const SweepParams& sp, uint32_t nrows, cudaStream_t stream) {
+    switch (c.kpl) {
+    case 16:
+        return ares ? launch_sweep_t<16, 256, true, 8>(sp, nrows, stream)
+                    : launch_sweep_t<16, 256, false, 8>(sp, nrows, stream);
     case 32:
-        return ares ? launch_sweep_t<32, 256, true>(sp, nrows, stream) : launch_sweep_t<32, 256, false>(sp, nrows, stream);
+        return ares ? launch_sweep_t<32, 256, true, 8>(sp, nrows, stream)
+                    : launch_sweep_t<32, 256, false, 8>(sp, nrows, stream);
     case 64:
-        return ares ? launch_sweep_t<64, 256, true>(sp, nrows, stream) : launch_sweep_t<64, 256, false>(sp, nrows, stream);
+        return ares ? launch_sweep_t<64, 256, true, 4>(sp, nrows, stream)
+                    : launch_sweep_t<64, 256, false, 4>(sp, nrows, stream);
     default:
-        return ares ? launch_sweep_t<128, 128, true>(sp, nrows, stream)
-                    : launch_sweep_t<128, 128, false>(sp, nrows, stream);
+        return ares ? launch_sweep_t<128, 128, true, 4>(sp, nrows, stream)
+                    : launch_sweep_t<128, 128, false, 4>(sp, nrows, stream);
     }
 }
 
 template <int FOLD>
-static cudaError_t launch_rescore(uint32_t kp, const RescoreParams& rp, uint32_t nrows, cudaStream_t stream) {
+static cudaError_t launch_rescore(TensorCfg c, const RescoreParams& rp, uint32_t nrows, cudaStream_t stream) {
     const dim3 grid((nrows + 7) / 8);
-    switch (kp) {
-    case 32: rescore_kernel<FOLD, 32><<<grid, 256, 0, stream>>>(rp); break;
-    case 64: rescore_kernel<FOLD, 64><<<grid, 256, 0, stream>>>(rp); break;
-    default: rescore_kernel<FOLD, 128><<<grid, 256, 0, stream>>>(rp); break;
+    switch (c.kpl) {
+    case 16: rescore_kernel<FOLD, 32, 2><<<grid, 256, 0, stream>>>(rp); break;
+    case 32: rescore_kernel<FOLD, 64, 2><<<grid, 256, 0, stream>>>(rp); break;
+    case 64: rescore_kernel<FOLD, 64, 1><<<grid, 256, 0, stream>>>(rp); break;
+    default: rescore_kernel<FOLD, 128, 1><<<grid, 256, 0, stream>>>(rp); break;
     }
     return cudaGetLastError();
 }
@@ -656,7 +775,8 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     const uint32_t n = a.n, d = a.d, nrows = a.row_end - a.row_begin;
     const uint32_t npad = (n + 255) / 256 * 256;
     const uint32_t kc = (d + 63) / 64;
-    const uint32_t kp = a.kp;
+    const TensorCfg cfg = tensor_cfg(a.klist);
+    const uint32_t kp = cfg.kpl * cfg.nseg;
     const int cosine = a.fold == kCosine;
     uint8_t* w = static_cast<uint8_t*>(a.workspace);
     auto take = [&](size_t x) {
@@ -696,15 +816,24 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     launches += 2;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
-    SweepParams sp{xh, alpha, gmax + 2, n, npad, kc, a.row_begin, a.row_end, cand};
+    // Column groups: a group's fp16 reference tiles (BN x d x 2 B each) must
+    // stay L2-resident while every CTA streams them (126 MB L2; keep ~40 MB).
+    const uint32_t bn = cfg.kpl == 128 ? 128 : 256;
+    const uint64_t tile_bytes = uint64_t(bn) * kc * 128;
+    const uint32_t ntiles = (n + bn - 1) / bn;
+    uint32_t group_tiles = uint32_t((40ull << 20) / tile_bytes);
+    if (group_tiles < 1) group_tiles = 1;
+    if (group_tiles > ntiles) group_tiles = ntiles;
+    const char* dbg = getenv("KNN_B200_DEBUG_SWEEP");
+    SweepParams sp{xh, alpha, n, npad, kc, a.row_begin, a.row_end, group_tiles, dbg ? atoi(dbg) : 0, cand};
     if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
-    if ((e = launch_sweep(kp, kc <= uint32_t(TS_MAX_RES_KC), sp, nrows, st)) != cudaSuccess) return e;
+    if ((e = launch_sweep(cfg, kc <= uint32_t(TS_MAX_RES_KC), sp, nrows, st)) != cudaSuccess) return e;
     if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
     ++launches;
 
     RescoreParams rp{a.X, n, d, a.klist, kp, a.row_begin, a.row_end, cand, alpha, rho, xnorm, gmax, maxabs,
                      a.fold, a.out_sqrt, a.out_index, a.out_dist, fb_count, fb_rows, rescored};
-    e = cosine ? launch_rescore<kCosine>(kp, rp, nrows, st) : launch_rescore<kSqEuclidean>(kp, rp, nrows, st);
+    e = cosine ? launch_rescore<kCosine>(cfg, rp, nrows, st) : launch_rescore<kSqEuclidean>(cfg, rp, nrows, st);
     if (e != cudaSuccess) return e;
     ++launches;
 
@@ -716,7 +845,7 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     r.fallback_rows = nfb;
     if (nfb) {
         if ((e = launch_exact_fused(a.fold, a.X, n, d, a.klist, fb_rows, 0, nfb, a.out_index, a.out_dist, a.out_sqrt,
-                                    a.row_begin, st)) != cudaSuccess)
+                                    a.row_begin, a.exact_scratch, a.sm_count, st)) != cudaSuccess)
             return e;
         ++launches;
     }
