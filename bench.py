@@ -344,8 +344,13 @@ def main():
     sweep_avg_s = statistics.mean(sweep_ms) / 1e3
     achieved = alg_flop / sweep_avg_s / 1e12
     if tensor:
-        peak = peaks.get("bf16_tflops", 1590.0)
-        peak_src = "measured bf16 dense burst (MEASURED_PEAKS.json; fp16 runs at the bf16 rate)" if peaks else "fallback"
+        # A sweep that runs for >100 ms sits under the 1 kW power cap: compare
+        # against the measured SUSTAINED cuBLAS rate (B200_PROFILING.md).
+        long_kernel = statistics.mean(sweep_ms) > 100.0
+        key = "bf16_tflops_sustained" if long_kernel else "bf16_tflops"
+        peak = peaks.get(key, 1400.0 if long_kernel else 1590.0)
+        peak_src = (f"measured bf16 dense {'sustained' if long_kernel else 'burst'} ({key}, MEASURED_PEAKS.json; "
+                    "fp16 runs at the bf16 rate)") if peaks else "fallback (B200_PROFILING.md)"
         bound = "tensor"
     else:
         sm = peaks.get("sm_max_mhz", 1965.0)

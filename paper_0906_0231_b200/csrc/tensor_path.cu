@@ -197,6 +197,14 @@ tensor_sweep_kernel(const SweepParams p) {
                     for (uint32_t t = t0; t < t1; ++t) {
                         for (uint32_t kc = 0; kc < p.kc; ++kc) {
                             ptx::mbar_wait(empty_bar(stage), phase ^ 1);
+                            if (p.debug_mode == 3) {  // profiling: MMA on stale tiles, no loads
+                                ptx::mbar_arrive(full_bar(stage));
+                                if (++stage == S) {
+                                    stage = 0;
+                                    phase ^= 1;
+                                }
+                                continue;
+                            }
                             ptx::mbar_arrive_expect_tx(full_bar(stage), L::STAGE);
                             uint8_t* dst = stage_smem + stage * L::STAGE;
                             ptx::bulk_g2s(ptx::smem_u32(dst), p.xh + (size_t(kc) * p.npad + size_t(t) * BN) * 128,
@@ -344,7 +352,7 @@ tensor_sweep_kernel(const SweepParams p) {
                     const uint32_t cbase = t * BN + seg0;
                     const uint32_t taddr = lane_addr + b * BN + seg0;
                     const bool first = DIRECT && g == 0 && t == 0;
-                    if (p.debug_mode) {  // pipeline-ceiling experiments (KNN_B200_DEBUG_SWEEP)
+                    if (p.debug_mode) {  // pipeline-ceiling experiments (KNN_B200_DEBUG_SWEEP=1,2,3)
                         uint32_t vd[32];
                         if (p.debug_mode == 1)
                             for (int c0 = 0; c0 < SEG_COLS; c0 += 32) {
