@@ -50,7 +50,8 @@ struct TSLayout {
     static constexpr uint32_t STAGE = B_CHUNK + (ARES ? 0 : TS_A_CHUNK);
     static constexpr uint32_t A_BYTES = ARES ? TS_MAX_RES_KC * TS_A_CHUNK : 0;
     static constexpr uint32_t LIST_ROWS = TS_BM * NSEG;                 // list "columns"
-    static constexpr uint32_t LISTS = LIST_ROWS * KPL * 8;
+    static constexpr bool REGLIST = KPL == 16;  // lists in registers, no shared-memory list arrays
+    static constexpr uint32_t LISTS = REGLIST ? 0 : LIST_ROWS * KPL * 8;
     static constexpr uint32_t MISC = 256;
     static constexpr uint32_t AVAIL = TS_SMEM_MAX - 1024 - MISC - LISTS - A_BYTES;
     static constexpr int STAGES_RAW = int(AVAIL / STAGE);
@@ -67,7 +68,8 @@ struct SweepParams {
     uint32_t n, npad, kc;
     uint32_t row_begin, row_end;
     uint32_t group_tiles;  // column tiles per L2-resident column group
-    int debug_mode;        // profiling only: 1 = epilogue loads TMEM but skips the filter, 2 = releases only
+    int debug_mode;        // profiling only (KNN_B200_DEBUG_SWEEP): 1 = TMEM loads only, 2 = release only,
+                           // 3 = no TMA loads, 4 = filter without insertions
     uint64_t* cand;       // [(row_end - row_begin) * NSEG * KPL], segment-major per row;
                           // also the list state carried between column groups
 };
@@ -134,7 +136,8 @@ tensor_sweep_kernel(const SweepParams p) {
     constexpr int NSEG = L::NSEG;
     constexpr int SEG_COLS = BN / NSEG;  // columns of a tile one epilogue warp filters
     static_assert(SEG_COLS % 64 == 0 && KPL % 16 == 0 && KPL <= SEG_COLS, "tile / list shape");
-    constexpr bool DIRECT = KPL % 32 == 0;  // fill the first KPL columns without the filter
+    constexpr bool REGLIST = L::REGLIST;
+    constexpr bool DIRECT = !REGLIST && KPL % 32 == 0;  // fill the first KPL columns without the filter
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* a_smem = smem;
@@ -269,9 +272,9 @@ tensor_sweep_kernel(const SweepParams p) {
         const int quad = warp & 3;       // TMEM lanes 32*quad .. +31 are this warp's
         const int seg = ew / 4;          // which column segment of every tile
         const int rl = quad * 32 + lane;
-        const int li = seg * TS_BM + rl;  // this thread's list
-        float* my_a = list_a + li;
-        uint32_t* my_i = list_i + li;
+        const int lidx = seg * TS_BM + rl;  // this thread's list
+        float* my_a = list_a + lidx;
+        uint32_t* my_i = list_i + lidx;
         const uint32_t a_base = ptx::smem_u32(my_a), i_base = ptx::smem_u32(my_i);
         const float kInf = __int_as_float(0x7f800000);
         const uint32_t lane_addr = tmem + (uint32_t(quad * 32) << 16);
@@ -287,6 +290,44 @@ tensor_sweep_kernel(const SweepParams p) {
                 bt[4 * q + 3] = f.w;
             }
         };
+        // Register-resident list (KPL == 16): replacing the maximum is 32
+        // selects plus a 4-level (value, slot) max tree -- no memory on the
+        // critical path.  Larger lists live in shared memory.
+        float la[REGLIST ? KPL : 1];
+        uint32_t lx[REGLIST ? KPL : 1];
+        ListMax thr{kInf, 0};
+        auto reg_argmax = [&]() -> ListMax {
+            float mv[8];
+            uint32_t ms[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const bool r = la[2 * i + 1] > la[2 * i];
+                mv[i] = r ? la[2 * i + 1] : la[2 * i];
+                ms[i] = r ? 2 * i + 1 : 2 * i;
+            }
+#pragma unroll
+            for (int w = 4; w >= 1; w >>= 1)
+#pragma unroll
+                for (int i = 0; i < w; ++i) {
+                    const bool r = mv[i + w] > mv[i];
+                    mv[i] = r ? mv[i + w] : mv[i];
+                    ms[i] = r ? ms[i + w] : ms[i];
+                }
+            return ListMax{mv[0], ms[0]};
+        };
+        auto insert = [&](float y, uint32_t col) {
+            if constexpr (REGLIST) {
+#pragma unroll
+                for (int s = 0; s < KPL; ++s) {
+                    const bool h = uint32_t(s) == thr.slot;
+                    la[s] = h ? y : la[s];
+                    lx[s] = h ? col : lx[s];
+                }
+                thr = reg_argmax();
+            } else {
+                thr = list_replace_max<KPL, L::STRIDE>(a_base, i_base, thr.slot, y, col);
+            }
+        };
         uint32_t tcount = 0;
         for (uint32_t g = 0; g < ngroups; ++g) {
             const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
@@ -296,13 +337,21 @@ tensor_sweep_kernel(const SweepParams p) {
                 uint64_t* state = p.cand + (size_t(row - p.row_begin) * NSEG + seg) * KPL;
                 // Columns are ranked by y = fl(beta_j - 2 dot): alpha_i is
                 // constant along a row; the rescore forms A = alpha_i + y in fp64.
-                ListMax thr{valid ? kInf : -kInf, 0};
-                if (g == 0 || !valid) {
+                if constexpr (REGLIST) {
+#pragma unroll
+                    for (int s = 0; s < KPL; ++s) {
+                        const uint64_t key = (g == 0 || !valid) ? kEmptyKey : state[s];
+                        la[s] = key == kEmptyKey ? kInf : ordered_to_float(uint32_t(key >> 32));
+                        lx[s] = uint32_t(key);
+                    }
+                    thr = reg_argmax();
+                } else if (g == 0 || !valid) {
 #pragma unroll 4
                     for (int s = 0; s < KPL; ++s) {
                         my_a[s * L::LIST_ROWS] = kInf;
                         my_i[s * L::LIST_ROWS] = 0xffffffffu;
                     }
+                    thr = ListMax{kInf, 0};
                 } else {
                     for (int s = 0; s < KPL; ++s) {
                         const uint64_t key = state[s];
@@ -311,21 +360,25 @@ tensor_sweep_kernel(const SweepParams p) {
                     }
                     thr = list_rescan<KPL, L::STRIDE>(a_base);
                 }
-                // direct: position of this chunk among the first KPL columns
-                // this thread sees (first tile of group 0), or -1
+                if (!valid) thr.a = -kInf;  // padding rows admit nothing
+                // One 32-column chunk.  direct: position among the first KPL
+                // columns this thread sees (first tile of group 0, shared-memory
+                // lists only), or -1.
                 auto process = [&](const uint32_t (&v)[32], const float (&bt)[32], uint32_t col0, int direct) {
-                    if (direct >= 0) {  // first KPL columns: fill the list directly
+                    if constexpr (!REGLIST) {
+                        if (direct >= 0) {  // first KPL columns: fill the list directly
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const uint32_t col = col0 + j;
-                            my_a[(direct + j) * L::LIST_ROWS] =
-                                col < p.n ? __fmaf_rn(-2.0f, __uint_as_float(v[j]), bt[j]) : kInf;
-                            my_i[(direct + j) * L::LIST_ROWS] = col < p.n ? col : 0xffffffffu;
+                            for (int j = 0; j < 32; ++j) {
+                                const uint32_t col = col0 + j;
+                                my_a[(direct + j) * L::LIST_ROWS] =
+                                    col < p.n ? __fmaf_rn(-2.0f, __uint_as_float(v[j]), bt[j]) : kInf;
+                                my_i[(direct + j) * L::LIST_ROWS] = col < p.n ? col : 0xffffffffu;
+                            }
+                            if (direct + 32 == KPL && valid) thr = list_rescan<KPL, L::STRIDE>(a_base);
+                            return;
                         }
-                        if (direct + 32 == KPL && valid) thr = list_rescan<KPL, L::STRIDE>(a_base);
-                        return;
                     }
-                    // hot path: FFMA + FMNMX per distance, min as a tree
+                    // hot path: FFMA + FMNMX per distance (min as a tree), one vote
                     float m[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i)
@@ -335,13 +388,45 @@ tensor_sweep_kernel(const SweepParams p) {
                     for (int w = 8; w >= 1; w >>= 1)
 #pragma unroll
                         for (int i = 0; i < w; ++i) m[i] = fminf(m[i], m[i + w]);
-                    if (__any_sync(0xffffffffu, m[0] < thr.a)) {
+                    if (!__any_sync(0xffffffffu, m[0] < thr.a) || p.debug_mode == 4) return;
+                    // rare path: per-lane pair mask, then a warp-uniform walk over
+                    // the admitted pairs; a pair's two values are picked with a
+                    // 4-level select tree (no dynamic register indexing, one copy
+                    // of the insertion code per call site)
+                    float ye[16], yo[16];
+                    uint32_t pm = 0;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const float y = __fmaf_rn(-2.0f, __uint_as_float(v[j]), bt[j]);
-                            const uint32_t col = col0 + j;
-                            if (y < thr.a && col < p.n)
-                                thr = list_replace_max<KPL, L::STRIDE>(a_base, i_base, thr.slot, y, col);
+                    for (int i = 0; i < 16; ++i) {
+                        ye[i] = __fmaf_rn(-2.0f, __uint_as_float(v[2 * i]), bt[2 * i]);
+                        yo[i] = __fmaf_rn(-2.0f, __uint_as_float(v[2 * i + 1]), bt[2 * i + 1]);
+                        if (fminf(ye[i], yo[i]) < thr.a) pm |= 1u << i;
+                    }
+                    uint32_t any = __reduce_or_sync(0xffffffffu, pm);
+                    while (any) {
+                        const int i = __ffs(any) - 1;
+                        any &= any - 1;
+                        if ((pm >> i) & 1u) {
+                            float e8[8], o8[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                e8[q] = (i & 8) ? ye[q + 8] : ye[q];
+                                o8[q] = (i & 8) ? yo[q + 8] : yo[q];
+                            }
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                e8[q] = (i & 4) ? e8[q + 4] : e8[q];
+                                o8[q] = (i & 4) ? o8[q + 4] : o8[q];
+                            }
+#pragma unroll
+                            for (int q = 0; q < 2; ++q) {
+                                e8[q] = (i & 2) ? e8[q + 2] : e8[q];
+                                o8[q] = (i & 2) ? o8[q + 2] : o8[q];
+                            }
+                            const float y0 = (i & 1) ? e8[1] : e8[0];
+                            const float y1 = (i & 1) ? o8[1] : o8[0];
+                            const uint32_t col = col0 + 2 * i;
+                            if (y0 < thr.a && col < p.n) insert(y0, col);
+                            if (y1 < thr.a && col + 1 < p.n) insert(y1, col + 1);
                         }
                     }
                 };
@@ -352,7 +437,11 @@ tensor_sweep_kernel(const SweepParams p) {
                     const uint32_t cbase = t * BN + seg0;
                     const uint32_t taddr = lane_addr + b * BN + seg0;
                     const bool first = DIRECT && g == 0 && t == 0;
-                    if (p.debug_mode) {  // pipeline-ceiling experiments (KNN_B200_DEBUG_SWEEP=1,2,3)
+                    // Next tile's column norms into L1 now, so the in-loop
+                    // loads of that tile hit L1 instead of paying L2 latency.
+                    if (lane < SEG_COLS / 32 && t + 1 < t1)
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(p.alpha + cbase + BN + lane * 32));
+                    if (p.debug_mode && p.debug_mode != 4) {  // pipeline-ceiling experiments
                         uint32_t vd[32];
                         if (p.debug_mode == 1)
                             for (int c0 = 0; c0 < SEG_COLS; c0 += 32) {
@@ -366,34 +455,41 @@ tensor_sweep_kernel(const SweepParams p) {
                         continue;
                     }
                     uint32_t va[32], vb[32];
-                    float ba[32], bb[32];
-                    // software pipeline: chunk c+1's TMEM read and beta load are
-                    // in flight while chunk c is filtered
+                    float bt[32];
+                    // software pipeline: chunk c+1's TMEM read is in flight while
+                    // chunk c is filtered; the column norms come from L1
+                    // (prefetched one tile ahead)
                     ptx::tmem_ld_32x32b_x32(taddr, va);
-                    load_beta(cbase, ba);
 #pragma unroll 1
                     for (int c0 = 0; c0 < SEG_COLS; c0 += 64) {
                         ptx::tmem_wait_ld();
                         ptx::tmem_ld_32x32b_x32(taddr + c0 + 32, vb);
-                        load_beta(cbase + c0 + 32, bb);
-                        process(va, ba, cbase + c0, (first && c0 < KPL) ? c0 : -1);
+                        load_beta(cbase + c0, bt);
+                        process(va, bt, cbase + c0, (first && c0 < KPL) ? c0 : -1);
                         ptx::tmem_wait_ld();
                         if (c0 + 64 < SEG_COLS) {
                             ptx::tmem_ld_32x32b_x32(taddr + c0 + 64, va);
-                            load_beta(cbase + c0 + 64, ba);
                         } else {  // this warp's part of the accumulator is in registers: release it
                             ptx::tc_fence_before();
                             __syncwarp();
                             if (lane == 0) ptx::mbar_arrive(tempty_bar(b));
                         }
-                        process(vb, bb, cbase + c0 + 32, (first && c0 + 32 < KPL) ? c0 + 32 : -1);
+                        load_beta(cbase + c0 + 32, bt);
+                        process(vb, bt, cbase + c0 + 32, (first && c0 + 32 < KPL) ? c0 + 32 : -1);
                     }
                 }
                 if (valid) {
                     for (int s = 0; s < KPL; ++s) {
-                        const uint32_t col = my_i[s * L::LIST_ROWS];
-                        state[s] = col == 0xffffffffu ? kEmptyKey
-                                                      : (uint64_t(float_to_ordered(my_a[s * L::LIST_ROWS])) << 32) | col;
+                        float a;
+                        uint32_t col;
+                        if constexpr (REGLIST) {
+                            a = la[s];
+                            col = lx[s];
+                        } else {
+                            a = my_a[s * L::LIST_ROWS];
+                            col = my_i[s * L::LIST_ROWS];
+                        }
+                        state[s] = col == 0xffffffffu ? kEmptyKey : (uint64_t(float_to_ordered(a)) << 32) | col;
                     }
                 }
             }
