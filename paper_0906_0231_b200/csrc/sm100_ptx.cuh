@@ -158,5 +158,17 @@ __device__ __forceinline__ void tmem_ld_32x32b_x2(uint32_t taddr, uint32_t (&v)[
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// Packed FP32x2 FMA (SASS FFMA2): {v.x, v.y} * -2 + {b.x, b.y}, each lane
+// rounded once exactly like __fmaf_rn.
+__device__ __forceinline__ float2 ffma2_m2(uint32_t v0, uint32_t v1, float b0, float b1) {
+    unsigned long long vv, bb, r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(vv) : "r"(v0), "r"(v1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(b0), "f"(b1));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(vv), "l"(0xC0000000C0000000ull), "l"(bb));
+    float2 out;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(out.x), "=f"(out.y) : "l"(r));
+    return out;
+}
+
 }  // namespace ptx
 }  // namespace knnb

@@ -378,12 +378,13 @@ tensor_sweep_kernel(const SweepParams p) {
                             return;
                         }
                     }
-                    // hot path: FFMA + FMNMX per distance (min as a tree), one vote
+                    // hot path: one FFMA2 per two distances, a FMNMX(3) min tree, one vote
                     float m[16];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        m[i] = fminf(__fmaf_rn(-2.0f, __uint_as_float(v[2 * i]), bt[2 * i]),
-                                     __fmaf_rn(-2.0f, __uint_as_float(v[2 * i + 1]), bt[2 * i + 1]));
+                    for (int i = 0; i < 16; ++i) {
+                        const float2 y2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], bt[2 * i], bt[2 * i + 1]);
+                        m[i] = fminf(y2.x, y2.y);
+                    }
 #pragma unroll
                     for (int w = 8; w >= 1; w >>= 1)
 #pragma unroll
@@ -397,8 +398,9 @@ tensor_sweep_kernel(const SweepParams p) {
                     uint32_t pm = 0;
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
-                        ye[i] = __fmaf_rn(-2.0f, __uint_as_float(v[2 * i]), bt[2 * i]);
-                        yo[i] = __fmaf_rn(-2.0f, __uint_as_float(v[2 * i + 1]), bt[2 * i + 1]);
+                        const float2 y2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], bt[2 * i], bt[2 * i + 1]);
+                        ye[i] = y2.x;
+                        yo[i] = y2.y;
                         if (fminf(ye[i], yo[i]) < thr.a) pm |= 1u << i;
                     }
                     uint32_t any = __reduce_or_sync(0xffffffffu, pm);
