@@ -84,7 +84,7 @@ typedef struct {
                                   (EngineResult::pair_evaluations, engine.hpp:28) */
     uint64_t distance_evals;   /* ordered (query, reference) distances the kernels executed */
     uint64_t rescored;         /* candidates re-scored by the exact fold (TENSOR) */
-    uint32_t fallback_rows;    /* rows recomputed by the EXACT kernel (TENSOR) */
+    uint32_t fallback_rows;    /* rows without a first-pass proof, finished by the band-capture pass (TENSOR) */
     uint32_t kernel_launches;  /* device kernels launched by this call */
     int32_t arith_used;        /* knn_b200_arith actually run */
     int32_t n_devices;         /* GPUs used */
@@ -93,6 +93,8 @@ typedef struct {
     double kernel_ms;          /* all kernels, CUDA events */
     double d2h_ms;             /* device->host copy, CUDA events */
     double sweep_ms;           /* the dominant distance+top-k kernel alone, CUDA events */
+    uint32_t exact_rows;       /* rows recomputed by the EXACT kernel (TENSOR: capture overflow) */
+    uint32_t reserved;
 } knn_b200_stats;
 
 typedef struct knn_b200_ctx knn_b200_ctx;

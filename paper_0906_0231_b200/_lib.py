@@ -49,6 +49,8 @@ class Stats(ctypes.Structure):
         ("kernel_ms", ctypes.c_double),
         ("d2h_ms", ctypes.c_double),
         ("sweep_ms", ctypes.c_double),
+        ("exact_rows", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
     ]
 
     def as_dict(self) -> dict:

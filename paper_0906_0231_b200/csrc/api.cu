@@ -87,7 +87,7 @@ struct knn_b200_ctx {
     int sm_count = 148;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};  // [0..3] call phases, [4..5] around the sweep kernel
-    DevBuf vectors, staged, flags, out_index, out_dist, tensor_ws, exact_ws;
+    DevBuf vectors, staged, flags, out_index, out_dist, tensor_ws, exact_ws, capture_ws;
     unsigned long long* host_flags = nullptr;  // pinned
     std::mutex mu;
 };
@@ -122,6 +122,7 @@ struct Counters {
     uint64_t distance_evals = 0;
     uint64_t rescored = 0;
     uint32_t fallback_rows = 0;
+    uint32_t exact_rows = 0;
     int arith_used = KNN_B200_ARITH_EXACT;
 };
 
@@ -199,11 +200,20 @@ void solve_rows_core(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, 
         ta.stream = stream;
         ta.ev_sweep0 = ctx->ev[4];
         ta.ev_sweep1 = ctx->ev[5];
+        ta.alloc2 = [](void* c, size_t bytes) -> void* {
+            try {
+                return static_cast<knn_b200_ctx*>(c)->capture_ws.get(bytes);
+            } catch (...) {
+                return nullptr;
+            }
+        };
+        ta.alloc2_ctx = ctx;
         knnb::TensorPathResult tr;
         cuda_check(knnb::run_tensor_path(ta, tr), "tensor path");
         ctr.launches += tr.launches;
         ctr.rescored += tr.rescored;
         ctr.fallback_rows += tr.fallback_rows;
+        ctr.exact_rows += tr.exact_rows;
         return;
     }
     ctr.arith_used = KNN_B200_ARITH_EXACT;
@@ -223,6 +233,7 @@ void fill_stats(knn_b200_stats* st, const Counters& ctr, uint64_t pairs, int nde
     st->distance_evals = ctr.distance_evals;
     st->rescored = ctr.rescored;
     st->fallback_rows = ctr.fallback_rows;
+    st->exact_rows = ctr.exact_rows;
     st->kernel_launches = ctr.launches;
     st->arith_used = ctr.arith_used;
     st->n_devices = ndev;
@@ -291,6 +302,7 @@ void knn_b200_destroy(knn_b200_ctx* ctx) {
     ctx->out_dist.release();
     ctx->tensor_ws.release();
     ctx->exact_ws.release();
+    ctx->capture_ws.release();
     if (ctx->host_flags) cudaFreeHost(ctx->host_flags);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
@@ -459,6 +471,7 @@ int knn_b200_solve_multi(const float* host_vectors, uint32_t n, uint32_t d, uint
                 tot.distance_evals += c.distance_evals;
                 tot.rescored += c.rescored;
                 tot.fallback_rows += c.fallback_rows;
+                tot.exact_rows += c.exact_rows;
                 tot.arith_used = c.arith_used;
             }
             fill_stats(stats, tot, uint64_t(n) * (n - 1) / 2, int(use));

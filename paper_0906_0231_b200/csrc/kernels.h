@@ -47,10 +47,15 @@ struct TensorPathArgs {
     int sm_count;
     cudaStream_t stream;
     cudaEvent_t ev_sweep0, ev_sweep1;  // optional, around the sweep kernel
+    // grow-only allocator for the second (band-capture) pass, sized on the
+    // host once the number of unproven rows is known
+    void* (*alloc2)(void* ctx, size_t bytes);
+    void* alloc2_ctx;
 };
 struct TensorPathResult {
     unsigned long long rescored = 0;
-    uint32_t fallback_rows = 0;
+    uint32_t fallback_rows = 0;  // rows without a first-pass proof (band-capture pass)
+    uint32_t exact_rows = 0;     // rows recomputed by the EXACT kernel
     uint32_t launches = 0;
 };
 uint32_t tensor_kp_for(uint32_t klist);  // 0 = unsupported

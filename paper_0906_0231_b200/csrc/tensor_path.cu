@@ -72,6 +72,14 @@ struct SweepParams {
                            // 3 = no TMA loads, 4 = filter without insertions
     uint64_t* cand;       // [(row_end - row_begin) * NSEG * KPL], segment-major per row;
                           // also the list state carried between column groups
+    const uint8_t* xa;    // A-operand (query) planes: xh itself, or the gathered rows of a second pass
+    uint32_t npad_a;
+    // band-capture pass (CAPTURE kernels): per query slot a fixed y threshold;
+    // every column with y <= threshold is appended to the slot's buffer
+    const float* cap_thr;
+    uint32_t* cap_cnt;
+    uint64_t* cap_buf;
+    uint32_t cap;
 };
 
 // Per-row candidate list: KPL unsorted (y, index) entries in shared memory --
@@ -128,7 +136,7 @@ __device__ __noinline__ ListMax list_replace_max(uint32_t a_base, uint32_t i_bas
 // come from HBM once per group instead of once per row block.  The per-row
 // candidate lists are written to `cand` at the end of each item and read
 // back when the row block's next group starts.
-template <int KPL, int BN, bool ARES, int EW>
+template <int KPL, int BN, bool ARES, int EW, bool CAPTURE>
 __global__ void __launch_bounds__(TSLayout<KPL, BN, ARES, EW>::THREADS, 1)
 tensor_sweep_kernel(const SweepParams p) {
     using L = TSLayout<KPL, BN, ARES, EW>;
@@ -136,7 +144,7 @@ tensor_sweep_kernel(const SweepParams p) {
     constexpr int NSEG = L::NSEG;
     constexpr int SEG_COLS = BN / NSEG;  // columns of a tile one epilogue warp filters
     static_assert(SEG_COLS % 64 == 0 && KPL % 16 == 0 && KPL <= SEG_COLS, "tile / list shape");
-    constexpr bool REGLIST = L::REGLIST;
+    constexpr bool REGLIST = L::REGLIST && !CAPTURE;
     constexpr bool DIRECT = !REGLIST && KPL % 32 == 0;  // fill the first KPL columns without the filter
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -194,7 +202,7 @@ tensor_sweep_kernel(const SweepParams p) {
                         ptx::mbar_arrive_expect_tx(afull_bar, p.kc * TS_A_CHUNK);
                         for (uint32_t kc = 0; kc < p.kc; ++kc)
                             ptx::bulk_g2s(ptx::smem_u32(a_smem + kc * TS_A_CHUNK),
-                                          p.xh + (size_t(kc) * p.npad + r0) * 128, TS_A_CHUNK, afull_bar);
+                                          p.xa + (size_t(kc) * p.npad_a + r0) * 128, TS_A_CHUNK, afull_bar);
                         a_phase ^= 1;
                     }
                     for (uint32_t t = t0; t < t1; ++t) {
@@ -214,7 +222,7 @@ tensor_sweep_kernel(const SweepParams p) {
                                           L::B_CHUNK, full_bar(stage));
                             if constexpr (!ARES)
                                 ptx::bulk_g2s(ptx::smem_u32(dst + L::B_CHUNK),
-                                              p.xh + (size_t(kc) * p.npad + r0) * 128, TS_A_CHUNK, full_bar(stage));
+                                              p.xa + (size_t(kc) * p.npad_a + r0) * 128, TS_A_CHUNK, full_bar(stage));
                             if (++stage == S) {
                                 stage = 0;
                                 phase ^= 1;
@@ -315,8 +323,12 @@ tensor_sweep_kernel(const SweepParams p) {
                 }
             return ListMax{mv[0], ms[0]};
         };
+        uint32_t cap_slot = 0;
         auto insert = [&](float y, uint32_t col) {
-            if constexpr (REGLIST) {
+            if constexpr (CAPTURE) {
+                const uint32_t at = atomicAdd(p.cap_cnt + cap_slot, 1u);
+                if (at < p.cap) p.cap_buf[size_t(cap_slot) * p.cap + at] = (uint64_t(float_to_ordered(y)) << 32) | col;
+            } else if constexpr (REGLIST) {
 #pragma unroll
                 for (int s = 0; s < KPL; ++s) {
                     const bool h = uint32_t(s) == thr.slot;
@@ -337,7 +349,11 @@ tensor_sweep_kernel(const SweepParams p) {
                 uint64_t* state = p.cand + (size_t(row - p.row_begin) * NSEG + seg) * KPL;
                 // Columns are ranked by y = fl(beta_j - 2 dot): alpha_i is
                 // constant along a row; the rescore forms A = alpha_i + y in fp64.
-                if constexpr (REGLIST) {
+                if constexpr (CAPTURE) {
+                    cap_slot = row - p.row_begin;
+                    // fixed threshold: admit y <= cap_thr (strict < against its successor)
+                    thr = ListMax{valid ? nextafterf(p.cap_thr[cap_slot], kInf) : -kInf, 0};
+                } else if constexpr (REGLIST) {
 #pragma unroll
                     for (int s = 0; s < KPL; ++s) {
                         const uint64_t key = (g == 0 || !valid) ? kEmptyKey : state[s];
@@ -480,7 +496,7 @@ tensor_sweep_kernel(const SweepParams p) {
                         process(vb, bt, cbase + c0 + 32, (first && c0 + 32 < KPL) ? c0 + 32 : -1);
                     }
                 }
-                if (valid) {
+                if (valid && !CAPTURE) {
                     for (int s = 0; s < KPL; ++s) {
                         float a;
                         uint32_t col;
@@ -632,7 +648,9 @@ struct RescoreParams {
     float* out_dist;
     uint32_t* fb_count;
     uint32_t* fb_rows;
+    float* fb_thr;        // capture threshold (y space) for each unproven row
     unsigned long long* rescored;
+    int force_capture;    // testing: treat every row as unproven (KNN_B200_FORCE_CAPTURE=1)
 };
 
 constexpr double kTcSafety = 4.0;  // tensor-core accumulation error allowance
@@ -655,6 +673,31 @@ __device__ __forceinline__ float exact_fold_rows(const float* __restrict__ a, co
         for (uint32_t j = 0; j < d; ++j) acc = fold_step<FOLD>(__ldg(a + j), __ldg(b + j), acc);
     }
     return fold_finalize<FOLD>(acc);
+}
+
+// Upper bound (scaled A space) on the approximate distance of any column whose
+// exact reference distance is <= T: s^2 T' + 2E, DESIGN.md §4.
+template <int FOLD>
+__device__ __forceinline__ double proof_bound(uint32_t d, const unsigned int* maxabs, const unsigned long long* gmax,
+                                              double nx, double rh, double al, double T) {
+    const double u = 5.9604644775390625e-08;  // 2^-24
+    const double dd = double(d);
+    const int e = scale_exponent(*maxabs);
+    const double s2 = ldexp(1.0, 2 * e);
+    const double xnmax = __longlong_as_double((long long)gmax[0]);
+    const double rhomax = __longlong_as_double((long long)gmax[1]);
+    const double alphamax = __longlong_as_double((long long)gmax[2]);
+    const double Tp = T + fabs(T) * 2.0 * (dd + 3.0) * u + 1e-300;
+    const double ctc = 2.0 * kTcSafety * dd * 2.0 * u;  // 2 * c * d * 2^-23
+    if (FOLD == kCosine) {
+        const double eref = (dd + 2.0) * u * ((nx + rh) * (xnmax + rhomax) / s2 + 1.0);
+        const double eacc = ctc * nx * xnmax + 2.0 * (rh * xnmax + rhomax * (nx + rh)) + u * 2.0 * s2 * (fabs(Tp) + 2.0);
+        return 2.0 * s2 * (Tp + 2.0 * eref) + 2.0 * eacc;
+    }
+    const double rr = rh + rhomax;
+    const double e_all = (ctc + 6.0 * u) * nx * xnmax + (dd + 3.0) * u * (al + alphamax) +
+                         rr * (2.0 * sqrt(s2 * fmax(Tp, 0.0)) + rr);
+    return s2 * Tp + 2.0 * e_all;
 }
 
 template <int FOLD, int KP, int NSEG>
@@ -743,6 +786,7 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         }
     }
     bool complete;
+    double cap_y = __longlong_as_double(0x7ff0000000000000ll);  // +inf: capture everything
     if (!any_full) {
         complete = true;  // every column was offered into a non-full list: the list holds all of them
     } else if (valid < p.klist) {
@@ -752,33 +796,17 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         const double T = double(ordered_to_float(uint32_t(kth >> 32)));
         // the list ranks y = fl(beta - 2 dot); A = alpha_q + y exactly in fp64
         const double a_max = double(p.alpha[q]) + double(ordered_to_float(uint32_t(last_approx >> 32)));
-        const double u = 5.9604644775390625e-08;  // 2^-24
-        const double dd = double(p.d);
-        const int e = scale_exponent(*p.maxabs);
-        const double s2 = ldexp(1.0, 2 * e);
-        const double xnmax = __longlong_as_double((long long)p.gmax[0]);
-        const double rhomax = __longlong_as_double((long long)p.gmax[1]);
-        const double alphamax = __longlong_as_double((long long)p.gmax[2]);
-        const double nx = p.xnorm[q], rh = p.rho[q], al = double(p.alpha[q]);
-        const double Tp = T + fabs(T) * 2.0 * (dd + 3.0) * u + 1e-300;
-        const double ctc = 2.0 * kTcSafety * dd * 2.0 * u;  // 2 * c * d * 2^-23
-        double bound;
-        if (FOLD == kCosine) {
-            const double eref = (dd + 2.0) * u * ((nx + rh) * (xnmax + rhomax) / s2 + 1.0);
-            const double eacc = ctc * nx * xnmax + 2.0 * (rh * xnmax + rhomax * (nx + rh)) + u * 2.0 * s2 * (fabs(Tp) + 2.0);
-            bound = 2.0 * s2 * (Tp + 2.0 * eref) + 2.0 * eacc;
-        } else {
-            const double rr = rh + rhomax;
-            const double e_all = (ctc + 6.0 * u) * nx * xnmax + (dd + 3.0) * u * (al + alphamax) +
-                                 rr * (2.0 * sqrt(s2 * fmax(Tp, 0.0)) + rr);
-            bound = s2 * Tp + 2.0 * e_all;
-        }
-        complete = a_max > bound;
+        const double bound = proof_bound<FOLD>(p.d, p.maxabs, p.gmax, p.xnorm[q], p.rho[q], double(p.alpha[q]), T);
+        complete = a_max > bound && !p.force_capture;
+        // every true neighbor has A <= bound, i.e. y <= bound - alpha_q: the
+        // second (band-capture) pass collects exactly that band
+        cap_y = bound - double(p.alpha[q]);
     }
     if (!complete) {
         if (lane == 0) {
             const uint32_t at = atomicAdd(p.fb_count, 1u);
             p.fb_rows[at] = q;
+            p.fb_thr[at] = __double2float_ru(cap_y);
         }
         return;
     }
@@ -787,6 +815,98 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         const float dv = ordered_to_float(uint32_t(key >> 32));
         p.out_index[size_t(slot) * p.klist + t] = uint32_t(key);
         p.out_dist[size_t(slot) * p.klist + t] = p.out_sqrt ? __fsqrt_rn(dv) : dv;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// second pass for unproven rows: band capture
+
+// Copy the swizzled fp16 rows rows[0..m) into a compact plane set (re-swizzled
+// for their new row positions); padding rows are zero.
+__global__ void gather_rows_kernel(const uint8_t* __restrict__ xh, uint32_t npad, uint32_t kc,
+                                   const uint32_t* __restrict__ rows, uint32_t m, uint32_t mpad,
+                                   uint8_t* __restrict__ xa) {
+    const uint32_t total = kc * mpad * 8;  // 16-byte units
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < total; u += gridDim.x * blockDim.x) {
+        const uint32_t unit = u & 7, r = (u >> 3) % mpad, c = (u >> 3) / mpad;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r < m) {
+            const uint32_t src = rows[r];
+            v = *reinterpret_cast<const uint4*>(xh + (size_t(c) * npad + src) * 128 + ((unit ^ (src & 7)) << 4));
+        }
+        *reinterpret_cast<uint4*>(xa + (size_t(c) * mpad + r) * 128 + ((unit ^ (r & 7)) << 4)) = v;
+    }
+}
+
+struct Rescore2Params {
+    const float* X;
+    uint32_t n, d, klist;
+    uint32_t row_begin;
+    const uint32_t* rows;   // unproven rows (pass-1 order)
+    uint32_t m;
+    const uint32_t* cnt;
+    const uint64_t* buf;
+    uint32_t cap;
+    int out_sqrt;
+    uint32_t* out_index;
+    float* out_dist;
+    uint32_t* fb2_count;
+    uint32_t* fb2_rows;
+    unsigned long long* rescored;
+};
+
+// Exact fold of every captured column of an unproven row (one warp per row);
+// the captured band contains every true neighbor by construction, so the
+// exact top-k of the buffer is the answer.  Overflowing rows go to the exact
+// kernel.
+template <int FOLD>
+__global__ void __launch_bounds__(128) rescore_capture_kernel(const Rescore2Params p) {
+    extern __shared__ uint64_t keys2[];  // [4][cap]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t slot = blockIdx.x * 4 + warp;
+    if (slot >= p.m) return;
+    const uint32_t q = p.rows[slot];
+    uint64_t* ks = keys2 + size_t(warp) * p.cap;
+    const uint32_t c = p.cnt[slot];
+    if (c > p.cap) {
+        if (lane == 0) p.fb2_rows[atomicAdd(p.fb2_count, 1u)] = q;
+        return;
+    }
+    const float* xq = p.X + size_t(q) * p.d;
+    const bool vec = (p.d % 4 == 0);
+    const uint64_t* in = p.buf + size_t(slot) * p.cap;
+    uint32_t valid = 0;
+    for (uint32_t i = lane; i < c; i += 32) {
+        const uint32_t col = uint32_t(in[i]);
+        uint64_t key = kEmptyKey;
+        if (col != q) {
+            const float* xc = p.X + size_t(col) * p.d;
+            const float dist = col > q ? exact_fold_rows<FOLD>(xc, xq, p.d, vec) : exact_fold_rows<FOLD>(xq, xc, p.d, vec);
+            key = make_key(dist, col);
+            ++valid;
+        }
+        ks[i] = key;
+    }
+    for (int o = 16; o; o >>= 1) valid += __shfl_xor_sync(0xffffffffu, valid, o);
+    __syncwarp();
+    if (lane == 0) atomicAdd(p.rescored, (unsigned long long)valid);
+    if (valid < p.klist) {  // cannot happen for a correct band; stay exact
+        if (lane == 0) p.fb2_rows[atomicAdd(p.fb2_count, 1u)] = q;
+        return;
+    }
+    // keys are unique (distinct columns) except the empty self slot: the
+    // rank of an element is the number of smaller keys
+    const size_t orow = size_t(q - p.row_begin);
+    for (uint32_t i = lane; i < c; i += 32) {
+        const uint64_t mk = ks[i];
+        if (mk == kEmptyKey) continue;
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < c; ++j) rank += ks[j] < mk;
+        if (rank < p.klist) {
+            const float dv = ordered_to_float(uint32_t(mk >> 32));
+            p.out_index[orow * p.klist + rank] = uint32_t(mk);
+            p.out_dist[orow * p.klist + rank] = p.out_sqrt ? __fsqrt_rn(dv) : dv;
+        }
     }
 }
 
@@ -803,7 +923,10 @@ struct TensorCfg {
 
 static TensorCfg tensor_cfg(uint32_t klist) {
     const uint32_t margin = klist / 4 > 8 ? klist / 4 : 8;
-    if (klist + 1 + 5 <= 16) return {16, 2};
+    if (klist + 1 + 5 <= 16) {
+        const char* e = getenv("KNN_B200_LIST16_SEGMENTS");  // tuning knob: 2 (default) or 1
+        return {16, (e && atoi(e) == 1) ? 1u : 2u};
+    }
     if (klist + 1 + margin <= 32) return {32, 2};
     if (klist + 1 + margin <= 64) return {64, 1};
     if (klist + 1 + margin <= 128) return {128, 1};
@@ -813,6 +936,18 @@ static TensorCfg tensor_cfg(uint32_t klist) {
 uint32_t tensor_kp_for(uint32_t klist) {
     const TensorCfg c = tensor_cfg(klist);
     return c.kpl * c.nseg;
+}
+
+size_t capture_workspace_bytes(uint32_t m, uint32_t d, uint32_t cap) {
+    const uint32_t mpad = (m + TS_BM - 1) / TS_BM * TS_BM;
+    const uint32_t kc = (d + 63) / 64;
+    size_t b = 0;
+    auto add = [&](size_t x) { b += (x + 255) / 256 * 256; };
+    add(size_t(kc) * mpad * 128);
+    add(size_t(m) * 4 + 8);
+    add(size_t(m) * cap * 8);
+    add(size_t(m) * 4);
+    return b;
 }
 
 size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t rows, uint32_t kp) {
@@ -829,13 +964,14 @@ size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t rows, uint32_t kp
     add(64);                       // scalars
     add(size_t(rows) * kp * 8);    // cand
     add(size_t(rows) * 4);         // fallback rows
+    add(size_t(rows) * 4);         // capture thresholds
     return b;
 }
 
-template <int KPL, int BN, bool ARES, int EW>
+template <int KPL, int BN, bool ARES, int EW, bool CAPTURE = false>
 static cudaError_t launch_sweep_t(const SweepParams& sp, uint32_t nrows, cudaStream_t stream) {
     using L = TSLayout<KPL, BN, ARES, EW>;
-    auto kern = tensor_sweep_kernel<KPL, BN, ARES, EW>;
+    auto kern = tensor_sweep_kernel<KPL, BN, ARES, EW, CAPTURE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::SMEM));
     if (e != cudaSuccess) return e;
     const uint32_t nrb = (nrows + TS_BM - 1) / TS_BM;
@@ -851,6 +987,9 @@ static cudaError_t launch_sweep_t(const SweepParams& sp, uint32_t nrows, cudaStr
 static cudaError_t launch_sweep(TensorCfg c, bool ares, const SweepParams& sp, uint32_t nrows, cudaStream_t stream) {
     switch (c.kpl) {
     case 16:
+        if (c.nseg == 1)
+            return ares ? launch_sweep_t<16, 256, true, 4>(sp, nrows, stream)
+                        : launch_sweep_t<16, 256, false, 4>(sp, nrows, stream);
         return ares ? launch_sweep_t<16, 256, true, 8>(sp, nrows, stream)
                     : launch_sweep_t<16, 256, false, 8>(sp, nrows, stream);
     case 32:
@@ -865,11 +1004,19 @@ static cudaError_t launch_sweep(TensorCfg c, bool ares, const SweepParams& sp, u
     }
 }
 
+static cudaError_t launch_capture_sweep(bool ares, const SweepParams& sp, uint32_t nrows, cudaStream_t stream) {
+    return ares ? launch_sweep_t<16, 256, true, 8, true>(sp, nrows, stream)
+                : launch_sweep_t<16, 256, false, 8, true>(sp, nrows, stream);
+}
+
 template <int FOLD>
 static cudaError_t launch_rescore(TensorCfg c, const RescoreParams& rp, uint32_t nrows, cudaStream_t stream) {
     const dim3 grid((nrows + 7) / 8);
     switch (c.kpl) {
-    case 16: rescore_kernel<FOLD, 32, 2><<<grid, 256, 0, stream>>>(rp); break;
+    case 16:
+        if (c.nseg == 1) rescore_kernel<FOLD, 16, 1><<<grid, 256, 0, stream>>>(rp);
+        else rescore_kernel<FOLD, 32, 2><<<grid, 256, 0, stream>>>(rp);
+        break;
     case 32: rescore_kernel<FOLD, 64, 2><<<grid, 256, 0, stream>>>(rp); break;
     case 64: rescore_kernel<FOLD, 64, 1><<<grid, 256, 0, stream>>>(rp); break;
     default: rescore_kernel<FOLD, 128, 1><<<grid, 256, 0, stream>>>(rp); break;
@@ -899,6 +1046,7 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     uint8_t* scal = take(64);
     uint64_t* cand = reinterpret_cast<uint64_t*>(take(size_t(nrows) * kp * 8));
     uint32_t* fb_rows = reinterpret_cast<uint32_t*>(take(size_t(nrows) * 4));
+    float* fb_thr = reinterpret_cast<float*>(take(size_t(nrows) * 4));
     unsigned int* maxabs = reinterpret_cast<unsigned int*>(scal);
     uint32_t* fb_count = reinterpret_cast<uint32_t*>(scal + 4);
     unsigned long long* gmax = reinterpret_cast<unsigned long long*>(scal + 8);
@@ -931,29 +1079,79 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     if (group_tiles < 1) group_tiles = 1;
     if (group_tiles > ntiles) group_tiles = ntiles;
     const char* dbg = getenv("KNN_B200_DEBUG_SWEEP");
-    SweepParams sp{xh, alpha, n, npad, kc, a.row_begin, a.row_end, group_tiles, dbg ? atoi(dbg) : 0, cand};
+    SweepParams sp{xh,      alpha,   n,       npad,    kc, a.row_begin, a.row_end, group_tiles, dbg ? atoi(dbg) : 0,
+                   cand,    xh,      npad,    nullptr, nullptr, nullptr, 0};
     if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
     if ((e = launch_sweep(cfg, kc <= uint32_t(TS_MAX_RES_KC), sp, nrows, st)) != cudaSuccess) return e;
     if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
     ++launches;
 
-    RescoreParams rp{a.X, n, d, a.klist, kp, a.row_begin, a.row_end, cand, alpha, rho, xnorm, gmax, maxabs,
-                     a.fold, a.out_sqrt, a.out_index, a.out_dist, fb_count, fb_rows, rescored};
+    RescoreParams rp{a.X,  n,         d,          a.klist,  kp,       a.row_begin, a.row_end, cand,
+                     alpha, rho,      xnorm,      gmax,     maxabs,   a.fold,      a.out_sqrt, a.out_index,
+                     a.out_dist, fb_count, fb_rows, fb_thr, rescored, 0};
+    {
+        const char* fc = getenv("KNN_B200_FORCE_CAPTURE");
+        rp.force_capture = fc && atoi(fc) != 0;
+    }
     e = cosine ? launch_rescore<kCosine>(cfg, rp, nrows, st) : launch_rescore<kSqEuclidean>(cfg, rp, nrows, st);
     if (e != cudaSuccess) return e;
     ++launches;
 
-    // Rows without a completeness proof: exact recomputation (rare).
+    // Rows without a completeness proof: a second tensor pass captures the
+    // whole proven band of each such row, then exact re-scoring; only rows
+    // whose band overflows the capture buffer are recomputed exactly.
     if ((e = cudaMemcpyAsync(a.host_scratch, scal, 64, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
     const uint32_t nfb = *reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(a.host_scratch) + 4);
     r.rescored = *reinterpret_cast<const unsigned long long*>(static_cast<const uint8_t*>(a.host_scratch) + 32);
     r.fallback_rows = nfb;
     if (nfb) {
-        if ((e = launch_exact_fused(a.fold, a.X, n, d, a.klist, fb_rows, 0, nfb, a.out_index, a.out_dist, a.out_sqrt,
-                                    a.row_begin, a.exact_scratch, a.sm_count, st)) != cudaSuccess)
+        const uint32_t mpad = (nfb + TS_BM - 1) / TS_BM * TS_BM;
+        const uint32_t cap = kp >= 128 ? 1024 : 512;
+        uint8_t* w2 = static_cast<uint8_t*>(a.alloc2(a.alloc2_ctx, capture_workspace_bytes(nfb, d, cap)));
+        if (!w2) return cudaErrorMemoryAllocation;
+        auto take2 = [&](size_t x) {
+            uint8_t* q = w2;
+            w2 += (x + 255) / 256 * 256;
+            return q;
+        };
+        uint8_t* xa = take2(size_t(kc) * mpad * 128);
+        uint32_t* cap_cnt = reinterpret_cast<uint32_t*>(take2(size_t(nfb) * 4 + 8));
+        uint64_t* cap_buf = reinterpret_cast<uint64_t*>(take2(size_t(nfb) * cap * 8));
+        uint32_t* fb2_rows = reinterpret_cast<uint32_t*>(take2(size_t(nfb) * 4));
+        uint32_t* fb2_count = cap_cnt + nfb;
+        if ((e = cudaMemsetAsync(cap_cnt, 0, size_t(nfb) * 4 + 8, st)) != cudaSuccess) return e;
+        gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xh, npad, kc, fb_rows, nfb, mpad, xa);
+        SweepParams cp{xh,      alpha,  n,    npad,   kc,      0,   nfb, group_tiles, 0,
+                       nullptr, xa,     mpad, fb_thr, cap_cnt, cap_buf, cap};
+        if ((e = launch_capture_sweep(kc <= uint32_t(TS_MAX_RES_KC), cp, nfb, st)) != cudaSuccess) return e;
+        Rescore2Params r2{a.X,     n,       d,         a.klist,   a.row_begin, fb_rows,   nfb,      cap_cnt,
+                          cap_buf, cap,     a.out_sqrt, a.out_index, a.out_dist, fb2_count, fb2_rows, rescored};
+        const size_t smem2 = size_t(4) * cap * 8;
+        if (cosine) {
+            cudaFuncSetAttribute(rescore_capture_kernel<kCosine>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+            rescore_capture_kernel<kCosine><<<(nfb + 3) / 4, 128, smem2, st>>>(r2);
+        } else {
+            cudaFuncSetAttribute(rescore_capture_kernel<kSqEuclidean>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem2));
+            rescore_capture_kernel<kSqEuclidean><<<(nfb + 3) / 4, 128, smem2, st>>>(r2);
+        }
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        launches += 3;
+        if ((e = cudaMemcpyAsync(a.host_scratch, fb2_count, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+        if ((e = cudaMemcpyAsync(static_cast<uint8_t*>(a.host_scratch) + 32, rescored, 8, cudaMemcpyDeviceToHost, st)) !=
+            cudaSuccess)
             return e;
-        ++launches;
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+        const uint32_t nfb2 = *static_cast<const uint32_t*>(a.host_scratch);
+        r.rescored = *reinterpret_cast<const unsigned long long*>(static_cast<const uint8_t*>(a.host_scratch) + 32);
+        r.exact_rows = nfb2;
+        if (nfb2) {
+            if ((e = launch_exact_fused(a.fold, a.X, n, d, a.klist, fb2_rows, 0, nfb2, a.out_index, a.out_dist,
+                                        a.out_sqrt, a.row_begin, a.exact_scratch, a.sm_count, st)) != cudaSuccess)
+                return e;
+            ++launches;
+        }
     }
     r.launches = launches;
     return cudaSuccess;

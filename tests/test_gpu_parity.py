@@ -20,7 +20,18 @@ from tests.helpers import assert_lists_bit_equal, golden_input
 pytestmark = pytest.mark.gpu
 
 ROOT = Path(__file__).resolve().parents[1]
-ARITHS = ["exact", "tensor"]
+ARITHS = ["exact", "tensor", "tensor+capture"]
+
+
+@pytest.fixture(autouse=True)
+def _capture_mode(request, monkeypatch):
+    """'tensor+capture' runs the TENSOR policy with every row forced through
+    the second, band-capture pass (KNN_B200_FORCE_CAPTURE)."""
+    arith = request.node.callspec.params.get("arith") if hasattr(request.node, "callspec") else None
+    if arith == "tensor+capture":
+        monkeypatch.setenv("KNN_B200_FORCE_CAPTURE", "1")
+    else:
+        monkeypatch.delenv("KNN_B200_FORCE_CAPTURE", raising=False)
 
 
 @pytest.fixture(scope="module")
@@ -38,7 +49,7 @@ def metric_obj(name):
 
 def arith_id(name):
     from paper_0906_0231_b200 import _lib
-    return _lib.ARITH_NAMES[name]
+    return _lib.ARITH_NAMES[name.split("+")[0]]
 
 
 @pytest.mark.parametrize("arith", ARITHS)
@@ -159,7 +170,9 @@ def test_c1_sampled_rows(ctx, c_oracle, arith):
 def _run_binary(path: Path, args, arith: str, timeout=900):
     if not path.exists():
         pytest.skip(f"{path} not built (needs /root/reference at build time)")
-    env = dict(os.environ, KNN_B200_ARITH=arith)
+    env = dict(os.environ, KNN_B200_ARITH=arith.split("+")[0])
+    if arith.endswith("+capture"):
+        env["KNN_B200_FORCE_CAPTURE"] = "1"
     p = subprocess.run([str(path), *args], capture_output=True, text=True, timeout=timeout, env=env)
     return p
 
@@ -180,3 +193,25 @@ def test_reference_acceptance_gate_on_dropin(arith):
     p = _run_binary(ROOT / "oracle" / "_ref" / "acceptance_b200", ["--skip", "4", "--skip", "5"], arith)
     assert p.returncode == 0, p.stdout + p.stderr
     assert p.stdout.count("PASS") == 5, p.stdout
+
+
+@pytest.mark.parametrize("arith", ["tensor", "tensor+capture"])
+def test_full_size_c2_sampled_rows(ctx, c_oracle, arith):
+    """Config C2 (n=1M, d=256, k=10, Euclidean, seed 1) at full size on the
+    GPU (inputs from the device generator, bit-identical to
+    generate_dataset), checked on 96 sampled rows by the exact oracle."""
+    import torch
+    from paper_0906_0231_b200 import euclidean, generate_torch, solve_rows_torch
+    n, d, k = 1_000_000, 256, 10
+    x = generate_torch(ctx, n, d, 1)
+    idx, dist, st = solve_rows_torch(ctx, x, k, euclidean(), 0, n, arith_id(arith), want_stats=True)
+    xh = x.cpu().numpy()
+    assert np.array_equal(xh[:3], c_oracle.generate(3, d, 1))  # device generator == SplitMix64 stream
+    rows = np.random.default_rng(7).choice(n, 96, replace=False).astype(np.uint32)
+    ri, rd = c_oracle.rows_topk(xh, k, "sqeuclidean", rows)
+    gi = idx.cpu().numpy().view(np.uint32)[rows]
+    gd = dist.cpu().numpy()[rows]
+    assert_lists_bit_equal(gi, gd, ri, np.sqrt(rd), f"C2 sampled [{arith}]")
+    assert st["arith_used"] == 2
+    if arith == "tensor":
+        assert st["fallback_rows"] < n // 1000

@@ -8,7 +8,7 @@ from paper_0906_0231_b200 import Context, _lib, distance_by_name
 
 co = oracle.c_oracle()
 ctx = Context(0)
-cases = [(300, 17, 12, "sqeuclidean"), (2048, 64, 10, "sqeuclidean"), (2048, 64, 10, "hellinger"),
+cases = [(3000, 1024, 100, "sqeuclidean"), (5000, 512, 100, "sqeuclidean"), (300, 17, 12, "sqeuclidean"), (2048, 64, 10, "sqeuclidean"), (2048, 64, 10, "hellinger"),
          (1000, 300, 10, "sqeuclidean"), (1500, 128, 32, "cosine"), (777, 33, 100, "sqeuclidean"),
          (4096, 256, 10, "euclidean")]
 for n, d, k, m in cases:
@@ -25,7 +25,7 @@ for n, d, k, m in cases:
     ok_i = (idx == ri).all(axis=1)
     ok_d = (dist.view(np.uint32) == rd.view(np.uint32)).all(axis=1)
     print(f"n={n} d={d} k={k} {m}: arith={st['arith_used']} idx_rows_bad={int((~ok_i).sum())} "
-          f"dist_rows_bad={int((~ok_d).sum())} fallback={st['fallback_rows']} rescored={st['rescored']} "
+          f"dist_rows_bad={int((~ok_d).sum())} fallback={st['fallback_rows']} exact_rows={st['exact_rows']} rescored={st['rescored']} "
           f"sweep_ms={st['sweep_ms']:.3f} t={dt:.3f}s", flush=True)
     if (~ok_i).any():
         r = int(np.argmin(ok_i))
