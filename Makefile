@@ -51,7 +51,16 @@ $(ENGINE_A): $(PKG)/host/engine_b200.cpp include/knn_b200.h
 REF_LINK := $(ENGINE_A) oracle/_ref/libtknn_ref_noengine.a -L$(PKG)/lib -lknn_b200 \
             -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib' -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib' -lpthread
 
-ref-bins: oracle/_ref/acceptance_b200 build/test_engine_b200
+ref-bins: oracle/_ref/acceptance_b200 build/test_engine_b200 build/tknn_b200 oracle/_ref/tknn_ref
+
+# The reference CLI (tools/main.cpp, unmodified) against the B200 drop-in, and
+# against the reference engine for comparison; CLI11 is the minimal shim in
+# tools/cli11_shim (the real one is not in the image).
+build/tknn_b200: $(REF)/tools/main.cpp tools/cli11_shim/CLI11.hpp $(ENGINE_A) $(LIB) oracle
+	$(CXX) $(REF_FLAGS) -Itools/cli11_shim -I$(REF)/include -o $@ $< $(REF_LINK)
+
+oracle/_ref/tknn_ref: $(REF)/tools/main.cpp tools/cli11_shim/CLI11.hpp oracle
+	$(CXX) $(REF_FLAGS) -Itools/cli11_shim -I$(REF)/include -o $@ $< oracle/_ref/libtknn_ref.a -lpthread
 
 oracle/_ref/acceptance_b200: $(REF)/tests/acceptance.cpp $(ENGINE_A) $(LIB) oracle
 	$(CXX) $(REF_FLAGS) -I$(REF)/include -o $@ $< $(REF_LINK)
