@@ -658,11 +658,30 @@ constexpr double kTcSafety = 4.0;  // tensor-core accumulation error allowance (
 template <int FOLD>
 __device__ __forceinline__ float exact_fold_rows(const float* __restrict__ a, const float* __restrict__ b, uint32_t d,
                                                  bool vec) {
+    // The fold is strictly sequential over coordinates (bit parity); the
+    // loads are batched 8 float4 deep so the random row reads overlap.
     float acc = 0.0f;
     if (vec) {
         const float4* a4 = reinterpret_cast<const float4*>(a);
         const float4* b4 = reinterpret_cast<const float4*>(b);
-        for (uint32_t j = 0; j < d / 4; ++j) {
+        const uint32_t d4 = d / 4;
+        uint32_t j = 0;
+        for (; j + 8 <= d4; j += 8) {
+            float4 x[8], y[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                x[t] = __ldg(a4 + j + t);
+                y[t] = __ldg(b4 + j + t);
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                acc = fold_step<FOLD>(x[t].x, y[t].x, acc);
+                acc = fold_step<FOLD>(x[t].y, y[t].y, acc);
+                acc = fold_step<FOLD>(x[t].z, y[t].z, acc);
+                acc = fold_step<FOLD>(x[t].w, y[t].w, acc);
+            }
+        }
+        for (; j < d4; ++j) {
             const float4 x = __ldg(a4 + j), y = __ldg(b4 + j);
             acc = fold_step<FOLD>(x.x, y.x, acc);
             acc = fold_step<FOLD>(x.y, y.y, acc);
@@ -712,35 +731,99 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     const float* xq = p.X + size_t(q) * p.d;
     const bool vec = (p.d % 4 == 0);
     constexpr int PER = (KP + 31) / 32;
-    uint32_t valid = 0;
+    const double alpha_q = double(p.alpha[q]);
+    // approximate keys and their rank (keys are unique: distinct columns)
+    uint64_t ak[PER];
+    uint32_t arank[PER];
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
         const int i = lane + 32 * m;
-        if (i >= KP) break;
-        const uint64_t c = cand[i];
-        uint64_t key = kEmptyKey;
-        const uint32_t col = uint32_t(c);
-        if (c != kEmptyKey && col != q) {
+        ak[m] = i < KP ? cand[i] : kEmptyKey;
+        if (i < KP) keys_s[warp][i] = ak[m];
+        arank[m] = 0;
+    }
+    __syncwarp();
+    for (int j = 0; j < KP; ++j) {
+        const uint64_t o = keys_s[warp][j];
+#pragma unroll
+        for (int m = 0; m < PER; ++m) arank[m] += (o < ak[m]) || (o == ak[m] && j < lane + 32 * m);
+    }
+    __syncwarp();
+    // exact fold of candidate m of this lane into keys_s
+    uint64_t ek[PER];
+    bool done[PER];
+    uint32_t valid = 0;
+    auto rescore_one = [&](int m) {
+        const uint32_t col = uint32_t(ak[m]);
+        ek[m] = kEmptyKey;
+        done[m] = true;
+        if (ak[m] != kEmptyKey && col != q) {
             const float* xc = p.X + size_t(col) * p.d;
             // Reference argument order (larger index first) -- the fold is
             // symmetric bit for bit, kept for clarity.
             const float dist = col > q ? exact_fold_rows<FOLD>(xc, xq, p.d, vec) : exact_fold_rows<FOLD>(xq, xc, p.d, vec);
-            key = make_key(dist, col);
+            ek[m] = make_key(dist, col);
             ++valid;
         }
-        keys_s[warp][i] = key;
-    }
-    for (int o = 16; o; o >>= 1) valid += __shfl_xor_sync(0xffffffffu, valid, o);
-    __syncwarp();
-    if (lane == 0) atomicAdd(p.rescored, (unsigned long long)valid);
-
-    // rank sort of the exact keys (unique except the empty ones, which sort last)
-    uint64_t mine[PER];
-    uint32_t rank[PER];
+    };
+    auto kth_exact = [&]() -> uint64_t {  // klist-th smallest exact key among the computed ones
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < PER; ++m)
+            if (lane + 32 * m < KP) keys_s[warp][lane + 32 * m] = done[m] ? ek[m] : kEmptyKey;
+        __syncwarp();
+        uint64_t kth = kEmptyKey;
+#pragma unroll
+        for (int m = 0; m < PER; ++m) {
+            if (lane + 32 * m >= KP || !done[m] || ek[m] == kEmptyKey) continue;
+            uint32_t r = 0;
+            for (int j = 0; j < KP; ++j) r += keys_s[warp][j] < ek[m];
+            if (r == p.klist - 1) kth = ek[m];
+        }
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t other = __shfl_xor_sync(0xffffffffu, kth, o);
+            kth = other < kth ? other : kth;
+        }
+        return kth;
+    };
+    // Phase 1: the k + 4 best candidates by approximate distance.
+    const uint32_t r1 = p.klist + 4 < uint32_t(KP) ? p.klist + 4 : uint32_t(KP);
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
-        const int i = lane + 32 * m;
-        mine[m] = i < KP ? keys_s[warp][i] : kEmptyKey;
+        done[m] = false;
+        ek[m] = kEmptyKey;
+        if (lane + 32 * m < KP && arank[m] < r1) rescore_one(m);
+    }
+    // Phase 2: any other candidate whose approximate distance is inside the
+    // bound implied by phase 1's k-th exact distance (those beyond cannot be
+    // among the k nearest); everything when no bound exists.
+    {
+        const uint64_t kth1 = kth_exact();
+        double lim = __longlong_as_double(0x7ff0000000000000ll);
+        if (kth1 != kEmptyKey)
+            lim = proof_bound<FOLD>(p.d, p.maxabs, p.gmax, p.xnorm[q], p.rho[q], alpha_q,
+                                    double(ordered_to_float(uint32_t(kth1 >> 32))));
+#pragma unroll
+        for (int m = 0; m < PER; ++m) {
+            if (lane + 32 * m >= KP || done[m]) continue;
+            const double a = alpha_q + double(ordered_to_float(uint32_t(ak[m] >> 32)));
+            if (ak[m] != kEmptyKey && a <= lim) rescore_one(m);
+            else done[m] = true;  // excluded: stays empty
+        }
+    }
+    for (int o = 16; o; o >>= 1) valid += __shfl_xor_sync(0xffffffffu, valid, o);
+    if (lane == 0) atomicAdd(p.rescored, (unsigned long long)valid);
+    // final order of the exact keys
+    uint64_t mine[PER];
+    uint32_t rank[PER];
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < PER; ++m)
+        if (lane + 32 * m < KP) keys_s[warp][lane + 32 * m] = ek[m];
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+        mine[m] = lane + 32 * m < KP ? ek[m] : kEmptyKey;
         rank[m] = 0;
     }
     for (int j = 0; j < KP; ++j) {
@@ -748,7 +831,6 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
 #pragma unroll
         for (int m = 0; m < PER; ++m) rank[m] += (o < mine[m]) || (o == mine[m] && j < lane + 32 * m);
     }
-    // the k-th exact key (T) and the largest approximate key of the list
     __syncwarp();
 #pragma unroll
     for (int m = 0; m < PER; ++m)
