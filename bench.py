@@ -238,12 +238,11 @@ def main():
     from paper_0906_0231_b200 import Context, _lib, distance_by_name, generate_torch, solve_rows_torch
 
     rank, world, local = dist_env()
-    if world > 1:
-        torch.cuda.set_device(local)
+    launched = "RANK" in os.environ and "MASTER_ADDR" in os.environ  # torchrun (any world size)
+    torch.cuda.set_device(local if launched else 0)
+    if launched:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.device(f"cuda:{local if world > 1 else 0}")
+    dev = torch.device(f"cuda:{local if launched else 0}")
     ctx = Context(dev.index)
     n, d, k = cfg["n"], cfg["d"], cfg["k"]
     metric = distance_by_name(cfg["metric"])
@@ -259,14 +258,14 @@ def main():
         xd = x.double()
         x = (xd / xd.norm(dim=1, keepdim=True).clamp_min(1e-300)).float().contiguous()
         del xd
-    if world > 1:
-        dist.broadcast(x, src=0)
+    if launched:
+        dist.broadcast(x, src=0)  # NCCL broadcast of the reference set
     torch.cuda.synchronize()
     out_idx = torch.empty((r1 - r0, klist), dtype=torch.int32, device=dev)
     out_dist = torch.empty((r1 - r0, klist), dtype=torch.float32, device=dev)
 
     def barrier():
-        if world > 1:
+        if launched:
             dist.barrier(device_ids=[dev.index])
         torch.cuda.synchronize()
 
@@ -299,7 +298,7 @@ def main():
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if world > 1:
+    if launched:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     pairs = n * (n - 1) / 2
@@ -320,7 +319,7 @@ def main():
     for _ in range(args.steps):
         if rank == 0:
             x_e2e.copy_(x_host, non_blocking=True)
-        if world > 1:
+        if launched:
             dist.broadcast(x_e2e, src=0)
         solve_rows_torch(ctx, x_e2e, k, metric, r0, r1, arith, out=(out_idx, out_dist))
         idx_host.copy_(out_idx, non_blocking=True)
@@ -328,7 +327,7 @@ def main():
     e1.record(stream)
     barrier()
     t2 = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
-    if world > 1:
+    if launched:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     e2e_ms = float(t2.item())
     e2e_value = pairs * args.steps / (e2e_ms / 1e3)
@@ -358,6 +357,12 @@ def main():
         peak_src = f"FP32 SIMT nominal 148 SM x 128 lanes x 2 flop x {sm:.0f} MHz (no measured FP32 peak)"
         bound = "fp32"
 
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists() and not args.n:
+        entry = json.loads(tfile.read_text()).get(args.config)
+        if entry and tensor:
+            traffic = entry["dram_bytes_per_launch"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -371,7 +376,8 @@ def main():
                 "d2h_bytes_per_step": n * klist * 8},
         "gpu_launches": launches,
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes/launch (DRAM, ncu)",
+                     "peak_source": peak_src,
                      "kernel_ms": statistics.mean(sweep_ms),
                      "alg_flop_per_launch": alg_flop},
         "clocks": clk,
@@ -386,7 +392,7 @@ def main():
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "error": str(e)}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if launched:
         dist.destroy_process_group()
     return 0
 
