@@ -31,6 +31,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "sm100_ptx.cuh"
+#include "sweep_common.cuh"
 
 namespace knnb {
 
@@ -81,53 +82,6 @@ struct SweepParams {
     uint64_t* cap_buf;
     uint32_t cap;
 };
-
-// Per-row candidate list: KPL unsorted (y, index) entries in shared memory --
-// a [KPL][LIST_ROWS] float array and a [KPL][LIST_ROWS] index array, so the
-// 32 lanes of a warp touch consecutive words -- plus its maximum, the
-// admission threshold (the reference's heap root, heap.hpp:86-90).  The list
-// keeps the KPL smallest y with ties broken arbitrarily: the completeness
-// proof only needs "every column outside the list has y >= the list maximum".
-// Replacing the maximum and rescanning costs KPL independent shared loads and
-// runs warp-convergently: a warp pays once per column any of its rows admits.
-struct ListMax {
-    float a;
-    uint32_t slot;
-};
-
-__device__ __forceinline__ float lds_f32(uint32_t addr) {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-    return v;
-}
-
-__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
-    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
-}
-
-__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-
-template <int KPL, uint32_t STRIDE>
-__device__ __forceinline__ ListMax list_rescan(uint32_t a_base) {
-    // pass 1: maximum (independent loads, a max tree); pass 2: its slot
-    float m = lds_f32(a_base);
-#pragma unroll 32
-    for (int i = 1; i < KPL; ++i) m = fmaxf(m, lds_f32(a_base + i * STRIDE));
-    uint32_t slot = 0;
-#pragma unroll 32
-    for (int i = KPL - 1; i >= 0; --i) slot = (lds_f32(a_base + i * STRIDE) == m) ? uint32_t(i) : slot;
-    return ListMax{m, slot};
-}
-
-template <int KPL, uint32_t STRIDE>
-__device__ __noinline__ ListMax list_replace_max(uint32_t a_base, uint32_t i_base, uint32_t slot, float a,
-                                                 uint32_t col) {
-    sts_f32(a_base + slot * STRIDE, a);
-    sts_u32(i_base + slot * STRIDE, col);
-    return list_rescan<KPL, STRIDE>(a_base);
-}
 
 // Persistent sweep.  Work item = (column group g, row block rb); every CTA
 // walks g = 0, 1, ... and, inside a group, its row blocks rb = blockIdx.x,
@@ -743,6 +697,26 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         arank[m] = 0;
     }
     __syncwarp();
+    if constexpr (NSEG == 3) {
+        // symmetric sweep: the column-side list was seeded with copies of
+        // row-side entries -- keep the first copy of each key (the list
+        // maxima below still count every copy)
+#pragma unroll
+        for (int m = 0; m < PER; ++m) {
+            const int i = lane + 32 * m;
+            if (i >= KP || ak[m] == kEmptyKey) continue;
+            for (int j = 0; j < i; ++j)
+                if (keys_s[warp][j] == ak[m]) {
+                    ak[m] = kEmptyKey;
+                    break;
+                }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < PER; ++m)
+            if (lane + 32 * m < KP) keys_s[warp][lane + 32 * m] = ak[m];
+        __syncwarp();
+    }
     for (int j = 0; j < KP; ++j) {
         const uint64_t o = keys_s[warp][j];
 #pragma unroll
@@ -1020,6 +994,15 @@ uint32_t tensor_kp_for(uint32_t klist) {
     return c.kpl * c.nseg;
 }
 
+// Symmetric sweep (sym_path.cu): whole problems with k <= 10 and d <= 256,
+// where each tile serves its rows and its columns.  Opt-in (KNN_B200_SYM=1).
+static bool sym_selected(uint32_t n, uint32_t d, uint32_t klist, uint32_t row_begin, uint32_t row_end) {
+    const char* e = getenv("KNN_B200_SYM");
+    if (!e || atoi(e) == 0) return false;
+    const TensorCfg c = tensor_cfg(klist);
+    return c.kpl == 16 && c.nseg == 2 && row_begin == 0 && row_end == n && d <= 256 && n >= 1024;
+}
+
 size_t capture_workspace_bytes(uint32_t m, uint32_t d, uint32_t cap) {
     const uint32_t mpad = (m + TS_BM - 1) / TS_BM * TS_BM;
     const uint32_t kc = (d + 63) / 64;
@@ -1032,7 +1015,11 @@ size_t capture_workspace_bytes(uint32_t m, uint32_t d, uint32_t cap) {
     return b;
 }
 
-size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t rows, uint32_t kp) {
+size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32_t row_end, uint32_t klist,
+                              int sm_count) {
+    const uint32_t rows = row_end - row_begin;
+    const bool sym = sym_selected(n, d, klist, row_begin, row_end);
+    const uint32_t kp = sym ? 48 : tensor_kp_for(klist);
     const uint32_t npad = (n + 255) / 256 * 256;
     const uint32_t kc = (d + 63) / 64;
     size_t b = 0;
@@ -1047,6 +1034,7 @@ size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t rows, uint32_t kp
     add(size_t(rows) * kp * 8);    // cand
     add(size_t(rows) * 4);         // fallback rows
     add(size_t(rows) * 4);         // capture thresholds
+    if (sym) add(sym_workspace_bytes(n, sm_count));
     return b;
 }
 
@@ -1101,6 +1089,7 @@ static cudaError_t launch_rescore(TensorCfg c, const RescoreParams& rp, uint32_t
         break;
     case 32: rescore_kernel<FOLD, 64, 2><<<grid, 256, 0, stream>>>(rp); break;
     case 64: rescore_kernel<FOLD, 64, 1><<<grid, 256, 0, stream>>>(rp); break;
+    case 48: rescore_kernel<FOLD, 48, 3><<<grid, 256, 0, stream>>>(rp); break;  // symmetric: R0 | R1 | C
     default: rescore_kernel<FOLD, 128, 1><<<grid, 256, 0, stream>>>(rp); break;
     }
     return cudaGetLastError();
@@ -1110,8 +1099,9 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     const uint32_t n = a.n, d = a.d, nrows = a.row_end - a.row_begin;
     const uint32_t npad = (n + 255) / 256 * 256;
     const uint32_t kc = (d + 63) / 64;
-    const TensorCfg cfg = tensor_cfg(a.klist);
-    const uint32_t kp = cfg.kpl * cfg.nseg;
+    const bool sym = sym_selected(n, d, a.klist, a.row_begin, a.row_end);
+    const TensorCfg cfg = sym ? TensorCfg{48, 3} : tensor_cfg(a.klist);
+    const uint32_t kp = sym ? 48 : cfg.kpl * cfg.nseg;
     const int cosine = a.fold == kCosine;
     uint8_t* w = static_cast<uint8_t*>(a.workspace);
     auto take = [&](size_t x) {
@@ -1129,6 +1119,7 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     uint64_t* cand = reinterpret_cast<uint64_t*>(take(size_t(nrows) * kp * 8));
     uint32_t* fb_rows = reinterpret_cast<uint32_t*>(take(size_t(nrows) * 4));
     float* fb_thr = reinterpret_cast<float*>(take(size_t(nrows) * 4));
+    void* sym_ws = sym ? take(sym_workspace_bytes(n, a.sm_count)) : nullptr;
     unsigned int* maxabs = reinterpret_cast<unsigned int*>(scal);
     uint32_t* fb_count = reinterpret_cast<uint32_t*>(scal + 4);
     unsigned long long* gmax = reinterpret_cast<unsigned long long*>(scal + 8);
@@ -1164,9 +1155,14 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     SweepParams sp{xh,      alpha,   n,       npad,    kc, a.row_begin, a.row_end, group_tiles, dbg ? atoi(dbg) : 0,
                    cand,    xh,      npad,    nullptr, nullptr, nullptr, 0};
     if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
-    if ((e = launch_sweep(cfg, kc <= uint32_t(TS_MAX_RES_KC), sp, nrows, st)) != cudaSuccess) return e;
+    if (sym) {
+        if ((e = run_sym_sweep(xh, alpha, n, npad, kc, cand, sym_ws, a.sm_count, st)) != cudaSuccess) return e;
+        launches += 3;
+    } else {
+        if ((e = launch_sweep(cfg, kc <= uint32_t(TS_MAX_RES_KC), sp, nrows, st)) != cudaSuccess) return e;
+        ++launches;
+    }
     if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
-    ++launches;
 
     RescoreParams rp{a.X,  n,         d,          a.klist,  kp,       a.row_begin, a.row_end, cand,
                      alpha, rho,      xnorm,      gmax,     maxabs,   a.fold,      a.out_sqrt, a.out_index,
