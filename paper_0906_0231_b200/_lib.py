@@ -7,10 +7,13 @@ Loading fails loudly when it is missing: there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libknn_b200.so"
+# KNN_B200_LIB: an alternative in-tree build of the same library (tuning
+# experiments); the default is the library `make` builds.
+LIB_PATH = Path(os.environ.get("KNN_B200_LIB") or Path(__file__).resolve().parent / "lib" / "libknn_b200.so")
 
 # Every exported symbol of include/knn_b200.h (checked by the CPU test suite).
 EXPORTS = (

@@ -3,33 +3,45 @@
 // rows"; the reference's k_smallest_push offers each tile entry to both
 // endpoints, src/select.cpp:60-91).
 //
-// Geometry.  P blocks of 128 query rows (UMMA M), Q tiles of 256 columns
-// (UMMA N); tile(i) = i / 256.  An unordered pair {i, j} with tile(i) <
-// tile(j) is computed once, in the tile (block(i), tile(j)): the row side
-// offers j to i's list, the column side offers i to j's list.  Pairs inside
-// one tile are handled by a diagonal prepass with the row side only (both
-// directions are rows there).
+// Geometry.  nrb blocks of 128 query rows (UMMA M), T tiles of 256 columns
+// (UMMA N); tile(i) = i / 256, so tile t holds blocks 2t and 2t+1.  The G
+// persistent CTAs take the blocks in waves: wave w = blocks [wG, wG+Gw), CTA
+// c holds block wG+c (G is even, so a wave's rows are whole tiles
+// [t_lo, t_hi]).  Every unordered pair is covered once:
+//   * prepass (diag launch): each block against its own tile, row side only,
+//     self excluded -- both directions are rows there;
+//   * band: each block against the other tiles of its own wave, row side
+//     only (both directions again, since every block of the wave does it);
+//   * rectangle: each block against every later tile (t > t_hi), both sides:
+//     the row side offers column j to row i's lists, the column side offers
+//     row i to row j's column-side list.
 //
-// Ownership without locks.
-//   * Row-side lists (two 16-entry segments per row) live in the registers of
-//     the CTA holding the row's block for its whole sweep.
-//   * Column-side lists (one 16-entry list per row) live in global memory and
-//     are loaded into shared memory for one visit of a tile.  The visitors of
-//     tile q are the blocks p = 0 .. 2q-1; visitor p waits until the tile's
-//     version counter reads p and bumps it when done, so visits are exclusive
-//     and ordered.  Each CTA takes its blocks in increasing order
-//     (boustrophedon waves, the reference's lane_of_row, schedule.cpp:40-44,
-//     to balance the triangle), so the lowest unfinished visit is always
-//     runnable: no deadlock.
-//   * Column-side candidates found by the row-owning threads are queued per
-//     column in shared memory and merged by one thread per column.
-//   * A prepass sweeps each block's own tile (row side, self excluded) and
-//     seeds the column-side list of every row with a copy of its row-side
-//     top 16, so column-side thresholds start finite (the rescore drops the
-//     duplicate copies; list maxima still bound their exclusions).
+// Ownership.
+//   * Row-side lists (two 16-entry segments per row, by column half) live in
+//     registers of the CTA holding the block, for the whole wave.
+//   * Column-side lists (one 16-entry list per row) live in global memory in
+//     shared-memory layout ([tile][slot][256] y and index planes).  A visit
+//     filters the tile's columns against published thresholds (a stale
+//     threshold is an upper bound: lists only improve), queues candidates in
+//     shared memory, and merges them into the tile's lists: a list-agent warp
+//     bulk-loads the tile's y plane (double-buffered) once a per-tile version
+//     counter says the previous visitor is done, the merging threads write
+//     changed entries through to global memory, and the agent bumps the
+//     version -- the visits of a tile are exclusive and in a fixed order.
+//   * Rectangle steps are rotated (CTA r visits tile (s + 2r) mod L at step
+//     s), so consecutive visitors of a tile are two steps apart: the agent's
+//     version wait, list load and store overlap the sweep instead of forming a
+//     lock-step chain; the 2G-tile window still fits in L2.  Late waves whose
+//     rectangle is narrower than 2G tiles visit in plain order (rank = r).
+// Deadlock freedom: releases wait only on the CTA's own merge, and a load
+// waits only on the tile's previous visitor, which sits at a strictly earlier
+// (wave, step) -- or, in plain order, a smaller rank.  Modelled for many n by
+// tools/sym_schedule_check.py (tests/test_sym_schedule.py).
 // Completeness: every column not in one of a row's three lists was rejected
-// by a list whose maximum only decreases; the rescore's proof uses the
-// smallest maximum over full lists.
+// by (or evicted from) the list it was offered to, whose maximum only
+// decreases; the rescore's proof uses the smallest maximum over full lists.
+// The prepass seeds each column-side list with a copy of the row's top 16,
+// so thresholds start finite; the rescore drops the duplicate copies.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -46,17 +58,17 @@ constexpr int SY_BM = 128;
 constexpr int SY_BN = 256;
 constexpr int SY_KPL = 16;
 constexpr int SY_EW = 8;
-constexpr int SY_THREADS = 64 + 32 * SY_EW;
-constexpr int SY_QC = 12;    // shared queue entries per column
+constexpr int SY_AGENT_WARP = 2 + SY_EW;
+constexpr int SY_THREADS = 64 + 32 * SY_EW + 32;
+constexpr int SY_QC = 8;     // shared queue entries per column
 constexpr int SY_OVF = 128;  // global overflow entries per column (a block has 128 rows)
 constexpr uint32_t SY_A_CHUNK = SY_BM * 128;
 constexpr uint32_t SY_B_CHUNK = SY_BN * 128;
 constexpr int SY_STAGES = 3;
-constexpr uint32_t SY_A_BYTES = 4 * SY_A_CHUNK;  // d <= 256: the block's rows stay resident
-constexpr uint32_t SY_CL_BYTES = SY_KPL * SY_BN * 8;          // column lists (y, idx) [16][256]
-constexpr uint32_t SY_Q_BYTES = SY_QC * SY_BN * 8;            // queues (y, row) [QC][256]
-constexpr uint32_t SY_SMEM = 1024 + SY_A_BYTES + SY_STAGES * SY_B_CHUNK + SY_CL_BYTES + 2 * SY_BN * 4 +
-                             SY_Q_BYTES + SY_BN * 4 + 256;
+constexpr uint32_t SY_A_BYTES = 4 * SY_A_CHUNK;            // d <= 256: the block's rows stay resident
+constexpr uint32_t SY_LIST_PLANE = SY_KPL * SY_BN * 4;     // one [16][256] y plane (double-buffered)
+constexpr uint32_t SY_SMEM = 1024 + SY_A_BYTES + SY_STAGES * SY_B_CHUNK + 2 * SY_LIST_PLANE +
+                             2 * SY_QC * SY_BN * 4 + 2 * SY_BN * 4 + 256;
 static_assert(SY_SMEM <= 232448, "symmetric sweep shared memory");
 
 struct SymParams {
@@ -64,12 +76,14 @@ struct SymParams {
     const float* alpha;
     uint32_t n, npad, kc;
     uint32_t nrb, ntiles;
-    int diag;              // 1: prepass over each block's own tile
-    uint64_t* cand;        // [nrb*128][48]: row-side segments at [0,32); column list copied to [32,48) later
-    uint64_t* cstate;      // [ntiles*256][16] column-side lists
-    uint32_t* version;     // [ntiles] completed visits
-    uint64_t* overflow;    // [gridDim][256][SY_OVF]
-    int dbg;               // dev timing knob (KNN_B200_SYM_DEBUG): 1 = no visit ordering (racy), 2 = no column side
+    int diag;            // 1: prepass over each block's own tile
+    uint64_t* cand;      // [nrb*128][48]: row-side segments at [0,32); column list copied to [32,48) later
+    float* cla;          // [ntiles][16][256] column-side list y
+    uint32_t* cli;       // [ntiles][16][256] column-side list index
+    float* thr_pub;      // [ntiles*256] published column-side prefilter thresholds
+    uint32_t* version;   // [ntiles] completed rectangle visits
+    uint64_t* overflow;  // [gridDim][256][SY_OVF]
+    int dbg;             // dev timing knob (KNN_B200_SYM_DEBUG): 2 = no column side, 3 = also no rotation (wrong results)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
@@ -84,25 +98,54 @@ __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
 
 __device__ __forceinline__ void epi_barrier() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-// Block taken by CTA c in wave w (boustrophedon, schedule.cpp:40-44).
-__device__ __forceinline__ uint32_t sym_block(uint32_t w, uint32_t c, uint32_t G) {
-    return w * G + ((w & 1) ? G - 1 - c : c);
-}
+// One CTA's visits in one wave.
+struct SymWave {
+    uint32_t b, r, Gw, t_lo, t_hi, nband, L, base;
+    bool rot, live;
+    __device__ SymWave(const SymParams& p, uint32_t w, uint32_t c) {
+        const uint32_t G = gridDim.x;
+        Gw = p.nrb - w * G < G ? p.nrb - w * G : G;
+        r = c;
+        b = w * G + c;
+        live = c < Gw;
+        t_lo = (w * G) / 2;
+        t_hi = (w * G + Gw - 1) / 2;
+        nband = t_hi - t_lo;  // the wave's tiles except the block's own
+        L = p.ntiles > t_hi + 1 ? p.ntiles - t_hi - 1 : 0;
+        rot = 2 * Gw <= L && p.dbg != 3;
+        base = G * w;
+    }
+    __device__ uint32_t visits(int diag) const { return diag ? 1u : nband + L; }
+    __device__ uint32_t tile(int diag, uint32_t j) const {
+        if (diag) return b / 2;
+        if (j < nband) {
+            const uint32_t t = t_lo + j;
+            return t >= b / 2 ? t + 1 : t;
+        }
+        const uint32_t s = j - nband;
+        return t_hi + 1 + (rot ? (s + 2 * r) % L : s);
+    }
+    // position of this CTA's visit among the wave's visits of rectangle tile t
+    __device__ uint32_t rank(uint32_t t) const {
+        if (!rot) return base + r;
+        const uint32_t qq = t - t_hi - 1;
+        const uint32_t c1 = qq / 2 < Gw - 1 ? qq / 2 : Gw - 1;
+        return base + (r <= c1 ? c1 - r : c1 + 1 + (Gw - 1 - r));
+    }
+};
 
 __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* a_smem = smem;
     uint8_t* stage_smem = smem + SY_A_BYTES;
-    float* cl_a = reinterpret_cast<float*>(stage_smem + SY_STAGES * SY_B_CHUNK);  // [16][256]
-    uint32_t* cl_i = reinterpret_cast<uint32_t*>(cl_a + SY_KPL * SY_BN);           // [16][256]
-    float* thr_c = reinterpret_cast<float*>(cl_i + SY_KPL * SY_BN);                // [256]
-    float* thr_p = thr_c + SY_BN;                                                   // [256] prefilter
-    float* q_y = thr_p + SY_BN;                                                     // [QC][256]
+    float* cl_a = reinterpret_cast<float*>(stage_smem + SY_STAGES * SY_B_CHUNK);  // [2][16][256] y planes
+    float* q_y = cl_a + 2 * SY_KPL * SY_BN;                                         // [QC][256]
     uint32_t* q_r = reinterpret_cast<uint32_t*>(q_y + SY_QC * SY_BN);              // [QC][256]
-    uint32_t* q_n = q_r + SY_QC * SY_BN;                                            // [256]
+    float* thr_p = reinterpret_cast<float*>(q_r + SY_QC * SY_BN);                  // [256]
+    uint32_t* q_n = reinterpret_cast<uint32_t*>(thr_p + SY_BN);                    // [256]
     uint64_t* bars = reinterpret_cast<uint64_t*>(q_n + SY_BN);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * SY_STAGES + 6);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * SY_STAGES + 9);
     constexpr int S = SY_STAGES;
 
     const int warp = threadIdx.x >> 5;
@@ -116,17 +159,8 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
     auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * S + 2 + b); };
     const uint32_t afull_bar = bar0 + 8u * (2 * S + 4);
     const uint32_t aempty_bar = bar0 + 8u * (2 * S + 5);
-    // tiles of block pb: the diagonal tile (prepass) or every tile above it
-    auto tile_range = [&](uint32_t pb, uint32_t& q0, uint32_t& q1) {
-        const uint32_t qd = pb / 2;
-        if (p.diag) {
-            q0 = qd;
-            q1 = qd + 1;
-        } else {
-            q0 = qd + 1;
-            q1 = p.ntiles > q0 ? p.ntiles : q0;
-        }
-    };
+    auto lfull_bar = [&](int b) { return bar0 + 8u * (2 * S + 6 + b); };  // column-list y plane loaded
+    const uint32_t lmerged_bar = bar0 + 8u * (2 * S + 8);  // column lists merged (8 epilogue warps)
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < S; ++s) {
@@ -139,6 +173,9 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
         }
         ptx::mbar_init(afull_bar, 1);
         ptx::mbar_init(aempty_bar, 1);
+        ptx::mbar_init(lfull_bar(0), 1);
+        ptx::mbar_init(lfull_bar(1), 1);
+        ptx::mbar_init(lmerged_bar, SY_EW);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 2 * SY_BN);
@@ -146,6 +183,7 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const bool colside = !p.diag && p.dbg != 2 && p.dbg != 3;
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
@@ -153,18 +191,18 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
             int stage = 0;
             uint32_t phase = 0, a_phase = 0;
             for (uint32_t w = 0; w < waves; ++w) {
-                const uint32_t pb = sym_block(w, c, G);
-                if (pb >= p.nrb) continue;
-                uint32_t q0, q1;
-                tile_range(pb, q0, q1);
-                if (q0 >= q1) continue;
+                const SymWave sw(p, w, c);
+                if (!sw.live) continue;
+                const uint32_t nv = sw.visits(p.diag);
+                if (nv == 0) continue;
                 ptx::mbar_wait(aempty_bar, a_phase ^ 1);
                 ptx::mbar_arrive_expect_tx(afull_bar, p.kc * SY_A_CHUNK);
                 for (uint32_t kc = 0; kc < p.kc; ++kc)
                     ptx::bulk_g2s(ptx::smem_u32(a_smem + kc * SY_A_CHUNK),
-                                  p.xh + (size_t(kc) * p.npad + size_t(pb) * SY_BM) * 128, SY_A_CHUNK, afull_bar);
+                                  p.xh + (size_t(kc) * p.npad + size_t(sw.b) * SY_BM) * 128, SY_A_CHUNK, afull_bar);
                 a_phase ^= 1;
-                for (uint32_t q = q0; q < q1; ++q)
+                for (uint32_t j = 0; j < nv; ++j) {
+                    const uint32_t q = sw.tile(p.diag, j);
                     for (uint32_t kc = 0; kc < p.kc; ++kc) {
                         ptx::mbar_wait(empty_bar(stage), phase ^ 1);
                         ptx::mbar_arrive_expect_tx(full_bar(stage), SY_B_CHUNK);
@@ -176,6 +214,7 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
                             phase ^= 1;
                         }
                     }
+                }
             }
         }
     } else if (warp == 1) {
@@ -185,14 +224,13 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
             int stage = 0;
             uint32_t phase = 0, a_phase = 0, tcount = 0;
             for (uint32_t w = 0; w < waves; ++w) {
-                const uint32_t pb = sym_block(w, c, G);
-                if (pb >= p.nrb) continue;
-                uint32_t q0, q1;
-                tile_range(pb, q0, q1);
-                if (q0 >= q1) continue;
+                const SymWave sw(p, w, c);
+                if (!sw.live) continue;
+                const uint32_t nv = sw.visits(p.diag);
+                if (nv == 0) continue;
                 ptx::mbar_wait(afull_bar, a_phase);
                 a_phase ^= 1;
-                for (uint32_t q = q0; q < q1; ++q, ++tcount) {
+                for (uint32_t j = 0; j < nv; ++j, ++tcount) {
                     const uint32_t b = tcount & 1, use = tcount >> 1;
                     ptx::mbar_wait(tempty_bar(b), (use & 1) ^ 1);
                     ptx::tc_fence_after();
@@ -217,13 +255,65 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
                 ptx::mma_commit(aempty_bar);
             }
         }
+    } else if (warp == SY_AGENT_WARP) {
+        // ---------------- list agent: ordered, exclusive rectangle visits ----------------
+        // Visit v's y plane is loaded into buffer v % 2 once the tile's
+        // previous visitor has released it; visit v is released as soon as
+        // the epilogue has merged it (the merging threads write changed
+        // entries straight to global memory and fence).  Releases never wait
+        // on other CTAs, so the waits-for graph follows (wave, step, rank)
+        // strictly downwards: no deadlock.
+        if (lane == 0 && colside) {
+            uint32_t merged_phase = 0, vbase = 0;
+            for (uint32_t w = 0; w < waves; ++w) {
+                const SymWave sw(p, w, c);
+                if (!sw.live || sw.L == 0) continue;
+                uint32_t nload = 0, nrel = 0, spins = 0, nap = 32;
+                uint32_t lt = sw.tile(0, sw.nband), lver = sw.rank(lt);  // next load
+                uint32_t rt = lt, rver = lver;                               // next release
+                while (nrel < sw.L) {
+                    bool progressed = false;
+                    if (nload < sw.L && nload < nrel + 2 && ld_acquire_u32(p.version + lt) == lver) {
+                        ptx::fence_proxy_async_global();
+                        const uint32_t v = vbase + nload;
+                        ptx::mbar_arrive_expect_tx(lfull_bar(v & 1), SY_LIST_PLANE);
+                        ptx::bulk_g2s(ptx::smem_u32(cl_a + (v & 1) * SY_KPL * SY_BN),
+                                      p.cla + size_t(lt) * SY_KPL * SY_BN, SY_LIST_PLANE, lfull_bar(v & 1));
+                        if (++nload < sw.L) {
+                            lt = sw.tile(0, sw.nband + nload);
+                            lver = sw.rank(lt);
+                        }
+                        progressed = true;
+                    }
+                    if (nrel < nload && ptx::mbar_test(lmerged_bar, merged_phase)) {
+                        merged_phase ^= 1;
+                        __threadfence();
+                        st_release_u32(p.version + rt, rver + 1);
+                        if (++nrel < sw.L) {
+                            rt = sw.tile(0, sw.nband + nrel);
+                            rver = sw.rank(rt);
+                        }
+                        progressed = true;
+                    }
+                    if (progressed) {
+                        spins = 0;
+                        nap = 32;
+                    } else {
+                        __nanosleep(nap);  // back off: this warp shares a scheduler with epilogue warps
+                        nap = nap < 512 ? 2 * nap : 512;
+                        if (++spins == (1u << 25)) __trap();  // ordering bug: fail, do not hang
+                    }
+                }
+                vbase += sw.L;
+            }
+        }
     } else {
         // ---------------- epilogue: 8 warps, thread = (row of the block, column half) ----------------
         const int ew = warp - 2;
         const int quad = warp & 3;
         const int seg = ew / 4;
         const int rl = quad * 32 + lane;
-        const uint32_t et = uint32_t(ew) * 32 + lane;  // 0..255: column owner in flushes
+        const uint32_t et = uint32_t(ew) * 32 + lane;  // 0..255: column owner in merges
         const float kInf = __int_as_float(0x7f800000);
         const uint32_t lane_addr = tmem + (uint32_t(quad * 32) << 16);
         const uint32_t seg0 = seg * (SY_BN / 2);
@@ -231,6 +321,7 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
         float la[SY_KPL];
         uint32_t lx[SY_KPL];
         ListMax thr{kInf, 0};
+        uint32_t vcount = 0;  // rectangle visits so far (list buffer and phase)
         auto reg_argmax = [&]() -> ListMax {
             float mv[8];
             uint32_t ms[8];
@@ -270,13 +361,17 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
                 bt[4 * q4 + 3] = f.w;
             }
         };
+        // prefetched published threshold of this thread's column in the next rectangle visit
+        auto thr_fetch = [&](uint32_t t) -> float {
+            const uint32_t crow = t * SY_BN + et;
+            return crow < p.n ? __ldcg(p.thr_pub + crow) : -kInf;
+        };
         uint32_t tcount = 0;
         for (uint32_t w = 0; w < waves; ++w) {
-            const uint32_t pb = sym_block(w, c, G);
-            if (pb >= p.nrb) continue;
-            uint32_t q0, q1;
-            tile_range(pb, q0, q1);
-            const uint32_t row = pb * SY_BM + rl;
+            const SymWave sw(p, w, c);
+            if (!sw.live) continue;
+            const uint32_t nv = sw.visits(p.diag);
+            const uint32_t row = sw.b * SY_BM + rl;
             const bool valid = row < p.n;
             uint64_t* rstate = p.cand + size_t(row) * 48 + seg * SY_KPL;
 #pragma unroll
@@ -293,43 +388,22 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
             // fl(alpha_i - 2 dot) < thrC_j: y' >= -alpha_j bounds |y'| and the
             // slack covers both roundings (2^-24 each) many times over.
             const float c_lim = valid ? __fmul_rn(-alpha_i, 1.0f - 1e-6f) : -kInf;
-            for (uint32_t q = q0; q < q1; ++q, ++tcount) {
+            float thr_next = (colside && sw.L) ? thr_fetch(sw.tile(0, sw.nband)) : -kInf;
+            for (uint32_t j = 0; j < nv; ++j, ++tcount) {
+                const uint32_t q = sw.tile(p.diag, j);
                 const uint32_t b = tcount & 1, use = tcount >> 1;
-                const bool sym = !p.diag && p.dbg != 2;
+                const bool sym = colside && j >= sw.nband;
                 if (sym) {
-                    // exclusive, ordered visit of tile q (visitors 0 .. 2q-1)
-                    if (et == 0 && p.dbg != 1) {
-                        uint32_t spins = 0;
-                        while (ld_acquire_u32(p.version + q) != pb) {
-                            __nanosleep(64);
-                            if (++spins == (1u << 27)) __trap();  // ordering bug: fail, do not hang
-                        }
-                    }
-                    epi_barrier();
-                    const uint32_t crow = q * SY_BN + et;
-                    const uint64_t* cs = p.cstate + size_t(crow) * SY_KPL;
-                    float cm = -kInf;
-#pragma unroll
-                    for (int s = 0; s < SY_KPL; ++s) {
-                        const uint64_t key = __ldcg(reinterpret_cast<const unsigned long long*>(cs + s));
-                        const float a = key == kEmptyKey ? kInf : ordered_to_float(uint32_t(key >> 32));
-                        cl_a[s * SY_BN + et] = a;
-                        cl_i[s * SY_BN + et] = uint32_t(key);
-                        cm = fmaxf(cm, a);
-                    }
-                    const bool live = crow < p.n;
-                    thr_c[et] = live ? cm : -kInf;
-                    thr_p[et] = !live ? -kInf
-                                : cm == kInf ? kInf
-                                             : __fadd_rn(cm, 1e-6f * __fadd_rn(fabsf(cm), p.alpha[crow]));
+                    thr_p[et] = thr_next;
                     q_n[et] = 0;
                     epi_barrier();
+                    if (j + 1 < nv) thr_next = thr_fetch(sw.tile(0, j + 1));
                 }
                 ptx::mbar_wait(tfull_bar(b), use & 1);
                 ptx::tc_fence_after();
                 const uint32_t cbase = q * SY_BN + seg0;
                 const uint32_t taddr = lane_addr + b * SY_BN + seg0;
-                auto process = [&](const uint32_t (&v)[32], const float (&bt)[32], uint32_t col0, uint32_t cloc) {
+                auto process_row = [&](const uint32_t (&v)[32], const float (&bt)[32], uint32_t col0) {
                     // row side: y = fl(beta_j - 2 dot)
                     float m[16];
 #pragma unroll
@@ -368,8 +442,10 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
                             }
                         }
                     }
-                    if (!sym) return;
-                    // column side: candidate row i for column j's list, y' = fl(alpha_i - 2 dot)
+                };
+                // column side: candidate row i for column j's list, y' = fl(alpha_i - 2 dot)
+                // (a second pass over TMEM keeps each pass's registers at the row pass's level)
+                auto process_col = [&](const uint32_t (&v)[32], uint32_t cloc) {
                     float tc[32];
                     load_vec32(thr_p + cloc, tc);
                     float zm[16];
@@ -408,7 +484,7 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
                             for (int e = 0; e < 2; ++e) {
                                 const uint32_t jl = cloc + 2 * i + e;  // tile-local column
                                 const float yv = e ? y2.y : y2.x;
-                                if (yv < thr_c[jl]) {
+                                if (yv < thr_p[jl]) {
                                     uint32_t at;
                                     asm volatile("atom.shared.add.u32 %0, [%1], 1;"
                                                  : "=r"(at)
@@ -426,34 +502,59 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
                         }
                     }
                 };
+                auto release_tmem = [&]() {
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(tempty_bar(b));
+                };
                 uint32_t va[32], vb[32];
-                float ba[32], bb[32];
-                ptx::tmem_ld_32x32b_x32(taddr, va);
-                load_vec32(p.alpha + cbase, ba);
+                {
+                    float ba[32], bb[32];
+                    ptx::tmem_ld_32x32b_x32(taddr, va);
+                    load_vec32(p.alpha + cbase, ba);
 #pragma unroll 1
-                for (int c0 = 0; c0 < SY_BN / 2; c0 += 64) {
-                    ptx::tmem_wait_ld();
-                    ptx::tmem_ld_32x32b_x32(taddr + c0 + 32, vb);
-                    load_vec32(p.alpha + cbase + c0 + 32, bb);
-                    process(va, ba, cbase + c0, seg0 + c0);
-                    ptx::tmem_wait_ld();
-                    if (c0 + 64 < SY_BN / 2) {
-                        ptx::tmem_ld_32x32b_x32(taddr + c0 + 64, va);
-                        load_vec32(p.alpha + cbase + c0 + 64, ba);
-                    } else {
-                        ptx::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(tempty_bar(b));
+                    for (int c0 = 0; c0 < SY_BN / 2; c0 += 64) {
+                        ptx::tmem_wait_ld();
+                        ptx::tmem_ld_32x32b_x32(taddr + c0 + 32, vb);
+                        load_vec32(p.alpha + cbase + c0 + 32, bb);
+                        process_row(va, ba, cbase + c0);
+                        ptx::tmem_wait_ld();
+                        if (c0 + 64 < SY_BN / 2) {
+                            ptx::tmem_ld_32x32b_x32(taddr + c0 + 64, va);
+                            load_vec32(p.alpha + cbase + c0 + 64, ba);
+                        } else if (sym) {
+                            ptx::tmem_ld_32x32b_x32(taddr, va);  // column pass, first slice
+                        } else {
+                            release_tmem();
+                        }
+                        process_row(vb, bb, cbase + c0 + 32);
                     }
-                    process(vb, bb, cbase + c0 + 32, seg0 + c0 + 32);
                 }
                 if (sym) {
-                    epi_barrier();
-                    // flush: thread et owns column et of the tile (row crow's list)
+#pragma unroll 1
+                    for (int c0 = 0; c0 < SY_BN / 2; c0 += 64) {
+                        ptx::tmem_wait_ld();
+                        ptx::tmem_ld_32x32b_x32(taddr + c0 + 32, vb);
+                        process_col(va, seg0 + c0);
+                        ptx::tmem_wait_ld();
+                        if (c0 + 64 < SY_BN / 2) ptx::tmem_ld_32x32b_x32(taddr + c0 + 64, va);
+                        else release_tmem();
+                        process_col(vb, seg0 + c0 + 32);
+                    }
+                }
+                if (sym) {
+                    epi_barrier();  // every candidate queued
+                    const uint32_t lb = vcount & 1;
+                    ptx::mbar_wait(lfull_bar(lb), (vcount >> 1) & 1);
+                    ++vcount;
+                    // merge: thread et owns column et of the tile (row crow's list)
                     const uint32_t crow = q * SY_BN + et;
                     if (crow < p.n) {
-                        const uint32_t a_base = ptx::smem_u32(cl_a + et), i_base = ptx::smem_u32(cl_i + et);
+                        const uint32_t a_base = ptx::smem_u32(cl_a + lb * SY_KPL * SY_BN + et);
+                        float* ga = p.cla + size_t(q) * SY_KPL * SY_BN + et;
+                        uint32_t* gi = p.cli + size_t(q) * SY_KPL * SY_BN + et;
                         ListMax cmx = list_rescan<SY_KPL, SY_BN * 4>(a_base);
+                        bool wrote = false;
                         const uint32_t nq = min(q_n[et], uint32_t(SY_QC + SY_OVF));
                         for (uint32_t e = 0; e < nq; ++e) {
                             float yv;
@@ -466,21 +567,22 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
                                 yv = __uint_as_float(uint32_t(k >> 32));
                                 r = uint32_t(k);
                             }
-                            if (yv < cmx.a) cmx = list_replace_max<SY_KPL, SY_BN * 4>(a_base, i_base, cmx.slot, yv, r);
+                            if (yv < cmx.a) {
+                                sts_f32(a_base + cmx.slot * (SY_BN * 4), yv);
+                                ga[cmx.slot * SY_BN] = yv;
+                                gi[cmx.slot * SY_BN] = r;
+                                wrote = true;
+                                cmx = list_rescan<SY_KPL, SY_BN * 4>(a_base);
+                            }
                         }
-                        uint64_t* cs = p.cstate + size_t(crow) * SY_KPL;
-#pragma unroll
-                        for (int s = 0; s < SY_KPL; ++s) {
-                            const uint32_t ci = cl_i[s * SY_BN + et];
-                            cs[s] = ci == 0xffffffffu ? kEmptyKey
-                                                      : (uint64_t(float_to_ordered(cl_a[s * SY_BN + et])) << 32) | ci;
-                        }
+                        if (wrote) __threadfence();  // changed entries before the agent's release
+                        if (nq)
+                            p.thr_pub[crow] = cmx.a == kInf ? kInf
+                                                            : __fadd_rn(cmx.a, 1e-6f * __fadd_rn(fabsf(cmx.a),
+                                                                                                 p.alpha[crow]));
                     }
-                    epi_barrier();
-                    if (et == 0) {
-                        __threadfence();
-                        st_release_u32(p.version + q, pb + 1);
-                    }
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(lmerged_bar);
                 }
             }
             if (valid) {
@@ -491,8 +593,8 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
             if (p.diag) {
                 // seed the row's column-side list with its row-side top 16
                 // (both halves of the row meet in shared memory)
-                float* sa = cl_a;        // [2][16][128] scratch
-                uint32_t* si = cl_i;
+                float* sa = cl_a;  // [2][16][128] scratch
+                uint32_t* si = reinterpret_cast<uint32_t*>(cl_a + SY_KPL * SY_BN);
 #pragma unroll
                 for (int s = 0; s < SY_KPL; ++s) {
                     sa[(seg * SY_KPL + s) * SY_BM + rl] = la[s];
@@ -507,7 +609,10 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
                         va2[s] = sa[s * SY_BM + rl];
                         vi2[s] = si[s * SY_BM + rl];
                     }
-                    uint64_t* cs = p.cstate + size_t(row) * SY_KPL;
+                    const uint32_t t = row / SY_BN, pos = row % SY_BN;
+                    float* ga = p.cla + size_t(t) * SY_KPL * SY_BN + pos;
+                    uint32_t* gi = p.cli + size_t(t) * SY_KPL * SY_BN + pos;
+                    float mx = -kInf;
                     // 16 smallest of 32 (repeated minimum extraction)
                     for (int s = 0; s < SY_KPL; ++s) {
                         float bv = va2[0];
@@ -525,8 +630,12 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
                             va2[t2] = t2 == best ? kInf : va2[t2];
                             vi2[t2] = t2 == best ? 0xfffffffeu : vi2[t2];
                         }
-                        cs[s] = bi >= 0xfffffffeu ? kEmptyKey : (uint64_t(float_to_ordered(bv)) << 32) | bi;
+                        const bool empty = bi >= 0xfffffffeu;
+                        ga[s * SY_BN] = empty ? kInf : bv;
+                        gi[s * SY_BN] = empty ? 0xffffffffu : bi;
+                        mx = fmaxf(mx, empty ? kInf : bv);
                     }
+                    p.thr_pub[row] = mx == kInf ? kInf : __fadd_rn(mx, 1e-6f * __fadd_rn(fabsf(mx), p.alpha[row]));
                 }
                 epi_barrier();
             }
@@ -541,20 +650,24 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
 }
 
 // cand[row][32..48) = the row's column-side list
-__global__ void sym_concat_kernel(uint64_t* cand, const uint64_t* cstate, uint32_t n) {
+__global__ void sym_concat_kernel(uint64_t* cand, const float* cla, const uint32_t* cli, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n * SY_KPL) return;
     const uint32_t row = i / SY_KPL, s = i % SY_KPL;
-    cand[size_t(row) * 48 + 32 + s] = cstate[size_t(row) * SY_KPL + s];
+    const size_t at = size_t(row / SY_BN) * SY_KPL * SY_BN + size_t(s) * SY_BN + row % SY_BN;
+    const uint32_t ci = cli[at];
+    cand[size_t(row) * 48 + 32 + s] = ci == 0xffffffffu ? kEmptyKey : make_key(cla[at], ci);
 }
 
 size_t sym_workspace_bytes(uint32_t n, int sm_count) {
     const uint32_t ntiles = (n + SY_BN - 1) / SY_BN;
     size_t b = 0;
     auto add = [&](size_t x) { b += (x + 255) / 256 * 256; };
-    add(size_t(ntiles) * SY_BN * SY_KPL * 8);        // cstate
-    add(size_t(ntiles) * 4);                          // versions
-    add(size_t(sm_count) * SY_BN * SY_OVF * 8);      // overflow queues
+    add(size_t(ntiles) * SY_BN * SY_KPL * 4);     // cla
+    add(size_t(ntiles) * SY_BN * SY_KPL * 4);     // cli
+    add(size_t(ntiles) * SY_BN * 4);              // thr_pub
+    add(size_t(ntiles) * 4);                      // versions
+    add(size_t(sm_count) * SY_BN * SY_OVF * 8);  // overflow queues
     return b;
 }
 
@@ -568,7 +681,9 @@ cudaError_t run_sym_sweep(const uint8_t* xh, const float* alpha, uint32_t n, uin
         w += (x + 255) / 256 * 256;
         return q;
     };
-    uint64_t* cstate = reinterpret_cast<uint64_t*>(take(size_t(ntiles) * SY_BN * SY_KPL * 8));
+    float* cla = reinterpret_cast<float*>(take(size_t(ntiles) * SY_BN * SY_KPL * 4));
+    uint32_t* cli = reinterpret_cast<uint32_t*>(take(size_t(ntiles) * SY_BN * SY_KPL * 4));
+    float* thr_pub = reinterpret_cast<float*>(take(size_t(ntiles) * SY_BN * 4));
     uint32_t* version = reinterpret_cast<uint32_t*>(take(size_t(ntiles) * 4));
     uint64_t* overflow = reinterpret_cast<uint64_t*>(take(size_t(sm_count) * SY_BN * SY_OVF * 8));
     cudaError_t e;
@@ -576,18 +691,22 @@ cudaError_t run_sym_sweep(const uint8_t* xh, const float* alpha, uint32_t n, uin
         cudaSuccess)
         return e;
     if ((e = cudaMemsetAsync(version, 0, size_t(ntiles) * 4, st)) != cudaSuccess) return e;
-    const uint32_t grid = nrb < uint32_t(sm_count) ? nrb : uint32_t(sm_count);
+    // persistent: one CTA per SM; an even count when there is more than one
+    // wave, so every wave's rows are whole tiles
+    uint32_t grid = nrb < uint32_t(sm_count) ? nrb : uint32_t(sm_count);
+    if (grid < nrb) grid &= ~1u;
     const char* dbg = getenv("KNN_B200_SYM_DEBUG");
-    SymParams sp{xh, alpha, n, npad, kc, nrb, ntiles, 1, cand, cstate, version, overflow, dbg ? atoi(dbg) : 0};
-    tensor_sym_kernel<<<grid, SY_THREADS, SY_SMEM, st>>>(sp);  // diagonal prepass
+    SymParams sp{xh, alpha, n, npad, kc, nrb, ntiles, 1, cand, cla, cli, thr_pub, version, overflow,
+                 dbg ? atoi(dbg) : 0};
+    tensor_sym_kernel<<<grid, SY_THREADS, SY_SMEM, st>>>(sp);  // prepass: own tiles, seeds column lists
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     sp.diag = 0;
-    // every CTA spins on other CTAs' visits: all must be resident (one per SM)
+    // CTAs wait on each other's tile visits: all must be resident (one per SM)
     void* args[] = {&sp};
     if ((e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tensor_sym_kernel), dim3(grid), dim3(SY_THREADS),
                                          args, SY_SMEM, st)) != cudaSuccess)
         return e;
-    sym_concat_kernel<<<(n * SY_KPL + 255) / 256, 256, 0, st>>>(cand, cstate, n);
+    sym_concat_kernel<<<(n * SY_KPL + 255) / 256, 256, 0, st>>>(cand, cla, cli, n);
     return cudaGetLastError();
 }
 

@@ -51,12 +51,15 @@ struct TSLayout {
     static constexpr uint32_t STAGE = B_CHUNK + (ARES ? 0 : TS_A_CHUNK);
     static constexpr uint32_t A_BYTES = ARES ? TS_MAX_RES_KC * TS_A_CHUNK : 0;
     static constexpr uint32_t LIST_ROWS = TS_BM * NSEG;                 // list "columns"
-    static constexpr bool REGLIST = KPL == 16;  // lists in registers, no shared-memory list arrays
+    static constexpr bool REGLIST = KPL <= 16;  // lists in registers, no shared-memory list arrays
     static constexpr uint32_t LISTS = REGLIST ? 0 : LIST_ROWS * KPL * 8;
     static constexpr uint32_t MISC = 256;
     static constexpr uint32_t AVAIL = TS_SMEM_MAX - 1024 - MISC - LISTS - A_BYTES;
     static constexpr int STAGES_RAW = int(AVAIL / STAGE);
-    static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
+#ifndef KNN_TS_STAGE_CAP
+#define KNN_TS_STAGE_CAP 6
+#endif
+    static constexpr int STAGES = STAGES_RAW > KNN_TS_STAGE_CAP ? KNN_TS_STAGE_CAP : STAGES_RAW;
     static_assert(STAGES >= 2, "shared memory budget too small for a 2-stage ring");
     static constexpr uint32_t SMEM = 1024 + A_BYTES + STAGES * STAGE + LISTS + MISC;
     static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
@@ -97,7 +100,8 @@ tensor_sweep_kernel(const SweepParams p) {
     constexpr int S = L::STAGES;
     constexpr int NSEG = L::NSEG;
     constexpr int SEG_COLS = BN / NSEG;  // columns of a tile one epilogue warp filters
-    static_assert(SEG_COLS % 64 == 0 && KPL % 16 == 0 && KPL <= SEG_COLS, "tile / list shape");
+    static_assert(SEG_COLS % 64 == 0 && (KPL % 16 == 0 || KPL < 16) && KPL % 2 == 0 && KPL <= SEG_COLS,
+                  "tile / list shape");
     constexpr bool REGLIST = L::REGLIST && !CAPTURE;
     constexpr bool DIRECT = !REGLIST && KPL % 32 == 0;  // fill the first KPL columns without the filter
     extern __shared__ uint8_t smem_raw[];
@@ -252,29 +256,33 @@ tensor_sweep_kernel(const SweepParams p) {
                 bt[4 * q + 3] = f.w;
             }
         };
-        // Register-resident list (KPL == 16): replacing the maximum is 32
+        // Register-resident list (KPL <= 16): replacing the maximum is 2 KPL
         // selects plus a 4-level (value, slot) max tree -- no memory on the
         // critical path.  Larger lists live in shared memory.
         float la[REGLIST ? KPL : 1];
         uint32_t lx[REGLIST ? KPL : 1];
         ListMax thr{kInf, 0};
         auto reg_argmax = [&]() -> ListMax {
-            float mv[8];
-            uint32_t ms[8];
+            constexpr int H = REGLIST ? KPL / 2 : 1;
+            float mv[H];
+            uint32_t ms[H];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const bool r = la[2 * i + 1] > la[2 * i];
-                mv[i] = r ? la[2 * i + 1] : la[2 * i];
+            for (int i = 0; i < H; ++i) {
+                const bool r = la[REGLIST ? 2 * i + 1 : 0] > la[REGLIST ? 2 * i : 0];
+                mv[i] = r ? la[REGLIST ? 2 * i + 1 : 0] : la[REGLIST ? 2 * i : 0];
                 ms[i] = r ? 2 * i + 1 : 2 * i;
             }
+            // tournament over H entries (any H; odd levels carry their last entry)
 #pragma unroll
-            for (int w = 4; w >= 1; w >>= 1)
+            for (int h = H; h > 1; h = (h + 1) / 2) {
+                const int h2 = (h + 1) / 2;
 #pragma unroll
-                for (int i = 0; i < w; ++i) {
-                    const bool r = mv[i + w] > mv[i];
-                    mv[i] = r ? mv[i + w] : mv[i];
-                    ms[i] = r ? ms[i + w] : ms[i];
+                for (int i = 0; i + h2 < h; ++i) {
+                    const bool r = mv[i + h2] > mv[i];
+                    mv[i] = r ? mv[i + h2] : mv[i];
+                    ms[i] = r ? ms[i + h2] : ms[i];
                 }
+            }
             return ListMax{mv[0], ms[0]};
         };
         uint32_t cap_slot = 0;
@@ -981,7 +989,19 @@ static TensorCfg tensor_cfg(uint32_t klist) {
     const uint32_t margin = klist / 4 > 8 ? klist / 4 : 8;
     if (klist + 1 + 5 <= 16) {
         const char* e = getenv("KNN_B200_LIST16_SEGMENTS");  // tuning knob: 2 (default) or 1
-        return {16, (e && atoi(e) == 1) ? 1u : 2u};
+        if (e && atoi(e) == 1) return {16, 1};
+        // Two column-half segments per row.  Shorter lists mean fewer and
+        // cheaper insertions (each list sees ~KPL ln(n / KPL) records) but a
+        // lower proof bound: at C2 (k = 10) KPL 12 is fastest end to end --
+        // 0.3% of rows go to the capture pass -- against 16 (no fallback) and
+        // 10 (5% fallback).  Tuning knob KNN_B200_KPL: 8, 10, 12, 14 or 16.
+        const char* kp = getenv("KNN_B200_KPL");
+        const uint32_t want = kp ? uint32_t(atoi(kp)) : 12u;
+        if (want == 8 && klist <= 4) return {8, 2};
+        if (want == 10 && klist <= 10) return {10, 2};
+        if (want == 12 && klist + 1 <= 12) return {12, 2};
+        if (want == 14 && klist + 1 <= 14) return {14, 2};
+        return {16, 2};
     }
     if (klist + 1 + margin <= 32) return {32, 2};
     if (klist + 1 + margin <= 64) return {64, 1};
@@ -1056,6 +1076,18 @@ static cudaError_t launch_sweep_t(const SweepParams& sp, uint32_t nrows, cudaStr
 
 static cudaError_t launch_sweep(TensorCfg c, bool ares, const SweepParams& sp, uint32_t nrows, cudaStream_t stream) {
     switch (c.kpl) {
+    case 8:
+        return ares ? launch_sweep_t<8, 256, true, 8>(sp, nrows, stream)
+                    : launch_sweep_t<8, 256, false, 8>(sp, nrows, stream);
+    case 10:
+        return ares ? launch_sweep_t<10, 256, true, 8>(sp, nrows, stream)
+                    : launch_sweep_t<10, 256, false, 8>(sp, nrows, stream);
+    case 12:
+        return ares ? launch_sweep_t<12, 256, true, 8>(sp, nrows, stream)
+                    : launch_sweep_t<12, 256, false, 8>(sp, nrows, stream);
+    case 14:
+        return ares ? launch_sweep_t<14, 256, true, 8>(sp, nrows, stream)
+                    : launch_sweep_t<14, 256, false, 8>(sp, nrows, stream);
     case 16:
         if (c.nseg == 1)
             return ares ? launch_sweep_t<16, 256, true, 4>(sp, nrows, stream)
@@ -1083,6 +1115,10 @@ template <int FOLD>
 static cudaError_t launch_rescore(TensorCfg c, const RescoreParams& rp, uint32_t nrows, cudaStream_t stream) {
     const dim3 grid((nrows + 7) / 8);
     switch (c.kpl) {
+    case 8: rescore_kernel<FOLD, 16, 2><<<grid, 256, 0, stream>>>(rp); break;
+    case 10: rescore_kernel<FOLD, 20, 2><<<grid, 256, 0, stream>>>(rp); break;
+    case 12: rescore_kernel<FOLD, 24, 2><<<grid, 256, 0, stream>>>(rp); break;
+    case 14: rescore_kernel<FOLD, 28, 2><<<grid, 256, 0, stream>>>(rp); break;
     case 16:
         if (c.nseg == 1) rescore_kernel<FOLD, 16, 1><<<grid, 256, 0, stream>>>(rp);
         else rescore_kernel<FOLD, 32, 2><<<grid, 256, 0, stream>>>(rp);
