@@ -245,10 +245,13 @@ tensor_sweep_kernel(const SweepParams p) {
         const float kInf = __int_as_float(0x7f800000);
         const uint32_t lane_addr = tmem + (uint32_t(quad * 32) << 16);
         const uint32_t seg0 = seg * SEG_COLS;
-        auto load_beta = [&](uint32_t col0, float (&bt)[32]) {
+        // columns per TMEM load / filter step (16-column chunks with the
+        // norms pipelined too measured 6% slower at C2)
+        constexpr int W = 32;
+        auto load_beta = [&](uint32_t col0, float (&bt)[W]) {
             const float4* beta4 = reinterpret_cast<const float4*>(p.alpha + col0);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < W / 4; ++q) {
                 const float4 f = __ldg(beta4 + q);
                 bt[4 * q] = f.x;
                 bt[4 * q + 1] = f.y;
@@ -339,32 +342,33 @@ tensor_sweep_kernel(const SweepParams p) {
                     thr = list_rescan<KPL, L::STRIDE>(a_base);
                 }
                 if (!valid) thr.a = -kInf;  // padding rows admit nothing
-                // One 32-column chunk.  direct: position among the first KPL
+                // One W-column chunk.  direct: position among the first KPL
                 // columns this thread sees (first tile of group 0, shared-memory
                 // lists only), or -1.
-                auto process = [&](const uint32_t (&v)[32], const float (&bt)[32], uint32_t col0, int direct) {
+                auto process = [&](const uint32_t (&v)[W], const float (&bt)[W], uint32_t col0, int direct) {
+                    constexpr int P = W / 2;  // column pairs
                     if constexpr (!REGLIST) {
                         if (direct >= 0) {  // first KPL columns: fill the list directly
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) {
+                            for (int j = 0; j < W; ++j) {
                                 const uint32_t col = col0 + j;
                                 my_a[(direct + j) * L::LIST_ROWS] =
                                     col < p.n ? __fmaf_rn(-2.0f, __uint_as_float(v[j]), bt[j]) : kInf;
                                 my_i[(direct + j) * L::LIST_ROWS] = col < p.n ? col : 0xffffffffu;
                             }
-                            if (direct + 32 == KPL && valid) thr = list_rescan<KPL, L::STRIDE>(a_base);
+                            if (direct + W == KPL && valid) thr = list_rescan<KPL, L::STRIDE>(a_base);
                             return;
                         }
                     }
                     // hot path: one FFMA2 per two distances, a FMNMX(3) min tree, one vote
-                    float m[16];
+                    float m[P];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
+                    for (int i = 0; i < P; ++i) {
                         const float2 y2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], bt[2 * i], bt[2 * i + 1]);
                         m[i] = fminf(y2.x, y2.y);
                     }
 #pragma unroll
-                    for (int w = 8; w >= 1; w >>= 1)
+                    for (int w = P / 2; w >= 1; w >>= 1)
 #pragma unroll
                         for (int i = 0; i < w; ++i) m[i] = fminf(m[i], m[i + w]);
                     if (!__any_sync(0xffffffffu, m[0] < thr.a) || p.debug_mode == 4) return;
@@ -372,10 +376,10 @@ tensor_sweep_kernel(const SweepParams p) {
                     // the admitted pairs; a pair's two values are picked with a
                     // 4-level select tree (no dynamic register indexing, one copy
                     // of the insertion code per call site)
-                    float ye[16], yo[16];
+                    float ye[P], yo[P];
                     uint32_t pm = 0;
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
+                    for (int i = 0; i < P; ++i) {
                         const float2 y2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], bt[2 * i], bt[2 * i + 1]);
                         ye[i] = y2.x;
                         yo[i] = y2.y;
@@ -389,8 +393,13 @@ tensor_sweep_kernel(const SweepParams p) {
                             float e8[8], o8[8];
 #pragma unroll
                             for (int q = 0; q < 8; ++q) {
-                                e8[q] = (i & 8) ? ye[q + 8] : ye[q];
-                                o8[q] = (i & 8) ? yo[q + 8] : yo[q];
+                                if constexpr (P == 16) {
+                                    e8[q] = (i & 8) ? ye[q + 8] : ye[q];
+                                    o8[q] = (i & 8) ? yo[q + 8] : yo[q];
+                                } else {
+                                    e8[q] = ye[q];
+                                    o8[q] = yo[q];
+                                }
                             }
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
