@@ -43,11 +43,14 @@ constexpr int TS_MAX_RES_KC = 4;              // A resident in smem when d <= 25
 // EW epilogue warps (4 or 8).  With 8, two warps share each TMEM lane
 // quadrant and split every tile's columns in halves; each half keeps its own
 // list of KPL entries per row (NSEG = 2 list segments per row).
-template <int KPL, int BN, bool ARES, int EW>
+// PAIR: a cluster of two CTAs runs M = 256 tcgen05.mma (cta_group::2); each
+// CTA stages its own 128 query rows and half of every reference tile, which
+// halves the L2->SM operand traffic per CTA.
+template <int KPL, int BN, bool ARES, int EW, bool PAIR = false>
 struct TSLayout {
     static constexpr int NSEG = EW / 4;
     static constexpr int THREADS = 64 + 32 * EW;  // warp 0 TMA producer, warp 1 MMA issuer, epilogue warps
-    static constexpr uint32_t B_CHUNK = BN * 128;
+    static constexpr uint32_t B_CHUNK = (PAIR ? BN / 2 : BN) * 128;
     static constexpr uint32_t STAGE = B_CHUNK + (ARES ? 0 : TS_A_CHUNK);
     static constexpr uint32_t A_BYTES = ARES ? TS_MAX_RES_KC * TS_A_CHUNK : 0;
     static constexpr uint32_t LIST_ROWS = TS_BM * NSEG;                 // list "columns"
@@ -59,7 +62,9 @@ struct TSLayout {
 #ifndef KNN_TS_STAGE_CAP
 #define KNN_TS_STAGE_CAP 6
 #endif
-    static constexpr int STAGES = STAGES_RAW > KNN_TS_STAGE_CAP ? KNN_TS_STAGE_CAP : STAGES_RAW;
+    // (PAIR stages are half-size: allow twice as many for the same bytes in flight)
+    static constexpr int STAGE_CAP = PAIR ? 2 * KNN_TS_STAGE_CAP : KNN_TS_STAGE_CAP;
+    static constexpr int STAGES = STAGES_RAW > STAGE_CAP ? STAGE_CAP : STAGES_RAW;
     static_assert(STAGES >= 2, "shared memory budget too small for a 2-stage ring");
     static constexpr uint32_t SMEM = 1024 + A_BYTES + STAGES * STAGE + LISTS + MISC;
     static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
@@ -93,10 +98,11 @@ struct SweepParams {
 // come from HBM once per group instead of once per row block.  The per-row
 // candidate lists are written to `cand` at the end of each item and read
 // back when the row block's next group starts.
-template <int KPL, int BN, bool ARES, int EW, bool CAPTURE>
-__global__ void __launch_bounds__(TSLayout<KPL, BN, ARES, EW>::THREADS, 1)
+template <int KPL, int BN, bool ARES, int EW, bool CAPTURE, bool PAIR = false>
+__global__ void __launch_bounds__(TSLayout<KPL, BN, ARES, EW, PAIR>::THREADS, 1)
 tensor_sweep_kernel(const SweepParams p) {
-    using L = TSLayout<KPL, BN, ARES, EW>;
+    using L = TSLayout<KPL, BN, ARES, EW, PAIR>;
+    static_assert(!PAIR || (ARES && !CAPTURE), "CTA pairs: resident A, no capture");
     constexpr int S = L::STAGES;
     constexpr int NSEG = L::NSEG;
     constexpr int SEG_COLS = BN / NSEG;  // columns of a tile one epilogue warp filters
@@ -119,6 +125,15 @@ tensor_sweep_kernel(const SweepParams p) {
     const uint32_t ntiles = (p.n + BN - 1) / BN;
     const uint32_t nrb = (p.row_end - p.row_begin + TS_BM - 1) / TS_BM;
     const uint32_t ngroups = (ntiles + p.group_tiles - 1) / p.group_tiles;
+    // Work units: row blocks, or (PAIR) pairs of row blocks 2u (leader) and
+    // 2u+1 (peer); an odd last pair's peer block is all padding rows.
+    uint32_t rank = 0;
+    if constexpr (PAIR) rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    const uint32_t unit0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
+    const uint32_t unit_step = PAIR ? gridDim.x / 2 : gridDim.x;
+    const uint32_t nunits = PAIR ? (nrb + 1) / 2 : nrb;
+    auto unit_block = [&](uint32_t u) { return PAIR ? 2 * u + rank : u; };
     const uint32_t bar0 = ptx::smem_u32(bars);
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto empty_bar = [&](int s) { return bar0 + 8u * (S + s); };
@@ -126,23 +141,39 @@ tensor_sweep_kernel(const SweepParams p) {
     auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * S + 2 + b); };
     const uint32_t afull_bar = bar0 + 8u * (2 * S + 4);
     const uint32_t aempty_bar = bar0 + 8u * (2 * S + 5);
+    // PAIR: many barriers complete through the other CTA (multicast commits,
+    // forwarded arrivals); wait without a long suspend hint
+    auto wait = [&](uint32_t bar, uint32_t parity) {
+        if constexpr (PAIR) ptx::mbar_wait_nohint(bar, parity);
+        else ptx::mbar_wait(bar, parity);
+    };
 
     if (warp == 0 && lane == 0) {
+        // PAIR: the leader's operand barriers also count the peer's
+        // forwarded arrival, and its accumulator-empty barriers the peer's
+        // epilogue warps; MMA completions are multicast to both CTAs.
+        const uint32_t fwd = PAIR && leader ? 2 : 1;
         for (int s = 0; s < S; ++s) {
-            ptx::mbar_init(full_bar(s), 1);
+            ptx::mbar_init(full_bar(s), fwd);
             ptx::mbar_init(empty_bar(s), 1);
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(tfull_bar(b), 1);
-            ptx::mbar_init(tempty_bar(b), EW);  // one arrive per epilogue warp
+            ptx::mbar_init(tempty_bar(b), (PAIR ? 2 : 1) * EW);  // one arrive per epilogue warp
         }
-        ptx::mbar_init(afull_bar, 1);
+        ptx::mbar_init(afull_bar, fwd);
         ptx::mbar_init(aempty_bar, 1);
         ptx::fence_mbar_init();
     }
-    if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), L::TMEM_COLS);
-    ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) {
+        if (warp == 1) ptx::tmem_alloc_pair(ptx::smem_u32(tmem_slot), L::TMEM_COLS);
+        ptx::tc_fence_before();
+        ptx::cluster_sync();
+    } else {
+        if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), L::TMEM_COLS);
+        ptx::tc_fence_before();
+        __syncthreads();
+    }
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -153,10 +184,10 @@ tensor_sweep_kernel(const SweepParams p) {
             uint32_t phase = 0, a_phase = 0;
             for (uint32_t g = 0; g < ngroups; ++g) {
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
-                for (uint32_t rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
-                    const uint32_t r0 = p.row_begin + rb * TS_BM;
+                for (uint32_t u = unit0; u < nunits; u += unit_step) {
+                    const uint32_t r0 = p.row_begin + unit_block(u) * TS_BM;
                     if constexpr (ARES) {  // A stays resident for the item; reload once the MMA released it
-                        ptx::mbar_wait(aempty_bar, a_phase ^ 1);
+                        wait(aempty_bar, a_phase ^ 1);
                         ptx::mbar_arrive_expect_tx(afull_bar, p.kc * TS_A_CHUNK);
                         for (uint32_t kc = 0; kc < p.kc; ++kc)
                             ptx::bulk_g2s(ptx::smem_u32(a_smem + kc * TS_A_CHUNK),
@@ -165,7 +196,7 @@ tensor_sweep_kernel(const SweepParams p) {
                     }
                     for (uint32_t t = t0; t < t1; ++t) {
                         for (uint32_t kc = 0; kc < p.kc; ++kc) {
-                            ptx::mbar_wait(empty_bar(stage), phase ^ 1);
+                            wait(empty_bar(stage), phase ^ 1);
                             if (p.debug_mode == 3) {  // profiling: MMA on stale tiles, no loads
                                 ptx::mbar_arrive(full_bar(stage));
                                 if (++stage == S) {
@@ -176,7 +207,9 @@ tensor_sweep_kernel(const SweepParams p) {
                             }
                             ptx::mbar_arrive_expect_tx(full_bar(stage), L::STAGE);
                             uint8_t* dst = stage_smem + stage * L::STAGE;
-                            ptx::bulk_g2s(ptx::smem_u32(dst), p.xh + (size_t(kc) * p.npad + size_t(t) * BN) * 128,
+                            // PAIR: this CTA's half of the tile's columns
+                            ptx::bulk_g2s(ptx::smem_u32(dst),
+                                          p.xh + (size_t(kc) * p.npad + size_t(t) * BN + rank * (BN / 2)) * 128,
                                           L::B_CHUNK, full_bar(stage));
                             if constexpr (!ARES)
                                 ptx::bulk_g2s(ptx::smem_u32(dst + L::B_CHUNK),
@@ -190,26 +223,59 @@ tensor_sweep_kernel(const SweepParams p) {
                 }
             }
         }
-    } else if (warp == 1) {
-        // ---------------- MMA issuer (one lane) ----------------
+    } else if (warp == 1 && PAIR && !leader) {
+        // ---------------- peer: forward operand arrivals to the leader ----------------
         if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_f16_f32(TS_BM, BN);
+            const uint32_t lead_full0 = ptx::mapa_shared(full_bar(0), 0);
+            const uint32_t lead_afull = ptx::mapa_shared(afull_bar, 0);
+            int stage = 0;
+            uint32_t phase = 0, a_phase = 0;
+            for (uint32_t g = 0; g < ngroups; ++g) {
+                const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
+                for (uint32_t u = unit0; u < nunits; u += unit_step) {
+                    wait(afull_bar, a_phase);
+                    a_phase ^= 1;
+                    ptx::mbar_arrive_remote_relaxed(lead_afull);
+                    for (uint32_t t = t0; t < t1; ++t)
+                        for (uint32_t kc = 0; kc < p.kc; ++kc) {
+                            wait(full_bar(stage), phase);
+                            ptx::mbar_arrive_remote_relaxed(lead_full0 + 8u * stage);
+                            if (++stage == S) {
+                                stage = 0;
+                                phase ^= 1;
+                            }
+                        }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (one lane; PAIR: the leader's) ----------------
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_f16_f32(PAIR ? 2 * TS_BM : TS_BM, BN);
+            auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+                if constexpr (PAIR) ptx::mma_f16_ss_pair(d, a, b, idesc, acc);
+                else ptx::mma_f16_ss(d, a, b, idesc, acc);
+            };
+            auto commit = [&](uint32_t bar) {
+                if constexpr (PAIR) ptx::mma_commit_pair(bar);
+                else ptx::mma_commit(bar);
+            };
             int stage = 0;
             uint32_t phase = 0, a_phase = 0, tcount = 0;
             for (uint32_t g = 0; g < ngroups; ++g) {
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
-                for (uint32_t rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
+                for (uint32_t u = unit0; u < nunits; u += unit_step) {
                     if constexpr (ARES) {
-                        ptx::mbar_wait(afull_bar, a_phase);
+                        wait(afull_bar, a_phase);
                         a_phase ^= 1;
                     }
                     for (uint32_t t = t0; t < t1; ++t, ++tcount) {
                         const uint32_t b = tcount & 1, use = tcount >> 1;
-                        ptx::mbar_wait(tempty_bar(b), (use & 1) ^ 1);
+                        wait(tempty_bar(b), (use & 1) ^ 1);
                         ptx::tc_fence_after();
                         const uint32_t d_tmem = tmem + b * BN;
                         for (uint32_t kc = 0; kc < p.kc; ++kc) {
-                            ptx::mbar_wait(full_bar(stage), phase);
+                            wait(full_bar(stage), phase);
                             ptx::tc_fence_after();
                             const uint8_t* bsm = stage_smem + stage * L::STAGE;
                             const uint8_t* asm_ = ARES ? a_smem + kc * TS_A_CHUNK : bsm + L::B_CHUNK;
@@ -217,18 +283,18 @@ tensor_sweep_kernel(const SweepParams p) {
                             const uint32_t b_addr = ptx::smem_u32(bsm);
 #pragma unroll
                             for (uint32_t k = 0; k < 4; ++k) {  // UMMA_K = 16 fp16 = 32 B inside the swizzle atom
-                                ptx::mma_f16_ss(d_tmem, ptx::sw128_kmajor_desc(a_addr + 32 * k),
-                                                ptx::sw128_kmajor_desc(b_addr + 32 * k), idesc, (kc | k) != 0);
+                                mma(d_tmem, ptx::sw128_kmajor_desc(a_addr + 32 * k),
+                                    ptx::sw128_kmajor_desc(b_addr + 32 * k), (kc | k) != 0);
                             }
-                            ptx::mma_commit(empty_bar(stage));
+                            commit(empty_bar(stage));
                             if (++stage == S) {
                                 stage = 0;
                                 phase ^= 1;
                             }
                         }
-                        ptx::mma_commit(tfull_bar(b));
+                        commit(tfull_bar(b));
                     }
-                    if constexpr (ARES) ptx::mma_commit(aempty_bar);  // A may be replaced once these MMAs retire
+                    if constexpr (ARES) commit(aempty_bar);  // A may be replaced once these MMAs retire
                 }
             }
         }
@@ -306,10 +372,21 @@ tensor_sweep_kernel(const SweepParams p) {
             }
         };
         uint32_t tcount = 0;
+        // accumulator release: PAIR peers arrive on the leader's barrier
+        const uint32_t tempty_rel0 = PAIR && !leader ? ptx::mapa_shared(tempty_bar(0), 0) : tempty_bar(0);
+        auto release_acc = [&](uint32_t b) {
+            if constexpr (PAIR) {
+                if (!leader) {
+                    ptx::mbar_arrive_remote_relaxed(tempty_rel0 + 8u * b);
+                    return;
+                }
+            }
+            ptx::mbar_arrive(tempty_bar(b));
+        };
         for (uint32_t g = 0; g < ngroups; ++g) {
             const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
-            for (uint32_t rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
-                const uint32_t row = p.row_begin + rb * TS_BM + rl;
+            for (uint32_t u = unit0; u < nunits; u += unit_step) {
+                const uint32_t row = p.row_begin + unit_block(u) * TS_BM + rl;
                 const bool valid = row < p.row_end;
                 uint64_t* state = p.cand + (size_t(row - p.row_begin) * NSEG + seg) * KPL;
                 // Columns are ranked by y = fl(beta_j - 2 dot): alpha_i is
@@ -421,7 +498,7 @@ tensor_sweep_kernel(const SweepParams p) {
                 };
                 for (uint32_t t = t0; t < t1; ++t, ++tcount) {
                     const uint32_t b = tcount & 1, use = tcount >> 1;
-                    ptx::mbar_wait(tfull_bar(b), use & 1);
+                    wait(tfull_bar(b), use & 1);
                     ptx::tc_fence_after();
                     const uint32_t cbase = t * BN + seg0;
                     const uint32_t taddr = lane_addr + b * BN + seg0;
@@ -440,7 +517,7 @@ tensor_sweep_kernel(const SweepParams p) {
                             }
                         ptx::tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(tempty_bar(b));
+                        if (lane == 0) release_acc(b);
                         continue;
                     }
                     uint32_t va[32], vb[32];
@@ -461,7 +538,7 @@ tensor_sweep_kernel(const SweepParams p) {
                         } else {  // this warp's part of the accumulator is in registers: release it
                             ptx::tc_fence_before();
                             __syncwarp();
-                            if (lane == 0) ptx::mbar_arrive(tempty_bar(b));
+                            if (lane == 0) release_acc(b);
                         }
                         load_beta(cbase + c0 + 32, bt);
                         process(vb, bt, cbase + c0 + 32, (first && c0 + 32 < KPL) ? c0 + 32 : -1);
@@ -485,10 +562,18 @@ tensor_sweep_kernel(const SweepParams p) {
         }
     }
     ptx::tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem, L::TMEM_COLS);
+    if constexpr (PAIR) {
+        ptx::cluster_sync();  // neither CTA frees TMEM while the pair's MMAs may write it
+        if (warp == 1) {
+            ptx::tc_fence_after();
+            ptx::tmem_dealloc_pair(tmem, L::TMEM_COLS);
+        }
+    } else {
+        __syncthreads();
+        if (warp == 1) {
+            ptx::tc_fence_after();
+            ptx::tmem_dealloc(tmem, L::TMEM_COLS);
+        }
     }
 }
 
@@ -1067,6 +1152,33 @@ size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32
     return b;
 }
 
+// CTA-pair sweep (cluster of 2): one pair per two SMs, persistent.
+template <int KPL, int BN, int EW>
+static cudaError_t launch_sweep_pair(const SweepParams& sp, uint32_t nrows, cudaStream_t stream) {
+    using L = TSLayout<KPL, BN, true, EW, true>;
+    auto kern = tensor_sweep_kernel<KPL, BN, true, EW, false, true>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::SMEM));
+    if (e != cudaSuccess) return e;
+    const uint32_t npairs = (nrows + 2 * TS_BM - 1) / (2 * TS_BM);
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t grid_pairs = npairs < uint32_t(sms / 2) ? npairs : uint32_t(sms / 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * grid_pairs);
+    cfg.blockDim = dim3(L::THREADS);
+    cfg.dynamicSmemBytes = L::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, sp);
+}
+
 template <int KPL, int BN, bool ARES, int EW, bool CAPTURE = false>
 static cudaError_t launch_sweep_t(const SweepParams& sp, uint32_t nrows, cudaStream_t stream) {
     using L = TSLayout<KPL, BN, ARES, EW>;
@@ -1204,7 +1316,19 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         if ((e = run_sym_sweep(xh, alpha, n, npad, kc, cand, sym_ws, a.sm_count, st)) != cudaSuccess) return e;
         launches += 3;
     } else {
-        if ((e = launch_sweep(cfg, kc <= uint32_t(TS_MAX_RES_KC), sp, nrows, st)) != cudaSuccess) return e;
+        // CTA pairs (default; KNN_B200_PAIR=0 disables) need whole 256-row
+        // pairs of blocks inside the padded planes.  At C2 they halve the
+        // L2->SM operand traffic and cut the sweep ~3%.
+        const char* pe = getenv("KNN_B200_PAIR");
+        const bool pair = !(pe && atoi(pe) == 0) && kc <= uint32_t(TS_MAX_RES_KC) && cfg.nseg == 2 &&
+                          (cfg.kpl == 12 || cfg.kpl == 16) && a.row_begin % 256 == 0 &&
+                          a.row_begin + (nrows + 255) / 256 * 256 <= npad;
+        if (pair) {
+            e = cfg.kpl == 12 ? launch_sweep_pair<12, 256, 8>(sp, nrows, st) : launch_sweep_pair<16, 256, 8>(sp, nrows, st);
+            if (e != cudaSuccess) return e;
+        } else if ((e = launch_sweep(cfg, kc <= uint32_t(TS_MAX_RES_KC), sp, nrows, st)) != cudaSuccess) {
+            return e;
+        }
         ++launches;
     }
     if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
