@@ -134,6 +134,11 @@ tensor_sweep_kernel(const SweepParams p) {
     const uint32_t unit_step = PAIR ? gridDim.x / 2 : gridDim.x;
     const uint32_t nunits = PAIR ? (nrb + 1) / 2 : nrb;
     auto unit_block = [&](uint32_t u) { return PAIR ? 2 * u + rank : u; };
+    // Column groups: all of them in order (lists carry over from group to
+    // group) -- except in CAPTURE mode, whose fixed thresholds let blockIdx.y
+    // take a share of the groups so that few rows still fill the GPU.
+    const uint32_t g_first = CAPTURE ? blockIdx.y : 0;
+    const uint32_t g_step = CAPTURE ? gridDim.y : 1;
     const uint32_t bar0 = ptx::smem_u32(bars);
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto empty_bar = [&](int s) { return bar0 + 8u * (S + s); };
@@ -182,7 +187,7 @@ tensor_sweep_kernel(const SweepParams p) {
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0, a_phase = 0;
-            for (uint32_t g = 0; g < ngroups; ++g) {
+            for (uint32_t g = g_first; g < ngroups; g += g_step) {
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
                 for (uint32_t u = unit0; u < nunits; u += unit_step) {
                     const uint32_t r0 = p.row_begin + unit_block(u) * TS_BM;
@@ -230,7 +235,7 @@ tensor_sweep_kernel(const SweepParams p) {
             const uint32_t lead_afull = ptx::mapa_shared(afull_bar, 0);
             int stage = 0;
             uint32_t phase = 0, a_phase = 0;
-            for (uint32_t g = 0; g < ngroups; ++g) {
+            for (uint32_t g = g_first; g < ngroups; g += g_step) {
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
                 for (uint32_t u = unit0; u < nunits; u += unit_step) {
                     wait(afull_bar, a_phase);
@@ -262,7 +267,7 @@ tensor_sweep_kernel(const SweepParams p) {
             };
             int stage = 0;
             uint32_t phase = 0, a_phase = 0, tcount = 0;
-            for (uint32_t g = 0; g < ngroups; ++g) {
+            for (uint32_t g = g_first; g < ngroups; g += g_step) {
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
                 for (uint32_t u = unit0; u < nunits; u += unit_step) {
                     if constexpr (ARES) {
@@ -383,7 +388,7 @@ tensor_sweep_kernel(const SweepParams p) {
             }
             ptx::mbar_arrive(tempty_bar(b));
         };
-        for (uint32_t g = 0; g < ngroups; ++g) {
+        for (uint32_t g = g_first; g < ngroups; g += g_step) {
             const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
             for (uint32_t u = unit0; u < nunits; u += unit_step) {
                 const uint32_t row = p.row_begin + unit_block(u) * TS_BM + rl;
@@ -1190,7 +1195,14 @@ static cudaError_t launch_sweep_t(const SweepParams& sp, uint32_t nrows, cudaStr
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const dim3 grid(nrb < uint32_t(sms) ? nrb : uint32_t(sms));  // persistent: one CTA per SM
+    dim3 grid(nrb < uint32_t(sms) ? nrb : uint32_t(sms));  // persistent: one CTA per SM
+    if constexpr (CAPTURE) {  // few rows: split the column groups over blockIdx.y as well
+        const uint32_t ntiles = (sp.n + BN - 1) / BN;
+        const uint32_t ngroups = (ntiles + sp.group_tiles - 1) / sp.group_tiles;
+        uint32_t gy = uint32_t(sms) / grid.x;
+        gy = gy < 1 ? 1 : (gy > ngroups ? ngroups : gy);
+        grid.y = gy;
+    }
     kern<<<grid, L::THREADS, L::SMEM, stream>>>(sp);
     return cudaGetLastError();
 }
