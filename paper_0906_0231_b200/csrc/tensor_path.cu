@@ -146,12 +146,7 @@ tensor_sweep_kernel(const SweepParams p) {
     auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * S + 2 + b); };
     const uint32_t afull_bar = bar0 + 8u * (2 * S + 4);
     const uint32_t aempty_bar = bar0 + 8u * (2 * S + 5);
-    // PAIR: many barriers complete through the other CTA (multicast commits,
-    // forwarded arrivals); wait without a long suspend hint
-    auto wait = [&](uint32_t bar, uint32_t parity) {
-        if constexpr (PAIR) ptx::mbar_wait_nohint(bar, parity);
-        else ptx::mbar_wait(bar, parity);
-    };
+    auto wait = [&](uint32_t bar, uint32_t parity) { ptx::mbar_wait(bar, parity); };
 
     if (warp == 0 && lane == 0) {
         // PAIR: the leader's operand barriers also count the peer's
