@@ -1097,7 +1097,12 @@ static TensorCfg tensor_cfg(uint32_t klist) {
         if (want == 14 && klist + 1 <= 14) return {14, 2};
         return {16, 2};
     }
-    if (klist + 1 + margin <= 32) return {32, 2};
+    // Two 32-entry shared-memory segments hold k up to 47: each half of the
+    // columns holds about half of a row's neighbours (measured at n = 1M,
+    // d = 128: k = 24/32/40 in 0.44 s with 0 / 8 / 3879 rows to the capture
+    // pass, against 0.86 s for one 64-entry list at k = 24; 24-entry register
+    // lists spill and lose).
+    if (klist + 1 <= 48) return {32, 2};
     if (klist + 1 + margin <= 64) return {64, 1};
     if (klist + 1 + margin <= 128) return {128, 1};
     return {0, 0};  // not supported by the tensor sweep
@@ -1331,7 +1336,8 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
                           (cfg.kpl == 12 || cfg.kpl == 16) && a.row_begin % 256 == 0 &&
                           a.row_begin + (nrows + 255) / 256 * 256 <= npad;
         if (pair) {
-            e = cfg.kpl == 12 ? launch_sweep_pair<12, 256, 8>(sp, nrows, st) : launch_sweep_pair<16, 256, 8>(sp, nrows, st);
+            e = cfg.kpl == 12 ? launch_sweep_pair<12, 256, 8>(sp, nrows, st)
+                              : launch_sweep_pair<16, 256, 8>(sp, nrows, st);
             if (e != cudaSuccess) return e;
         } else if ((e = launch_sweep(cfg, kc <= uint32_t(TS_MAX_RES_KC), sp, nrows, st)) != cudaSuccess) {
             return e;
