@@ -437,18 +437,25 @@ tensor_sweep_kernel(const SweepParams p) {
                             return;
                         }
                     }
-                    // hot path: one FFMA2 per two distances, a FMNMX(3) min tree, one vote
-                    float m[P];
+                    // hot path: one FFMA2 per two distances, a 3-input FMNMX3
+                    // min tree (17 instructions for 32 values), one vote
+                    static_assert(W == 32, "min tree is laid out for 32 columns");
+                    float y[W];
 #pragma unroll
                     for (int i = 0; i < P; ++i) {
                         const float2 y2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], bt[2 * i], bt[2 * i + 1]);
-                        m[i] = fminf(y2.x, y2.y);
+                        y[2 * i] = y2.x;
+                        y[2 * i + 1] = y2.y;
                     }
+                    float r1[11], r2[4];
 #pragma unroll
-                    for (int w = P / 2; w >= 1; w >>= 1)
+                    for (int j = 0; j < 10; ++j) r1[j] = fminf(fminf(y[3 * j], y[3 * j + 1]), y[3 * j + 2]);
+                    r1[10] = fminf(y[30], y[31]);
 #pragma unroll
-                        for (int i = 0; i < w; ++i) m[i] = fminf(m[i], m[i + w]);
-                    if (!__any_sync(0xffffffffu, m[0] < thr.a) || p.debug_mode == 4) return;
+                    for (int j = 0; j < 3; ++j) r2[j] = fminf(fminf(r1[3 * j], r1[3 * j + 1]), r1[3 * j + 2]);
+                    r2[3] = fminf(r1[9], r1[10]);
+                    const float mmin = fminf(fminf(fminf(r2[0], r2[1]), r2[2]), r2[3]);
+                    if (!__any_sync(0xffffffffu, mmin < thr.a) || p.debug_mode == 4) return;
                     // rare path: per-lane pair mask, then a warp-uniform walk over
                     // the admitted pairs; a pair's two values are picked with a
                     // 4-level select tree (no dynamic register indexing, one copy
