@@ -22,6 +22,7 @@
 //            rigorous bound on |A - s^2 D_ref|.  Rows without a
 //            proof are recomputed by the EXACT kernel.
 // Result: bit-identical to brute_force_knn.
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -89,6 +90,7 @@ struct SweepParams {
     uint32_t* cap_cnt;
     uint64_t* cap_buf;
     uint32_t cap;
+    const float* bmin;  // [npad / 32] smallest column norm of every 32-column chunk
 };
 
 // Persistent sweep.  Work item = (column group g, row block rb); every CTA
@@ -422,10 +424,12 @@ tensor_sweep_kernel(const SweepParams p) {
                 // One W-column chunk.  direct: position among the first KPL
                 // columns this thread sees (first tile of group 0, shared-memory
                 // lists only), or -1.
-                auto process = [&](const uint32_t (&v)[W], const float (&bt)[W], uint32_t col0, int direct) {
+                auto process = [&](const uint32_t (&v)[W], uint32_t col0, int direct) {
                     constexpr int P = W / 2;  // column pairs
+                    float bt[W];              // the chunk's column norms, loaded only when needed
                     if constexpr (!REGLIST) {
                         if (direct >= 0) {  // first KPL columns: fill the list directly
+                            load_beta(col0, bt);
 #pragma unroll
                             for (int j = 0; j < W; ++j) {
                                 const uint32_t col = col0 + j;
@@ -437,25 +441,49 @@ tensor_sweep_kernel(const SweepParams p) {
                             return;
                         }
                     }
-                    // hot path: one FFMA2 per two distances, a 3-input FMNMX3
-                    // min tree (17 instructions for 32 values), one vote
-                    static_assert(W == 32, "min tree is laid out for 32 columns");
-                    float y[W];
-#pragma unroll
-                    for (int i = 0; i < P; ++i) {
-                        const float2 y2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], bt[2 * i], bt[2 * i + 1]);
-                        y[2 * i] = y2.x;
-                        y[2 * i + 1] = y2.y;
-                    }
+                    // hot path: y_j = fl(beta_j - 2 dot_j) < thr needs
+                    // dot_j > (beta_j - thr) / 2 >= h = (min beta of the chunk - thr) / 2,
+                    // so the raw dots are tested against h: a 3-input FMNMX3 max
+                    // tree (17 instructions for 32 values), one FADD/FMUL, one
+                    // vote, and no column-norm loads.  At the boundary y ~ thr,
+                    // so y's rounding is ~2^-24 |thr|; the slack covers it and
+                    // h's own rounding many times over -- a superset of the
+                    // exact test, which the rare path then applies unchanged.
+                    static_assert(W == 32, "max tree is laid out for 32 columns");
                     float r1[11], r2[4];
 #pragma unroll
-                    for (int j = 0; j < 10; ++j) r1[j] = fminf(fminf(y[3 * j], y[3 * j + 1]), y[3 * j + 2]);
-                    r1[10] = fminf(y[30], y[31]);
+                    for (int j = 0; j < 10; ++j)
+                        r1[j] = fmaxf(fmaxf(__uint_as_float(v[3 * j]), __uint_as_float(v[3 * j + 1])),
+                                      __uint_as_float(v[3 * j + 2]));
+                    r1[10] = fmaxf(__uint_as_float(v[30]), __uint_as_float(v[31]));
 #pragma unroll
-                    for (int j = 0; j < 3; ++j) r2[j] = fminf(fminf(r1[3 * j], r1[3 * j + 1]), r1[3 * j + 2]);
-                    r2[3] = fminf(r1[9], r1[10]);
-                    const float mmin = fminf(fminf(fminf(r2[0], r2[1]), r2[2]), r2[3]);
-                    if (!__any_sync(0xffffffffu, mmin < thr.a) || p.debug_mode == 4) return;
+                    for (int j = 0; j < 3; ++j) r2[j] = fmaxf(fmaxf(r1[3 * j], r1[3 * j + 1]), r1[3 * j + 2]);
+                    r2[3] = fmaxf(r1[9], r1[10]);
+                    const float dmax = fmaxf(fmaxf(fmaxf(r2[0], r2[1]), r2[2]), r2[3]);
+                    const float bm = __ldg(p.bmin + (col0 >> 5));
+                    float h = __fmul_rn(__fsub_rn(bm, thr.a), 0.5f);
+                    if (fabsf(h) < kInf) h = __fsub_rn(h, 9.5367431640625e-07f * (fabsf(bm) + fabsf(thr.a)));  // 2^-20
+                    if (!__any_sync(0xffffffffu, dmax > h) || p.debug_mode == 4) return;
+                    load_beta(col0, bt);
+                    // second stage: the exact test (FFMA2 + FMNMX3 min tree, one
+                    // vote) before the per-pair mask and walk
+                    {
+                        float y[W], q1[11], q2[4];
+#pragma unroll
+                        for (int i = 0; i < P; ++i) {
+                            const float2 y2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], bt[2 * i], bt[2 * i + 1]);
+                            y[2 * i] = y2.x;
+                            y[2 * i + 1] = y2.y;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 10; ++j) q1[j] = fminf(fminf(y[3 * j], y[3 * j + 1]), y[3 * j + 2]);
+                        q1[10] = fminf(y[30], y[31]);
+#pragma unroll
+                        for (int j = 0; j < 3; ++j) q2[j] = fminf(fminf(q1[3 * j], q1[3 * j + 1]), q1[3 * j + 2]);
+                        q2[3] = fminf(q1[9], q1[10]);
+                        if (!__any_sync(0xffffffffu, fminf(fminf(fminf(q2[0], q2[1]), q2[2]), q2[3]) < thr.a))
+                            return;
+                    }
                     // rare path: per-lane pair mask, then a warp-uniform walk over
                     // the admitted pairs; a pair's two values are picked with a
                     // 4-level select tree (no dynamic register indexing, one copy
@@ -528,17 +556,15 @@ tensor_sweep_kernel(const SweepParams p) {
                         continue;
                     }
                     uint32_t va[32], vb[32];
-                    float bt[32];
                     // software pipeline: chunk c+1's TMEM read is in flight while
-                    // chunk c is filtered; the column norms come from L1
-                    // (prefetched one tile ahead)
+                    // chunk c is filtered; column norms come from L1 (prefetched
+                    // one tile ahead) and only for chunks that reach the rare path
                     ptx::tmem_ld_32x32b_x32(taddr, va);
 #pragma unroll 1
                     for (int c0 = 0; c0 < SEG_COLS; c0 += 64) {
                         ptx::tmem_wait_ld();
                         ptx::tmem_ld_32x32b_x32(taddr + c0 + 32, vb);
-                        load_beta(cbase + c0, bt);
-                        process(va, bt, cbase + c0, (first && c0 < KPL) ? c0 : -1);
+                        process(va, cbase + c0, (first && c0 < KPL) ? c0 : -1);
                         ptx::tmem_wait_ld();
                         if (c0 + 64 < SEG_COLS) {
                             ptx::tmem_ld_32x32b_x32(taddr + c0 + 64, va);
@@ -547,8 +573,7 @@ tensor_sweep_kernel(const SweepParams p) {
                             __syncwarp();
                             if (lane == 0) release_acc(b);
                         }
-                        load_beta(cbase + c0 + 32, bt);
-                        process(vb, bt, cbase + c0 + 32, (first && c0 + 32 < KPL) ? c0 + 32 : -1);
+                        process(vb, cbase + c0 + 32, (first && c0 + 32 < KPL) ? c0 + 32 : -1);
                     }
                 }
                 if (valid && !CAPTURE) {
@@ -586,6 +611,34 @@ tensor_sweep_kernel(const SweepParams p) {
 
 // ---------------------------------------------------------------------------
 // prep kernels
+
+// Sort key for the norm-sorted order: ||x - mu||^2 (any order is correct; this
+// one makes every 32-column chunk's norms nearly equal, so the sweep's
+// hot-path bound, which uses the chunk's smallest norm, is nearly exact).
+__global__ void row_key_kernel(const float* __restrict__ X, uint32_t n, uint32_t d, const float* __restrict__ mu,
+                               float* __restrict__ key, uint32_t* __restrict__ idx) {
+    const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (row >= n) return;
+    float s = 0.0f;
+    for (uint32_t k = lane; k < d; k += 32) {
+        const float v = X[size_t(row) * d + k] - mu[k];
+        s += v * v;
+    }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+        key[row] = s;
+        idx[row] = row;
+    }
+}
+
+// bmin[c] = smallest alpha of columns [32c, 32c + 32) (the sweep's hot-path bound)
+__global__ void chunk_min_kernel(const float* __restrict__ alpha, uint32_t nchunks, float* __restrict__ bmin) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= nchunks) return;
+    float m = alpha[size_t(warp) * 32 + lane];
+    for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) bmin[warp] = m;
+}
 
 __device__ __forceinline__ void atomic_max_pos_double(unsigned long long* addr, double v) {
     // non-negative doubles order like their bit patterns
@@ -641,7 +694,7 @@ struct PrepOut {
 // One warp per (padded) row.
 __global__ void prep_kernel(const float* __restrict__ X, uint32_t n, uint32_t d, uint32_t npad, uint32_t kc,
                             const float* __restrict__ mu, const unsigned int* __restrict__ maxabs, int cosine,
-                            PrepOut o) {
+                            const uint32_t* __restrict__ perm, PrepOut o) {
     const uint32_t warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp_global >= npad) return;
@@ -655,7 +708,7 @@ __global__ void prep_kernel(const float* __restrict__ X, uint32_t n, uint32_t d,
     for (uint32_t k = lane; k < kpad; k += 32) {
         __half h = __float2half_rn(0.0f);
         if (row < n && k < d) {
-            const float x = X[size_t(row) * d + k];
+            const float x = X[size_t(perm ? perm[row] : row) * d + k];
             const float m = cosine ? 0.0f : mu[k];
             const float v = __fsub_rn(x, m);
             h = __float2half_rn(__fmul_rn(v, s));
@@ -714,6 +767,7 @@ struct RescoreParams {
     float* fb_thr;        // capture threshold (y space) for each unproven row
     unsigned long long* rescored;
     int force_capture;    // testing: treat every row as unproven (KNN_B200_FORCE_CAPTURE=1)
+    const uint32_t* perm;  // norm-sorted order: sweep row/column r is input row perm[r] (or null)
 };
 
 constexpr double kTcSafety = 4.0;  // tensor-core accumulation error allowance
@@ -789,9 +843,10 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t slot = blockIdx.x * 8 + warp;
     if (slot >= p.row_end - p.row_begin) return;
-    const uint32_t q = p.row_begin + slot;
+    const uint32_t q = p.row_begin + slot;               // sweep order
+    const uint32_t qo = p.perm ? p.perm[q] : q;          // input order
     const uint64_t* cand = p.cand + size_t(slot) * KP;
-    const float* xq = p.X + size_t(q) * p.d;
+    const float* xq = p.X + size_t(qo) * p.d;
     const bool vec = (p.d % 4 == 0);
     constexpr int PER = (KP + 31) / 32;
     const double alpha_q = double(p.alpha[q]);
@@ -837,14 +892,15 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     bool done[PER];
     uint32_t valid = 0;
     auto rescore_one = [&](int m) {
-        const uint32_t col = uint32_t(ak[m]);
+        const uint32_t cs = uint32_t(ak[m]);
         ek[m] = kEmptyKey;
         done[m] = true;
-        if (ak[m] != kEmptyKey && col != q) {
+        if (ak[m] != kEmptyKey && cs != q) {
+            const uint32_t col = p.perm ? p.perm[cs] : cs;  // input index: the reference's tie-break
             const float* xc = p.X + size_t(col) * p.d;
             // Reference argument order (larger index first) -- the fold is
             // symmetric bit for bit, kept for clarity.
-            const float dist = col > q ? exact_fold_rows<FOLD>(xc, xq, p.d, vec) : exact_fold_rows<FOLD>(xq, xc, p.d, vec);
+            const float dist = col > qo ? exact_fold_rows<FOLD>(xc, xq, p.d, vec) : exact_fold_rows<FOLD>(xq, xc, p.d, vec);
             ek[m] = make_key(dist, col);
             ++valid;
         }
@@ -975,11 +1031,12 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         }
         return;
     }
+    const size_t orow = size_t(qo - p.row_begin);  // input order (perm only on whole problems)
     for (uint32_t t = lane; t < p.klist; t += 32) {
         const uint64_t key = keys_s[warp][t];
         const float dv = ordered_to_float(uint32_t(key >> 32));
-        p.out_index[size_t(slot) * p.klist + t] = uint32_t(key);
-        p.out_dist[size_t(slot) * p.klist + t] = p.out_sqrt ? __fsqrt_rn(dv) : dv;
+        p.out_index[orow * p.klist + t] = uint32_t(key);
+        p.out_dist[orow * p.klist + t] = p.out_sqrt ? __fsqrt_rn(dv) : dv;
     }
 }
 
@@ -1018,6 +1075,7 @@ struct Rescore2Params {
     uint32_t* fb2_count;
     uint32_t* fb2_rows;
     unsigned long long* rescored;
+    const uint32_t* perm;  // as in RescoreParams
 };
 
 // Exact fold of every captured column of an unproven row (one warp per row);
@@ -1030,23 +1088,25 @@ __global__ void __launch_bounds__(128) rescore_capture_kernel(const Rescore2Para
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t slot = blockIdx.x * 4 + warp;
     if (slot >= p.m) return;
-    const uint32_t q = p.rows[slot];
+    const uint32_t q = p.rows[slot];            // sweep order
+    const uint32_t qo = p.perm ? p.perm[q] : q;  // input order
     uint64_t* ks = keys2 + size_t(warp) * p.cap;
     const uint32_t c = p.cnt[slot];
     if (c > p.cap) {
-        if (lane == 0) p.fb2_rows[atomicAdd(p.fb2_count, 1u)] = q;
+        if (lane == 0) p.fb2_rows[atomicAdd(p.fb2_count, 1u)] = qo;
         return;
     }
-    const float* xq = p.X + size_t(q) * p.d;
+    const float* xq = p.X + size_t(qo) * p.d;
     const bool vec = (p.d % 4 == 0);
     const uint64_t* in = p.buf + size_t(slot) * p.cap;
     uint32_t valid = 0;
     for (uint32_t i = lane; i < c; i += 32) {
-        const uint32_t col = uint32_t(in[i]);
+        const uint32_t cs = uint32_t(in[i]);
         uint64_t key = kEmptyKey;
-        if (col != q) {
+        if (cs != q) {
+            const uint32_t col = p.perm ? p.perm[cs] : cs;
             const float* xc = p.X + size_t(col) * p.d;
-            const float dist = col > q ? exact_fold_rows<FOLD>(xc, xq, p.d, vec) : exact_fold_rows<FOLD>(xq, xc, p.d, vec);
+            const float dist = col > qo ? exact_fold_rows<FOLD>(xc, xq, p.d, vec) : exact_fold_rows<FOLD>(xq, xc, p.d, vec);
             key = make_key(dist, col);
             ++valid;
         }
@@ -1056,12 +1116,12 @@ __global__ void __launch_bounds__(128) rescore_capture_kernel(const Rescore2Para
     __syncwarp();
     if (lane == 0) atomicAdd(p.rescored, (unsigned long long)valid);
     if (valid < p.klist) {  // cannot happen for a correct band; stay exact
-        if (lane == 0) p.fb2_rows[atomicAdd(p.fb2_count, 1u)] = q;
+        if (lane == 0) p.fb2_rows[atomicAdd(p.fb2_count, 1u)] = qo;
         return;
     }
     // keys are unique (distinct columns) except the empty self slot: the
     // rank of an element is the number of smaller keys
-    const size_t orow = size_t(q - p.row_begin);
+    const size_t orow = size_t(qo - p.row_begin);
     for (uint32_t i = lane; i < c; i += 32) {
         const uint64_t mk = ks[i];
         if (mk == kEmptyKey) continue;
@@ -1141,6 +1201,26 @@ size_t capture_workspace_bytes(uint32_t m, uint32_t d, uint32_t cap) {
     return b;
 }
 
+// Norm-sorted order (whole problems): keys, the permutation, and CUB's
+// radix-sort scratch.
+static size_t sort_temp_bytes(uint32_t n) {
+    size_t t = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t, static_cast<const float*>(nullptr), static_cast<float*>(nullptr),
+                                    static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), int(n));
+    return t;
+}
+
+static size_t sort_workspace_bytes(uint32_t n) {
+    return 4 * ((size_t(n) * 4 + 255) / 256 * 256) + (sort_temp_bytes(n) + 255) / 256 * 256;
+}
+
+// Sort the sweep's rows and columns by norm when the call covers the whole
+// problem (KNN_B200_SORT=0 disables; cosine norms are all equal already).
+static bool sort_selected(uint32_t n, uint32_t row_begin, uint32_t row_end, int cosine) {
+    const char* e = getenv("KNN_B200_SORT");
+    return !(e && atoi(e) == 0) && !cosine && row_begin == 0 && row_end == n;
+}
+
 size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32_t row_end, uint32_t klist,
                               int sm_count) {
     const uint32_t rows = row_end - row_begin;
@@ -1152,6 +1232,7 @@ size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32
     auto add = [&](size_t x) { b += (x + 255) / 256 * 256; };
     add(size_t(kc) * npad * 128);  // xh
     add(size_t(npad) * 4);         // alpha
+    add(size_t(npad / 32) * 4);    // bmin
     add(size_t(npad) * 8);         // rho
     add(size_t(npad) * 8);         // xnorm
     add(size_t(d) * 8);            // mu acc
@@ -1161,6 +1242,7 @@ size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32
     add(size_t(rows) * 4);         // fallback rows
     add(size_t(rows) * 4);         // capture thresholds
     if (sym) add(sym_workspace_bytes(n, sm_count));
+    if (row_begin == 0 && row_end == n) add(sort_workspace_bytes(n));  // norm-sorted order
     return b;
 }
 
@@ -1287,6 +1369,7 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     };
     uint8_t* xh = take(size_t(kc) * npad * 128);
     float* alpha = reinterpret_cast<float*>(take(size_t(npad) * 4));
+    float* bmin = reinterpret_cast<float*>(take(size_t(npad / 32) * 4));
     double* rho = reinterpret_cast<double*>(take(size_t(npad) * 8));
     double* xnorm = reinterpret_cast<double*>(take(size_t(npad) * 8));
     double* muacc = reinterpret_cast<double*>(take(size_t(d) * 8));
@@ -1296,6 +1379,21 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     uint32_t* fb_rows = reinterpret_cast<uint32_t*>(take(size_t(nrows) * 4));
     float* fb_thr = reinterpret_cast<float*>(take(size_t(nrows) * 4));
     void* sym_ws = sym ? take(sym_workspace_bytes(n, a.sm_count)) : nullptr;
+    const bool sorted = sort_selected(n, a.row_begin, a.row_end, cosine);
+    float* skey = nullptr;
+    float* skey2 = nullptr;
+    uint32_t* sidx = nullptr;
+    uint32_t* perm = nullptr;
+    void* stemp = nullptr;
+    size_t stemp_bytes = 0;
+    if (a.row_begin == 0 && a.row_end == n) {  // reserved by tensor_workspace_bytes
+        skey = reinterpret_cast<float*>(take(size_t(n) * 4));
+        skey2 = reinterpret_cast<float*>(take(size_t(n) * 4));
+        sidx = reinterpret_cast<uint32_t*>(take(size_t(n) * 4));
+        perm = reinterpret_cast<uint32_t*>(take(size_t(n) * 4));
+        stemp_bytes = sort_temp_bytes(n);
+        stemp = take(stemp_bytes);
+    }
     unsigned int* maxabs = reinterpret_cast<unsigned int*>(scal);
     uint32_t* fb_count = reinterpret_cast<uint32_t*>(scal + 4);
     unsigned long long* gmax = reinterpret_cast<unsigned long long*>(scal + 8);
@@ -1314,9 +1412,18 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         if ((e = cudaMemsetAsync(mu, 0, size_t(d) * 4, st)) != cudaSuccess) return e;
     }
     maxabs_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, uint64_t(n) * d, d, mu, maxabs);
+    if (sorted) {
+        row_key_kernel<<<(n * 32 + 255) / 256, 256, 0, st>>>(a.X, n, d, mu, skey, sidx);
+        if ((e = cub::DeviceRadixSort::SortPairs(stemp, stemp_bytes, skey, skey2, sidx, perm, int(n), 0, 32, st)) !=
+            cudaSuccess)
+            return e;
+        launches += 2;
+    }
     PrepOut po{xh, alpha, rho, xnorm, gmax};
-    prep_kernel<<<(npad * 32 + 255) / 256, 256, 0, st>>>(a.X, n, d, npad, kc, mu, maxabs, cosine, po);
-    launches += 2;
+    prep_kernel<<<(npad * 32 + 255) / 256, 256, 0, st>>>(a.X, n, d, npad, kc, mu, maxabs, cosine,
+                                                          sorted ? perm : nullptr, po);
+    chunk_min_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(alpha, npad / 32, bmin);
+    launches += 3;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
     // Column groups: a group's fp16 reference tiles (BN x d x 2 B each) must
@@ -1329,7 +1436,7 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     if (group_tiles > ntiles) group_tiles = ntiles;
     const char* dbg = getenv("KNN_B200_DEBUG_SWEEP");
     SweepParams sp{xh,      alpha,   n,       npad,    kc, a.row_begin, a.row_end, group_tiles, dbg ? atoi(dbg) : 0,
-                   cand,    xh,      npad,    nullptr, nullptr, nullptr, 0};
+                   cand,    xh,      npad,    nullptr, nullptr, nullptr, 0, bmin};
     if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
     if (sym) {
         if ((e = run_sym_sweep(xh, alpha, n, npad, kc, cand, sym_ws, a.sm_count, st)) != cudaSuccess) return e;
@@ -1355,7 +1462,7 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
 
     RescoreParams rp{a.X,  n,         d,          a.klist,  kp,       a.row_begin, a.row_end, cand,
                      alpha, rho,      xnorm,      gmax,     maxabs,   a.fold,      a.out_sqrt, a.out_index,
-                     a.out_dist, fb_count, fb_rows, fb_thr, rescored, 0};
+                     a.out_dist, fb_count, fb_rows, fb_thr, rescored, 0, sorted ? perm : nullptr};
     {
         const char* fc = getenv("KNN_B200_FORCE_CAPTURE");
         rp.force_capture = fc && atoi(fc) != 0;
@@ -1390,10 +1497,11 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         if ((e = cudaMemsetAsync(cap_cnt, 0, size_t(nfb) * 4 + 8, st)) != cudaSuccess) return e;
         gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xh, npad, kc, fb_rows, nfb, mpad, xa);
         SweepParams cp{xh,      alpha,  n,    npad,   kc,      0,   nfb, group_tiles, 0,
-                       nullptr, xa,     mpad, fb_thr, cap_cnt, cap_buf, cap};
+                       nullptr, xa,     mpad, fb_thr, cap_cnt, cap_buf, cap, bmin};
         if ((e = launch_capture_sweep(kc <= uint32_t(TS_MAX_RES_KC), cp, nfb, st)) != cudaSuccess) return e;
         Rescore2Params r2{a.X,     n,       d,         a.klist,   a.row_begin, fb_rows,   nfb,      cap_cnt,
-                          cap_buf, cap,     a.out_sqrt, a.out_index, a.out_dist, fb2_count, fb2_rows, rescored};
+                          cap_buf, cap,     a.out_sqrt, a.out_index, a.out_dist, fb2_count, fb2_rows, rescored,
+                          sorted ? perm : nullptr};
         const size_t smem2 = size_t(4) * cap * 8;
         if (cosine) {
             cudaFuncSetAttribute(rescore_capture_kernel<kCosine>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
