@@ -465,25 +465,6 @@ tensor_sweep_kernel(const SweepParams p) {
                     if (fabsf(h) < kInf) h = __fsub_rn(h, 9.5367431640625e-07f * (fabsf(bm) + fabsf(thr.a)));  // 2^-20
                     if (!__any_sync(0xffffffffu, dmax > h) || p.debug_mode == 4) return;
                     load_beta(col0, bt);
-                    // second stage: the exact test (FFMA2 + FMNMX3 min tree, one
-                    // vote) before the per-pair mask and walk
-                    {
-                        float y[W], q1[11], q2[4];
-#pragma unroll
-                        for (int i = 0; i < P; ++i) {
-                            const float2 y2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], bt[2 * i], bt[2 * i + 1]);
-                            y[2 * i] = y2.x;
-                            y[2 * i + 1] = y2.y;
-                        }
-#pragma unroll
-                        for (int j = 0; j < 10; ++j) q1[j] = fminf(fminf(y[3 * j], y[3 * j + 1]), y[3 * j + 2]);
-                        q1[10] = fminf(y[30], y[31]);
-#pragma unroll
-                        for (int j = 0; j < 3; ++j) q2[j] = fminf(fminf(q1[3 * j], q1[3 * j + 1]), q1[3 * j + 2]);
-                        q2[3] = fminf(q1[9], q1[10]);
-                        if (!__any_sync(0xffffffffu, fminf(fminf(fminf(q2[0], q2[1]), q2[2]), q2[3]) < thr.a))
-                            return;
-                    }
                     // rare path: per-lane pair mask, then a warp-uniform walk over
                     // the admitted pairs; a pair's two values are picked with a
                     // 4-level select tree (no dynamic register indexing, one copy
