@@ -61,6 +61,11 @@ constexpr int SY_EW = 8;
 constexpr int SY_AGENT_WARP = 2 + SY_EW;
 constexpr int SY_THREADS = 64 + 32 * SY_EW + 32;
 constexpr int SY_QC = 8;     // shared queue entries per column
+// consecutive visitors of a rectangle tile are SY_SPREAD steps apart (the
+// 148 x SY_SPREAD-tile window of fp16 tiles must stay L2-resident)
+#ifndef SY_SPREAD
+#define SY_SPREAD 2
+#endif
 constexpr int SY_OVF = 128;  // global overflow entries per column (a block has 128 rows)
 constexpr uint32_t SY_A_CHUNK = SY_BM * 128;
 constexpr uint32_t SY_B_CHUNK = SY_BN * 128;
@@ -68,7 +73,7 @@ constexpr int SY_STAGES = 3;
 constexpr uint32_t SY_A_BYTES = 4 * SY_A_CHUNK;            // d <= 256: the block's rows stay resident
 constexpr uint32_t SY_LIST_PLANE = SY_KPL * SY_BN * 4;     // one [16][256] y plane (double-buffered)
 constexpr uint32_t SY_SMEM = 1024 + SY_A_BYTES + SY_STAGES * SY_B_CHUNK + 2 * SY_LIST_PLANE +
-                             2 * SY_QC * SY_BN * 4 + 2 * SY_BN * 4 + 256;
+                             2 * SY_QC * SY_BN * 4 + 2 * SY_BN * 4 + 32 + 256;
 static_assert(SY_SMEM <= 232448, "symmetric sweep shared memory");
 
 struct SymParams {
@@ -83,6 +88,7 @@ struct SymParams {
     float* thr_pub;      // [ntiles*256] published column-side prefilter thresholds
     uint32_t* version;   // [ntiles] completed rectangle visits
     uint64_t* overflow;  // [gridDim][256][SY_OVF]
+    const float* bmin;   // [npad / 32] smallest column norm per 32-column chunk
     int dbg;             // dev timing knob (KNN_B200_SYM_DEBUG): 2 = no column side, 3 = also no rotation (wrong results)
 };
 
@@ -112,7 +118,7 @@ struct SymWave {
         t_hi = (w * G + Gw - 1) / 2;
         nband = t_hi - t_lo;  // the wave's tiles except the block's own
         L = p.ntiles > t_hi + 1 ? p.ntiles - t_hi - 1 : 0;
-        rot = 2 * Gw <= L && p.dbg != 3;
+        rot = SY_SPREAD * Gw <= L && p.dbg != 3;
         base = G * w;
     }
     __device__ uint32_t visits(int diag) const { return diag ? 1u : nband + L; }
@@ -123,13 +129,13 @@ struct SymWave {
             return t >= b / 2 ? t + 1 : t;
         }
         const uint32_t s = j - nband;
-        return t_hi + 1 + (rot ? (s + 2 * r) % L : s);
+        return t_hi + 1 + (rot ? (s + SY_SPREAD * r) % L : s);
     }
     // position of this CTA's visit among the wave's visits of rectangle tile t
     __device__ uint32_t rank(uint32_t t) const {
         if (!rot) return base + r;
         const uint32_t qq = t - t_hi - 1;
-        const uint32_t c1 = qq / 2 < Gw - 1 ? qq / 2 : Gw - 1;
+        const uint32_t c1 = qq / SY_SPREAD < Gw - 1 ? qq / SY_SPREAD : Gw - 1;
         return base + (r <= c1 ? c1 - r : c1 + 1 + (Gw - 1 - r));
     }
 };
@@ -144,7 +150,8 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
     uint32_t* q_r = reinterpret_cast<uint32_t*>(q_y + SY_QC * SY_BN);              // [QC][256]
     float* thr_p = reinterpret_cast<float*>(q_r + SY_QC * SY_BN);                  // [256]
     uint32_t* q_n = reinterpret_cast<uint32_t*>(thr_p + SY_BN);                    // [256]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(q_n + SY_BN);
+    float* chunk_thr = reinterpret_cast<float*>(q_n + SY_BN);                      // [8] per 32 columns
+    uint64_t* bars = reinterpret_cast<uint64_t*>(chunk_thr + 8);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * SY_STAGES + 9);
     constexpr int S = SY_STAGES;
 
@@ -383,11 +390,6 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
             thr = reg_argmax();
             if (!valid) thr.a = -kInf;
             const float alpha_i = valid ? p.alpha[row] : kInf;
-            // column-side prefilter: fl(-2 dot - thrP_j) < -alpha_i (1 - 1e-6),
-            // thrP_j = thrC_j + 1e-6 (|thrC_j| + alpha_j), is a superset of
-            // fl(alpha_i - 2 dot) < thrC_j: y' >= -alpha_j bounds |y'| and the
-            // slack covers both roundings (2^-24 each) many times over.
-            const float c_lim = valid ? __fmul_rn(-alpha_i, 1.0f - 1e-6f) : -kInf;
             float thr_next = (colside && sw.L) ? thr_fetch(sw.tile(0, sw.nband)) : -kInf;
             for (uint32_t j = 0; j < nv; ++j, ++tcount) {
                 const uint32_t q = sw.tile(p.diag, j);
@@ -396,6 +398,9 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
                 if (sym) {
                     thr_p[et] = thr_next;
                     q_n[et] = 0;
+                    float cm = thr_next;  // this warp's 32 columns: the column-side chunk bound
+                    for (int o = 16; o; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+                    if (lane == 0) chunk_thr[et >> 5] = cm;
                     epi_barrier();
                     if (j + 1 < nv) thr_next = thr_fetch(sw.tile(0, j + 1));
                 }
@@ -403,19 +408,40 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
                 ptx::tc_fence_after();
                 const uint32_t cbase = q * SY_BN + seg0;
                 const uint32_t taddr = lane_addr + b * SY_BN + seg0;
-                auto process_row = [&](const uint32_t (&v)[32], const float (&bt)[32], uint32_t col0) {
-                    // row side: y = fl(beta_j - 2 dot)
-                    float m[16];
+                // One 32-column chunk (col0: global column, cloc: tile-local).
+                // Hot path, both sides on the raw dots and one max tree:
+                //   row side    y  = fl(beta_j - 2 dot) < thr_i    needs dot > (bmin_chunk - thr_i) / 2;
+                //   column side y' = fl(alpha_i - 2 dot) < thrP_j  needs dot > (alpha_i - max_chunk thrP) / 2.
+                // Both bounds get a 2^-20 slack (rounding of y at y ~ thr is
+                // ~2^-24 |thr|), so they are supersets of the exact tests the
+                // rare paths then apply.
+                auto process = [&](const uint32_t (&v)[32], uint32_t col0, uint32_t cloc) {
+                    float r1[11], r2[4];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const float2 y2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], bt[2 * i], bt[2 * i + 1]);
-                        m[i] = fminf(y2.x, y2.y);
+                    for (int j2 = 0; j2 < 10; ++j2)
+                        r1[j2] = fmaxf(fmaxf(__uint_as_float(v[3 * j2]), __uint_as_float(v[3 * j2 + 1])),
+                                       __uint_as_float(v[3 * j2 + 2]));
+                    r1[10] = fmaxf(__uint_as_float(v[30]), __uint_as_float(v[31]));
+#pragma unroll
+                    for (int j2 = 0; j2 < 3; ++j2) r2[j2] = fmaxf(fmaxf(r1[3 * j2], r1[3 * j2 + 1]), r1[3 * j2 + 2]);
+                    r2[3] = fmaxf(r1[9], r1[10]);
+                    const float dmax = fmaxf(fmaxf(fmaxf(r2[0], r2[1]), r2[2]), r2[3]);
+                    const float bm = __ldg(p.bmin + (col0 >> 5));
+                    float hr = __fmul_rn(__fsub_rn(bm, thr.a), 0.5f);
+                    if (fabsf(hr) < kInf) hr = __fsub_rn(hr, 9.5367431640625e-07f * (fabsf(bm) + fabsf(thr.a)));
+                    const bool fire_r = dmax > hr;
+                    bool fire_c = false;
+                    if (sym && valid) {
+                        const float tcm = chunk_thr[cloc >> 5];
+                        float hc = __fmul_rn(__fsub_rn(alpha_i, tcm), 0.5f);
+                        if (fabsf(hc) < kInf) hc = __fsub_rn(hc, 9.5367431640625e-07f * (fabsf(alpha_i) + fabsf(tcm)));
+                        fire_c = dmax > hc;
                     }
-#pragma unroll
-                    for (int w2 = 8; w2 >= 1; w2 >>= 1)
-#pragma unroll
-                        for (int i = 0; i < w2; ++i) m[i] = fminf(m[i], m[i + w2]);
-                    if (__any_sync(0xffffffffu, m[0] < thr.a)) {
+                    if (!__any_sync(0xffffffffu, fire_r || fire_c)) return;
+                    if (__any_sync(0xffffffffu, fire_r)) {
+                        // row side rare path: exact y, per-lane pair mask, warp-uniform walk
+                        float bt[32];
+                        load_vec32(p.alpha + col0, bt);
                         uint32_t pm = 0;
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
@@ -442,34 +468,21 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
                             }
                         }
                     }
-                };
-                // column side: candidate row i for column j's list, y' = fl(alpha_i - 2 dot)
-                // (a second pass over TMEM keeps each pass's registers at the row pass's level)
-                auto process_col = [&](const uint32_t (&v)[32], uint32_t cloc) {
-                    float tc[32];
-                    load_vec32(thr_p + cloc, tc);
-                    float zm[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const float2 z2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], -tc[2 * i], -tc[2 * i + 1]);
-                        zm[i] = fminf(z2.x, z2.y);
-                    }
-#pragma unroll
-                    for (int w2 = 8; w2 >= 1; w2 >>= 1)
-#pragma unroll
-                        for (int i = 0; i < w2; ++i) zm[i] = fminf(zm[i], zm[i + w2]);
-                    const bool ccand = zm[0] < c_lim;
-                    if (__any_sync(0xffffffffu, ccand)) {
+                    if (fire_c) {
+                        // column side: exact prefilter per column, fl(-2 dot - thrP_j) <
+                        // -alpha_i (1 - 1e-6) is a superset of fl(alpha_i - 2 dot) < thrP_j
+                        // (y' >= -alpha_j bounds |y'|; the slack covers both roundings),
+                        // then per-lane queue pushes (no convergence needed)
+                        float tc[32];
+                        load_vec32(thr_p + cloc, tc);
+                        const float c_lim = __fmul_rn(-alpha_i, 1.0f - 1e-6f);
                         uint32_t pm = 0;
-                        if (ccand) {
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) {
-                                const float2 z2 =
-                                    ptx::ffma2_m2(v[2 * i], v[2 * i + 1], -tc[2 * i], -tc[2 * i + 1]);
-                                if (fminf(z2.x, z2.y) < c_lim) pm |= 1u << i;
-                            }
+                        for (int i = 0; i < 16; ++i) {
+                            const float2 z2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], -tc[2 * i], -tc[2 * i + 1]);
+                            if (fminf(z2.x, z2.y) < c_lim) pm |= 1u << i;
                         }
-                        while (pm) {  // per-lane: queue pushes need no warp convergence
+                        while (pm) {
                             const int i = __ffs(pm) - 1;
                             pm &= pm - 1;
                             uint32_t v0 = v[0], v1 = v[1];
@@ -502,45 +515,22 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
                         }
                     }
                 };
-                auto release_tmem = [&]() {
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(tempty_bar(b));
-                };
                 uint32_t va[32], vb[32];
-                {
-                    float ba[32], bb[32];
-                    ptx::tmem_ld_32x32b_x32(taddr, va);
-                    load_vec32(p.alpha + cbase, ba);
+                ptx::tmem_ld_32x32b_x32(taddr, va);
 #pragma unroll 1
-                    for (int c0 = 0; c0 < SY_BN / 2; c0 += 64) {
-                        ptx::tmem_wait_ld();
-                        ptx::tmem_ld_32x32b_x32(taddr + c0 + 32, vb);
-                        load_vec32(p.alpha + cbase + c0 + 32, bb);
-                        process_row(va, ba, cbase + c0);
-                        ptx::tmem_wait_ld();
-                        if (c0 + 64 < SY_BN / 2) {
-                            ptx::tmem_ld_32x32b_x32(taddr + c0 + 64, va);
-                            load_vec32(p.alpha + cbase + c0 + 64, ba);
-                        } else if (sym) {
-                            ptx::tmem_ld_32x32b_x32(taddr, va);  // column pass, first slice
-                        } else {
-                            release_tmem();
-                        }
-                        process_row(vb, bb, cbase + c0 + 32);
+                for (int c0 = 0; c0 < SY_BN / 2; c0 += 64) {
+                    ptx::tmem_wait_ld();
+                    ptx::tmem_ld_32x32b_x32(taddr + c0 + 32, vb);
+                    process(va, cbase + c0, seg0 + c0);
+                    ptx::tmem_wait_ld();
+                    if (c0 + 64 < SY_BN / 2) {
+                        ptx::tmem_ld_32x32b_x32(taddr + c0 + 64, va);
+                    } else {
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(tempty_bar(b));
                     }
-                }
-                if (sym) {
-#pragma unroll 1
-                    for (int c0 = 0; c0 < SY_BN / 2; c0 += 64) {
-                        ptx::tmem_wait_ld();
-                        ptx::tmem_ld_32x32b_x32(taddr + c0 + 32, vb);
-                        process_col(va, seg0 + c0);
-                        ptx::tmem_wait_ld();
-                        if (c0 + 64 < SY_BN / 2) ptx::tmem_ld_32x32b_x32(taddr + c0 + 64, va);
-                        else release_tmem();
-                        process_col(vb, seg0 + c0 + 32);
-                    }
+                    process(vb, cbase + c0 + 32, seg0 + c0 + 32);
                 }
                 if (sym) {
                     epi_barrier();  // every candidate queued
@@ -549,7 +539,7 @@ __global__ void __launch_bounds__(SY_THREADS, 1) tensor_sym_kernel(const SymPara
                     ++vcount;
                     // merge: thread et owns column et of the tile (row crow's list)
                     const uint32_t crow = q * SY_BN + et;
-                    if (crow < p.n) {
+                    if (crow < p.n && q_n[et] != 0) {
                         const uint32_t a_base = ptx::smem_u32(cl_a + lb * SY_KPL * SY_BN + et);
                         float* ga = p.cla + size_t(q) * SY_KPL * SY_BN + et;
                         uint32_t* gi = p.cli + size_t(q) * SY_KPL * SY_BN + et;
@@ -671,8 +661,8 @@ size_t sym_workspace_bytes(uint32_t n, int sm_count) {
     return b;
 }
 
-cudaError_t run_sym_sweep(const uint8_t* xh, const float* alpha, uint32_t n, uint32_t npad, uint32_t kc,
-                          uint64_t* cand, void* ws, int sm_count, cudaStream_t st) {
+cudaError_t run_sym_sweep(const uint8_t* xh, const float* alpha, const float* bmin, uint32_t n, uint32_t npad,
+                          uint32_t kc, uint64_t* cand, void* ws, int sm_count, cudaStream_t st) {
     const uint32_t ntiles = (n + SY_BN - 1) / SY_BN;
     const uint32_t nrb = (n + SY_BM - 1) / SY_BM;
     uint8_t* w = static_cast<uint8_t*>(ws);
@@ -696,7 +686,7 @@ cudaError_t run_sym_sweep(const uint8_t* xh, const float* alpha, uint32_t n, uin
     uint32_t grid = nrb < uint32_t(sm_count) ? nrb : uint32_t(sm_count);
     if (grid < nrb) grid &= ~1u;
     const char* dbg = getenv("KNN_B200_SYM_DEBUG");
-    SymParams sp{xh, alpha, n, npad, kc, nrb, ntiles, 1, cand, cla, cli, thr_pub, version, overflow,
+    SymParams sp{xh, alpha, n, npad, kc, nrb, ntiles, 1, cand, cla, cli, thr_pub, version, overflow, bmin,
                  dbg ? atoi(dbg) : 0};
     tensor_sym_kernel<<<grid, SY_THREADS, SY_SMEM, st>>>(sp);  // prepass: own tiles, seeds column lists
     if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -1166,8 +1166,8 @@ uint32_t tensor_kp_for(uint32_t klist) {
 static bool sym_selected(uint32_t n, uint32_t d, uint32_t klist, uint32_t row_begin, uint32_t row_end) {
     const char* e = getenv("KNN_B200_SYM");
     if (!e || atoi(e) == 0) return false;
-    const TensorCfg c = tensor_cfg(klist);
-    return c.kpl == 16 && c.nseg == 2 && row_begin == 0 && row_end == n && d <= 256 && n >= 1024;
+    // its lists: two 16-entry row-side segments and one 16-entry column-side list
+    return klist + 1 + 5 <= 16 && row_begin == 0 && row_end == n && d <= 256 && n >= 1024;
 }
 
 size_t capture_workspace_bytes(uint32_t m, uint32_t d, uint32_t cap) {
@@ -1420,7 +1420,7 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
                    cand,    xh,      npad,    nullptr, nullptr, nullptr, 0, bmin};
     if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
     if (sym) {
-        if ((e = run_sym_sweep(xh, alpha, n, npad, kc, cand, sym_ws, a.sm_count, st)) != cudaSuccess) return e;
+        if ((e = run_sym_sweep(xh, alpha, bmin, n, npad, kc, cand, sym_ws, a.sm_count, st)) != cudaSuccess) return e;
         launches += 3;
     } else {
         // CTA pairs (default; KNN_B200_PAIR=0 disables) need whole 256-row

@@ -13,3 +13,9 @@ from sym_schedule_check import check  # noqa: E402
                                    (5000, 8), (9999, 6), (30000, 10), (12345, 16), (70000, 132)])
 def test_visit_protocol(n, sms):
     assert check(n, sms) == "ok"
+
+
+@pytest.mark.parametrize("spread", [1, 4, 8])
+def test_visit_protocol_spreads(spread):
+    for n, sms in ((100000, 148), (30000, 10), (262144, 148)):
+        assert check(n, sms, spread) == "ok"

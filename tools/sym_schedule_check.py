@@ -16,7 +16,7 @@ from collections import defaultdict
 BM, BN = 128, 256
 
 
-def visit_sequences(n: int, sms: int = 148):
+def visit_sequences(n: int, sms: int = 148, spread: int = 2):
     nrb, T = (n + BM - 1) // BM, (n + BN - 1) // BN
     G = min(nrb, sms)
     if G < nrb:
@@ -31,11 +31,11 @@ def visit_sequences(n: int, sms: int = 148):
                 continue
             t_hi = (w * G + Gw - 1) // 2
             L = T - t_hi - 1 if T > t_hi + 1 else 0
-            rot = 2 * Gw <= L
+            rot = spread * Gw <= L
             for s in range(L):
-                qq = (s + 2 * c) % L if rot else s
+                qq = (s + spread * c) % L if rot else s
                 if rot:
-                    c1 = min(qq // 2, Gw - 1)
+                    c1 = min(qq // spread, Gw - 1)
                     rk = c1 - c if c <= c1 else c1 + 1 + (Gw - 1 - c)
                 else:
                     rk = c
@@ -44,8 +44,8 @@ def visit_sequences(n: int, sms: int = 148):
     return seqs
 
 
-def check(n: int, sms: int = 148) -> str:
-    seqs = visit_sequences(n, sms)
+def check(n: int, sms: int = 148, spread: int = 2) -> str:
+    seqs = visit_sequences(n, sms, spread)
     per = defaultdict(list)
     for seq in seqs:
         for t, v, _ in seq:
