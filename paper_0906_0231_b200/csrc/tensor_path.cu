@@ -93,6 +93,30 @@ struct SweepParams {
     const float* bmin;  // [npad / 32] smallest column norm of every 32-column chunk
 };
 
+// Candidate keys from the norm-sorted sweep carry sweep-order column indices;
+// map them to input indices once (the rescores and the reference's
+// (distance, index) tie-break work in input order).
+__global__ void remap_kernel(uint64_t* __restrict__ keys, size_t count, const uint32_t* __restrict__ perm) {
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += size_t(gridDim.x) * blockDim.x) {
+        const uint64_t k = keys[i];
+        if (k != kEmptyKey) keys[i] = (k & 0xffffffff00000000ull) | perm[uint32_t(k)];
+    }
+}
+
+// The same for the capture buffers: only the first min(cnt, cap) entries of
+// each slot were written.
+__global__ void remap_capture_kernel(uint64_t* __restrict__ buf, const uint32_t* __restrict__ cnt, uint32_t m,
+                                     uint32_t cap, const uint32_t* __restrict__ perm) {
+    const uint32_t slot = blockIdx.x;
+    if (slot >= m) return;
+    const uint32_t c = min(cnt[slot], cap);
+    uint64_t* b = buf + size_t(slot) * cap;
+    for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) {
+        const uint64_t k = b[i];
+        b[i] = (k & 0xffffffff00000000ull) | perm[uint32_t(k)];
+    }
+}
+
 // Persistent sweep.  Work item = (column group g, row block rb); every CTA
 // walks g = 0, 1, ... and, inside a group, its row blocks rb = blockIdx.x,
 // blockIdx.x + gridDim.x, ...  All CTAs therefore stream the same column
@@ -873,11 +897,10 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     bool done[PER];
     uint32_t valid = 0;
     auto rescore_one = [&](int m) {
-        const uint32_t cs = uint32_t(ak[m]);
+        const uint32_t col = uint32_t(ak[m]);  // input order (remap_kernel)
         ek[m] = kEmptyKey;
         done[m] = true;
-        if (ak[m] != kEmptyKey && cs != q) {
-            const uint32_t col = p.perm ? p.perm[cs] : cs;  // input index: the reference's tie-break
+        if (ak[m] != kEmptyKey && col != qo) {
             const float* xc = p.X + size_t(col) * p.d;
             // Reference argument order (larger index first) -- the fold is
             // symmetric bit for bit, kept for clarity.
@@ -1082,10 +1105,9 @@ __global__ void __launch_bounds__(128) rescore_capture_kernel(const Rescore2Para
     const uint64_t* in = p.buf + size_t(slot) * p.cap;
     uint32_t valid = 0;
     for (uint32_t i = lane; i < c; i += 32) {
-        const uint32_t cs = uint32_t(in[i]);
+        const uint32_t col = uint32_t(in[i]);  // input order (remap_kernel)
         uint64_t key = kEmptyKey;
-        if (cs != q) {
-            const uint32_t col = p.perm ? p.perm[cs] : cs;
+        if (col != qo) {
             const float* xc = p.X + size_t(col) * p.d;
             const float dist = col > qo ? exact_fold_rows<FOLD>(xc, xq, p.d, vec) : exact_fold_rows<FOLD>(xq, xc, p.d, vec);
             key = make_key(dist, col);
@@ -1440,6 +1462,10 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         ++launches;
     }
     if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
+    if (sorted) {
+        remap_kernel<<<a.sm_count * 8, 256, 0, st>>>(cand, size_t(nrows) * kp, perm);
+        ++launches;
+    }
 
     RescoreParams rp{a.X,  n,         d,          a.klist,  kp,       a.row_begin, a.row_end, cand,
                      alpha, rho,      xnorm,      gmax,     maxabs,   a.fold,      a.out_sqrt, a.out_index,
@@ -1480,6 +1506,10 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         SweepParams cp{xh,      alpha,  n,    npad,   kc,      0,   nfb, group_tiles, 0,
                        nullptr, xa,     mpad, fb_thr, cap_cnt, cap_buf, cap, bmin};
         if ((e = launch_capture_sweep(kc <= uint32_t(TS_MAX_RES_KC), cp, nfb, st)) != cudaSuccess) return e;
+        if (sorted) {
+            remap_capture_kernel<<<nfb, 128, 0, st>>>(cap_buf, cap_cnt, nfb, cap, perm);
+            ++launches;
+        }
         Rescore2Params r2{a.X,     n,       d,         a.klist,   a.row_begin, fb_rows,   nfb,      cap_cnt,
                           cap_buf, cap,     a.out_sqrt, a.out_index, a.out_dist, fb2_count, fb2_rows, rescored,
                           sorted ? perm : nullptr};
