@@ -772,7 +772,7 @@ struct RescoreParams {
     float* fb_thr;        // capture threshold (y space) for each unproven row
     unsigned long long* rescored;
     int force_capture;    // testing: treat every row as unproven (KNN_B200_FORCE_CAPTURE=1)
-    const uint32_t* perm;  // norm-sorted order: sweep row/column r is input row perm[r] (or null)
+    const uint32_t* rowpos;  // norm-sorted columns: input row q sits at position rowpos[q] of alpha/rho/xnorm (or null)
 };
 
 constexpr double kTcSafety = 4.0;  // tensor-core accumulation error allowance
@@ -848,8 +848,8 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t slot = blockIdx.x * 8 + warp;
     if (slot >= p.row_end - p.row_begin) return;
-    const uint32_t q = p.row_begin + slot;               // sweep order
-    const uint32_t qo = p.perm ? p.perm[q] : q;          // input order
+    const uint32_t qo = p.row_begin + slot;               // input order
+    const uint32_t q = p.rowpos ? p.rowpos[qo] : qo;      // its position in the sorted per-row arrays
     const uint64_t* cand = p.cand + size_t(slot) * KP;
     const float* xq = p.X + size_t(qo) * p.d;
     const bool vec = (p.d % 4 == 0);
@@ -1030,12 +1030,12 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     if (!complete) {
         if (lane == 0) {
             const uint32_t at = atomicAdd(p.fb_count, 1u);
-            p.fb_rows[at] = q;
+            p.fb_rows[at] = qo;  // input order
             p.fb_thr[at] = __double2float_ru(cap_y);
         }
         return;
     }
-    const size_t orow = size_t(qo - p.row_begin);  // input order (perm only on whole problems)
+    const size_t orow = slot;
     for (uint32_t t = lane; t < p.klist; t += 32) {
         const uint64_t key = keys_s[warp][t];
         const float dv = ordered_to_float(uint32_t(key >> 32));
@@ -1049,15 +1049,18 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
 
 // Copy the swizzled fp16 rows rows[0..m) into a compact plane set (re-swizzled
 // for their new row positions); padding rows are zero.
+// xa row r = xh row map[rows[r]] (map: input index -> sorted position, or
+// null), re-swizzled for its new position.  rows null: rows[r] = row0 + r.
 __global__ void gather_rows_kernel(const uint8_t* __restrict__ xh, uint32_t npad, uint32_t kc,
-                                   const uint32_t* __restrict__ rows, uint32_t m, uint32_t mpad,
-                                   uint8_t* __restrict__ xa) {
+                                   const uint32_t* __restrict__ rows, uint32_t row0, uint32_t m, uint32_t mpad,
+                                   const uint32_t* __restrict__ map, uint8_t* __restrict__ xa) {
     const uint32_t total = kc * mpad * 8;  // 16-byte units
     for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < total; u += gridDim.x * blockDim.x) {
         const uint32_t unit = u & 7, r = (u >> 3) % mpad, c = (u >> 3) / mpad;
         uint4 v = make_uint4(0, 0, 0, 0);
         if (r < m) {
-            const uint32_t src = rows[r];
+            const uint32_t in = rows ? rows[r] : row0 + r;
+            const uint32_t src = map ? map[in] : in;
             v = *reinterpret_cast<const uint4*>(xh + (size_t(c) * npad + src) * 128 + ((unit ^ (src & 7)) << 4));
         }
         *reinterpret_cast<uint4*>(xa + (size_t(c) * mpad + r) * 128 + ((unit ^ (r & 7)) << 4)) = v;
@@ -1079,7 +1082,6 @@ struct Rescore2Params {
     uint32_t* fb2_count;
     uint32_t* fb2_rows;
     unsigned long long* rescored;
-    const uint32_t* perm;  // as in RescoreParams
 };
 
 // Exact fold of every captured column of an unproven row (one warp per row);
@@ -1092,8 +1094,7 @@ __global__ void __launch_bounds__(128) rescore_capture_kernel(const Rescore2Para
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t slot = blockIdx.x * 4 + warp;
     if (slot >= p.m) return;
-    const uint32_t q = p.rows[slot];            // sweep order
-    const uint32_t qo = p.perm ? p.perm[q] : q;  // input order
+    const uint32_t qo = p.rows[slot];  // input order
     uint64_t* ks = keys2 + size_t(warp) * p.cap;
     const uint32_t c = p.cnt[slot];
     if (c > p.cap) {
@@ -1214,14 +1215,19 @@ static size_t sort_temp_bytes(uint32_t n) {
 }
 
 static size_t sort_workspace_bytes(uint32_t n) {
-    return 4 * ((size_t(n) * 4 + 255) / 256 * 256) + (sort_temp_bytes(n) + 255) / 256 * 256;
+    return 5 * ((size_t(n) * 4 + 255) / 256 * 256) + (sort_temp_bytes(n) + 255) / 256 * 256;
 }
 
-// Sort the sweep's rows and columns by norm when the call covers the whole
-// problem (KNN_B200_SORT=0 disables; cosine norms are all equal already).
-static bool sort_selected(uint32_t n, uint32_t row_begin, uint32_t row_end, int cosine) {
+__global__ void invert_perm_kernel(const uint32_t* __restrict__ perm, uint32_t n, uint32_t* __restrict__ pos) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) pos[perm[i]] = i;
+}
+
+// Sort the sweep's columns by norm (KNN_B200_SORT=0 disables; cosine norms
+// are all equal already; the symmetric sweep keeps input order).  Query rows
+// stay in input order: the sweep reads them from compact gathered planes.
+static bool sort_selected(int cosine, bool sym) {
     const char* e = getenv("KNN_B200_SORT");
-    return !(e && atoi(e) == 0) && !cosine && row_begin == 0 && row_end == n;
+    return !(e && atoi(e) == 0) && !cosine && !sym;
 }
 
 size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32_t row_end, uint32_t klist,
@@ -1245,7 +1251,8 @@ size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32
     add(size_t(rows) * 4);         // fallback rows
     add(size_t(rows) * 4);         // capture thresholds
     if (sym) add(sym_workspace_bytes(n, sm_count));
-    if (row_begin == 0 && row_end == n) add(sort_workspace_bytes(n));  // norm-sorted order
+    add(sort_workspace_bytes(n));                                 // norm-sorted columns
+    add(size_t(kc) * ((rows + 255) / 256 * 256) * 128);          // query rows in input order
     return b;
 }
 
@@ -1382,21 +1389,16 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     uint32_t* fb_rows = reinterpret_cast<uint32_t*>(take(size_t(nrows) * 4));
     float* fb_thr = reinterpret_cast<float*>(take(size_t(nrows) * 4));
     void* sym_ws = sym ? take(sym_workspace_bytes(n, a.sm_count)) : nullptr;
-    const bool sorted = sort_selected(n, a.row_begin, a.row_end, cosine);
-    float* skey = nullptr;
-    float* skey2 = nullptr;
-    uint32_t* sidx = nullptr;
-    uint32_t* perm = nullptr;
-    void* stemp = nullptr;
-    size_t stemp_bytes = 0;
-    if (a.row_begin == 0 && a.row_end == n) {  // reserved by tensor_workspace_bytes
-        skey = reinterpret_cast<float*>(take(size_t(n) * 4));
-        skey2 = reinterpret_cast<float*>(take(size_t(n) * 4));
-        sidx = reinterpret_cast<uint32_t*>(take(size_t(n) * 4));
-        perm = reinterpret_cast<uint32_t*>(take(size_t(n) * 4));
-        stemp_bytes = sort_temp_bytes(n);
-        stemp = take(stemp_bytes);
-    }
+    const bool sorted = sort_selected(cosine, sym);
+    float* skey = reinterpret_cast<float*>(take(size_t(n) * 4));
+    float* skey2 = reinterpret_cast<float*>(take(size_t(n) * 4));
+    uint32_t* sidx = reinterpret_cast<uint32_t*>(take(size_t(n) * 4));
+    uint32_t* perm = reinterpret_cast<uint32_t*>(take(size_t(n) * 4));    // sorted position -> input row
+    uint32_t* rowpos = reinterpret_cast<uint32_t*>(take(size_t(n) * 4));  // input row -> sorted position
+    size_t stemp_bytes = sort_temp_bytes(n);
+    void* stemp = take(stemp_bytes);
+    const uint32_t qpad = (nrows + 255) / 256 * 256;
+    uint8_t* xq_planes = take(size_t(kc) * qpad * 128);  // the call's query rows, input order
     unsigned int* maxabs = reinterpret_cast<unsigned int*>(scal);
     uint32_t* fb_count = reinterpret_cast<uint32_t*>(scal + 4);
     unsigned long long* gmax = reinterpret_cast<unsigned long long*>(scal + 8);
@@ -1420,13 +1422,19 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         if ((e = cub::DeviceRadixSort::SortPairs(stemp, stemp_bytes, skey, skey2, sidx, perm, int(n), 0, 32, st)) !=
             cudaSuccess)
             return e;
-        launches += 2;
+        invert_perm_kernel<<<a.sm_count * 4, 256, 0, st>>>(perm, n, rowpos);
+        launches += 3;
     }
     PrepOut po{xh, alpha, rho, xnorm, gmax};
     prep_kernel<<<(npad * 32 + 255) / 256, 256, 0, st>>>(a.X, n, d, npad, kc, mu, maxabs, cosine,
                                                           sorted ? perm : nullptr, po);
     chunk_min_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(alpha, npad / 32, bmin);
     launches += 3;
+    if (sorted) {  // query rows back in input order for the A operand
+        gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xh, npad, kc, nullptr, a.row_begin, nrows, qpad, rowpos,
+                                                           xq_planes);
+        ++launches;
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
     // Column groups: a group's fp16 reference tiles (BN x d x 2 B each) must
@@ -1438,8 +1446,12 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     if (group_tiles < 1) group_tiles = 1;
     if (group_tiles > ntiles) group_tiles = ntiles;
     const char* dbg = getenv("KNN_B200_DEBUG_SWEEP");
-    SweepParams sp{xh,      alpha,   n,       npad,    kc, a.row_begin, a.row_end, group_tiles, dbg ? atoi(dbg) : 0,
-                   cand,    xh,      npad,    nullptr, nullptr, nullptr, 0, bmin};
+    // sorted: the A operand is the compact input-order copy of the call's rows
+    const uint32_t sr0 = sorted ? 0 : a.row_begin, sr1 = sorted ? nrows : a.row_end;
+    const uint8_t* xa_rows = sorted ? xq_planes : xh;
+    const uint32_t npad_a = sorted ? qpad : npad;
+    SweepParams sp{xh,   alpha,  n,       npad,    kc, sr0, sr1, group_tiles, dbg ? atoi(dbg) : 0,
+                   cand, xa_rows, npad_a, nullptr, nullptr, nullptr, 0, bmin};
     if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
     if (sym) {
         if ((e = run_sym_sweep(xh, alpha, bmin, n, npad, kc, cand, sym_ws, a.sm_count, st)) != cudaSuccess) return e;
@@ -1450,8 +1462,7 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         // L2->SM operand traffic and cut the sweep ~3%.
         const char* pe = getenv("KNN_B200_PAIR");
         const bool pair = !(pe && atoi(pe) == 0) && kc <= uint32_t(TS_MAX_RES_KC) && cfg.nseg == 2 &&
-                          (cfg.kpl == 12 || cfg.kpl == 16) && a.row_begin % 256 == 0 &&
-                          a.row_begin + (nrows + 255) / 256 * 256 <= npad;
+                          (cfg.kpl == 12 || cfg.kpl == 16) && sr0 % 256 == 0 && sr0 + (nrows + 255) / 256 * 256 <= npad_a;
         if (pair) {
             e = cfg.kpl == 12 ? launch_sweep_pair<12, 256, 8>(sp, nrows, st)
                               : launch_sweep_pair<16, 256, 8>(sp, nrows, st);
@@ -1469,7 +1480,7 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
 
     RescoreParams rp{a.X,  n,         d,          a.klist,  kp,       a.row_begin, a.row_end, cand,
                      alpha, rho,      xnorm,      gmax,     maxabs,   a.fold,      a.out_sqrt, a.out_index,
-                     a.out_dist, fb_count, fb_rows, fb_thr, rescored, 0, sorted ? perm : nullptr};
+                     a.out_dist, fb_count, fb_rows, fb_thr, rescored, 0, sorted ? rowpos : nullptr};
     {
         const char* fc = getenv("KNN_B200_FORCE_CAPTURE");
         rp.force_capture = fc && atoi(fc) != 0;
@@ -1502,7 +1513,8 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         uint32_t* fb2_rows = reinterpret_cast<uint32_t*>(take2(size_t(nfb) * 4));
         uint32_t* fb2_count = cap_cnt + nfb;
         if ((e = cudaMemsetAsync(cap_cnt, 0, size_t(nfb) * 4 + 8, st)) != cudaSuccess) return e;
-        gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xh, npad, kc, fb_rows, nfb, mpad, xa);
+        gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xh, npad, kc, fb_rows, 0, nfb, mpad,
+                                                           sorted ? rowpos : nullptr, xa);
         SweepParams cp{xh,      alpha,  n,    npad,   kc,      0,   nfb, group_tiles, 0,
                        nullptr, xa,     mpad, fb_thr, cap_cnt, cap_buf, cap, bmin};
         if ((e = launch_capture_sweep(kc <= uint32_t(TS_MAX_RES_KC), cp, nfb, st)) != cudaSuccess) return e;
@@ -1511,8 +1523,7 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
             ++launches;
         }
         Rescore2Params r2{a.X,     n,       d,         a.klist,   a.row_begin, fb_rows,   nfb,      cap_cnt,
-                          cap_buf, cap,     a.out_sqrt, a.out_index, a.out_dist, fb2_count, fb2_rows, rescored,
-                          sorted ? perm : nullptr};
+                          cap_buf, cap,     a.out_sqrt, a.out_index, a.out_dist, fb2_count, fb2_rows, rescored};
         const size_t smem2 = size_t(4) * cap * 8;
         if (cosine) {
             cudaFuncSetAttribute(rescore_capture_kernel<kCosine>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
