@@ -40,6 +40,8 @@ constexpr int TS_BM = 128;
 constexpr uint32_t TS_A_CHUNK = TS_BM * 128;  // 128 rows x 128 B (64 fp16 of K)
 constexpr uint32_t TS_SMEM_MAX = 232448;
 constexpr int TS_MAX_RES_KC = 4;              // A resident in smem when d <= 256
+constexpr int kTriCap = 192;   // triangle mode: column-side buffer entries per row
+constexpr int kTriRank = 12;   // its threshold: the 12th of a row's 24 sample candidates
 
 // EW epilogue warps (4 or 8).  With 8, two warps share each TMEM lane
 // quadrant and split every tile's columns in halves; each half keeps its own
@@ -91,6 +93,14 @@ struct SweepParams {
     uint64_t* cap_buf;
     uint32_t cap;
     const float* bmin;  // [npad / 32] smallest column norm of every 32-column chunk
+    // triangle mode (TRI kernels): rows and columns are the same sorted set;
+    // a row unit sweeps only tiles >= its own and also offers each of its rows
+    // to the columns' fixed-threshold buffers (the column side)
+    const float* tc;     // [npad] column-side threshold: a row enters column j's buffer iff y' < tc[j]
+    const float* tcmax;  // [npad / 32] its maximum per 32-column chunk
+    uint64_t* cbuf;      // [npad][ccap] column-side candidates (y', row)
+    uint32_t* ccnt;      // [npad] their counts
+    uint32_t ccap;
 };
 
 // Candidate keys from the norm-sorted sweep carry sweep-order column indices;
@@ -124,11 +134,12 @@ __global__ void remap_capture_kernel(uint64_t* __restrict__ buf, const uint32_t*
 // come from HBM once per group instead of once per row block.  The per-row
 // candidate lists are written to `cand` at the end of each item and read
 // back when the row block's next group starts.
-template <int KPL, int BN, bool ARES, int EW, bool CAPTURE, bool PAIR = false>
+template <int KPL, int BN, bool ARES, int EW, bool CAPTURE, bool PAIR = false, bool TRI = false>
 __global__ void __launch_bounds__(TSLayout<KPL, BN, ARES, EW, PAIR>::THREADS, 1)
 tensor_sweep_kernel(const SweepParams p) {
     using L = TSLayout<KPL, BN, ARES, EW, PAIR>;
     static_assert(!PAIR || (ARES && !CAPTURE), "CTA pairs: resident A, no capture");
+    static_assert(!TRI || (PAIR && BN == 256 && KPL <= 16), "triangle mode: CTA pairs, 256-column tiles");
     constexpr int S = L::STAGES;
     constexpr int NSEG = L::NSEG;
     constexpr int SEG_COLS = BN / NSEG;  // columns of a tile one epilogue warp filters
@@ -160,6 +171,8 @@ tensor_sweep_kernel(const SweepParams p) {
     const uint32_t unit_step = PAIR ? gridDim.x / 2 : gridDim.x;
     const uint32_t nunits = PAIR ? (nrb + 1) / 2 : nrb;
     auto unit_block = [&](uint32_t u) { return PAIR ? 2 * u + rank : u; };
+    // TRI: a pair unit's 256 rows are exactly tile u; it sweeps tiles >= u
+    auto tri_start = [&](uint32_t u) -> uint32_t { return TRI ? u : 0u; };
     // Column groups: all of them in order (lists carry over from group to
     // group) -- except in CAPTURE mode, whose fixed thresholds let blockIdx.y
     // take a share of the groups so that few rows still fill the GPU.
@@ -212,6 +225,8 @@ tensor_sweep_kernel(const SweepParams p) {
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
                 for (uint32_t u = unit0; u < nunits; u += unit_step) {
                     const uint32_t r0 = p.row_begin + unit_block(u) * TS_BM;
+                    const uint32_t ts = max(t0, tri_start(u));
+                    if (ts >= t1) continue;
                     if constexpr (ARES) {  // A stays resident for the item; reload once the MMA released it
                         wait(aempty_bar, a_phase ^ 1);
                         ptx::mbar_arrive_expect_tx(afull_bar, p.kc * TS_A_CHUNK);
@@ -220,7 +235,7 @@ tensor_sweep_kernel(const SweepParams p) {
                                           p.xa + (size_t(kc) * p.npad_a + r0) * 128, TS_A_CHUNK, afull_bar);
                         a_phase ^= 1;
                     }
-                    for (uint32_t t = t0; t < t1; ++t) {
+                    for (uint32_t t = ts; t < t1; ++t) {
                         for (uint32_t kc = 0; kc < p.kc; ++kc) {
                             wait(empty_bar(stage), phase ^ 1);
                             if (p.debug_mode == 3) {  // profiling: MMA on stale tiles, no loads
@@ -259,10 +274,12 @@ tensor_sweep_kernel(const SweepParams p) {
             for (uint32_t g = g_first; g < ngroups; g += g_step) {
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
                 for (uint32_t u = unit0; u < nunits; u += unit_step) {
+                    const uint32_t ts = max(t0, tri_start(u));
+                    if (ts >= t1) continue;
                     wait(afull_bar, a_phase);
                     a_phase ^= 1;
                     ptx::mbar_arrive_remote_relaxed(lead_afull);
-                    for (uint32_t t = t0; t < t1; ++t)
+                    for (uint32_t t = ts; t < t1; ++t)
                         for (uint32_t kc = 0; kc < p.kc; ++kc) {
                             wait(full_bar(stage), phase);
                             ptx::mbar_arrive_remote_relaxed(lead_full0 + 8u * stage);
@@ -291,11 +308,13 @@ tensor_sweep_kernel(const SweepParams p) {
             for (uint32_t g = g_first; g < ngroups; g += g_step) {
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
                 for (uint32_t u = unit0; u < nunits; u += unit_step) {
+                    const uint32_t ts = max(t0, tri_start(u));
+                    if (ts >= t1) continue;
                     if constexpr (ARES) {
                         wait(afull_bar, a_phase);
                         a_phase ^= 1;
                     }
-                    for (uint32_t t = t0; t < t1; ++t, ++tcount) {
+                    for (uint32_t t = ts; t < t1; ++t, ++tcount) {
                         const uint32_t b = tcount & 1, use = tcount >> 1;
                         wait(tempty_bar(b), (use & 1) ^ 1);
                         ptx::tc_fence_after();
@@ -412,8 +431,12 @@ tensor_sweep_kernel(const SweepParams p) {
         for (uint32_t g = g_first; g < ngroups; g += g_step) {
             const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
             for (uint32_t u = unit0; u < nunits; u += unit_step) {
+                const uint32_t tsu = tri_start(u), ts = max(t0, tsu);
+                if (ts >= t1) continue;
+                const bool fresh = TRI ? t0 <= tsu : g == 0;  // the unit's first group with work
                 const uint32_t row = p.row_begin + unit_block(u) * TS_BM + rl;
                 const bool valid = row < p.row_end;
+                const float alpha_i = TRI && valid ? p.alpha[row] : kInf;  // column side: this row's norm
                 uint64_t* state = p.cand + (size_t(row - p.row_begin) * NSEG + seg) * KPL;
                 // Columns are ranked by y = fl(beta_j - 2 dot): alpha_i is
                 // constant along a row; the rescore forms A = alpha_i + y in fp64.
@@ -424,12 +447,12 @@ tensor_sweep_kernel(const SweepParams p) {
                 } else if constexpr (REGLIST) {
 #pragma unroll
                     for (int s = 0; s < KPL; ++s) {
-                        const uint64_t key = (g == 0 || !valid) ? kEmptyKey : state[s];
+                        const uint64_t key = (fresh || !valid) ? kEmptyKey : state[s];
                         la[s] = key == kEmptyKey ? kInf : ordered_to_float(uint32_t(key >> 32));
                         lx[s] = uint32_t(key);
                     }
                     thr = reg_argmax();
-                } else if (g == 0 || !valid) {
+                } else if (fresh || !valid) {
 #pragma unroll 4
                     for (int s = 0; s < KPL; ++s) {
                         my_a[s * L::LIST_ROWS] = kInf;
@@ -448,7 +471,7 @@ tensor_sweep_kernel(const SweepParams p) {
                 // One W-column chunk.  direct: position among the first KPL
                 // columns this thread sees (first tile of group 0, shared-memory
                 // lists only), or -1.
-                auto process = [&](const uint32_t (&v)[W], uint32_t col0, int direct) {
+                auto process = [&](const uint32_t (&v)[W], uint32_t col0, int direct, bool cside) {
                     constexpr int P = W / 2;  // column pairs
                     float bt[W];              // the chunk's column norms, loaded only when needed
                     if constexpr (!REGLIST) {
@@ -487,7 +510,66 @@ tensor_sweep_kernel(const SweepParams p) {
                     const float bm = __ldg(p.bmin + (col0 >> 5));
                     float h = __fmul_rn(__fsub_rn(bm, thr.a), 0.5f);
                     if (fabsf(h) < kInf) h = __fsub_rn(h, 9.5367431640625e-07f * (fabsf(bm) + fabsf(thr.a)));  // 2^-20
-                    if (!__any_sync(0xffffffffu, dmax > h) || p.debug_mode == 4) return;
+                    const bool fire_r = dmax > h;
+                    bool fire_c = false;
+                    if constexpr (TRI) {
+                        // column side: y' = fl(alpha_i - 2 dot) < tc_j needs
+                        // dot > (alpha_i - max_chunk tc) / 2 (same slack argument)
+                        if (cside && valid) {
+                            const float tcm = __ldg(p.tcmax + (col0 >> 5));
+                            float hc = __fmul_rn(__fsub_rn(alpha_i, tcm), 0.5f);
+                            if (fabsf(hc) < kInf)
+                                hc = __fsub_rn(hc, 9.5367431640625e-07f * (fabsf(alpha_i) + fabsf(tcm)));
+                            fire_c = dmax > hc;
+                        }
+                    }
+                    if (!__any_sync(0xffffffffu, fire_r || fire_c) || p.debug_mode == 4) return;
+                    if constexpr (TRI) {
+                        if (fire_c) {  // per lane: exact y' against each column's threshold, append
+                            float tcv[W];
+                            {
+                                const float4* t4 = reinterpret_cast<const float4*>(p.tc + col0);
+#pragma unroll
+                                for (int q4 = 0; q4 < W / 4; ++q4) {
+                                    const float4 f = __ldg(t4 + q4);
+                                    tcv[4 * q4] = f.x;
+                                    tcv[4 * q4 + 1] = f.y;
+                                    tcv[4 * q4 + 2] = f.z;
+                                    tcv[4 * q4 + 3] = f.w;
+                                }
+                            }
+                            // mask of admitted columns, then one append site per
+                            // admitted column (a select tree picks its dot; the
+                            // scalar FMA reproduces the FFMA2 value bit for bit)
+                            uint32_t cm = 0;
+#pragma unroll
+                            for (int i = 0; i < P; ++i) {
+                                const float2 y2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], alpha_i, alpha_i);
+                                if (y2.x < tcv[2 * i]) cm |= 1u << (2 * i);
+                                if (y2.y < tcv[2 * i + 1]) cm |= 1u << (2 * i + 1);
+                            }
+                            while (cm) {
+                                const int bpos = __ffs(cm) - 1;
+                                cm &= cm - 1;
+                                const uint32_t col = col0 + bpos;
+                                if (col >= p.n) continue;
+                                uint32_t t16[16];
+#pragma unroll
+                                for (int q = 0; q < 16; ++q) t16[q] = (bpos & 16) ? v[q + 16] : v[q];
+#pragma unroll
+                                for (int q = 0; q < 8; ++q) t16[q] = (bpos & 8) ? t16[q + 8] : t16[q];
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) t16[q] = (bpos & 4) ? t16[q + 4] : t16[q];
+#pragma unroll
+                                for (int q = 0; q < 2; ++q) t16[q] = (bpos & 2) ? t16[q + 2] : t16[q];
+                                const uint32_t vb = (bpos & 1) ? t16[1] : t16[0];
+                                const float yv = __fmaf_rn(-2.0f, __uint_as_float(vb), alpha_i);
+                                const uint32_t at = atomicAdd(p.ccnt + col, 1u);
+                                if (at < p.ccap) p.cbuf[size_t(col) * p.ccap + at] = make_key(yv, row);
+                            }
+                        }
+                        if (!__any_sync(0xffffffffu, fire_r)) return;
+                    }
                     load_beta(col0, bt);
                     // rare path: per-lane pair mask, then a warp-uniform walk over
                     // the admitted pairs; a pair's two values are picked with a
@@ -536,13 +618,14 @@ tensor_sweep_kernel(const SweepParams p) {
                         }
                     }
                 };
-                for (uint32_t t = t0; t < t1; ++t, ++tcount) {
+                for (uint32_t t = ts; t < t1; ++t, ++tcount) {
                     const uint32_t b = tcount & 1, use = tcount >> 1;
                     wait(tfull_bar(b), use & 1);
                     ptx::tc_fence_after();
                     const uint32_t cbase = t * BN + seg0;
                     const uint32_t taddr = lane_addr + b * BN + seg0;
                     const bool first = DIRECT && g == 0 && t == 0;
+                    const bool cside = TRI && t > tsu;  // tiles above the unit's own: both sides
                     // Next tile's column norms into L1 now, so the in-loop
                     // loads of that tile hit L1 instead of paying L2 latency.
                     if (lane < SEG_COLS / 32 && t + 1 < t1)
@@ -569,7 +652,7 @@ tensor_sweep_kernel(const SweepParams p) {
                     for (int c0 = 0; c0 < SEG_COLS; c0 += 64) {
                         ptx::tmem_wait_ld();
                         ptx::tmem_ld_32x32b_x32(taddr + c0 + 32, vb);
-                        process(va, cbase + c0, (first && c0 < KPL) ? c0 : -1);
+                        process(va, cbase + c0, (first && c0 < KPL) ? c0 : -1, cside);
                         ptx::tmem_wait_ld();
                         if (c0 + 64 < SEG_COLS) {
                             ptx::tmem_ld_32x32b_x32(taddr + c0 + 64, va);
@@ -578,7 +661,7 @@ tensor_sweep_kernel(const SweepParams p) {
                             __syncwarp();
                             if (lane == 0) release_acc(b);
                         }
-                        process(vb, cbase + c0 + 32, (first && c0 + 32 < KPL) ? c0 + 32 : -1);
+                        process(vb, cbase + c0 + 32, (first && c0 + 32 < KPL) ? c0 + 32 : -1, cside);
                     }
                 }
                 if (valid && !CAPTURE) {
@@ -634,6 +717,47 @@ __global__ void row_key_kernel(const float* __restrict__ X, uint32_t n, uint32_t
         key[row] = s;
         idx[row] = row;
     }
+}
+
+// ---- triangle mode helpers --------------------------------------------------
+
+__global__ void iota_stride_kernel(uint32_t* __restrict__ out, uint32_t m, uint32_t stride) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) out[i] = i * stride;
+}
+
+__global__ void gather_alpha_kernel(const float* __restrict__ alpha, const uint32_t* __restrict__ rows, uint32_t m,
+                                    uint32_t mpad, float* __restrict__ out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mpad; i += gridDim.x * blockDim.x)
+        out[i] = i < m ? alpha[rows[i]] : __int_as_float(0x7f800000);
+}
+
+// Column-side threshold of row j: the r-th smallest y among its KP sample
+// candidates (any value is correct -- it only sets how many rows the column
+// side appends); padding rows get -inf (never admit).
+__global__ void tri_threshold_kernel(const uint64_t* __restrict__ cand, uint32_t n, uint32_t npad, uint32_t kp,
+                                     uint32_t r, float* __restrict__ tc) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < npad; j += gridDim.x * blockDim.x) {
+        float t = -__int_as_float(0x7f800000);
+        if (j < n) {
+            const uint64_t* c = cand + size_t(j) * kp;
+            uint64_t best = kEmptyKey;
+            for (uint32_t a = 0; a < kp; ++a) {
+                uint32_t below = 0;
+                for (uint32_t b = 0; b < kp; ++b) below += c[b] < c[a];
+                if (below == r - 1) best = c[a];
+            }
+            t = best == kEmptyKey ? __int_as_float(0x7f800000) : ordered_to_float(uint32_t(best >> 32));
+        }
+        tc[j] = t;
+    }
+}
+
+__global__ void chunk_max_kernel(const float* __restrict__ v, uint32_t nchunks, float* __restrict__ out) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= nchunks) return;
+    float m = v[size_t(warp) * 32 + lane];
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) out[warp] = m;
 }
 
 // bmin[c] = smallest alpha of columns [32c, 32c + 32) (the sweep's hot-path bound)
@@ -773,6 +897,10 @@ struct RescoreParams {
     unsigned long long* rescored;
     int force_capture;    // testing: treat every row as unproven (KNN_B200_FORCE_CAPTURE=1)
     const uint32_t* rowpos;  // norm-sorted columns: input row q sits at position rowpos[q] of alpha/rho/xnorm (or null)
+    const uint32_t* rowperm;  // triangle sweep: slot s is sorted position s, input row rowperm[s] (or null)
+    const uint64_t* xbuf;     // [slots][XC] extra candidates (column side of the triangle sweep)
+    const uint32_t* xcnt;     // [slots] their counts (> XC: overflowed)
+    const float* xbound;      // [slots] y bound of the column side's exclusions
 };
 
 constexpr double kTcSafety = 4.0;  // tensor-core accumulation error allowance
@@ -841,29 +969,36 @@ __device__ __forceinline__ double proof_bound(uint32_t d, const unsigned int* ma
     return s2 * Tp + 2.0 * e_all;
 }
 
-template <int FOLD, int KP, int NSEG>
+// XC > 0: up to XC extra candidates per row (the triangle sweep's column side,
+// p.xbuf/p.xcnt) whose exclusions are bounded by p.xbound[slot].
+template <int FOLD, int KP, int NSEG, int XC = 0>
 __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     constexpr int KPL = KP / NSEG;
-    __shared__ uint64_t keys_s[8][KP];
+    constexpr int KT = KP + XC;  // candidates per row
+    __shared__ uint64_t keys_s[8][KT];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t slot = blockIdx.x * 8 + warp;
     if (slot >= p.row_end - p.row_begin) return;
-    const uint32_t qo = p.row_begin + slot;               // input order
-    const uint32_t q = p.rowpos ? p.rowpos[qo] : qo;      // its position in the sorted per-row arrays
+    // slot: input order, or (p.rowperm) a position in the sorted order
+    const uint32_t qo = p.rowperm ? p.rowperm[slot] : p.row_begin + slot;  // input row
+    const uint32_t q = p.rowperm ? slot : (p.rowpos ? p.rowpos[qo] : qo);  // its sorted position
     const uint64_t* cand = p.cand + size_t(slot) * KP;
     const float* xq = p.X + size_t(qo) * p.d;
     const bool vec = (p.d % 4 == 0);
-    constexpr int PER = (KP + 31) / 32;
+    constexpr int PER = (KT + 31) / 32;
+    const uint32_t xn = XC ? p.xcnt[slot] : 0;
+    // candidates actually present (the rank loops stop there; the rest are empty)
+    const int KA = XC ? KP + int(xn < uint32_t(XC) ? xn : uint32_t(XC)) : KP;
+    const uint64_t* xb = XC ? p.xbuf + size_t(slot) * XC : nullptr;
     const double alpha_q = double(p.alpha[q]);
-    // approximate keys and their rank (keys are unique: distinct columns)
+    // approximate keys (unique: distinct columns)
     uint64_t ak[PER];
-    uint32_t arank[PER];
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
         const int i = lane + 32 * m;
-        ak[m] = i < KP ? cand[i] : kEmptyKey;
-        if (i < KP) keys_s[warp][i] = ak[m];
-        arank[m] = 0;
+        if constexpr (XC > 0) ak[m] = i < KP ? cand[i] : (i < KT && uint32_t(i - KP) < xn ? xb[i - KP] : kEmptyKey);
+        else ak[m] = i < KP ? cand[i] : kEmptyKey;
+        if (i < KT) keys_s[warp][i] = ak[m];
     }
     __syncwarp();
     if constexpr (NSEG == 3) {
@@ -885,11 +1020,6 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         for (int m = 0; m < PER; ++m)
             if (lane + 32 * m < KP) keys_s[warp][lane + 32 * m] = ak[m];
         __syncwarp();
-    }
-    for (int j = 0; j < KP; ++j) {
-        const uint64_t o = keys_s[warp][j];
-#pragma unroll
-        for (int m = 0; m < PER; ++m) arank[m] += (o < ak[m]) || (o == ak[m] && j < lane + 32 * m);
     }
     __syncwarp();
     // exact fold of candidate m of this lane into keys_s
@@ -913,14 +1043,14 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         __syncwarp();
 #pragma unroll
         for (int m = 0; m < PER; ++m)
-            if (lane + 32 * m < KP) keys_s[warp][lane + 32 * m] = done[m] ? ek[m] : kEmptyKey;
+            if (lane + 32 * m < KT) keys_s[warp][lane + 32 * m] = done[m] ? ek[m] : kEmptyKey;
         __syncwarp();
         uint64_t kth = kEmptyKey;
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
-            if (lane + 32 * m >= KP || !done[m] || ek[m] == kEmptyKey) continue;
+            if (lane + 32 * m >= KT || !done[m] || ek[m] == kEmptyKey) continue;
             uint32_t r = 0;
-            for (int j = 0; j < KP; ++j) r += keys_s[warp][j] < ek[m];
+            for (int j = 0; j < KA; ++j) r += keys_s[warp][j] < ek[m];
             if (r == p.klist - 1) kth = ek[m];
         }
         for (int o = 16; o; o >>= 1) {
@@ -929,13 +1059,36 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         }
         return kth;
     };
-    // Phase 1: the k + 4 best candidates by approximate distance.
-    const uint32_t r1 = p.klist + 4 < uint32_t(KP) ? p.klist + 4 : uint32_t(KP);
+    // Phase 1: the k + 4 best candidates by approximate distance, picked by
+    // k + 4 rounds of a warp-wide minimum (keys are unique: distinct columns).
+    const uint32_t r1 = p.klist + 4 < uint32_t(KT) ? p.klist + 4 : uint32_t(KT);
+    bool sel[PER];
+#pragma unroll
+    for (int m = 0; m < PER; ++m) sel[m] = false;
+    for (uint32_t r = 0; r < r1; ++r) {
+        uint64_t mn = kEmptyKey;
+        int mm = -1;
+#pragma unroll
+        for (int m = 0; m < PER; ++m)
+            if (!sel[m] && ak[m] < mn) {
+                mn = ak[m];
+                mm = m;
+            }
+        uint64_t wmin = mn;
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t other = __shfl_xor_sync(0xffffffffu, wmin, o);
+            wmin = other < wmin ? other : wmin;
+        }
+        if (wmin == kEmptyKey) break;
+#pragma unroll
+        for (int m = 0; m < PER; ++m)
+            if (m == mm && mn == wmin) sel[m] = true;
+    }
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
         done[m] = false;
         ek[m] = kEmptyKey;
-        if (lane + 32 * m < KP && arank[m] < r1) rescore_one(m);
+        if (sel[m]) rescore_one(m);
     }
     // Phase 2: any other candidate whose approximate distance is inside the
     // bound implied by phase 1's k-th exact distance (those beyond cannot be
@@ -948,7 +1101,7 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
                                     double(ordered_to_float(uint32_t(kth1 >> 32))));
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
-            if (lane + 32 * m >= KP || done[m]) continue;
+            if (lane + 32 * m >= KT || done[m]) continue;
             const double a = alpha_q + double(ordered_to_float(uint32_t(ak[m] >> 32)));
             if (ak[m] != kEmptyKey && a <= lim) rescore_one(m);
             else done[m] = true;  // excluded: stays empty
@@ -962,22 +1115,26 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     __syncwarp();
 #pragma unroll
     for (int m = 0; m < PER; ++m)
-        if (lane + 32 * m < KP) keys_s[warp][lane + 32 * m] = ek[m];
+        if (lane + 32 * m < KT) keys_s[warp][lane + 32 * m] = ek[m];
     __syncwarp();
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
-        mine[m] = lane + 32 * m < KP ? ek[m] : kEmptyKey;
+        mine[m] = lane + 32 * m < KT ? ek[m] : kEmptyKey;
         rank[m] = 0;
     }
-    for (int j = 0; j < KP; ++j) {
-        const uint64_t o = keys_s[warp][j];
+    // ranks of the computed keys only (empty entries are never output)
 #pragma unroll
-        for (int m = 0; m < PER; ++m) rank[m] += (o < mine[m]) || (o == mine[m] && j < lane + 32 * m);
+    for (int m = 0; m < PER; ++m) {
+        if (mine[m] == kEmptyKey) continue;
+        for (int j = 0; j < KA; ++j) {
+            const uint64_t o = keys_s[warp][j];
+            rank[m] += (o < mine[m]) || (o == mine[m] && j < lane + 32 * m);
+        }
     }
     __syncwarp();
 #pragma unroll
     for (int m = 0; m < PER; ++m)
-        if (lane + 32 * m < KP) keys_s[warp][rank[m]] = mine[m];
+        if (lane + 32 * m < KT && mine[m] != kEmptyKey) keys_s[warp][rank[m]] = mine[m];
     __syncwarp();
     // Each of the NSEG lists is unsorted; per list its largest key.  A list
     // holding an empty slot saw (and kept) every column of its segment, so
@@ -1010,9 +1167,21 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
             last_approx = segmax[s] < last_approx ? segmax[s] : last_approx;
         }
     }
+    bool x_overflow = false;
+    if constexpr (XC > 0) {
+        // the column side excluded only candidates with y >= xbound; a buffer
+        // that overflowed lost candidates -- no proof for this row
+        const float xbnd = p.xbound[slot];
+        if (xbnd < __int_as_float(0x7f800000)) {
+            const uint64_t xk = make_key(xbnd, 0u);
+            any_full = true;
+            last_approx = xk < last_approx ? xk : last_approx;
+        }
+        x_overflow = xn > uint32_t(XC);
+    }
     bool complete;
     double cap_y = __longlong_as_double(0x7ff0000000000000ll);  // +inf: capture everything
-    if (!any_full) {
+    if (!any_full && !x_overflow) {
         complete = true;  // every column was offered into a non-full list: the list holds all of them
     } else if (valid < p.klist) {
         complete = false;
@@ -1022,7 +1191,9 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         // the list ranks y = fl(beta - 2 dot); A = alpha_q + y exactly in fp64
         const double a_max = double(p.alpha[q]) + double(ordered_to_float(uint32_t(last_approx >> 32)));
         const double bound = proof_bound<FOLD>(p.d, p.maxabs, p.gmax, p.xnorm[q], p.rho[q], double(p.alpha[q]), T);
-        complete = a_max > bound && !p.force_capture;
+        // (an overflowed column-side buffer lost candidates: no proof, but T
+        // is still an upper bound on the k-th distance, so the band holds)
+        complete = a_max > bound && !p.force_capture && !x_overflow;
         // every true neighbor has A <= bound, i.e. y <= bound - alpha_q: the
         // second (band-capture) pass collects exactly that band
         cap_y = bound - double(p.alpha[q]);
@@ -1035,7 +1206,7 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         }
         return;
     }
-    const size_t orow = slot;
+    const size_t orow = p.rowperm ? size_t(qo) : size_t(slot);
     for (uint32_t t = lane; t < p.klist; t += 32) {
         const uint64_t key = keys_s[warp][t];
         const float dv = ordered_to_float(uint32_t(key >> 32));
@@ -1257,10 +1428,10 @@ size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32
 }
 
 // CTA-pair sweep (cluster of 2): one pair per two SMs, persistent.
-template <int KPL, int BN, int EW>
+template <int KPL, int BN, int EW, bool TRI = false>
 static cudaError_t launch_sweep_pair(const SweepParams& sp, uint32_t nrows, cudaStream_t stream) {
     using L = TSLayout<KPL, BN, true, EW, true>;
-    auto kern = tensor_sweep_kernel<KPL, BN, true, EW, false, true>;
+    auto kern = tensor_sweep_kernel<KPL, BN, true, EW, false, true, TRI>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::SMEM));
     if (e != cudaSuccess) return e;
     const uint32_t npairs = (nrows + 2 * TS_BM - 1) / (2 * TS_BM);
@@ -1452,8 +1623,68 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     const uint32_t npad_a = sorted ? qpad : npad;
     SweepParams sp{xh,   alpha,  n,       npad,    kc, sr0, sr1, group_tiles, dbg ? atoi(dbg) : 0,
                    cand, xa_rows, npad_a, nullptr, nullptr, nullptr, 0, bmin};
+    // Triangle mode (experimental, KNN_B200_TRI=1): each unordered pair once.
+    // A sample pass (every 8th sorted column) fixes every row's column-side
+    // threshold; the sweep then covers tiles >= each row pair's own, offering
+    // pairs to the row side (lists) and the column side (fixed-threshold
+    // buffers), and the rescore merges both.
+    const char* te = getenv("KNN_B200_TRI");
+    const bool tri = te && atoi(te) != 0 && sorted && a.row_begin == 0 && a.row_end == n && cfg.kpl == 12 &&
+                     cfg.nseg == 2 && kc <= uint32_t(TS_MAX_RES_KC) && n >= 4096;
+    uint64_t* tri_cbuf = nullptr;
+    uint32_t* tri_ccnt = nullptr;
+    float* tri_tc = nullptr;
     if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
-    if (sym) {
+    if (tri) {
+        const uint32_t stride = 8, sm = (n + stride - 1) / stride, spad = (sm + 255) / 256 * 256;
+        size_t need = 0;
+        auto add = [&](size_t x) { need += (x + 255) / 256 * 256; };
+        add(size_t(sm) * 4);                  // sample rows
+        add(size_t(kc) * spad * 128);         // sample planes
+        add(size_t(spad) * 4);                // sample alpha
+        add(size_t(spad / 32) * 4);           // sample bmin
+        add(size_t(n) * 24 * 8);              // sample lists
+        add(size_t(npad) * 4);                // tc
+        add(size_t(npad / 32) * 4);           // tcmax
+        add(size_t(npad) * kTriCap * 8);      // column-side buffers
+        add(size_t(npad) * 4);                // counts
+        uint8_t* w3 = static_cast<uint8_t*>(a.alloc2(a.alloc2_ctx, need));
+        if (!w3) return cudaErrorMemoryAllocation;
+        auto take3 = [&](size_t x) {
+            uint8_t* q = w3;
+            w3 += (x + 255) / 256 * 256;
+            return q;
+        };
+        uint32_t* srows = reinterpret_cast<uint32_t*>(take3(size_t(sm) * 4));
+        uint8_t* xs = take3(size_t(kc) * spad * 128);
+        float* alpha_s = reinterpret_cast<float*>(take3(size_t(spad) * 4));
+        float* bmin_s = reinterpret_cast<float*>(take3(size_t(spad / 32) * 4));
+        uint64_t* cand_s = reinterpret_cast<uint64_t*>(take3(size_t(n) * 24 * 8));
+        tri_tc = reinterpret_cast<float*>(take3(size_t(npad) * 4));
+        float* tcmax = reinterpret_cast<float*>(take3(size_t(npad / 32) * 4));
+        tri_cbuf = reinterpret_cast<uint64_t*>(take3(size_t(npad) * kTriCap * 8));
+        tri_ccnt = reinterpret_cast<uint32_t*>(take3(size_t(npad) * 4));
+        iota_stride_kernel<<<a.sm_count, 256, 0, st>>>(srows, sm, stride);
+        gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xh, npad, kc, srows, 0, sm, spad, nullptr, xs);
+        gather_alpha_kernel<<<a.sm_count, 256, 0, st>>>(alpha, srows, sm, spad, alpha_s);
+        chunk_min_kernel<<<(spad / 32 * 32 + 255) / 256, 256, 0, st>>>(alpha_s, spad / 32, bmin_s);
+        // sample pass: every row (sorted order) against the sample columns
+        uint32_t gts = uint32_t((40ull << 20) / (uint64_t(256) * kc * 128));
+        const uint32_t stiles = spad / 256;
+        gts = gts < 1 ? 1 : (gts > stiles ? stiles : gts);
+        SweepParams ss{xs,     alpha_s, sm,      spad,    kc, 0, n, gts, 0,
+                       cand_s, xh,      npad,    nullptr, nullptr, nullptr, 0, bmin_s};
+        if ((e = launch_sweep_pair<12, 256, 8>(ss, n, st)) != cudaSuccess) return e;
+        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, npad, 24, kTriRank, tri_tc);
+        chunk_max_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(tri_tc, npad / 32, tcmax);
+        if ((e = cudaMemsetAsync(tri_ccnt, 0, size_t(npad) * 4, st)) != cudaSuccess) return e;
+        // the triangle sweep: rows are the sorted set itself
+        SweepParams tp{xh,   alpha, n,    npad,    kc, 0, n, group_tiles, dbg ? atoi(dbg) : 0,
+                       cand, xh,    npad, nullptr, nullptr, nullptr, 0, bmin,
+                       tri_tc, tcmax, tri_cbuf, tri_ccnt, kTriCap};
+        if ((e = launch_sweep_pair<12, 256, 8, true>(tp, n, st)) != cudaSuccess) return e;
+        launches += 8;
+    } else if (sym) {
         if ((e = run_sym_sweep(xh, alpha, bmin, n, npad, kc, cand, sym_ws, a.sm_count, st)) != cudaSuccess) return e;
         launches += 3;
     } else {
@@ -1477,6 +1708,10 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         remap_kernel<<<a.sm_count * 8, 256, 0, st>>>(cand, size_t(nrows) * kp, perm);
         ++launches;
     }
+    if (tri) {  // column-side entries: sorted row ids -> input rows
+        remap_capture_kernel<<<n, 128, 0, st>>>(tri_cbuf, tri_ccnt, n, kTriCap, perm);
+        ++launches;
+    }
 
     RescoreParams rp{a.X,  n,         d,          a.klist,  kp,       a.row_begin, a.row_end, cand,
                      alpha, rho,      xnorm,      gmax,     maxabs,   a.fold,      a.out_sqrt, a.out_index,
@@ -1485,7 +1720,19 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         const char* fc = getenv("KNN_B200_FORCE_CAPTURE");
         rp.force_capture = fc && atoi(fc) != 0;
     }
-    e = cosine ? launch_rescore<kCosine>(cfg, rp, nrows, st) : launch_rescore<kSqEuclidean>(cfg, rp, nrows, st);
+    if (tri) {  // slots are sorted positions; both sides' candidates
+        rp.rowpos = nullptr;
+        rp.rowperm = perm;
+        rp.xbuf = tri_cbuf;
+        rp.xcnt = tri_ccnt;
+        rp.xbound = tri_tc;
+        const dim3 grid((nrows + 7) / 8);
+        if (cosine) rescore_kernel<kCosine, 24, 2, kTriCap><<<grid, 256, 0, st>>>(rp);
+        else rescore_kernel<kSqEuclidean, 24, 2, kTriCap><<<grid, 256, 0, st>>>(rp);
+        e = cudaGetLastError();
+    } else {
+        e = cosine ? launch_rescore<kCosine>(cfg, rp, nrows, st) : launch_rescore<kSqEuclidean>(cfg, rp, nrows, st);
+    }
     if (e != cudaSuccess) return e;
     ++launches;
 

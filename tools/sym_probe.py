@@ -1,4 +1,5 @@
-"""GPU probe of the symmetric TENSOR sweep (KNN_B200_SYM=1) against the oracle (dev tool)."""
+"""GPU probe of an opt-in sweep variant against the oracle (dev tool).
+usage: sym_probe.py [ENV_VAR]   (default KNN_B200_SYM; e.g. KNN_B200_TRI)"""
 import os, sys, time
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -6,11 +7,12 @@ import numpy as np
 import oracle
 from paper_0906_0231_b200 import Context, _lib, distance_by_name
 
+KNOB = sys.argv[1] if len(sys.argv) > 1 else "KNN_B200_SYM"
 co = oracle.c_oracle()
 ctx = Context(0)
 cases = [(1100, 33, 1, "sqeuclidean"), (2048, 64, 10, "sqeuclidean"), (2048, 64, 10, "hellinger"),
          (4096, 256, 10, "euclidean"), (5000, 100, 5, "cosine"), (3000, 17, 3, "sqeuclidean"),
-         (20000, 256, 10, "euclidean")]
+         (20000, 256, 10, "euclidean"), (70000, 64, 10, "sqeuclidean"), (9000, 200, 7, "hellinger")]
 for n, d, k, m in cases:
     x = co.generate(n, d, 11)
     if m == "cosine":
@@ -20,7 +22,7 @@ for n, d, k, m in cases:
     if m == "euclidean":
         rd = np.sqrt(rd)
     for sym in ("0", "1"):
-        os.environ["KNN_B200_SYM"] = sym
+        os.environ[KNOB] = sym
         t0 = time.time()
         idx, dist, st = ctx.solve(x, k, distance_by_name(m), _lib.ARITH_TENSOR)
         dt = time.time() - t0
