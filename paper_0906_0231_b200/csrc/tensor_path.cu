@@ -41,7 +41,8 @@ constexpr uint32_t TS_A_CHUNK = TS_BM * 128;  // 128 rows x 128 B (64 fp16 of K)
 constexpr uint32_t TS_SMEM_MAX = 232448;
 constexpr int TS_MAX_RES_KC = 4;              // A resident in smem when d <= 256
 constexpr int kTriCap = 192;   // triangle mode: column-side buffer entries per row
-constexpr int kTriRank = 12;   // its threshold: the 12th of a row's 24 sample candidates
+constexpr int kTriRank = 6;    // its threshold: the 6th of a row's 24 sample candidates
+constexpr int kTriStride = 12; // sample: every 12th sorted column (C2: 6 -> ~0.06% rows unproven)
 
 // EW epilogue warps (4 or 8).  With 8, two warps share each TMEM lane
 // quadrant and split every tile's columns in halves; each half keeps its own
@@ -749,6 +750,61 @@ __global__ void tri_threshold_kernel(const uint64_t* __restrict__ cand, uint32_t
             t = best == kEmptyKey ? __int_as_float(0x7f800000) : ordered_to_float(uint32_t(best >> 32));
         }
         tc[j] = t;
+    }
+}
+
+// Per row: the kTriSel smallest column-side candidates (warp minimum rounds)
+// and the bound for everything else -- min(threshold, the next key) -- so the
+// rescore handles a short fixed-size list.  An overflowed buffer is passed on
+// as a count above kTriSel (no proof).
+constexpr int kTriSel = 24;
+__global__ void tri_select_kernel(const uint64_t* __restrict__ buf, const uint32_t* __restrict__ cnt, uint32_t cap,
+                                  uint32_t n, const float* __restrict__ thr, uint64_t* __restrict__ out,
+                                  uint32_t* __restrict__ out_cnt, float* __restrict__ out_bound) {
+    const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const uint32_t c = cnt[row];
+    const uint32_t m = c < cap ? c : cap;
+    constexpr int PER = (192 + 31) / 32;
+    uint64_t k[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const uint32_t i = lane + 32 * q;
+        k[q] = i < m ? buf[size_t(row) * cap + i] : kEmptyKey;
+    }
+    uint64_t* o = out + size_t(row) * kTriSel;
+    uint64_t next = kEmptyKey;  // the (kTriSel+1)-th smallest
+    for (int r = 0; r <= kTriSel; ++r) {
+        uint64_t mn = kEmptyKey;
+        int mq = -1;
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+            if (k[q] < mn) {
+                mn = k[q];
+                mq = q;
+            }
+        uint64_t w = mn;
+        for (int s = 16; s; s >>= 1) {
+            const uint64_t other = __shfl_xor_sync(0xffffffffu, w, s);
+            w = other < w ? other : w;
+        }
+        if (r < kTriSel) {
+            if (lane == 0) o[r] = w;
+        } else {
+            next = w;
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+            if (q == mq && mn == w) k[q] = kEmptyKey;
+    }
+    if (lane == 0) {
+        float b = thr[row];
+        if (next != kEmptyKey) {
+            const float nb = ordered_to_float(uint32_t(next >> 32));
+            b = nb < b ? nb : b;
+        }
+        out_bound[row] = b;
+        out_cnt[row] = c > cap ? uint32_t(kTriSel) + 1 : (m < uint32_t(kTriSel) ? m : uint32_t(kTriSel));
     }
 }
 
@@ -1623,20 +1679,28 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     const uint32_t npad_a = sorted ? qpad : npad;
     SweepParams sp{xh,   alpha,  n,       npad,    kc, sr0, sr1, group_tiles, dbg ? atoi(dbg) : 0,
                    cand, xa_rows, npad_a, nullptr, nullptr, nullptr, 0, bmin};
-    // Triangle mode (experimental, KNN_B200_TRI=1): each unordered pair once.
-    // A sample pass (every 8th sorted column) fixes every row's column-side
-    // threshold; the sweep then covers tiles >= each row pair's own, offering
-    // pairs to the row side (lists) and the column side (fixed-threshold
-    // buffers), and the rescore merges both.
+    // Triangle mode (default for whole problems with k <= 11 and d <= 256;
+    // KNN_B200_TRI=0 disables): each unordered pair is computed once.  A
+    // sample pass (every kTriStride-th sorted column) fixes every row's
+    // column-side threshold; the sweep then covers only tiles >= each row
+    // pair's own, offering each pair to the row side (register lists) and to
+    // the column side (fixed-threshold append buffers), and the rescore merges
+    // both with a bound for each.
     const char* te = getenv("KNN_B200_TRI");
-    const bool tri = te && atoi(te) != 0 && sorted && a.row_begin == 0 && a.row_end == n && cfg.kpl == 12 &&
+    const bool tri = !(te && atoi(te) == 0) && sorted && a.row_begin == 0 && a.row_end == n && cfg.kpl == 12 &&
                      cfg.nseg == 2 && kc <= uint32_t(TS_MAX_RES_KC) && n >= 4096;
     uint64_t* tri_cbuf = nullptr;
     uint32_t* tri_ccnt = nullptr;
     float* tri_tc = nullptr;
+    uint64_t* tri_sel = nullptr;
+    uint32_t* tri_scnt = nullptr;
+    float* tri_sbound = nullptr;
     if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
     if (tri) {
-        const uint32_t stride = 8, sm = (n + stride - 1) / stride, spad = (sm + 255) / 256 * 256;
+        const char* se = getenv("KNN_B200_TRI_STRIDE");  // tuning: sample every stride-th column
+        const char* re = getenv("KNN_B200_TRI_RANK");    // tuning: threshold = rank-th of 24 sample candidates
+        const uint32_t stride = se ? uint32_t(atoi(se)) : uint32_t(kTriStride), trank = re ? uint32_t(atoi(re)) : uint32_t(kTriRank);
+        const uint32_t sm = (n + stride - 1) / stride, spad = (sm + 255) / 256 * 256;
         size_t need = 0;
         auto add = [&](size_t x) { need += (x + 255) / 256 * 256; };
         add(size_t(sm) * 4);                  // sample rows
@@ -1648,6 +1712,9 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         add(size_t(npad / 32) * 4);           // tcmax
         add(size_t(npad) * kTriCap * 8);      // column-side buffers
         add(size_t(npad) * 4);                // counts
+        add(size_t(n) * kTriSel * 8);         // selected column-side candidates
+        add(size_t(n) * 4);                   // their counts
+        add(size_t(n) * 4);                   // their bounds
         uint8_t* w3 = static_cast<uint8_t*>(a.alloc2(a.alloc2_ctx, need));
         if (!w3) return cudaErrorMemoryAllocation;
         auto take3 = [&](size_t x) {
@@ -1664,6 +1731,9 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         float* tcmax = reinterpret_cast<float*>(take3(size_t(npad / 32) * 4));
         tri_cbuf = reinterpret_cast<uint64_t*>(take3(size_t(npad) * kTriCap * 8));
         tri_ccnt = reinterpret_cast<uint32_t*>(take3(size_t(npad) * 4));
+        tri_sel = reinterpret_cast<uint64_t*>(take3(size_t(n) * kTriSel * 8));
+        tri_scnt = reinterpret_cast<uint32_t*>(take3(size_t(n) * 4));
+        tri_sbound = reinterpret_cast<float*>(take3(size_t(n) * 4));
         iota_stride_kernel<<<a.sm_count, 256, 0, st>>>(srows, sm, stride);
         gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xh, npad, kc, srows, 0, sm, spad, nullptr, xs);
         gather_alpha_kernel<<<a.sm_count, 256, 0, st>>>(alpha, srows, sm, spad, alpha_s);
@@ -1675,7 +1745,7 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         SweepParams ss{xs,     alpha_s, sm,      spad,    kc, 0, n, gts, 0,
                        cand_s, xh,      npad,    nullptr, nullptr, nullptr, 0, bmin_s};
         if ((e = launch_sweep_pair<12, 256, 8>(ss, n, st)) != cudaSuccess) return e;
-        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, npad, 24, kTriRank, tri_tc);
+        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, npad, 24, trank, tri_tc);
         chunk_max_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(tri_tc, npad / 32, tcmax);
         if ((e = cudaMemsetAsync(tri_ccnt, 0, size_t(npad) * 4, st)) != cudaSuccess) return e;
         // the triangle sweep: rows are the sorted set itself
@@ -1708,9 +1778,11 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         remap_kernel<<<a.sm_count * 8, 256, 0, st>>>(cand, size_t(nrows) * kp, perm);
         ++launches;
     }
-    if (tri) {  // column-side entries: sorted row ids -> input rows
+    if (tri) {  // column-side entries: sorted row ids -> input rows; keep each row's best kTriSel
         remap_capture_kernel<<<n, 128, 0, st>>>(tri_cbuf, tri_ccnt, n, kTriCap, perm);
-        ++launches;
+        tri_select_kernel<<<(n * 32 + 255) / 256, 256, 0, st>>>(tri_cbuf, tri_ccnt, kTriCap, n, tri_tc, tri_sel,
+                                                                 tri_scnt, tri_sbound);
+        launches += 2;
     }
 
     RescoreParams rp{a.X,  n,         d,          a.klist,  kp,       a.row_begin, a.row_end, cand,
@@ -1723,12 +1795,12 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     if (tri) {  // slots are sorted positions; both sides' candidates
         rp.rowpos = nullptr;
         rp.rowperm = perm;
-        rp.xbuf = tri_cbuf;
-        rp.xcnt = tri_ccnt;
-        rp.xbound = tri_tc;
+        rp.xbuf = tri_sel;
+        rp.xcnt = tri_scnt;
+        rp.xbound = tri_sbound;
         const dim3 grid((nrows + 7) / 8);
-        if (cosine) rescore_kernel<kCosine, 24, 2, kTriCap><<<grid, 256, 0, st>>>(rp);
-        else rescore_kernel<kSqEuclidean, 24, 2, kTriCap><<<grid, 256, 0, st>>>(rp);
+        if (cosine) rescore_kernel<kCosine, 24, 2, kTriSel><<<grid, 256, 0, st>>>(rp);
+        else rescore_kernel<kSqEuclidean, 24, 2, kTriSel><<<grid, 256, 0, st>>>(rp);
         e = cudaGetLastError();
     } else {
         e = cosine ? launch_rescore<kCosine>(cfg, rp, nrows, st) : launch_rescore<kSqEuclidean>(cfg, rp, nrows, st);

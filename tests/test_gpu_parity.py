@@ -195,13 +195,15 @@ def test_reference_acceptance_gate_on_dropin(arith):
     assert p.stdout.count("PASS") == 5, p.stdout
 
 
-@pytest.mark.parametrize("arith", ["tensor", "tensor+capture"])
-def test_full_size_c2_sampled_rows(ctx, c_oracle, arith):
+@pytest.mark.parametrize("arith", ["tensor", "tensor+capture", "tensor+rect"])
+def test_full_size_c2_sampled_rows(ctx, c_oracle, arith, monkeypatch):
     """Config C2 (n=1M, d=256, k=10, Euclidean, seed 1) at full size on the
     GPU (inputs from the device generator, bit-identical to
     generate_dataset), checked on 96 sampled rows by the exact oracle."""
     import torch
     from paper_0906_0231_b200 import euclidean, generate_torch, solve_rows_torch
+    if arith == "tensor+rect":  # the rectangular (both-direction) sweep instead of the triangle
+        monkeypatch.setenv("KNN_B200_TRI", "0")
     n, d, k = 1_000_000, 256, 10
     x = generate_torch(ctx, n, d, 1)
     idx, dist, st = solve_rows_torch(ctx, x, k, euclidean(), 0, n, arith_id(arith), want_stats=True)
@@ -213,9 +215,9 @@ def test_full_size_c2_sampled_rows(ctx, c_oracle, arith):
     gd = dist.cpu().numpy()[rows]
     assert_lists_bit_equal(gi, gd, ri, np.sqrt(rd), f"C2 sampled [{arith}]")
     assert st["arith_used"] == 2
-    if arith == "tensor":
-        # KPL 12 lists: ~0.3% of rows lack a completeness proof and take the
-        # band-capture pass (still bit-exact); more would mean a broken bound
+    if arith != "tensor+capture":
+        # ~0.1-0.3% of rows lack a completeness proof and take the band-capture
+        # pass (still bit-exact); more would mean a broken bound
         assert st["fallback_rows"] < n // 100
 
 
