@@ -43,6 +43,7 @@ constexpr int TS_MAX_RES_KC = 4;              // A resident in smem when d <= 25
 constexpr int kTriCap = 192;   // triangle mode: column-side buffer entries per row
 constexpr int kTriRank = 6;    // its threshold: the 6th of a row's 24 sample candidates
 constexpr int kTriStride = 12; // sample: every 12th sorted column (C2: 6 -> ~0.06% rows unproven)
+constexpr int kTriBucket = 1024;  // second order: thresholds sorted within 1024-column norm buckets
 
 // EW epilogue warps (4 or 8).  With 8, two warps share each TMEM lane
 // quadrant and split every tile's columns in halves; each half keeps its own
@@ -805,6 +806,35 @@ __global__ void tri_select_kernel(const uint64_t* __restrict__ buf, const uint32
         }
         out_bound[row] = b;
         out_cnt[row] = c > cap ? uint32_t(kTriSel) + 1 : (m < uint32_t(kTriSel) ? m : uint32_t(kTriSel));
+    }
+}
+
+// Second order for the triangle sweep: within consecutive buckets of the
+// norm order, sort by column-side threshold, so each 32-column chunk has
+// nearly equal norms (row-side bound) and nearly equal thresholds
+// (column-side bound).
+__global__ void tri_order_key_kernel(const float* __restrict__ tc, uint32_t n, uint32_t bucket,
+                                     unsigned long long* __restrict__ key, uint32_t* __restrict__ idx) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        key[p] = (uint64_t(p / bucket) << 32) | float_to_ordered(tc[p]);
+        idx[p] = p;
+    }
+}
+
+// Per-row arrays into the new order (position k holds old position order[k]).
+__global__ void tri_permute_kernel(const uint32_t* __restrict__ order, uint32_t n, uint32_t npad,
+                                   const float* __restrict__ alpha, const double* __restrict__ rho,
+                                   const double* __restrict__ xnorm, const float* __restrict__ tc,
+                                   const uint32_t* __restrict__ perm, float* __restrict__ alpha2,
+                                   double* __restrict__ rho2, double* __restrict__ xnorm2, float* __restrict__ tc2,
+                                   uint32_t* __restrict__ perm2) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < npad; k += gridDim.x * blockDim.x) {
+        const uint32_t q = k < n ? order[k] : k;
+        alpha2[k] = alpha[q];
+        rho2[k] = rho[q];
+        xnorm2[k] = xnorm[q];
+        tc2[k] = tc[q];
+        if (k < n) perm2[k] = perm[q];
     }
 }
 
@@ -1692,6 +1722,10 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     uint64_t* tri_cbuf = nullptr;
     uint32_t* tri_ccnt = nullptr;
     float* tri_tc = nullptr;
+    float* tri_alpha = nullptr;
+    double* tri_rho = nullptr;
+    double* tri_xnorm = nullptr;
+    uint32_t* tri_perm = nullptr;
     uint64_t* tri_sel = nullptr;
     uint32_t* tri_scnt = nullptr;
     float* tri_sbound = nullptr;
@@ -1715,6 +1749,17 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         add(size_t(n) * kTriSel * 8);         // selected column-side candidates
         add(size_t(n) * 4);                   // their counts
         add(size_t(n) * 4);                   // their bounds
+        size_t otemp = 0;                     // the second order
+        cub::DeviceRadixSort::SortPairs(nullptr, otemp, static_cast<const unsigned long long*>(nullptr),
+                                        static_cast<unsigned long long*>(nullptr), static_cast<const uint32_t*>(nullptr),
+                                        static_cast<uint32_t*>(nullptr), int(n));
+        add(otemp);
+        add(size_t(n) * 8 * 2);               // keys in / out
+        add(size_t(n) * 4 * 2);               // index in / order
+        add(size_t(npad) * 4 * 2);            // alpha2, tc2
+        add(size_t(npad) * 8 * 2);            // rho2, xnorm2
+        add(size_t(n) * 4);                   // perm2
+        add(size_t(npad / 32) * 4);           // bmin2
         uint8_t* w3 = static_cast<uint8_t*>(a.alloc2(a.alloc2_ctx, need));
         if (!w3) return cudaErrorMemoryAllocation;
         auto take3 = [&](size_t x) {
@@ -1734,6 +1779,17 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         tri_sel = reinterpret_cast<uint64_t*>(take3(size_t(n) * kTriSel * 8));
         tri_scnt = reinterpret_cast<uint32_t*>(take3(size_t(n) * 4));
         tri_sbound = reinterpret_cast<float*>(take3(size_t(n) * 4));
+        void* otmp = take3(otemp);
+        auto* okey = reinterpret_cast<unsigned long long*>(take3(size_t(n) * 8));
+        auto* okey2 = reinterpret_cast<unsigned long long*>(take3(size_t(n) * 8));
+        uint32_t* oidx = reinterpret_cast<uint32_t*>(take3(size_t(n) * 4));
+        uint32_t* order = reinterpret_cast<uint32_t*>(take3(size_t(n) * 4));
+        tri_alpha = reinterpret_cast<float*>(take3(size_t(npad) * 4));
+        float* tc2 = reinterpret_cast<float*>(take3(size_t(npad) * 4));
+        tri_rho = reinterpret_cast<double*>(take3(size_t(npad) * 8));
+        tri_xnorm = reinterpret_cast<double*>(take3(size_t(npad) * 8));
+        tri_perm = reinterpret_cast<uint32_t*>(take3(size_t(n) * 4));
+        float* bmin2 = reinterpret_cast<float*>(take3(size_t(npad / 32) * 4));
         iota_stride_kernel<<<a.sm_count, 256, 0, st>>>(srows, sm, stride);
         gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xh, npad, kc, srows, 0, sm, spad, nullptr, xs);
         gather_alpha_kernel<<<a.sm_count, 256, 0, st>>>(alpha, srows, sm, spad, alpha_s);
@@ -1745,15 +1801,25 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         SweepParams ss{xs,     alpha_s, sm,      spad,    kc, 0, n, gts, 0,
                        cand_s, xh,      npad,    nullptr, nullptr, nullptr, 0, bmin_s};
         if ((e = launch_sweep_pair<12, 256, 8>(ss, n, st)) != cudaSuccess) return e;
-        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, npad, 24, trank, tri_tc);
+        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, npad, 24, trank, tc2);
+        // second order: thresholds sorted within buckets of the norm order;
+        // the triangle sweep runs on a copy of the planes in that order
+        tri_order_key_kernel<<<a.sm_count * 4, 256, 0, st>>>(tc2, n, kTriBucket, okey, oidx);
+        if ((e = cub::DeviceRadixSort::SortPairs(otmp, otemp, okey, okey2, oidx, order, int(n), 0, 64, st)) !=
+            cudaSuccess)
+            return e;
+        tri_permute_kernel<<<a.sm_count * 4, 256, 0, st>>>(order, n, npad, alpha, rho, xnorm, tc2, perm, tri_alpha,
+                                                            tri_rho, tri_xnorm, tri_tc, tri_perm);
+        gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xh, npad, kc, order, 0, n, npad, nullptr, xq_planes);
+        chunk_min_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(tri_alpha, npad / 32, bmin2);
         chunk_max_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(tri_tc, npad / 32, tcmax);
         if ((e = cudaMemsetAsync(tri_ccnt, 0, size_t(npad) * 4, st)) != cudaSuccess) return e;
-        // the triangle sweep: rows are the sorted set itself
-        SweepParams tp{xh,   alpha, n,    npad,    kc, 0, n, group_tiles, dbg ? atoi(dbg) : 0,
-                       cand, xh,    npad, nullptr, nullptr, nullptr, 0, bmin,
+        // the triangle sweep: rows are the (re-ordered) set itself
+        SweepParams tp{xq_planes, tri_alpha, n,    npad,    kc, 0, n, group_tiles, dbg ? atoi(dbg) : 0,
+                       cand,      xq_planes, npad, nullptr, nullptr, nullptr, 0, bmin2,
                        tri_tc, tcmax, tri_cbuf, tri_ccnt, kTriCap};
         if ((e = launch_sweep_pair<12, 256, 8, true>(tp, n, st)) != cudaSuccess) return e;
-        launches += 8;
+        launches += 13;
     } else if (sym) {
         if ((e = run_sym_sweep(xh, alpha, bmin, n, npad, kc, cand, sym_ws, a.sm_count, st)) != cudaSuccess) return e;
         launches += 3;
@@ -1775,11 +1841,11 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     }
     if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
     if (sorted) {
-        remap_kernel<<<a.sm_count * 8, 256, 0, st>>>(cand, size_t(nrows) * kp, perm);
+        remap_kernel<<<a.sm_count * 8, 256, 0, st>>>(cand, size_t(nrows) * kp, tri ? tri_perm : perm);
         ++launches;
     }
-    if (tri) {  // column-side entries: sorted row ids -> input rows; keep each row's best kTriSel
-        remap_capture_kernel<<<n, 128, 0, st>>>(tri_cbuf, tri_ccnt, n, kTriCap, perm);
+    if (tri) {  // column-side entries: sweep-order row ids -> input rows; keep each row's best kTriSel
+        remap_capture_kernel<<<n, 128, 0, st>>>(tri_cbuf, tri_ccnt, n, kTriCap, tri_perm);
         tri_select_kernel<<<(n * 32 + 255) / 256, 256, 0, st>>>(tri_cbuf, tri_ccnt, kTriCap, n, tri_tc, tri_sel,
                                                                  tri_scnt, tri_sbound);
         launches += 2;
@@ -1794,7 +1860,10 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     }
     if (tri) {  // slots are sorted positions; both sides' candidates
         rp.rowpos = nullptr;
-        rp.rowperm = perm;
+        rp.rowperm = tri_perm;
+        rp.alpha = tri_alpha;
+        rp.rho = tri_rho;
+        rp.xnorm = tri_xnorm;
         rp.xbuf = tri_sel;
         rp.xcnt = tri_scnt;
         rp.xbound = tri_sbound;
