@@ -40,7 +40,7 @@ constexpr int TS_BM = 128;
 constexpr uint32_t TS_A_CHUNK = TS_BM * 128;  // 128 rows x 128 B (64 fp16 of K)
 constexpr uint32_t TS_SMEM_MAX = 232448;
 constexpr int TS_MAX_RES_KC = 4;              // A resident in smem when d <= 256
-constexpr int kTriCap = 192;   // triangle mode: column-side buffer entries per row
+constexpr int kTriCap = 256;   // triangle mode: column-side buffer entries per row
 constexpr int kTriRank = 6;    // its threshold: the 6th of a row's 24 sample candidates
 constexpr int kTriStride = 12; // sample: every 12th sorted column (C2: 6 -> ~0.06% rows unproven)
 constexpr int kTriBucket = 1024;  // second order: thresholds sorted within 1024-column norm buckets
@@ -64,6 +64,12 @@ struct TSLayout {
     static constexpr uint32_t MISC = 256;
     static constexpr uint32_t AVAIL = TS_SMEM_MAX - 1024 - MISC - LISTS - A_BYTES;
     static constexpr int STAGES_RAW = int(AVAIL / STAGE);
+// Triangle column side: admit y' against the chunk's largest threshold (1)
+// or each column's own (0).  1 saves eight loads per firing chunk; the few
+// extra candidates are filtered by the rescore (measured: -12 ms at C2).
+#ifndef KNN_TRI_CMAX
+#define KNN_TRI_CMAX 1
+#endif
 #ifndef KNN_TS_STAGE_CAP
 #define KNN_TS_STAGE_CAP 6
 #endif
@@ -514,11 +520,12 @@ tensor_sweep_kernel(const SweepParams p) {
                     if (fabsf(h) < kInf) h = __fsub_rn(h, 9.5367431640625e-07f * (fabsf(bm) + fabsf(thr.a)));  // 2^-20
                     const bool fire_r = dmax > h;
                     bool fire_c = false;
+                    float tcm = 0.0f;
                     if constexpr (TRI) {
                         // column side: y' = fl(alpha_i - 2 dot) < tc_j needs
                         // dot > (alpha_i - max_chunk tc) / 2 (same slack argument)
                         if (cside && valid) {
-                            const float tcm = __ldg(p.tcmax + (col0 >> 5));
+                            tcm = __ldg(p.tcmax + (col0 >> 5));
                             float hc = __fmul_rn(__fsub_rn(alpha_i, tcm), 0.5f);
                             if (fabsf(hc) < kInf)
                                 hc = __fsub_rn(hc, 9.5367431640625e-07f * (fabsf(alpha_i) + fabsf(tcm)));
@@ -529,7 +536,10 @@ tensor_sweep_kernel(const SweepParams p) {
                     if constexpr (TRI) {
                         if (fire_c) {  // per lane: exact y' against each column's threshold, append
                             float tcv[W];
-                            {
+                            if (KNN_TRI_CMAX) {
+#pragma unroll
+                                for (int q = 0; q < W; ++q) tcv[q] = tcm;
+                            } else {
                                 const float4* t4 = reinterpret_cast<const float4*>(p.tc + col0);
 #pragma unroll
                                 for (int q4 = 0; q4 < W / 4; ++q4) {
@@ -758,7 +768,7 @@ __global__ void tri_threshold_kernel(const uint64_t* __restrict__ cand, uint32_t
 // and the bound for everything else -- min(threshold, the next key) -- so the
 // rescore handles a short fixed-size list.  An overflowed buffer is passed on
 // as a count above kTriSel (no proof).
-constexpr int kTriSel = 24;
+constexpr int kTriSel = 32;
 __global__ void tri_select_kernel(const uint64_t* __restrict__ buf, const uint32_t* __restrict__ cnt, uint32_t cap,
                                   uint32_t n, const float* __restrict__ thr, uint64_t* __restrict__ out,
                                   uint32_t* __restrict__ out_cnt, float* __restrict__ out_bound) {
@@ -766,7 +776,7 @@ __global__ void tri_select_kernel(const uint64_t* __restrict__ buf, const uint32
     if (row >= n) return;
     const uint32_t c = cnt[row];
     const uint32_t m = c < cap ? c : cap;
-    constexpr int PER = (192 + 31) / 32;
+    constexpr int PER = (kTriCap + 31) / 32;
     uint64_t k[PER];
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
