@@ -1728,7 +1728,7 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     // both with a bound for each.
     const char* te = getenv("KNN_B200_TRI");
     const bool tri = !(te && atoi(te) == 0) && sorted && a.row_begin == 0 && a.row_end == n && cfg.kpl == 12 &&
-                     cfg.nseg == 2 && kc <= uint32_t(TS_MAX_RES_KC) && n >= 4096;
+                     cfg.nseg == 2 && kc <= uint32_t(TS_MAX_RES_KC) && n >= 393216;  // measured crossover: 262K rect, 524K tri
     uint64_t* tri_cbuf = nullptr;
     uint32_t* tri_ccnt = nullptr;
     float* tri_tc = nullptr;
