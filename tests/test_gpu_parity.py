@@ -239,3 +239,25 @@ def test_symmetric_sweep_opt_in(ctx, c_oracle, monkeypatch, n, d, k, m):
     idx, dist, st = ctx.solve(x, k, metric_obj(m), arith_id("tensor"))
     assert st["kernel_launches"] >= 3
     assert_lists_bit_equal(idx, dist, ri, rd, f"sym n={n} d={d} k={k} {m}")
+
+
+@pytest.mark.parametrize("n,d,k,m", [(400000, 48, 7, "sqeuclidean"), (393216, 32, 1, "hellinger"),
+                                     (450001, 100, 10, "euclidean")])
+def test_triangle_sweep_sampled_rows(ctx, c_oracle, n, d, k, m):
+    """The triangle sweep (each unordered pair once; the default from n =
+    393216 with k <= 11, d <= 256) on sampled rows against the exact oracle,
+    including the first and last rows of the norm order's extremes."""
+    from paper_0906_0231_b200 import generate_torch, solve_rows_torch
+    x = generate_torch(ctx, n, d, 77 + n)
+    idx, dist, st = solve_rows_torch(ctx, x, k, metric_obj(m), 0, n, arith_id("tensor"), want_stats=True)
+    xh = x.cpu().numpy()
+    norms = ((xh - xh.mean(0)) ** 2).sum(1)
+    rows = np.unique(np.concatenate([np.random.default_rng(n).choice(n, 40, replace=False),
+                                     np.argsort(norms)[:4], np.argsort(norms)[-4:], [0, n - 1]])).astype(np.uint32)
+    om = "sqeuclidean" if m == "euclidean" else m
+    ri, rd = c_oracle.rows_topk(xh, k, om, rows)
+    if m == "euclidean":
+        rd = np.sqrt(rd)
+    assert_lists_bit_equal(idx.cpu().numpy().view(np.uint32)[rows], dist.cpu().numpy()[rows], ri, rd,
+                           f"triangle n={n} d={d} k={k} {m}")
+    assert st["fallback_rows"] < n // 100
