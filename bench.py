@@ -379,6 +379,9 @@ def main():
                      "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes/launch (DRAM, ncu)",
                      "peak_source": peak_src,
                      "kernel_ms": statistics.mean(sweep_ms),
+                     "kernel": "tensor sweep phase, CUDA events on the solve stream: for whole problems with "
+                               "n >= 393216, k <= 11, d <= 256 the 1/12 sample pass + the triangle sweep (each "
+                               "unordered pair once), else the rectangular sweep",
                      "alg_flop_per_launch": alg_flop},
         "clocks": clk,
         "gpu_stats": {kk: last[kk] for kk in ("distance_evals", "rescored", "fallback_rows", "arith_used")},
