@@ -64,12 +64,6 @@ struct TSLayout {
     static constexpr uint32_t MISC = 256;
     static constexpr uint32_t AVAIL = TS_SMEM_MAX - 1024 - MISC - LISTS - A_BYTES;
     static constexpr int STAGES_RAW = int(AVAIL / STAGE);
-// Triangle column side: admit y' against the chunk's largest threshold (1)
-// or each column's own (0).  1 saves eight loads per firing chunk; the few
-// extra candidates are filtered by the rescore (measured: -12 ms at C2).
-#ifndef KNN_TRI_CMAX
-#define KNN_TRI_CMAX 1
-#endif
 #ifndef KNN_TS_STAGE_CAP
 #define KNN_TS_STAGE_CAP 6
 #endif
@@ -106,9 +100,10 @@ struct SweepParams {
     // to the columns' fixed-threshold buffers (the column side)
     const float* tc;     // [npad] column-side threshold: a row enters column j's buffer iff y' < tc[j]
     const float* tcmax;  // [npad / 32] its maximum per 32-column chunk
-    uint64_t* cbuf;      // [npad][ccap] column-side candidates (y', row)
-    uint32_t* ccnt;      // [npad] their counts
-    uint32_t ccap;
+    uint64_t* lkey;      // per epilogue warp: a private append log of column-side candidates,
+    uint32_t* lcol;      //   key (y', row) and column, logcap entries per warp (no atomics in the
+    uint32_t* lcnt;      //   sweep; tri_scatter_kernel bins them by column afterwards)
+    uint32_t logcap;
 };
 
 // Candidate keys from the norm-sorted sweep carry sweep-order column indices;
@@ -425,6 +420,9 @@ tensor_sweep_kernel(const SweepParams p) {
             }
         };
         uint32_t tcount = 0;
+        // TRI: this warp's column-side append log (count is warp-uniform)
+        uint32_t wlog_n = 0;
+        const size_t wlog_base = TRI ? size_t(blockIdx.x * EW + ew) * p.logcap : 0;
         // accumulator release: PAIR peers arrive on the leader's barrier
         const uint32_t tempty_rel0 = PAIR && !leader ? ptx::mapa_shared(tempty_bar(0), 0) : tempty_bar(0);
         auto release_acc = [&](uint32_t b) {
@@ -534,50 +532,45 @@ tensor_sweep_kernel(const SweepParams p) {
                     }
                     if (!__any_sync(0xffffffffu, fire_r || fire_c) || p.debug_mode == 4) return;
                     if constexpr (TRI) {
-                        if (fire_c) {  // per lane: exact y' against each column's threshold, append
-                            float tcv[W];
-                            if (KNN_TRI_CMAX) {
+                        if (__any_sync(0xffffffffu, fire_c)) {
+                            // admitted columns: y' < the chunk's largest threshold (the
+                            // rescore filters the few extra), then warp-aggregated appends
+                            // to this warp's private log: slots from a ballot prefix, no
+                            // atomic round trip (a select tree picks each dot; the scalar
+                            // FMA reproduces the FFMA2 value bit for bit)
+                            uint32_t cm = 0;
+                            if (fire_c) {
 #pragma unroll
-                                for (int q = 0; q < W; ++q) tcv[q] = tcm;
-                            } else {
-                                const float4* t4 = reinterpret_cast<const float4*>(p.tc + col0);
-#pragma unroll
-                                for (int q4 = 0; q4 < W / 4; ++q4) {
-                                    const float4 f = __ldg(t4 + q4);
-                                    tcv[4 * q4] = f.x;
-                                    tcv[4 * q4 + 1] = f.y;
-                                    tcv[4 * q4 + 2] = f.z;
-                                    tcv[4 * q4 + 3] = f.w;
+                                for (int i = 0; i < P; ++i) {
+                                    const float2 y2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], alpha_i, alpha_i);
+                                    if (y2.x < tcm) cm |= 1u << (2 * i);
+                                    if (y2.y < tcm) cm |= 1u << (2 * i + 1);
                                 }
                             }
-                            // mask of admitted columns, then one append site per
-                            // admitted column (a select tree picks its dot; the
-                            // scalar FMA reproduces the FFMA2 value bit for bit)
-                            uint32_t cm = 0;
-#pragma unroll
-                            for (int i = 0; i < P; ++i) {
-                                const float2 y2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], alpha_i, alpha_i);
-                                if (y2.x < tcv[2 * i]) cm |= 1u << (2 * i);
-                                if (y2.y < tcv[2 * i + 1]) cm |= 1u << (2 * i + 1);
-                            }
-                            while (cm) {
-                                const int bpos = __ffs(cm) - 1;
+                            while (__any_sync(0xffffffffu, cm != 0)) {
+                                const int bpos = cm ? __ffs(cm) - 1 : 0;
+                                const bool ok = cm != 0 && col0 + bpos < p.n;
                                 cm &= cm - 1;
-                                const uint32_t col = col0 + bpos;
-                                if (col >= p.n) continue;
-                                uint32_t t16[16];
+                                const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+                                if (ok) {
+                                    uint32_t t16[16];
 #pragma unroll
-                                for (int q = 0; q < 16; ++q) t16[q] = (bpos & 16) ? v[q + 16] : v[q];
+                                    for (int q = 0; q < 16; ++q) t16[q] = (bpos & 16) ? v[q + 16] : v[q];
 #pragma unroll
-                                for (int q = 0; q < 8; ++q) t16[q] = (bpos & 8) ? t16[q + 8] : t16[q];
+                                    for (int q = 0; q < 8; ++q) t16[q] = (bpos & 8) ? t16[q + 8] : t16[q];
 #pragma unroll
-                                for (int q = 0; q < 4; ++q) t16[q] = (bpos & 4) ? t16[q + 4] : t16[q];
+                                    for (int q = 0; q < 4; ++q) t16[q] = (bpos & 4) ? t16[q + 4] : t16[q];
 #pragma unroll
-                                for (int q = 0; q < 2; ++q) t16[q] = (bpos & 2) ? t16[q + 2] : t16[q];
-                                const uint32_t vb = (bpos & 1) ? t16[1] : t16[0];
-                                const float yv = __fmaf_rn(-2.0f, __uint_as_float(vb), alpha_i);
-                                const uint32_t at = atomicAdd(p.ccnt + col, 1u);
-                                if (at < p.ccap) p.cbuf[size_t(col) * p.ccap + at] = make_key(yv, row);
+                                    for (int q = 0; q < 2; ++q) t16[q] = (bpos & 2) ? t16[q + 2] : t16[q];
+                                    const uint32_t vb = (bpos & 1) ? t16[1] : t16[0];
+                                    const float yv = __fmaf_rn(-2.0f, __uint_as_float(vb), alpha_i);
+                                    const uint32_t slot = wlog_n + __popc(bal & ((1u << lane) - 1u));
+                                    if (slot < p.logcap) {
+                                        p.lkey[wlog_base + slot] = make_key(yv, row);
+                                        p.lcol[wlog_base + slot] = col0 + bpos;
+                                    }
+                                }
+                                wlog_n += __popc(bal);
                             }
                         }
                         if (!__any_sync(0xffffffffu, fire_r)) return;
@@ -691,6 +684,9 @@ tensor_sweep_kernel(const SweepParams p) {
                     }
                 }
             }
+        }
+        if constexpr (TRI) {
+            if (lane == 0) p.lcnt[blockIdx.x * EW + ew] = wlog_n;
         }
     }
     ptx::tc_fence_before();
@@ -845,6 +841,26 @@ __global__ void tri_permute_kernel(const uint32_t* __restrict__ order, uint32_t 
         xnorm2[k] = xnorm[q];
         tc2[k] = tc[q];
         if (k < n) perm2[k] = perm[q];
+    }
+}
+
+// Bin the sweep's per-warp append logs by column (one block per log); a log
+// that overflowed raises *overflow (the host then redoes the call without
+// the triangle).
+__global__ void tri_scatter_kernel(const uint64_t* __restrict__ lkey, const uint32_t* __restrict__ lcol,
+                                   const uint32_t* __restrict__ lcnt, uint32_t logcap, uint32_t* __restrict__ ccnt,
+                                   uint64_t* __restrict__ cbuf, uint32_t ccap, unsigned int* __restrict__ overflow) {
+    const uint32_t w = blockIdx.x;
+    uint32_t c = lcnt[w];
+    if (c > logcap) {
+        if (threadIdx.x == 0) atomicOr(overflow, 1u);
+        c = logcap;
+    }
+    const size_t base = size_t(w) * logcap;
+    for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) {
+        const uint32_t col = lcol[base + i];
+        const uint32_t at = atomicAdd(ccnt + col, 1u);
+        if (at < ccap) cbuf[size_t(col) * ccap + at] = lkey[base + i];
     }
 }
 
@@ -1630,7 +1646,15 @@ static cudaError_t launch_rescore(TensorCfg c, const RescoreParams& rp, uint32_t
     return cudaGetLastError();
 }
 
+static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResult& r, bool allow_tri);
+
 cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
+    return run_tensor_path_impl(a, r, true);
+}
+
+// allow_tri = false: the triangle sweep's append logs overflowed on this
+// input (pathological data); redo the call with the rectangular sweep.
+static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResult& r, bool allow_tri) {
     const uint32_t n = a.n, d = a.d, nrows = a.row_end - a.row_begin;
     const uint32_t npad = (n + 255) / 256 * 256;
     const uint32_t kc = (d + 63) / 64;
@@ -1727,7 +1751,7 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     // the column side (fixed-threshold append buffers), and the rescore merges
     // both with a bound for each.
     const char* te = getenv("KNN_B200_TRI");
-    const bool tri = !(te && atoi(te) == 0) && sorted && a.row_begin == 0 && a.row_end == n && cfg.kpl == 12 &&
+    const bool tri = allow_tri && !(te && atoi(te) == 0) && sorted && a.row_begin == 0 && a.row_end == n && cfg.kpl == 12 &&
                      cfg.nseg == 2 && kc <= uint32_t(TS_MAX_RES_KC) && n >= 393216;  // measured crossover: 262K rect, 524K tri
     uint64_t* tri_cbuf = nullptr;
     uint32_t* tri_ccnt = nullptr;
@@ -1770,6 +1794,15 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         add(size_t(npad) * 8 * 2);            // rho2, xnorm2
         add(size_t(n) * 4);                   // perm2
         add(size_t(npad / 32) * 4);           // bmin2
+        // per-epilogue-warp append logs, 3x the expected column-side volume
+        const uint32_t npairs = (n + 255) / 256;
+        const uint32_t gpairs = npairs < uint32_t(a.sm_count / 2) ? npairs : uint32_t(a.sm_count / 2);
+        const uint32_t nlogs = 2 * gpairs * 8;
+        const char* lce = getenv("KNN_B200_TRI_LOGCAP");  // testing: force the overflow fallback
+        const uint32_t logcap = lce ? uint32_t(atoi(lce)) : uint32_t(uint64_t(3) * n * 64 / nlogs + 4096);
+        add(size_t(nlogs) * logcap * 8);      // log keys
+        add(size_t(nlogs) * logcap * 4);      // log columns
+        add(size_t(nlogs) * 4);               // log counts
         uint8_t* w3 = static_cast<uint8_t*>(a.alloc2(a.alloc2_ctx, need));
         if (!w3) return cudaErrorMemoryAllocation;
         auto take3 = [&](size_t x) {
@@ -1800,6 +1833,9 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         tri_xnorm = reinterpret_cast<double*>(take3(size_t(npad) * 8));
         tri_perm = reinterpret_cast<uint32_t*>(take3(size_t(n) * 4));
         float* bmin2 = reinterpret_cast<float*>(take3(size_t(npad / 32) * 4));
+        uint64_t* lkey = reinterpret_cast<uint64_t*>(take3(size_t(nlogs) * logcap * 8));
+        uint32_t* lcol = reinterpret_cast<uint32_t*>(take3(size_t(nlogs) * logcap * 4));
+        uint32_t* lcnt = reinterpret_cast<uint32_t*>(take3(size_t(nlogs) * 4));
         iota_stride_kernel<<<a.sm_count, 256, 0, st>>>(srows, sm, stride);
         gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xh, npad, kc, srows, 0, sm, spad, nullptr, xs);
         gather_alpha_kernel<<<a.sm_count, 256, 0, st>>>(alpha, srows, sm, spad, alpha_s);
@@ -1827,8 +1863,10 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
         // the triangle sweep: rows are the (re-ordered) set itself
         SweepParams tp{xq_planes, tri_alpha, n,    npad,    kc, 0, n, group_tiles, dbg ? atoi(dbg) : 0,
                        cand,      xq_planes, npad, nullptr, nullptr, nullptr, 0, bmin2,
-                       tri_tc, tcmax, tri_cbuf, tri_ccnt, kTriCap};
+                       tri_tc, tcmax, lkey, lcol, lcnt, logcap};
         if ((e = launch_sweep_pair<12, 256, 8, true>(tp, n, st)) != cudaSuccess) return e;
+        tri_scatter_kernel<<<nlogs, 256, 0, st>>>(lkey, lcol, lcnt, logcap, tri_ccnt, tri_cbuf, kTriCap,
+                                                  reinterpret_cast<unsigned int*>(scal + 40));
         launches += 13;
     } else if (sym) {
         if ((e = run_sym_sweep(xh, alpha, bmin, n, npad, kc, cand, sym_ws, a.sm_count, st)) != cudaSuccess) return e;
@@ -1893,6 +1931,8 @@ cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     if ((e = cudaMemcpyAsync(a.host_scratch, scal, 64, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
     const uint32_t nfb = *reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(a.host_scratch) + 4);
+    if (tri && *reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(a.host_scratch) + 40) != 0)
+        return run_tensor_path_impl(a, r, false);
     r.rescored = *reinterpret_cast<const unsigned long long*>(static_cast<const uint8_t*>(a.host_scratch) + 32);
     r.fallback_rows = nfb;
     if (nfb) {

@@ -261,3 +261,17 @@ def test_triangle_sweep_sampled_rows(ctx, c_oracle, n, d, k, m):
     assert_lists_bit_equal(idx.cpu().numpy().view(np.uint32)[rows], dist.cpu().numpy()[rows], ri, rd,
                            f"triangle n={n} d={d} k={k} {m}")
     assert st["fallback_rows"] < n // 100
+
+
+def test_triangle_log_overflow_falls_back(ctx, c_oracle, monkeypatch):
+    """A triangle sweep whose column-side append logs overflow must redo the
+    call with the rectangular sweep: same bits (KNN_B200_TRI_LOGCAP forces it)."""
+    from paper_0906_0231_b200 import generate_torch, solve_rows_torch
+    n, d, k = 400000, 40, 5
+    x = generate_torch(ctx, n, d, 5)
+    monkeypatch.setenv("KNN_B200_TRI_LOGCAP", "64")
+    idx, dist, _ = solve_rows_torch(ctx, x, k, metric_obj("sqeuclidean"), 0, n, arith_id("tensor"))
+    rows = np.random.default_rng(3).choice(n, 32, replace=False).astype(np.uint32)
+    ri, rd = c_oracle.rows_topk(x.cpu().numpy(), k, "sqeuclidean", rows)
+    assert_lists_bit_equal(idx.cpu().numpy().view(np.uint32)[rows], dist.cpu().numpy()[rows], ri, rd,
+                           "triangle overflow fallback")
