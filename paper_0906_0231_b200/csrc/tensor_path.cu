@@ -2,25 +2,29 @@
 //
 // The reference (src/dist_kernel.cpp:42-115 + src/select.cpp:60-130) computes
 // every pair with the exact fold and funnels it into per-row heaps.  Here the
-// n x n work runs on the 5th-generation tensor cores instead:
+// n x n work runs on the 5th-generation tensor cores instead (DESIGN.md §3):
 //
 //   prep     x^_i = fp16_rn(s * (x_i - mu))   (mu = column mean, s = 2^e so
 //            |x^| <= 65504), stored as 128-byte-swizzled K-major planes
-//            [ceil(d/64)][npad][64]; alpha_i = ||x^_i||^2 (fp32); and, in fp64,
-//            the exact quantisation error rho_i = ||x^_i - s (x_i - mu)|| and
-//            ||x^_i|| for the error bound.  (cosine: mu = 0, alpha = s^2.)
-//   sweep    per CTA 128 query rows (UMMA M) against every reference tile of
-//            BN columns: TMA bulk copies -> smem ring -> tcgen05.mma kind::f16
-//            (FP32 accumulators in TMEM, double-buffered) -> 4 epilogue warps,
-//            one thread per query row, A = alpha_i + alpha_j - 2 x^_i.x^_j, kept
-//            in a per-row top-KP list (KP = k + margin) in shared memory.  The
-//            n x n matrix never leaves the SM.
+//            [ceil(d/64)][npad][64] with the columns sorted by norm;
+//            alpha_i = ||x^_i||^2 (fp32); and, in fp64, the exact quantisation
+//            error rho_i = ||x^_i - s (x_i - mu)|| and ||x^_i|| for the error
+//            bound.  (cosine: mu = 0, alpha = s^2, input order.)
+//   sweep    persistent tcgen05 kernel (CTA pairs, M = 256, when d <= 256):
+//            TMA bulk copies -> smem ring -> tcgen05.mma kind::f16 (FP32
+//            accumulators in TMEM, double-buffered) -> epilogue warps, one
+//            thread per (query row, column half), ranking y = beta_j - 2 dot
+//            in per-row lists after a per-chunk bound test on the raw dots.
+//            The n x n matrix never leaves the SM.  For large whole problems
+//            the triangle sweep computes each unordered pair once (row side
+//            into the lists, column side into fixed-threshold append logs).
 //   rescore  per row: the exact reference fold (FSUB/FMUL/FADD, coordinates in
-//            order) on the KP candidates, the top-k by (distance, index), and a
-//            proof that no row outside the list can belong to the top-k:
-//            A_max > s^2 T' + E, with T the exact k-th distance and E a
-//            rigorous bound on |A - s^2 D_ref|.  Rows without a
-//            proof are recomputed by the EXACT kernel.
+//            order) on the best candidates, the top-k by (distance, index), and
+//            a proof that nothing outside the candidates can belong to the
+//            top-k: A_max > s^2 T' + 2E, with T the exact k-th distance and E
+//            a rigorous bound on |A - s^2 D_ref|.  Rows without
+//            a proof take a band-capture second sweep, and the few whose band
+//            overflows are recomputed by the EXACT kernel.
 // Result: bit-identical to brute_force_knn.
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_fp16.h>
