@@ -242,7 +242,7 @@ def test_symmetric_sweep_opt_in(ctx, c_oracle, monkeypatch, n, d, k, m):
 
 
 @pytest.mark.parametrize("n,d,k,m", [(400000, 48, 7, "sqeuclidean"), (393216, 32, 1, "hellinger"),
-                                     (450001, 100, 10, "euclidean")])
+                                     (450001, 100, 10, "euclidean"), (420000, 33, 3, "sqeuclidean")])
 def test_triangle_sweep_sampled_rows(ctx, c_oracle, n, d, k, m):
     """The triangle sweep (each unordered pair once; the default from n =
     393216 with k <= 11, d <= 256) on sampled rows against the exact oracle,
