@@ -41,6 +41,11 @@
 namespace knnb {
 
 constexpr int TS_BM = 128;
+// A list slot holding only a bound: (threshold, kVirtualIdx).  The triangle
+// sweep seeds its row-side lists with the sample pass's threshold this way:
+// every column offered later and rejected has y >= the list maximum, so the
+// maximum stays a valid bound, and far fewer columns get inserted.
+constexpr uint32_t kVirtualIdx = 0xfffffffeu;
 constexpr uint32_t TS_A_CHUNK = TS_BM * 128;  // 128 rows x 128 B (64 fp16 of K)
 constexpr uint32_t TS_SMEM_MAX = 232448;
 constexpr int TS_MAX_RES_KC = 4;              // A resident in smem when d <= 256
@@ -116,7 +121,7 @@ struct SweepParams {
 __global__ void remap_kernel(uint64_t* __restrict__ keys, size_t count, const uint32_t* __restrict__ perm) {
     for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += size_t(gridDim.x) * blockDim.x) {
         const uint64_t k = keys[i];
-        if (k != kEmptyKey) keys[i] = (k & 0xffffffff00000000ull) | perm[uint32_t(k)];
+        if (k != kEmptyKey && uint32_t(k) != kVirtualIdx) keys[i] = (k & 0xffffffff00000000ull) | perm[uint32_t(k)];
     }
 }
 
@@ -457,7 +462,10 @@ tensor_sweep_kernel(const SweepParams p) {
                 } else if constexpr (REGLIST) {
 #pragma unroll
                     for (int s = 0; s < KPL; ++s) {
-                        const uint64_t key = (fresh || !valid) ? kEmptyKey : state[s];
+                        uint64_t key = (fresh || !valid) ? kEmptyKey : state[s];
+                        if constexpr (TRI) {
+                            if (fresh && valid) key = make_key(__ldg(p.tc + row), kVirtualIdx);
+                        }
                         la[s] = key == kEmptyKey ? kInf : ordered_to_float(uint32_t(key >> 32));
                         lx[s] = uint32_t(key);
                     }
@@ -1114,6 +1122,7 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         const int i = lane + 32 * m;
         if constexpr (XC > 0) ak[m] = i < KP ? cand[i] : (i < KT && uint32_t(i - KP) < xn ? xb[i - KP] : kEmptyKey);
         else ak[m] = i < KP ? cand[i] : kEmptyKey;
+        if (uint32_t(ak[m]) == kVirtualIdx) ak[m] = kEmptyKey;  // a bound, not a candidate (segmax reads cand[])
         if (i < KT) keys_s[warp][i] = ak[m];
     }
     __syncwarp();
@@ -1296,7 +1305,9 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         x_overflow = xn > uint32_t(XC);
     }
     bool complete;
-    double cap_y = __longlong_as_double(0x7ff0000000000000ll);  // +inf: capture everything
+    // no band (fewer than k candidates computed): -inf captures nothing and
+    // rescore_capture_kernel hands the row to the EXACT kernel directly
+    double cap_y = -__longlong_as_double(0x7ff0000000000000ll);
     if (!any_full && !x_overflow) {
         complete = true;  // every column was offered into a non-full list: the list holds all of them
     } else if (valid < p.klist) {
