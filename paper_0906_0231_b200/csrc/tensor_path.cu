@@ -1809,12 +1809,13 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         add(size_t(npad) * 8 * 2);            // rho2, xnorm2
         add(size_t(n) * 4);                   // perm2
         add(size_t(npad / 32) * 4);           // bmin2
-        // per-epilogue-warp append logs, 3x the expected column-side volume
+        // per-epilogue-warp append logs, 4x the expected column-side volume
+        // (C2: ~63M entries = 1/4 of the capacity; an overflow redoes the call)
         const uint32_t npairs = (n + 255) / 256;
         const uint32_t gpairs = npairs < uint32_t(a.sm_count / 2) ? npairs : uint32_t(a.sm_count / 2);
         const uint32_t nlogs = 2 * gpairs * 8;
         const char* lce = getenv("KNN_B200_TRI_LOGCAP");  // testing: force the overflow fallback
-        const uint32_t logcap = lce ? uint32_t(atoi(lce)) : uint32_t(uint64_t(3) * n * 64 / nlogs + 4096);
+        const uint32_t logcap = lce ? uint32_t(atoi(lce)) : uint32_t(uint64_t(4) * n * 64 / nlogs + 4096);
         add(size_t(nlogs) * logcap * 8);      // log keys
         add(size_t(nlogs) * logcap * 4);      // log columns
         add(size_t(nlogs) * 4);               // log counts
