@@ -275,3 +275,18 @@ def test_triangle_log_overflow_falls_back(ctx, c_oracle, monkeypatch):
     ri, rd = c_oracle.rows_topk(x.cpu().numpy(), k, "sqeuclidean", rows)
     assert_lists_bit_equal(idx.cpu().numpy().view(np.uint32)[rows], dist.cpu().numpy()[rows], ri, rd,
                            "triangle overflow fallback")
+
+
+def test_triangle_heavy_ties_sampled_rows(ctx, c_oracle):
+    """Triangle-size input with massive ties (256 distinct points): the
+    column side overflows and the call falls back; ties resolve by index."""
+    import torch
+    from paper_0906_0231_b200 import solve_rows_torch
+    n, d, k = 400000, 8, 10
+    xh = np.floor(c_oracle.generate(n, d, 9) * 2).astype(np.float32)
+    x = torch.from_numpy(xh).cuda()
+    idx, dist, _ = solve_rows_torch(ctx, x, k, metric_obj("sqeuclidean"), 0, n, arith_id("tensor"))
+    rows = np.random.default_rng(4).choice(n, 24, replace=False).astype(np.uint32)
+    ri, rd = c_oracle.rows_topk(xh, k, "sqeuclidean", rows)
+    assert_lists_bit_equal(idx.cpu().numpy().view(np.uint32)[rows], dist.cpu().numpy()[rows], ri, rd,
+                           "triangle heavy ties")
