@@ -772,49 +772,45 @@ __global__ void tri_threshold_kernel(const uint64_t* __restrict__ cand, uint32_t
     }
 }
 
-// Per row: the kTriSel smallest column-side candidates (warp minimum rounds)
+// Per row: the kTriSel smallest column-side candidates (by rank, unordered)
 // and the bound for everything else -- min(threshold, the next key) -- so the
 // rescore handles a short fixed-size list.  An overflowed buffer is passed on
 // as a count above kTriSel (no proof).
 constexpr int kTriSel = 32;
-__global__ void tri_select_kernel(const uint64_t* __restrict__ buf, const uint32_t* __restrict__ cnt, uint32_t cap,
-                                  uint32_t n, const float* __restrict__ thr, uint64_t* __restrict__ out,
-                                  uint32_t* __restrict__ out_cnt, float* __restrict__ out_bound) {
-    const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(256) tri_select_kernel(const uint64_t* __restrict__ buf, const uint32_t* __restrict__ cnt,
+                                                          uint32_t cap, uint32_t n, const float* __restrict__ thr,
+                                                          uint64_t* __restrict__ out, uint32_t* __restrict__ out_cnt,
+                                                          float* __restrict__ out_bound) {
+    __shared__ __align__(16) uint64_t ks[8][kTriCap + 2];
+    const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (row >= n) return;
     const uint32_t c = cnt[row];
     const uint32_t m = c < cap ? c : cap;
-    constexpr int PER = (kTriCap + 31) / 32;
-    uint64_t k[PER];
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const uint32_t i = lane + 32 * q;
-        k[q] = i < m ? buf[size_t(row) * cap + i] : kEmptyKey;
-    }
     uint64_t* o = out + size_t(row) * kTriSel;
     uint64_t next = kEmptyKey;  // the (kTriSel+1)-th smallest
-    for (int r = 0; r <= kTriSel; ++r) {
-        uint64_t mn = kEmptyKey;
-        int mq = -1;
-#pragma unroll
-        for (int q = 0; q < PER; ++q)
-            if (k[q] < mn) {
-                mn = k[q];
-                mq = q;
+    if (m <= uint32_t(kTriSel)) {
+        for (uint32_t i = lane; i < m; i += 32) o[i] = buf[size_t(row) * cap + i];
+    } else {
+        // a key's rank among the m (ties by position; keys are unique in
+        // practice -- one entry per row of the column) is its output slot
+        for (uint32_t i = lane; i < m; i += 32) ks[w][i] = buf[size_t(row) * cap + i];
+        if (lane == 0) ks[w][m] = kEmptyKey;  // pad to an even count
+        __syncwarp();
+        const uint32_t m2 = (m + 1) & ~1u;
+        for (uint32_t i = lane; i < m; i += 32) {
+            const uint64_t key = ks[w][i];
+            uint32_t r = 0;
+            for (uint32_t j = 0; j < m2; j += 2) {
+                const ulonglong2 two = *reinterpret_cast<const ulonglong2*>(&ks[w][j]);
+                r += (two.x < key || (two.x == key && j < i)) + (two.y < key || (two.y == key && j + 1 < i));
             }
-        uint64_t w = mn;
+            if (r < uint32_t(kTriSel)) o[r] = key;
+            else if (r == uint32_t(kTriSel)) next = key;
+        }
         for (int s = 16; s; s >>= 1) {
-            const uint64_t other = __shfl_xor_sync(0xffffffffu, w, s);
-            w = other < w ? other : w;
+            const uint64_t other = __shfl_xor_sync(0xffffffffu, next, s);
+            next = other < next ? other : next;
         }
-        if (r < kTriSel) {
-            if (lane == 0) o[r] = w;
-        } else {
-            next = w;
-        }
-#pragma unroll
-        for (int q = 0; q < PER; ++q)
-            if (q == mq && mn == w) k[q] = kEmptyKey;
     }
     if (lane == 0) {
         float b = thr[row];
@@ -1068,6 +1064,41 @@ __device__ __forceinline__ float exact_fold_rows(const float* __restrict__ a, co
     return fold_finalize<FOLD>(acc);
 }
 
+// The same fold with the query row staged in shared memory (d % 4 == 0): the
+// candidate row streams through a two-deep pipeline of 8-float4 batches, so
+// a batch's loads are in flight while the previous batch folds.  The fold is
+// symmetric in its operands bit for bit ((u-v)^2, u*v).
+constexpr uint32_t kStagedMaxD = 256;
+template <int FOLD>
+__device__ __forceinline__ float exact_fold_staged(const float* __restrict__ c, const float* q, uint32_t d) {
+    const float4* c4 = reinterpret_cast<const float4*>(c);
+    const float4* q4 = reinterpret_cast<const float4*>(q);
+    const uint32_t d4 = d / 4;
+    float acc = 0.0f;
+    float4 cur[8], nxt[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+        if (uint32_t(t) < d4) cur[t] = __ldg(c4 + t);
+    for (uint32_t j = 0; j < d4; j += 8) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            if (j + 8 + t < d4) nxt[t] = __ldg(c4 + j + 8 + t);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            if (j + t < d4) {
+                const float4 y = q4[j + t];
+                acc = fold_step<FOLD>(cur[t].x, y.x, acc);
+                acc = fold_step<FOLD>(cur[t].y, y.y, acc);
+                acc = fold_step<FOLD>(cur[t].z, y.z, acc);
+                acc = fold_step<FOLD>(cur[t].w, y.w, acc);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) cur[t] = nxt[t];
+    }
+    return fold_finalize<FOLD>(acc);
+}
+
 // Upper bound (scaled A space) on the approximate distance of any column whose
 // exact reference distance is <= T: s^2 T' + 2E, DESIGN.md §4.
 template <int FOLD>
@@ -1100,6 +1131,10 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     constexpr int KPL = KP / NSEG;
     constexpr int KT = KP + XC;  // candidates per row
     __shared__ uint64_t keys_s[8][KT];
+    __shared__ uint64_t ak_s[8][KT];   // approximate keys
+    __shared__ uint64_t ex_s[8][KT];   // exact keys of a batch
+    __shared__ uint16_t todo_s[8][KT];  // a batch's candidate slots
+    __shared__ __align__(16) float xq_s[8][kStagedMaxD];  // the query row (d <= kStagedMaxD, d % 4 == 0)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t slot = blockIdx.x * 8 + warp;
     if (slot >= p.row_end - p.row_begin) return;
@@ -1109,6 +1144,9 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     const uint64_t* cand = p.cand + size_t(slot) * KP;
     const float* xq = p.X + size_t(qo) * p.d;
     const bool vec = (p.d % 4 == 0);
+    const bool staged = vec && p.d <= kStagedMaxD;
+    if (staged)
+        for (uint32_t i = lane; i < p.d; i += 32) xq_s[warp][i] = __ldg(xq + i);
     constexpr int PER = (KT + 31) / 32;
     const uint32_t xn = XC ? p.xcnt[slot] : 0;
     // candidates actually present (the rank loops stop there; the rest are empty)
@@ -1147,22 +1185,48 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         __syncwarp();
     }
     __syncwarp();
-    // exact fold of candidate m of this lane into keys_s
+#pragma unroll
+    for (int m = 0; m < PER; ++m)
+        if (lane + 32 * m < KT) ak_s[warp][lane + 32 * m] = ak[m];
+    // exact fold of a batch of candidates: the wanted (lane, m) slots are
+    // compacted onto consecutive lanes, so a batch is one fold stream
     uint64_t ek[PER];
     bool done[PER];
     uint32_t valid = 0;
-    auto rescore_one = [&](int m) {
-        const uint32_t col = uint32_t(ak[m]);  // input order (remap_kernel)
-        ek[m] = kEmptyKey;
-        done[m] = true;
-        if (ak[m] != kEmptyKey && col != qo) {
-            const float* xc = p.X + size_t(col) * p.d;
-            // Reference argument order (larger index first) -- the fold is
-            // symmetric bit for bit, kept for clarity.
-            const float dist = col > qo ? exact_fold_rows<FOLD>(xc, xq, p.d, vec) : exact_fold_rows<FOLD>(xq, xc, p.d, vec);
-            ek[m] = make_key(dist, col);
-            ++valid;
+    auto rescore_batch = [&](const bool (&want)[PER]) {
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int m = 0; m < PER; ++m) {
+            const uint32_t b = __ballot_sync(0xffffffffu, want[m]);
+            if (want[m]) todo_s[warp][cnt + __popc(b & ((1u << lane) - 1u))] = uint16_t(lane + 32 * m);
+            cnt += __popc(b);
         }
+        __syncwarp();
+        for (uint32_t t = lane; t < cnt; t += 32) {
+            const int i = todo_s[warp][t];
+            const uint64_t a = ak_s[warp][i];
+            const uint32_t col = uint32_t(a);  // input order (remap_kernel)
+            uint64_t key = kEmptyKey;
+            if (a != kEmptyKey && col != qo) {
+                const float* xc = p.X + size_t(col) * p.d;
+                // Reference argument order (larger index first) -- the fold is
+                // symmetric bit for bit, kept for clarity.
+                const float dist = staged ? exact_fold_staged<FOLD>(xc, xq_s[warp], p.d)
+                                   : col > qo ? exact_fold_rows<FOLD>(xc, xq, p.d, vec)
+                                              : exact_fold_rows<FOLD>(xq, xc, p.d, vec);
+                key = make_key(dist, col);
+                ++valid;
+            }
+            ex_s[warp][i] = key;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < PER; ++m)
+            if (want[m]) {
+                ek[m] = ex_s[warp][lane + 32 * m];
+                done[m] = true;
+            }
+        __syncwarp();
     };
     auto kth_exact = [&]() -> uint64_t {  // klist-th smallest exact key among the computed ones
         __syncwarp();
@@ -1213,8 +1277,8 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     for (int m = 0; m < PER; ++m) {
         done[m] = false;
         ek[m] = kEmptyKey;
-        if (sel[m]) rescore_one(m);
     }
+    rescore_batch(sel);
     // Phase 2: any other candidate whose approximate distance is inside the
     // bound implied by phase 1's k-th exact distance (those beyond cannot be
     // among the k nearest); everything when no bound exists.
@@ -1224,13 +1288,17 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         if (kth1 != kEmptyKey)
             lim = proof_bound<FOLD>(p.d, p.maxabs, p.gmax, p.xnorm[q], p.rho[q], alpha_q,
                                     double(ordered_to_float(uint32_t(kth1 >> 32))));
+        bool want[PER], wany = false;
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
+            want[m] = false;
             if (lane + 32 * m >= KT || done[m]) continue;
             const double a = alpha_q + double(ordered_to_float(uint32_t(ak[m] >> 32)));
-            if (ak[m] != kEmptyKey && a <= lim) rescore_one(m);
+            if (ak[m] != kEmptyKey && a <= lim) want[m] = true;
             else done[m] = true;  // excluded: stays empty
+            wany |= want[m];
         }
+        if (__any_sync(0xffffffffu, wany)) rescore_batch(want);
     }
     for (int o = 16; o; o >>= 1) valid += __shfl_xor_sync(0xffffffffu, valid, o);
     if (lane == 0) atomicAdd(p.rescored, (unsigned long long)valid);
