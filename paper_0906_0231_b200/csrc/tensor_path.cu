@@ -588,8 +588,8 @@ tensor_sweep_kernel(const SweepParams p) {
                         if (!__any_sync(0xffffffffu, fire_r)) return;
                     }
                     load_beta(col0, bt);
-                    // rare path: per-lane pair mask, then a warp-uniform walk over
-                    // the admitted pairs; a pair's two values are picked with a
+                    // rare path: per-lane pair mask, then each lane walks its own
+                    // admitted pairs; a pair's two values are picked with a
                     // 4-level select tree (no dynamic register indexing, one copy
                     // of the insertion code per call site)
                     float ye[P], yo[P];
@@ -601,11 +601,10 @@ tensor_sweep_kernel(const SweepParams p) {
                         yo[i] = y2.y;
                         if (fminf(ye[i], yo[i]) < thr.a) pm |= 1u << i;
                     }
-                    uint32_t any = __reduce_or_sync(0xffffffffu, pm);
-                    while (any) {
-                        const int i = __ffs(any) - 1;
-                        any &= any - 1;
-                        if ((pm >> i) & 1u) {
+                    while (pm) {  // each lane walks its own pairs (the warp: max over lanes)
+                        const int i = __ffs(pm) - 1;
+                        pm &= pm - 1;
+                        {
                             float e8[8], o8[8];
 #pragma unroll
                             for (int q = 0; q < 8; ++q) {
