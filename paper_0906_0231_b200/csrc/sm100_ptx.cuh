@@ -176,6 +176,22 @@ __device__ __forceinline__ void mma_f16_ss_pair(uint32_t d_tmem, uint64_t a_desc
         : "memory");
 }
 
+// The same with E4M3 operands (kind::f8f6f4, K = 32 per instruction): a
+// 128-byte swizzled row chunk holds 128 elements instead of 64, so shared
+// memory descriptors and the four K steps per chunk are unchanged.  The
+// instruction descriptor is the same (E4M3 = format 0, like F16).
+__device__ __forceinline__ void mma_e4m3_ss_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t"
+        "}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // arrive once on the mbarrier at this offset in both CTAs of the pair when
 // the leader's issued MMAs complete
 __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {

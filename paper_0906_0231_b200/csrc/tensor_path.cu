@@ -28,6 +28,7 @@
 // Result: bit-identical to brute_force_knn.
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -113,6 +114,9 @@ struct SweepParams {
     uint32_t* lcol;      //   key (y', row) and column, logcap entries per warp (no atomics in the
     uint32_t* lcnt;      //   sweep; tri_scatter_kernel bins them by column afterwards)
     uint32_t logcap;
+    // E4M3 operands (kind::f8f6f4, PAIR kernels; the triangle's sample pass):
+    // xh/xa hold E4M3 planes, kc counts 128-element chunks
+    int e4m3;
 };
 
 // Candidate keys from the norm-sorted sweep carry sweep-order column indices;
@@ -308,8 +312,12 @@ tensor_sweep_kernel(const SweepParams p) {
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_f16_f32(PAIR ? 2 * TS_BM : TS_BM, BN);
             auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
-                if constexpr (PAIR) ptx::mma_f16_ss_pair(d, a, b, idesc, acc);
-                else ptx::mma_f16_ss(d, a, b, idesc, acc);
+                if constexpr (PAIR) {
+                    if (p.e4m3) ptx::mma_e4m3_ss_pair(d, a, b, idesc, acc);
+                    else ptx::mma_f16_ss_pair(d, a, b, idesc, acc);
+                } else {
+                    ptx::mma_f16_ss(d, a, b, idesc, acc);
+                }
             };
             auto commit = [&](uint32_t bar) {
                 if constexpr (PAIR) ptx::mma_commit_pair(bar);
@@ -745,16 +753,53 @@ __global__ void iota_stride_kernel(uint32_t* __restrict__ out, uint32_t m, uint3
 }
 
 __global__ void gather_alpha_kernel(const float* __restrict__ alpha, const uint32_t* __restrict__ rows, uint32_t m,
-                                    uint32_t mpad, float* __restrict__ out) {
+                                    uint32_t mpad, float scale, float* __restrict__ out) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mpad; i += gridDim.x * blockDim.x)
-        out[i] = i < m ? alpha[rows[i]] : __int_as_float(0x7f800000);
+        out[i] = i < m ? __fmul_rn(alpha[rows[i]], scale) : __int_as_float(0x7f800000);
+}
+
+// E4M3 copy of the swizzled fp16 planes for the triangle's sample pass: the
+// fp16 values (|h| <= 65504, prep_kernel) times 2^-8 fit E4M3 (max 448); a
+// 128-byte chunk row holds 128 elements, i.e. two fp16 chunks.  Dots come out
+// scaled by 2^-16; the sample pass's norms are scaled to match
+// (gather_alpha_kernel) and its thresholds scaled back (tri_threshold_kernel).
+constexpr float kE4m3Scale = 0.00390625f;  // 2^-8
+__global__ void e4m3_planes_kernel(const uint8_t* __restrict__ xh, uint32_t npad, uint32_t kc, uint32_t kc8,
+                                   uint8_t* __restrict__ x8) {
+    const uint32_t total = kc8 * npad * 8;  // 16-byte units of the E4M3 planes
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < total; u += gridDim.x * blockDim.x) {
+        const uint32_t unit = u & 7, r = (u >> 3) % npad, c8 = (u >> 3) / npad;
+        const uint32_t c = 2 * c8 + (unit >> 2);  // source fp16 chunk
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+        if (c < kc) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {  // two 16-byte fp16 units = 16 elements
+                const uint32_t lu = 2 * (unit & 3) + h;
+                const uint4 v = *reinterpret_cast<const uint4*>(xh + (size_t(c) * npad + r) * 128 + ((lu ^ (r & 7)) << 4));
+                const uint32_t hv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    __half2_raw h2;
+                    h2.x = uint16_t(hv[q]);
+                    h2.y = uint16_t(hv[q] >> 16);
+                    float2 f = __half22float2(__half2(h2));
+                    f.x = __fmul_rn(f.x, kE4m3Scale);
+                    f.y = __fmul_rn(f.y, kE4m3Scale);
+                    const uint32_t b2 = __nv_cvt_float2_to_fp8x2(f, __NV_SATFINITE, __NV_E4M3);
+                    w[(4 * h + q) >> 1] |= b2 << (16 * (q & 1));
+                }
+            }
+        }
+        *reinterpret_cast<uint4*>(x8 + (size_t(c8) * npad + r) * 128 + ((unit ^ (r & 7)) << 4)) =
+            make_uint4(w[0], w[1], w[2], w[3]);
+    }
 }
 
 // Column-side threshold of row j: the r-th smallest y among its KP sample
 // candidates (any value is correct -- it only sets how many rows the column
 // side appends); padding rows get -inf (never admit).
 __global__ void tri_threshold_kernel(const uint64_t* __restrict__ cand, uint32_t n, uint32_t npad, uint32_t kp,
-                                     uint32_t r, float* __restrict__ tc) {
+                                     uint32_t r, float unscale, float* __restrict__ tc) {
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < npad; j += gridDim.x * blockDim.x) {
         float t = -__int_as_float(0x7f800000);
         if (j < n) {
@@ -765,7 +810,7 @@ __global__ void tri_threshold_kernel(const uint64_t* __restrict__ cand, uint32_t
                 for (uint32_t b = 0; b < kp; ++b) below += c[b] < c[a];
                 if (below == r - 1) best = c[a];
             }
-            t = best == kEmptyKey ? __int_as_float(0x7f800000) : ordered_to_float(uint32_t(best >> 32));
+            t = best == kEmptyKey ? __int_as_float(0x7f800000) : __fmul_rn(ordered_to_float(uint32_t(best >> 32)), unscale);
         }
         tc[j] = t;
     }
@@ -1851,10 +1896,16 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         const char* re = getenv("KNN_B200_TRI_RANK");    // tuning: threshold = rank-th of 24 sample candidates
         const uint32_t stride = se ? uint32_t(atoi(se)) : uint32_t(kTriStride), trank = re ? uint32_t(atoi(re)) : uint32_t(kTriRank);
         const uint32_t sm = (n + stride - 1) / stride, spad = (sm + 255) / 256 * 256;
+        // the sample pass only sets thresholds (any value is correct), so it
+        // runs on E4M3 copies of the planes at twice the fp16 MMA rate
+        const char* fe = getenv("KNN_B200_TRI_E4M3");  // tuning: 0 = fp16 sample pass
+        const bool f8 = !(fe && atoi(fe) == 0);
+        const uint32_t skc = f8 ? (kc + 1) / 2 : kc;
         size_t need = 0;
         auto add = [&](size_t x) { need += (x + 255) / 256 * 256; };
         add(size_t(sm) * 4);                  // sample rows
-        add(size_t(kc) * spad * 128);         // sample planes
+        add(size_t(skc) * spad * 128);        // sample planes
+        if (f8) add(size_t(skc) * npad * 128);  // E4M3 planes of every row
         add(size_t(spad) * 4);                // sample alpha
         add(size_t(spad / 32) * 4);           // sample bmin
         add(size_t(n) * 24 * 8);              // sample lists
@@ -1894,7 +1945,8 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
             return q;
         };
         uint32_t* srows = reinterpret_cast<uint32_t*>(take3(size_t(sm) * 4));
-        uint8_t* xs = take3(size_t(kc) * spad * 128);
+        uint8_t* xs = take3(size_t(skc) * spad * 128);
+        uint8_t* x8 = f8 ? take3(size_t(skc) * npad * 128) : nullptr;
         float* alpha_s = reinterpret_cast<float*>(take3(size_t(spad) * 4));
         float* bmin_s = reinterpret_cast<float*>(take3(size_t(spad / 32) * 4));
         uint64_t* cand_s = reinterpret_cast<uint64_t*>(take3(size_t(n) * 24 * 8));
@@ -1920,17 +1972,21 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         uint32_t* lcol = reinterpret_cast<uint32_t*>(take3(size_t(nlogs) * logcap * 4));
         uint32_t* lcnt = reinterpret_cast<uint32_t*>(take3(size_t(nlogs) * 4));
         iota_stride_kernel<<<a.sm_count, 256, 0, st>>>(srows, sm, stride);
-        gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xh, npad, kc, srows, 0, sm, spad, nullptr, xs);
-        gather_alpha_kernel<<<a.sm_count, 256, 0, st>>>(alpha, srows, sm, spad, alpha_s);
+        if (f8) e4m3_planes_kernel<<<a.sm_count * 8, 256, 0, st>>>(xh, npad, kc, skc, x8);
+        const uint8_t* xrows = f8 ? x8 : xh;
+        gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xrows, npad, skc, srows, 0, sm, spad, nullptr, xs);
+        const float dscale = f8 ? kE4m3Scale * kE4m3Scale : 1.0f;  // dots of the E4M3 planes: 2^-16
+        gather_alpha_kernel<<<a.sm_count, 256, 0, st>>>(alpha, srows, sm, spad, dscale, alpha_s);
         chunk_min_kernel<<<(spad / 32 * 32 + 255) / 256, 256, 0, st>>>(alpha_s, spad / 32, bmin_s);
         // sample pass: every row (sorted order) against the sample columns
-        uint32_t gts = uint32_t((40ull << 20) / (uint64_t(256) * kc * 128));
+        uint32_t gts = uint32_t((40ull << 20) / (uint64_t(256) * skc * 128));
         const uint32_t stiles = spad / 256;
         gts = gts < 1 ? 1 : (gts > stiles ? stiles : gts);
-        SweepParams ss{xs,     alpha_s, sm,      spad,    kc, 0, n, gts, 0,
-                       cand_s, xh,      npad,    nullptr, nullptr, nullptr, 0, bmin_s};
+        SweepParams ss{xs,     alpha_s, sm,      spad,    skc, 0, n, gts, 0,
+                       cand_s, xrows,   npad,    nullptr, nullptr, nullptr, 0, bmin_s};
+        ss.e4m3 = f8;
         if ((e = launch_sweep_pair<12, 256, 8>(ss, n, st)) != cudaSuccess) return e;
-        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, npad, 24, trank, tc2);
+        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, npad, 24, trank, 1.0f / dscale, tc2);
         // second order: thresholds sorted within buckets of the norm order;
         // the triangle sweep runs on a copy of the planes in that order
         tri_order_key_kernel<<<a.sm_count * 4, 256, 0, st>>>(tc2, n, kTriBucket, okey, oidx);
@@ -1950,7 +2006,7 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         if ((e = launch_sweep_pair<12, 256, 8, true>(tp, n, st)) != cudaSuccess) return e;
         tri_scatter_kernel<<<nlogs, 256, 0, st>>>(lkey, lcol, lcnt, logcap, tri_ccnt, tri_cbuf, kTriCap,
                                                   reinterpret_cast<unsigned int*>(scal + 40));
-        launches += 13;
+        launches += f8 ? 14 : 13;
     } else if (sym) {
         if ((e = run_sym_sweep(xh, alpha, bmin, n, npad, kc, cand, sym_ws, a.sm_count, st)) != cudaSuccess) return e;
         launches += 3;

@@ -263,6 +263,24 @@ def test_triangle_sweep_sampled_rows(ctx, c_oracle, n, d, k, m):
     assert st["fallback_rows"] < n // 100
 
 
+def test_triangle_sample_precision_does_not_change_results(ctx, c_oracle, monkeypatch):
+    """The sample pass only sets thresholds: its E4M3 (default) and fp16
+    (KNN_B200_TRI_E4M3=0) forms must give the same bits on every row."""
+    import torch
+    from paper_0906_0231_b200 import generate_torch, solve_rows_torch
+    n, d, k = 400000, 200, 10
+    x = generate_torch(ctx, n, d, 31)
+    idx8, dist8, _ = solve_rows_torch(ctx, x, k, metric_obj("euclidean"), 0, n, arith_id("tensor"))
+    monkeypatch.setenv("KNN_B200_TRI_E4M3", "0")
+    idx16, dist16, _ = solve_rows_torch(ctx, x, k, metric_obj("euclidean"), 0, n, arith_id("tensor"))
+    assert (idx8 == idx16).all().item()
+    assert (dist8.view(torch.int32) == dist16.view(torch.int32)).all().item()
+    rows = np.random.default_rng(2).choice(n, 16, replace=False).astype(np.uint32)
+    ri, rd = c_oracle.rows_topk(x.cpu().numpy(), k, "sqeuclidean", rows)
+    assert_lists_bit_equal(idx8.cpu().numpy().view(np.uint32)[rows], dist8.cpu().numpy()[rows], ri, np.sqrt(rd),
+                           "triangle e4m3 sample")
+
+
 def test_triangle_log_overflow_falls_back(ctx, c_oracle, monkeypatch):
     """A triangle sweep whose column-side append logs overflow must redo the
     call with the rectangular sweep: same bits (KNN_B200_TRI_LOGCAP forces it)."""
