@@ -51,7 +51,8 @@ constexpr uint32_t TS_A_CHUNK = TS_BM * 128;  // 128 rows x 128 B (64 fp16 of K)
 constexpr uint32_t TS_SMEM_MAX = 232448;
 constexpr int TS_MAX_RES_KC = 4;              // A resident in smem when d <= 256
 constexpr int kTriCap = 256;   // triangle mode: column-side buffer entries per row
-constexpr int kTriRank = 6;    // its threshold: the 6th of a row's 24 sample candidates
+constexpr int kTriRank = 6;    // its threshold: the 6th smallest y over the row's sample columns
+constexpr int kTriSampleKpl = 6;  // sample lists: two of 6 per row hold the 6 smallest of the sample
 constexpr int kTriStride = 12; // sample: every 12th sorted column (C2: 6 -> ~0.06% rows unproven)
 constexpr int kTriBucket = 1024;  // second order: thresholds sorted within 1024-column norm buckets
 
@@ -1894,7 +1895,11 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
     if (tri) {
         const char* se = getenv("KNN_B200_TRI_STRIDE");  // tuning: sample every stride-th column
         const char* re = getenv("KNN_B200_TRI_RANK");    // tuning: threshold = rank-th of 24 sample candidates
-        const uint32_t stride = se ? uint32_t(atoi(se)) : uint32_t(kTriStride), trank = re ? uint32_t(atoi(re)) : uint32_t(kTriRank);
+        const uint32_t stride = se ? uint32_t(atoi(se)) : uint32_t(kTriStride);
+        const char* ke = getenv("KNN_B200_TRI_SAMPLE_KPL");  // tuning: 6 (default) or 12
+        const uint32_t skpl = ke && atoi(ke) == 12 ? 12u : uint32_t(kTriSampleKpl);
+        uint32_t trank = re ? uint32_t(atoi(re)) : uint32_t(kTriRank);
+        trank = trank < 1 ? 1 : (trank > skpl ? skpl : trank);  // the lists hold the skpl smallest
         const uint32_t sm = (n + stride - 1) / stride, spad = (sm + 255) / 256 * 256;
         // the sample pass only sets thresholds (any value is correct), so it
         // runs on E4M3 copies of the planes at twice the fp16 MMA rate
@@ -1908,7 +1913,7 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         if (f8) add(size_t(skc) * npad * 128);  // E4M3 planes of every row
         add(size_t(spad) * 4);                // sample alpha
         add(size_t(spad / 32) * 4);           // sample bmin
-        add(size_t(n) * 24 * 8);              // sample lists
+        add(size_t(n) * 2 * skpl * 8);        // sample lists
         add(size_t(npad) * 4);                // tc
         add(size_t(npad / 32) * 4);           // tcmax
         add(size_t(npad) * kTriCap * 8);      // column-side buffers
@@ -1949,7 +1954,7 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         uint8_t* x8 = f8 ? take3(size_t(skc) * npad * 128) : nullptr;
         float* alpha_s = reinterpret_cast<float*>(take3(size_t(spad) * 4));
         float* bmin_s = reinterpret_cast<float*>(take3(size_t(spad / 32) * 4));
-        uint64_t* cand_s = reinterpret_cast<uint64_t*>(take3(size_t(n) * 24 * 8));
+        uint64_t* cand_s = reinterpret_cast<uint64_t*>(take3(size_t(n) * 2 * skpl * 8));
         tri_tc = reinterpret_cast<float*>(take3(size_t(npad) * 4));
         float* tcmax = reinterpret_cast<float*>(take3(size_t(npad / 32) * 4));
         tri_cbuf = reinterpret_cast<uint64_t*>(take3(size_t(npad) * kTriCap * 8));
@@ -1985,8 +1990,9 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         SweepParams ss{xs,     alpha_s, sm,      spad,    skc, 0, n, gts, 0,
                        cand_s, xrows,   npad,    nullptr, nullptr, nullptr, 0, bmin_s};
         ss.e4m3 = f8;
-        if ((e = launch_sweep_pair<12, 256, 8>(ss, n, st)) != cudaSuccess) return e;
-        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, npad, 24, trank, 1.0f / dscale, tc2);
+        e = skpl == 12 ? launch_sweep_pair<12, 256, 8>(ss, n, st) : launch_sweep_pair<kTriSampleKpl, 256, 8>(ss, n, st);
+        if (e != cudaSuccess) return e;
+        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, npad, 2 * skpl, trank, 1.0f / dscale, tc2);
         // second order: thresholds sorted within buckets of the norm order;
         // the triangle sweep runs on a copy of the planes in that order
         tri_order_key_kernel<<<a.sm_count * 4, 256, 0, st>>>(tc2, n, kTriBucket, okey, oidx);
