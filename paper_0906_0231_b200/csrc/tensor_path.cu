@@ -495,63 +495,11 @@ tensor_sweep_kernel(const SweepParams p) {
                     thr = list_rescan<KPL, L::STRIDE>(a_base);
                 }
                 if (!valid) thr.a = -kInf;  // padding rows admit nothing
-                // One W-column chunk.  direct: position among the first KPL
-                // columns this thread sees (first tile of group 0, shared-memory
-                // lists only), or -1.
-                auto process = [&](const uint32_t (&v)[W], uint32_t col0, int direct, bool cside) {
+                // After a chunk's vote: the column side's appends (TRI), then the
+                // row side's rare path.
+                auto handle = [&](const uint32_t (&v)[W], uint32_t col0, bool fire_r, bool fire_c, float tcm) {
                     constexpr int P = W / 2;  // column pairs
-                    float bt[W];              // the chunk's column norms, loaded only when needed
-                    if constexpr (!REGLIST) {
-                        if (direct >= 0) {  // first KPL columns: fill the list directly
-                            load_beta(col0, bt);
-#pragma unroll
-                            for (int j = 0; j < W; ++j) {
-                                const uint32_t col = col0 + j;
-                                my_a[(direct + j) * L::LIST_ROWS] =
-                                    col < p.n ? __fmaf_rn(-2.0f, __uint_as_float(v[j]), bt[j]) : kInf;
-                                my_i[(direct + j) * L::LIST_ROWS] = col < p.n ? col : 0xffffffffu;
-                            }
-                            if (direct + W == KPL && valid) thr = list_rescan<KPL, L::STRIDE>(a_base);
-                            return;
-                        }
-                    }
-                    // hot path: y_j = fl(beta_j - 2 dot_j) < thr needs
-                    // dot_j > (beta_j - thr) / 2 >= h = (min beta of the chunk - thr) / 2,
-                    // so the raw dots are tested against h: a 3-input FMNMX3 max
-                    // tree (17 instructions for 32 values), one FADD/FMUL, one
-                    // vote, and no column-norm loads.  At the boundary y ~ thr,
-                    // so y's rounding is ~2^-24 |thr|; the slack covers it and
-                    // h's own rounding many times over -- a superset of the
-                    // exact test, which the rare path then applies unchanged.
-                    static_assert(W == 32, "max tree is laid out for 32 columns");
-                    float r1[11], r2[4];
-#pragma unroll
-                    for (int j = 0; j < 10; ++j)
-                        r1[j] = fmaxf(fmaxf(__uint_as_float(v[3 * j]), __uint_as_float(v[3 * j + 1])),
-                                      __uint_as_float(v[3 * j + 2]));
-                    r1[10] = fmaxf(__uint_as_float(v[30]), __uint_as_float(v[31]));
-#pragma unroll
-                    for (int j = 0; j < 3; ++j) r2[j] = fmaxf(fmaxf(r1[3 * j], r1[3 * j + 1]), r1[3 * j + 2]);
-                    r2[3] = fmaxf(r1[9], r1[10]);
-                    const float dmax = fmaxf(fmaxf(fmaxf(r2[0], r2[1]), r2[2]), r2[3]);
-                    const float bm = __ldg(p.bmin + (col0 >> 5));
-                    float h = __fmul_rn(__fsub_rn(bm, thr.a), 0.5f);
-                    if (fabsf(h) < kInf) h = __fsub_rn(h, 9.5367431640625e-07f * (fabsf(bm) + fabsf(thr.a)));  // 2^-20
-                    const bool fire_r = dmax > h;
-                    bool fire_c = false;
-                    float tcm = 0.0f;
-                    if constexpr (TRI) {
-                        // column side: y' = fl(alpha_i - 2 dot) < tc_j needs
-                        // dot > (alpha_i - max_chunk tc) / 2 (same slack argument)
-                        if (cside && valid) {
-                            tcm = __ldg(p.tcmax + (col0 >> 5));
-                            float hc = __fmul_rn(__fsub_rn(alpha_i, tcm), 0.5f);
-                            if (fabsf(hc) < kInf)
-                                hc = __fsub_rn(hc, 9.5367431640625e-07f * (fabsf(alpha_i) + fabsf(tcm)));
-                            fire_c = dmax > hc;
-                        }
-                    }
-                    if (!__any_sync(0xffffffffu, fire_r || fire_c) || p.debug_mode == 4) return;
+                    float bt[W];              // the chunk's column norms
                     if constexpr (TRI) {
                         if (__any_sync(0xffffffffu, fire_c)) {
                             // admitted columns: y' < the chunk's largest threshold (the
@@ -643,6 +591,72 @@ tensor_sweep_kernel(const SweepParams p) {
                         }
                     }
                 };
+                // hot path: y_j = fl(beta_j - 2 dot_j) < thr needs
+                // dot_j > (beta_j - thr) / 2 >= h = (min beta of the chunk - thr) / 2,
+                // so the raw dots are tested against h: a 3-input FMNMX3 max
+                // tree (15 instructions for 32 values), one compare, one vote
+                // per two chunks, and no column-norm loads.  At the boundary
+                // y ~ thr, so y's rounding is ~2^-24 |thr|; the slack covers it
+                // and h's own rounding many times over -- a superset of the
+                // exact test, which the rare path then applies unchanged.
+                static_assert(W == 32, "max tree is laid out for 32 columns");
+                auto vmax = [&](const uint32_t (&v)[W]) -> float {
+                    float r1[11], r2[4];
+#pragma unroll
+                    for (int j = 0; j < 10; ++j)
+                        r1[j] = fmaxf(fmaxf(__uint_as_float(v[3 * j]), __uint_as_float(v[3 * j + 1])),
+                                      __uint_as_float(v[3 * j + 2]));
+                    r1[10] = fmaxf(__uint_as_float(v[30]), __uint_as_float(v[31]));
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) r2[j] = fmaxf(fmaxf(r1[3 * j], r1[3 * j + 1]), r1[3 * j + 2]);
+                    r2[3] = fmaxf(r1[9], r1[10]);
+                    return fmaxf(fmaxf(fmaxf(r2[0], r2[1]), r2[2]), r2[3]);
+                };
+                // h for a chunk whose smallest column norm is bm (slack 2^-20)
+                auto row_bound = [&](float bm) -> float {
+                    float h = __fmul_rn(__fsub_rn(bm, thr.a), 0.5f);
+                    if (fabsf(h) < kInf) h = __fsub_rn(h, 9.5367431640625e-07f * (fabsf(bm) + fabsf(thr.a)));
+                    return h;
+                };
+                // column side: y' = fl(alpha_i - 2 dot) < tc_j needs
+                // dot > (alpha_i - max_chunk tc) / 2 (same slack argument)
+                auto col_bound = [&](float tcm) -> float {
+                    float hc = __fmul_rn(__fsub_rn(alpha_i, tcm), 0.5f);
+                    if (fabsf(hc) < kInf) hc = __fsub_rn(hc, 9.5367431640625e-07f * (fabsf(alpha_i) + fabsf(tcm)));
+                    return hc;
+                };
+                // One W-column chunk with its own bounds (the first tile of a
+                // fresh shared-memory list only): direct = position among the
+                // first KPL columns this thread sees, or -1.
+                auto process = [&](const uint32_t (&v)[W], uint32_t col0, int direct, bool cside) {
+                    float bt[W];
+                    if constexpr (!REGLIST) {
+                        if (direct >= 0) {  // first KPL columns: fill the list directly
+                            load_beta(col0, bt);
+#pragma unroll
+                            for (int j = 0; j < W; ++j) {
+                                const uint32_t col = col0 + j;
+                                my_a[(direct + j) * L::LIST_ROWS] =
+                                    col < p.n ? __fmaf_rn(-2.0f, __uint_as_float(v[j]), bt[j]) : kInf;
+                                my_i[(direct + j) * L::LIST_ROWS] = col < p.n ? col : 0xffffffffu;
+                            }
+                            if (direct + W == KPL && valid) thr = list_rescan<KPL, L::STRIDE>(a_base);
+                            return;
+                        }
+                    }
+                    const float dmax = vmax(v);
+                    const bool fire_r = dmax > row_bound(__ldg(p.bmin + (col0 >> 5)));
+                    bool fire_c = false;
+                    float tcm = 0.0f;
+                    if constexpr (TRI) {
+                        if (cside && valid) {
+                            tcm = __ldg(p.tcmax + (col0 >> 5));
+                            fire_c = dmax > col_bound(tcm);
+                        }
+                    }
+                    if (!__any_sync(0xffffffffu, fire_r || fire_c) || p.debug_mode == 4) return;
+                    handle(v, col0, fire_r, fire_c, tcm);
+                };
                 for (uint32_t t = ts; t < t1; ++t, ++tcount) {
                     const uint32_t b = tcount & 1, use = tcount >> 1;
                     wait(tfull_bar(b), use & 1);
@@ -668,25 +682,82 @@ tensor_sweep_kernel(const SweepParams p) {
                         if (lane == 0) release_acc(b);
                         continue;
                     }
+                    // This tile's chunk bounds, once per tile.  A row bound computed
+                    // before an insertion earlier in the tile is below the fresh
+                    // one (thr only falls), so it admits a superset: still exact.
+                    constexpr int NCH = SEG_COLS / 32;
+                    float hr[NCH], hcv[NCH], tcv[NCH];
+                    {
+                        float bmv[NCH];
+                        const float* bp = p.bmin + (cbase >> 5);
+                        if constexpr (NCH % 4 == 0) {
+#pragma unroll
+                            for (int q = 0; q < NCH / 4; ++q) {
+                                const float4 f = __ldg(reinterpret_cast<const float4*>(bp) + q);
+                                bmv[4 * q] = f.x, bmv[4 * q + 1] = f.y, bmv[4 * q + 2] = f.z, bmv[4 * q + 3] = f.w;
+                            }
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < NCH; ++q) bmv[q] = __ldg(bp + q);
+                        }
+#pragma unroll
+                        for (int q = 0; q < NCH; ++q) {
+                            hr[q] = row_bound(bmv[q]);
+                            hcv[q] = kInf;
+                            tcv[q] = 0.0f;
+                        }
+                        if constexpr (TRI) {
+                            if (cside) {
+                                const float* tp = p.tcmax + (cbase >> 5);
+#pragma unroll
+                                for (int q = 0; q < NCH; ++q) {
+                                    tcv[q] = __ldg(tp + q);
+                                    hcv[q] = valid ? col_bound(tcv[q]) : kInf;
+                                }
+                            }
+                        }
+                    }
                     uint32_t va[32], vb[32];
-                    // software pipeline: chunk c+1's TMEM read is in flight while
-                    // chunk c is filtered; column norms come from L1 (prefetched
-                    // one tile ahead) and only for chunks that reach the rare path
-                    ptx::tmem_ld_32x32b_x32(taddr, va);
+                    // two chunks per step: both TMEM reads, two independent max
+                    // trees, one vote; column norms only for chunks that reach
+                    // the rare path (from L1, prefetched one tile ahead)
 #pragma unroll 1
-                    for (int c0 = 0; c0 < SEG_COLS; c0 += 64) {
-                        ptx::tmem_wait_ld();
+                    for (int it = 0; it < NCH / 2; ++it) {
+                        const uint32_t c0 = uint32_t(it) * 64;
+                        ptx::tmem_ld_32x32b_x32(taddr + c0, va);
                         ptx::tmem_ld_32x32b_x32(taddr + c0 + 32, vb);
-                        process(va, cbase + c0, (first && c0 < KPL) ? c0 : -1, cside);
                         ptx::tmem_wait_ld();
-                        if (c0 + 64 < SEG_COLS) {
-                            ptx::tmem_ld_32x32b_x32(taddr + c0 + 64, va);
-                        } else {  // this warp's part of the accumulator is in registers: release it
+                        if (it + 1 == NCH / 2) {  // this warp's part of the accumulator is in registers: release it
                             ptx::tc_fence_before();
                             __syncwarp();
                             if (lane == 0) release_acc(b);
                         }
-                        process(vb, cbase + c0 + 32, (first && c0 + 32 < KPL) ? c0 + 32 : -1, cside);
+                        if constexpr (DIRECT) {
+                            if (first && c0 < uint32_t(KPL)) {
+                                process(va, cbase + c0, int(c0), cside);
+                                process(vb, cbase + c0 + 32, c0 + 32 < uint32_t(KPL) ? int(c0) + 32 : -1, cside);
+                                continue;
+                            }
+                        }
+                        float ha = hr[0], hb = hr[1], ca = hcv[0], cb = hcv[1], ta = tcv[0], tb = tcv[1];
+#pragma unroll
+                        for (int q = 1; q < NCH / 2; ++q) {
+                            const bool at = it == q;
+                            ha = at ? hr[2 * q] : ha;
+                            hb = at ? hr[2 * q + 1] : hb;
+                            if constexpr (TRI) {
+                                ca = at ? hcv[2 * q] : ca;
+                                cb = at ? hcv[2 * q + 1] : cb;
+                                ta = at ? tcv[2 * q] : ta;
+                                tb = at ? tcv[2 * q + 1] : tb;
+                            }
+                        }
+                        const float da = vmax(va), db = vmax(vb);
+                        const bool ra = da > ha, rb = db > hb;
+                        const bool fa = TRI && da > ca, fb = TRI && db > cb;
+                        if (!__any_sync(0xffffffffu, ra || rb || fa || fb) || p.debug_mode == 4) continue;
+                        if (__any_sync(0xffffffffu, ra || fa)) handle(va, cbase + c0, ra, fa, ta);
+                        if (__any_sync(0xffffffffu, rb || fb)) handle(vb, cbase + c0 + 32, rb, fb, tb);
                     }
                 }
                 if (valid && !CAPTURE) {
