@@ -497,24 +497,21 @@ tensor_sweep_kernel(const SweepParams p) {
                 if (!valid) thr.a = -kInf;  // padding rows admit nothing
                 // After a chunk's vote: the column side's appends (TRI), then the
                 // row side's rare path.
-                auto handle = [&](const uint32_t (&v)[W], uint32_t col0, bool fire_r, bool fire_c, float tcm) {
+                auto handle = [&](const uint32_t (&v)[W], uint32_t col0, bool fire_r, bool fire_c, float hc) {
                     constexpr int P = W / 2;  // column pairs
                     float bt[W];              // the chunk's column norms
                     if constexpr (TRI) {
                         if (__any_sync(0xffffffffu, fire_c)) {
-                            // admitted columns: y' < the chunk's largest threshold (the
-                            // rescore filters the few extra), then warp-aggregated appends
-                            // to this warp's private log: slots from a ballot prefix, no
-                            // atomic round trip (a select tree picks each dot; the scalar
-                            // FMA reproduces the FFMA2 value bit for bit)
+                            // admitted columns: dot > hc, a superset of y' < the chunk's
+                            // largest threshold (the rescore filters the few extra), then
+                            // warp-aggregated appends to this warp's private log: slots
+                            // from a ballot prefix, no atomic round trip (a select tree
+                            // picks each dot)
                             uint32_t cm = 0;
                             if (fire_c) {
 #pragma unroll
-                                for (int i = 0; i < P; ++i) {
-                                    const float2 y2 = ptx::ffma2_m2(v[2 * i], v[2 * i + 1], alpha_i, alpha_i);
-                                    if (y2.x < tcm) cm |= 1u << (2 * i);
-                                    if (y2.y < tcm) cm |= 1u << (2 * i + 1);
-                                }
+                                for (int j = 0; j < W; ++j)
+                                    if (__uint_as_float(v[j]) > hc) cm |= 1u << j;
                             }
                             while (__any_sync(0xffffffffu, cm != 0)) {
                                 const int bpos = cm ? __ffs(cm) - 1 : 0;
@@ -647,15 +644,15 @@ tensor_sweep_kernel(const SweepParams p) {
                     const float dmax = vmax(v);
                     const bool fire_r = dmax > row_bound(__ldg(p.bmin + (col0 >> 5)));
                     bool fire_c = false;
-                    float tcm = 0.0f;
+                    float hc = kInf;
                     if constexpr (TRI) {
                         if (cside && valid) {
-                            tcm = __ldg(p.tcmax + (col0 >> 5));
-                            fire_c = dmax > col_bound(tcm);
+                            hc = col_bound(__ldg(p.tcmax + (col0 >> 5)));
+                            fire_c = dmax > hc;
                         }
                     }
                     if (!__any_sync(0xffffffffu, fire_r || fire_c) || p.debug_mode == 4) return;
-                    handle(v, col0, fire_r, fire_c, tcm);
+                    handle(v, col0, fire_r, fire_c, hc);
                 };
                 for (uint32_t t = ts; t < t1; ++t, ++tcount) {
                     const uint32_t b = tcount & 1, use = tcount >> 1;
@@ -686,7 +683,7 @@ tensor_sweep_kernel(const SweepParams p) {
                     // before an insertion earlier in the tile is below the fresh
                     // one (thr only falls), so it admits a superset: still exact.
                     constexpr int NCH = SEG_COLS / 32;
-                    float hr[NCH], hcv[NCH], tcv[NCH];
+                    float hr[NCH], hcv[NCH];
                     {
                         float bmv[NCH];
                         const float* bp = p.bmin + (cbase >> 5);
@@ -704,15 +701,13 @@ tensor_sweep_kernel(const SweepParams p) {
                         for (int q = 0; q < NCH; ++q) {
                             hr[q] = row_bound(bmv[q]);
                             hcv[q] = kInf;
-                            tcv[q] = 0.0f;
                         }
                         if constexpr (TRI) {
                             if (cside) {
                                 const float* tp = p.tcmax + (cbase >> 5);
 #pragma unroll
                                 for (int q = 0; q < NCH; ++q) {
-                                    tcv[q] = __ldg(tp + q);
-                                    hcv[q] = valid ? col_bound(tcv[q]) : kInf;
+                                    hcv[q] = valid ? col_bound(__ldg(tp + q)) : kInf;
                                 }
                             }
                         }
@@ -739,7 +734,7 @@ tensor_sweep_kernel(const SweepParams p) {
                                 continue;
                             }
                         }
-                        float ha = hr[0], hb = hr[1], ca = hcv[0], cb = hcv[1], ta = tcv[0], tb = tcv[1];
+                        float ha = hr[0], hb = hr[1], ca = hcv[0], cb = hcv[1];
 #pragma unroll
                         for (int q = 1; q < NCH / 2; ++q) {
                             const bool at = it == q;
@@ -748,16 +743,14 @@ tensor_sweep_kernel(const SweepParams p) {
                             if constexpr (TRI) {
                                 ca = at ? hcv[2 * q] : ca;
                                 cb = at ? hcv[2 * q + 1] : cb;
-                                ta = at ? tcv[2 * q] : ta;
-                                tb = at ? tcv[2 * q + 1] : tb;
                             }
                         }
                         const float da = vmax(va), db = vmax(vb);
                         const bool ra = da > ha, rb = db > hb;
                         const bool fa = TRI && da > ca, fb = TRI && db > cb;
                         if (!__any_sync(0xffffffffu, ra || rb || fa || fb) || p.debug_mode == 4) continue;
-                        if (__any_sync(0xffffffffu, ra || fa)) handle(va, cbase + c0, ra, fa, ta);
-                        if (__any_sync(0xffffffffu, rb || fb)) handle(vb, cbase + c0 + 32, rb, fb, tb);
+                        if (__any_sync(0xffffffffu, ra || fa)) handle(va, cbase + c0, ra, fa, ca);
+                        if (__any_sync(0xffffffffu, rb || fb)) handle(vb, cbase + c0 + 32, rb, fb, cb);
                     }
                 }
                 if (valid && !CAPTURE) {
