@@ -1049,57 +1049,81 @@ struct PrepOut {
     unsigned long long* gmax;  // [0] max xnorm, [1] max rho, [2] max alpha
 };
 
-// One warp per (padded) row.
-__global__ void prep_kernel(const float* __restrict__ X, uint32_t n, uint32_t d, uint32_t npad, uint32_t kc,
-                            const float* __restrict__ mu, const unsigned int* __restrict__ maxabs, int cosine,
-                            const uint32_t* __restrict__ perm, PrepOut o) {
-    const uint32_t warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp_global >= npad) return;
-    const uint32_t row = warp_global;
+// One warp per (padded) row, grid-stride: each lane converts 8 consecutive
+// coordinates into one 16-byte unit of the swizzled planes (a full-unit
+// store); the three global maxima are reduced per block, then one atomic each.
+__global__ void __launch_bounds__(256) prep_kernel(const float* __restrict__ X, uint32_t n, uint32_t d, uint32_t npad,
+                                                   uint32_t kc, const float* __restrict__ mu,
+                                                   const unsigned int* __restrict__ maxabs, int cosine,
+                                                   const uint32_t* __restrict__ perm, PrepOut o) {
+    __shared__ double bmax[8][3];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int e = scale_exponent(*maxabs);
     const float s = ldexpf(1.0f, e);
     const double sd = ldexp(1.0, e);
-    double rho2 = 0, nrm2 = 0;
-    float alpha = 0.0f;
-    const uint32_t kpad = kc * 64;
-    for (uint32_t k = lane; k < kpad; k += 32) {
-        __half h = __float2half_rn(0.0f);
-        if (row < n && k < d) {
-            const float x = X[size_t(perm ? perm[row] : row) * d + k];
-            const float m = cosine ? 0.0f : mu[k];
-            const float v = __fsub_rn(x, m);
-            h = __float2half_rn(__fmul_rn(v, s));
-            const double hv = double(__half2float(h));
-            const double exact = (double(x) - double(m)) * sd;
-            rho2 += (hv - exact) * (hv - exact);
-            nrm2 += hv * hv;
-            const float hf = __half2float(h);
-            alpha = __fadd_rn(alpha, __fmul_rn(hf, hf));
+    double mx_xn = 0.0, mx_rho = 0.0, mx_a = 0.0;
+    for (uint32_t row = blockIdx.x * 8 + w; row < npad; row += gridDim.x * 8) {
+        double rho2 = 0, nrm2 = 0;
+        float alpha = 0.0f;
+        const float* xr = X + size_t(row < n ? (perm ? perm[row] : row) : 0) * d;
+        for (uint32_t u = lane; u < kc * 8; u += 32) {
+            const uint32_t k0 = u * 8;
+            uint32_t wd[4];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t k = k0 + q;
+                __half h = __float2half_rn(0.0f);
+                if (row < n && k < d) {
+                    const float x = xr[k];
+                    const float m = cosine ? 0.0f : mu[k];
+                    const float v = __fsub_rn(x, m);
+                    h = __float2half_rn(__fmul_rn(v, s));
+                    const double hv = double(__half2float(h));
+                    const double exact = (double(x) - double(m)) * sd;
+                    rho2 += (hv - exact) * (hv - exact);
+                    nrm2 += hv * hv;
+                    const float hf = __half2float(h);
+                    alpha = __fadd_rn(alpha, __fmul_rn(hf, hf));
+                }
+                const uint32_t hb = __half_as_ushort(h);
+                if (q & 1) wd[q >> 1] |= hb << 16;
+                else wd[q >> 1] = hb;
+            }
+            const uint32_t chunk = k0 >> 6, unit = (k0 & 63) >> 3;
+            *reinterpret_cast<uint4*>(o.xh + (size_t(chunk) * npad + row) * 128 + ((unit ^ (row & 7)) << 4)) =
+                make_uint4(wd[0], wd[1], wd[2], wd[3]);
         }
-        const uint32_t chunk = k >> 6, kk = k & 63;
-        const uint32_t off = ((((kk >> 3) ^ (row & 7)) << 4) | ((kk & 7) << 1));
-        *reinterpret_cast<__half*>(o.xh + (size_t(chunk) * npad + row) * 128 + off) = h;
-    }
-    for (int of = 16; of; of >>= 1) {
-        rho2 += __shfl_xor_sync(0xffffffffu, rho2, of);
-        nrm2 += __shfl_xor_sync(0xffffffffu, nrm2, of);
-        alpha = __fadd_rn(alpha, __shfl_xor_sync(0xffffffffu, alpha, of));
+        for (int of = 16; of; of >>= 1) {
+            rho2 += __shfl_xor_sync(0xffffffffu, rho2, of);
+            nrm2 += __shfl_xor_sync(0xffffffffu, nrm2, of);
+            alpha = __fadd_rn(alpha, __shfl_xor_sync(0xffffffffu, alpha, of));
+        }
+        if (lane == 0) {
+            if (row < n) {
+                const float a = cosine ? __fmul_rn(s, s) : alpha;
+                o.alpha[row] = a;
+                const double rho = sqrt(rho2) * (1.0 + 1e-12);
+                const double xn = sqrt(nrm2) * (1.0 + 1e-12);
+                o.rho[row] = rho;
+                o.xnorm[row] = xn;
+                mx_xn = fmax(mx_xn, xn);
+                mx_rho = fmax(mx_rho, rho);
+                mx_a = fmax(mx_a, double(a));
+            } else {
+                o.alpha[row] = __int_as_float(0x7f800000);
+            }
+        }
     }
     if (lane == 0) {
-        if (row < n) {
-            const float a = cosine ? __fmul_rn(s, s) : alpha;
-            o.alpha[row] = a;
-            const double rho = sqrt(rho2) * (1.0 + 1e-12);
-            const double xn = sqrt(nrm2) * (1.0 + 1e-12);
-            o.rho[row] = rho;
-            o.xnorm[row] = xn;
-            atomic_max_pos_double(o.gmax + 0, xn);
-            atomic_max_pos_double(o.gmax + 1, rho);
-            atomic_max_pos_double(o.gmax + 2, double(a));
-        } else {
-            o.alpha[row] = __int_as_float(0x7f800000);
-        }
+        bmax[w][0] = mx_xn;
+        bmax[w][1] = mx_rho;
+        bmax[w][2] = mx_a;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double m = 0.0;
+        for (int i = 0; i < 8; ++i) m = fmax(m, bmax[i][threadIdx.x]);
+        atomic_max_pos_double(o.gmax + threadIdx.x, m);
     }
 }
 
@@ -1909,8 +1933,7 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         launches += 3;
     }
     PrepOut po{xh, alpha, rho, xnorm, gmax};
-    prep_kernel<<<(npad * 32 + 255) / 256, 256, 0, st>>>(a.X, n, d, npad, kc, mu, maxabs, cosine,
-                                                          sorted ? perm : nullptr, po);
+    prep_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, n, d, npad, kc, mu, maxabs, cosine, sorted ? perm : nullptr, po);
     chunk_min_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(alpha, npad / 32, bmin);
     launches += 3;
     if (sorted) {  // query rows back in input order for the A operand
