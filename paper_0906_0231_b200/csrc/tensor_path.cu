@@ -863,21 +863,26 @@ __global__ void e4m3_planes_kernel(const uint8_t* __restrict__ xh, uint32_t npad
 // Column-side threshold of row j: the r-th smallest y among its KP sample
 // candidates (any value is correct -- it only sets how many rows the column
 // side appends); padding rows get -inf (never admit).
+// tl[j]: the largest of them -- a looser capture threshold for a row whose
+// triangle pass ends with fewer than k candidates (the capture re-checks it).
 __global__ void tri_threshold_kernel(const uint64_t* __restrict__ cand, uint32_t n, uint32_t npad, uint32_t kp,
-                                     uint32_t r, float unscale, float* __restrict__ tc) {
+                                     uint32_t r, float unscale, float* __restrict__ tc, float* __restrict__ tl) {
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < npad; j += gridDim.x * blockDim.x) {
-        float t = -__int_as_float(0x7f800000);
+        float t = -__int_as_float(0x7f800000), l = t;
         if (j < n) {
             const uint64_t* c = cand + size_t(j) * kp;
-            uint64_t best = kEmptyKey;
+            uint64_t best = kEmptyKey, last = 0;
             for (uint32_t a = 0; a < kp; ++a) {
                 uint32_t below = 0;
                 for (uint32_t b = 0; b < kp; ++b) below += c[b] < c[a];
                 if (below == r - 1) best = c[a];
+                if (c[a] != kEmptyKey && c[a] > last) last = c[a];
             }
             t = best == kEmptyKey ? __int_as_float(0x7f800000) : __fmul_rn(ordered_to_float(uint32_t(best >> 32)), unscale);
+            l = last == 0 ? l : __fmul_rn(ordered_to_float(uint32_t(last >> 32)), unscale);
         }
         tc[j] = t;
+        tl[j] = l;
     }
 }
 
@@ -948,15 +953,16 @@ __global__ void tri_order_key_kernel(const float* __restrict__ tc, uint32_t n, u
 __global__ void tri_permute_kernel(const uint32_t* __restrict__ order, uint32_t n, uint32_t npad,
                                    const float* __restrict__ alpha, const double* __restrict__ rho,
                                    const double* __restrict__ xnorm, const float* __restrict__ tc,
-                                   const uint32_t* __restrict__ perm, float* __restrict__ alpha2,
-                                   double* __restrict__ rho2, double* __restrict__ xnorm2, float* __restrict__ tc2,
-                                   uint32_t* __restrict__ perm2) {
+                                   const float* __restrict__ tl, const uint32_t* __restrict__ perm,
+                                   float* __restrict__ alpha2, double* __restrict__ rho2, double* __restrict__ xnorm2,
+                                   float* __restrict__ tc2, float* __restrict__ tl2, uint32_t* __restrict__ perm2) {
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < npad; k += gridDim.x * blockDim.x) {
         const uint32_t q = k < n ? order[k] : k;
         alpha2[k] = alpha[q];
         rho2[k] = rho[q];
         xnorm2[k] = xnorm[q];
         tc2[k] = tc[q];
+        tl2[k] = tl[q];
         if (k < n) perm2[k] = perm[q];
     }
 }
@@ -1154,6 +1160,7 @@ struct RescoreParams {
     const uint64_t* xbuf;     // [slots][XC] extra candidates (column side of the triangle sweep)
     const uint32_t* xcnt;     // [slots] their counts (> XC: overflowed)
     const float* xbound;      // [slots] y bound of the column side's exclusions
+    const float* xcap;        // [slots] capture threshold (y) for rows left with fewer than k candidates, or null
 };
 
 constexpr double kTcSafety = 4.0;  // tensor-core accumulation error allowance
@@ -1506,13 +1513,15 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         x_overflow = xn > uint32_t(XC);
     }
     bool complete;
-    // no band (fewer than k candidates computed): -inf captures nothing and
-    // rescore_capture_kernel hands the row to the EXACT kernel directly
+    // no band (fewer than k candidates computed): p.xcap's looser threshold
+    // when there is one (rescore_capture_kernel proves or rejects it), else
+    // -inf, which captures nothing: the row goes to the EXACT kernel
     double cap_y = -__longlong_as_double(0x7ff0000000000000ll);
     if (!any_full && !x_overflow) {
         complete = true;  // every column was offered into a non-full list: the list holds all of them
     } else if (valid < p.klist) {
         complete = false;
+        if (XC > 0 && p.xcap) cap_y = double(p.xcap[slot]);
     } else {
         const uint64_t kth = keys_s[warp][p.klist - 1];
         const double T = double(ordered_to_float(uint32_t(kth >> 32)));
@@ -1581,6 +1590,15 @@ struct Rescore2Params {
     uint32_t* fb2_count;
     uint32_t* fb2_rows;
     unsigned long long* rescored;
+    // the completeness check: every true neighbor's y is <= the row's
+    // threshold (proof_bound of the band's k-th exact distance)
+    const float* thr;            // [m] the capture thresholds (y)
+    const uint32_t* rowpos;      // input row -> position of alpha/rho/xnorm (or null)
+    const float* alpha;
+    const double* rho;
+    const double* xnorm;
+    const unsigned long long* gmax;
+    const unsigned int* maxabs;
 };
 
 // Exact fold of every captured column of an unproven row (one warp per row);
@@ -1624,6 +1642,30 @@ __global__ void __launch_bounds__(128) rescore_capture_kernel(const Rescore2Para
     }
     // keys are unique (distinct columns) except the empty self slot: the
     // rank of an element is the number of smaller keys
+    uint64_t kth = kEmptyKey;
+    for (uint32_t i = lane; i < c; i += 32) {
+        const uint64_t mk = ks[i];
+        if (mk == kEmptyKey) continue;
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < c; ++j) rank += ks[j] < mk;
+        if (rank == p.klist - 1) kth = mk;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const uint64_t other = __shfl_xor_sync(0xffffffffu, kth, o);
+        kth = other < kth ? other : kth;
+    }
+    // the band's k-th exact distance bounds the true k-th from above, so
+    // every true neighbor has y <= proof_bound(kth) - alpha_q: the band is
+    // complete when that is inside its threshold (always, for thresholds the
+    // rescore derived from a k-th distance; not always for a looser one)
+    const uint32_t q = p.rowpos ? p.rowpos[qo] : qo;
+    const double alpha_q = double(p.alpha[q]);
+    const double need = proof_bound<FOLD>(p.d, p.maxabs, p.gmax, p.xnorm[q], p.rho[q], alpha_q,
+                                          double(ordered_to_float(uint32_t(kth >> 32)))) - alpha_q;
+    if (!(need <= double(p.thr[slot]))) {
+        if (lane == 0) p.fb2_rows[atomicAdd(p.fb2_count, 1u)] = qo;
+        return;
+    }
     const size_t orow = size_t(qo - p.row_begin);
     for (uint32_t i = lane; i < c; i += 32) {
         const uint64_t mk = ks[i];
@@ -1978,6 +2020,7 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
     uint64_t* tri_sel = nullptr;
     uint32_t* tri_scnt = nullptr;
     float* tri_sbound = nullptr;
+    float* tri_tl = nullptr;
     if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
     if (tri) {
         const char* se = getenv("KNN_B200_TRI_STRIDE");  // tuning: sample every stride-th column
@@ -2015,7 +2058,7 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         add(otemp);
         add(size_t(n) * 8 * 2);               // keys in / out
         add(size_t(n) * 4 * 2);               // index in / order
-        add(size_t(npad) * 4 * 2);            // alpha2, tc2
+        add(size_t(npad) * 4 * 4);            // alpha2, tc2, tl, tl2
         add(size_t(npad) * 8 * 2);            // rho2, xnorm2
         add(size_t(n) * 4);                   // perm2
         add(size_t(npad / 32) * 4);           // bmin2
@@ -2056,6 +2099,8 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         uint32_t* order = reinterpret_cast<uint32_t*>(take3(size_t(n) * 4));
         tri_alpha = reinterpret_cast<float*>(take3(size_t(npad) * 4));
         float* tc2 = reinterpret_cast<float*>(take3(size_t(npad) * 4));
+        float* tl1 = reinterpret_cast<float*>(take3(size_t(npad) * 4));
+        tri_tl = reinterpret_cast<float*>(take3(size_t(npad) * 4));
         tri_rho = reinterpret_cast<double*>(take3(size_t(npad) * 8));
         tri_xnorm = reinterpret_cast<double*>(take3(size_t(npad) * 8));
         tri_perm = reinterpret_cast<uint32_t*>(take3(size_t(n) * 4));
@@ -2079,15 +2124,16 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         ss.e4m3 = f8;
         e = skpl == 12 ? launch_sweep_pair<12, 256, 8>(ss, n, st) : launch_sweep_pair<kTriSampleKpl, 256, 8>(ss, n, st);
         if (e != cudaSuccess) return e;
-        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, npad, 2 * skpl, trank, 1.0f / dscale, tc2);
+        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, npad, 2 * skpl, trank, 1.0f / dscale, tc2,
+                                                              tl1);
         // second order: thresholds sorted within buckets of the norm order;
         // the triangle sweep runs on a copy of the planes in that order
         tri_order_key_kernel<<<a.sm_count * 4, 256, 0, st>>>(tc2, n, kTriBucket, okey, oidx);
         if ((e = cub::DeviceRadixSort::SortPairs(otmp, otemp, okey, okey2, oidx, order, int(n), 0, 64, st)) !=
             cudaSuccess)
             return e;
-        tri_permute_kernel<<<a.sm_count * 4, 256, 0, st>>>(order, n, npad, alpha, rho, xnorm, tc2, perm, tri_alpha,
-                                                            tri_rho, tri_xnorm, tri_tc, tri_perm);
+        tri_permute_kernel<<<a.sm_count * 4, 256, 0, st>>>(order, n, npad, alpha, rho, xnorm, tc2, tl1, perm,
+                                                            tri_alpha, tri_rho, tri_xnorm, tri_tc, tri_tl, tri_perm);
         gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xh, npad, kc, order, 0, n, npad, nullptr, xq_planes);
         chunk_min_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(tri_alpha, npad / 32, bmin2);
         chunk_max_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(tri_tc, npad / 32, tcmax);
@@ -2147,6 +2193,7 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         rp.xbuf = tri_sel;
         rp.xcnt = tri_scnt;
         rp.xbound = tri_sbound;
+        rp.xcap = tri_tl;
         const dim3 grid((nrows + 7) / 8);
         if (cosine) rescore_kernel<kCosine, 24, 2, kTriSel><<<grid, 256, 0, st>>>(rp);
         else rescore_kernel<kSqEuclidean, 24, 2, kTriSel><<<grid, 256, 0, st>>>(rp);
@@ -2193,7 +2240,8 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
             ++launches;
         }
         Rescore2Params r2{a.X,     n,       d,         a.klist,   a.row_begin, fb_rows,   nfb,      cap_cnt,
-                          cap_buf, cap,     a.out_sqrt, a.out_index, a.out_dist, fb2_count, fb2_rows, rescored};
+                          cap_buf, cap,     a.out_sqrt, a.out_index, a.out_dist, fb2_count, fb2_rows, rescored,
+                          fb_thr,  sorted ? rowpos : nullptr, alpha, rho, xnorm, gmax, maxabs};
         const size_t smem2 = size_t(4) * cap * 8;
         if (cosine) {
             cudaFuncSetAttribute(rescore_capture_kernel<kCosine>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
