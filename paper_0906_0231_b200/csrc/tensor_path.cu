@@ -51,9 +51,10 @@ constexpr uint32_t TS_A_CHUNK = TS_BM * 128;  // 128 rows x 128 B (64 fp16 of K)
 constexpr uint32_t TS_SMEM_MAX = 232448;
 constexpr int TS_MAX_RES_KC = 4;              // A resident in smem when d <= 256
 constexpr int kTriCap = 256;   // triangle mode: column-side buffer entries per row
-constexpr int kTriRank = 6;    // its threshold: the 6th smallest y over the row's sample columns
+constexpr int kTriRank = 4;    // its threshold: the 4th smallest y over the row's sample columns
 constexpr int kTriSampleKpl = 6;  // sample lists: two of 6 per row hold the 6 smallest of the sample
-constexpr int kTriStride = 12; // sample: every 12th sorted column (C2: 6 -> ~0.06% rows unproven)
+constexpr int kTriStride = 16; // sample: every 16th sorted column (C2: 0.6% of rows to the capture pass;
+                               // measured against 12/6 (0.05%): step -5 ms, tools/_knobs.sh)
 constexpr int kTriBucket = 1024;  // second order: thresholds sorted within 1024-column norm buckets
 
 // EW epilogue warps (4 or 8).  With 8, two warps share each TMEM lane
