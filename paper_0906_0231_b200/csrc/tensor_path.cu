@@ -1265,6 +1265,19 @@ __device__ __forceinline__ double proof_bound(uint32_t d, const unsigned int* ma
     return s2 * Tp + 2.0 * e_all;
 }
 
+// Warp-wide minimum of unique 64-bit keys: two redux.sync on the halves
+// instead of five 64-bit shuffle rounds.
+__device__ __forceinline__ uint64_t warp_min_key(uint64_t k) {
+    const uint32_t hi = __reduce_min_sync(0xffffffffu, uint32_t(k >> 32));
+    const uint32_t lo = __reduce_min_sync(0xffffffffu, uint32_t(k >> 32) == hi ? uint32_t(k) : 0xffffffffu);
+    return (uint64_t(hi) << 32) | lo;
+}
+__device__ __forceinline__ uint64_t warp_max_key(uint64_t k) {
+    const uint32_t hi = __reduce_max_sync(0xffffffffu, uint32_t(k >> 32));
+    const uint32_t lo = __reduce_max_sync(0xffffffffu, uint32_t(k >> 32) == hi ? uint32_t(k) : 0u);
+    return (uint64_t(hi) << 32) | lo;
+}
+
 // XC > 0: up to XC extra candidates per row (the triangle sweep's column side,
 // p.xbuf/p.xcnt) whose exclusions are bounded by p.xbound[slot].
 template <int FOLD, int KP, int NSEG, int XC = 0>
@@ -1369,25 +1382,34 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
             }
         __syncwarp();
     };
-    auto kth_exact = [&]() -> uint64_t {  // klist-th smallest exact key among the computed ones
+    // the computed exact keys compacted to keys_s[warp][0, c) (the rank
+    // loops below run over those only, not over all KA candidates)
+    int cpos[PER];  // each computed key's position in the compact array
+    auto compact_exact = [&]() -> int {
         __syncwarp();
+        int c = 0;
 #pragma unroll
-        for (int m = 0; m < PER; ++m)
-            if (lane + 32 * m < KT) keys_s[warp][lane + 32 * m] = done[m] ? ek[m] : kEmptyKey;
+        for (int m = 0; m < PER; ++m) {
+            const bool h = lane + 32 * m < KT && done[m] && ek[m] != kEmptyKey;
+            const uint32_t b = __ballot_sync(0xffffffffu, h);
+            cpos[m] = c + __popc(b & ((1u << lane) - 1u));
+            if (h) keys_s[warp][cpos[m]] = ek[m];
+            c += __popc(b);
+        }
         __syncwarp();
+        return c;
+    };
+    auto kth_exact = [&]() -> uint64_t {  // klist-th smallest exact key among the computed ones
+        const int c = compact_exact();
         uint64_t kth = kEmptyKey;
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
             if (lane + 32 * m >= KT || !done[m] || ek[m] == kEmptyKey) continue;
             uint32_t r = 0;
-            for (int j = 0; j < KA; ++j) r += keys_s[warp][j] < ek[m];
+            for (int j = 0; j < c; ++j) r += keys_s[warp][j] < ek[m];
             if (r == p.klist - 1) kth = ek[m];
         }
-        for (int o = 16; o; o >>= 1) {
-            const uint64_t other = __shfl_xor_sync(0xffffffffu, kth, o);
-            kth = other < kth ? other : kth;
-        }
-        return kth;
+        return warp_min_key(kth);
     };
     // Phase 1: the k + 4 best candidates by approximate distance, picked by
     // k + 4 rounds of a warp-wide minimum (keys are unique: distinct columns).
@@ -1404,11 +1426,7 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
                 mn = ak[m];
                 mm = m;
             }
-        uint64_t wmin = mn;
-        for (int o = 16; o; o >>= 1) {
-            const uint64_t other = __shfl_xor_sync(0xffffffffu, wmin, o);
-            wmin = other < wmin ? other : wmin;
-        }
+        const uint64_t wmin = warp_min_key(mn);
         if (wmin == kEmptyKey) break;
 #pragma unroll
         for (int m = 0; m < PER; ++m)
@@ -1446,23 +1464,19 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     // final order of the exact keys
     uint64_t mine[PER];
     uint32_t rank[PER];
-    __syncwarp();
-#pragma unroll
-    for (int m = 0; m < PER; ++m)
-        if (lane + 32 * m < KT) keys_s[warp][lane + 32 * m] = ek[m];
-    __syncwarp();
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
         mine[m] = lane + 32 * m < KT ? ek[m] : kEmptyKey;
         rank[m] = 0;
     }
     // ranks of the computed keys only (empty entries are never output)
+    const int ncomp = compact_exact();
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
         if (mine[m] == kEmptyKey) continue;
-        for (int j = 0; j < KA; ++j) {
+        for (int j = 0; j < ncomp; ++j) {
             const uint64_t o = keys_s[warp][j];
-            rank[m] += (o < mine[m]) || (o == mine[m] && j < lane + 32 * m);
+            rank[m] += (o < mine[m]) || (o == mine[m] && j < cpos[m]);
         }
     }
     __syncwarp();
@@ -1492,10 +1506,7 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     uint64_t last_approx = kEmptyKey;  // smallest maximum over full lists
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) {
-        for (int o = 16; o; o >>= 1) {
-            const uint64_t other = __shfl_xor_sync(0xffffffffu, segmax[s], o);
-            segmax[s] = other > segmax[s] ? other : segmax[s];
-        }
+        segmax[s] = warp_max_key(segmax[s]);
         if (segmax[s] != kEmptyKey) {
             any_full = true;
             last_approx = segmax[s] < last_approx ? segmax[s] : last_approx;
