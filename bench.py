@@ -304,32 +304,47 @@ def main():
     pairs = n * (n - 1) / 2
     value = pairs * args.steps / (ms_max / 1e3)
 
-    # ---- e2e through the public API: pinned host input -> H2D (rank 0) ->
-    #      NCCL broadcast -> shard solve -> D2H of the shard's lists
-    x_host = torch.empty((n, d), dtype=torch.float32, pin_memory=True) if rank == 0 else None
-    if rank == 0:
-        x_host.copy_(x)
-    idx_host = torch.empty((r1 - r0, klist), dtype=torch.int32, pin_memory=True)
-    dist_host = torch.empty((r1 - r0, klist), dtype=torch.float32, pin_memory=True)
-    x_e2e = torch.empty_like(x)
-    barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        if rank == 0:
-            x_e2e.copy_(x_host, non_blocking=True)
-        if launched:
-            dist.broadcast(x_e2e, src=0)
-        solve_rows_torch(ctx, x_e2e, k, metric, r0, r1, arith, out=(out_idx, out_dist))
-        idx_host.copy_(out_idx, non_blocking=True)
-        dist_host.copy_(out_dist, non_blocking=True)
-    e1.record(stream)
-    barrier()
-    t2 = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+    # ---- e2e through the public API.  One GPU: the drop-in's own call,
+    #      knn_b200_solve (C ABI) with PAGEABLE host buffers as the reference's
+    #      Dataset / NeighborList vectors are (staged H2D, solve, staged D2H;
+    #      synchronous, so timed by the host clock around each call).
+    #      N GPUs: pinned host input -> H2D (rank 0) -> NCCL broadcast ->
+    #      shard solve -> D2H of the shard's lists, timed by CUDA events.
+    e2e_path = None
+    if not launched:
+        x_np = x.cpu().numpy()  # pageable
+        ctx.solve(x_np, k, metric, arith)  # staging buffers allocated outside the timed region
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter()
+        for _ in range(args.steps):
+            ctx.solve(x_np, k, metric, arith)
+        e2e_ms = (time.perf_counter() - t_e2e) * 1e3
+        e2e_path = "knn_b200_solve (C ABI), pageable host buffers in and out, host clock"
+        del x_np
     if launched:
+        x_host = torch.empty((n, d), dtype=torch.float32, pin_memory=True) if rank == 0 else None
+        if rank == 0:
+            x_host.copy_(x)
+        idx_host = torch.empty((r1 - r0, klist), dtype=torch.int32, pin_memory=True)
+        dist_host = torch.empty((r1 - r0, klist), dtype=torch.float32, pin_memory=True)
+        x_e2e = torch.empty_like(x)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            if rank == 0:
+                x_e2e.copy_(x_host, non_blocking=True)
+            dist.broadcast(x_e2e, src=0)
+            solve_rows_torch(ctx, x_e2e, k, metric, r0, r1, arith, out=(out_idx, out_dist))
+            idx_host.copy_(out_idx, non_blocking=True)
+            dist_host.copy_(out_dist, non_blocking=True)
+        e1.record(stream)
+        barrier()
+        t2 = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t2.item())
+        e2e_ms = float(t2.item())
+        e2e_path = "pinned host input, H2D on rank 0, NCCL broadcast, shard solve, D2H; CUDA events, max over ranks"
     e2e_value = pairs * args.steps / (e2e_ms / 1e3)
 
     # ---- roofline of the dominant kernel (the fused distance + top-k sweep)
@@ -373,14 +388,15 @@ def main():
                    "l2": f"inputs {n * d * 4 / 1e9:.2f} GB > 126 MB L2 (no flush needed)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms / args.steps,
                 "h2d_bytes_per_step": n * d * 4 if rank == 0 else 0,
-                "d2h_bytes_per_step": n * klist * 8},
+                "d2h_bytes_per_step": n * klist * 8 if not launched else (r1 - r0) * klist * 8,
+                "path": e2e_path},
         "gpu_launches": launches,
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes/launch (DRAM, ncu)",
                      "peak_source": peak_src,
                      "kernel_ms": statistics.mean(sweep_ms),
                      "kernel": "tensor sweep phase, CUDA events on the solve stream: for whole problems with "
-                               "n >= 393216, k <= 11, d <= 256 the 1/12 sample pass + the triangle sweep (each "
+                               "n >= 393216, k <= 11, d <= 256 the 1/16 sample pass + the triangle sweep (each "
                                "unordered pair once), else the rectangular sweep",
                      "alg_flop_per_launch": alg_flop},
         "clocks": clk,

@@ -1303,8 +1303,6 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         for (uint32_t i = lane; i < p.d; i += 32) xq_s[warp][i] = __ldg(xq + i);
     constexpr int PER = (KT + 31) / 32;
     const uint32_t xn = XC ? p.xcnt[slot] : 0;
-    // candidates actually present (the rank loops stop there; the rest are empty)
-    const int KA = XC ? KP + int(xn < uint32_t(XC) ? xn : uint32_t(XC)) : KP;
     const uint64_t* xb = XC ? p.xbuf + size_t(slot) * XC : nullptr;
     const double alpha_q = double(p.alpha[q]);
     // approximate keys (unique: distinct columns)

@@ -308,3 +308,25 @@ def test_triangle_heavy_ties_sampled_rows(ctx, c_oracle):
     ri, rd = c_oracle.rows_topk(xh, k, "sqeuclidean", rows)
     assert_lists_bit_equal(idx.cpu().numpy().view(np.uint32)[rows], dist.cpu().numpy()[rows], ri, rd,
                            "triangle heavy ties")
+
+
+@pytest.mark.gpu
+def test_staged_host_copies_match_device_path(ctx):
+    """Pageable host buffers of 16 MB and more go through the pinned staging
+    lanes (api.cu host_copy) in both directions: the results must equal the
+    device-resident path's bit for bit, for pageable and pinned inputs."""
+    import torch
+    from paper_0906_0231_b200 import generate_torch, solve_rows_torch
+    n, d, k = 70000, 64, 64  # 17.9 MB in, 17.9 MB per output array
+    xt = generate_torch(ctx, n, d, 5)
+    di, dd, _ = solve_rows_torch(ctx, xt, k, metric_obj("euclidean"), 0, n)
+    di = di.cpu().numpy().view(np.uint32)
+    dd = dd.cpu().numpy()
+    x_pageable = xt.cpu().numpy()
+    xp = xt.cpu().pin_memory()
+    x_pinned = xp.numpy()
+    for x in (x_pageable, x_pinned):
+        idx, dist, st = ctx.solve(x, k, metric_obj("euclidean"))
+        assert np.array_equal(idx, di)
+        assert np.array_equal(dist.view(np.uint32), dd.view(np.uint32))
+        assert st["h2d_ms"] > 0 and st["d2h_ms"] > 0
