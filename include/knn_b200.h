@@ -115,7 +115,9 @@ KNN_B200_API void knn_b200_destroy(knn_b200_ctx *ctx);
  * (pageable or pinned).  out_index/out_dist: n x min(k, n-1), host memory.
  * Validates n >= 2, d >= 1, k >= 1 (ConfigError) and, on the device, that
  * every coordinate is finite and inside the metric's domain
- * (ValidationError, message as in distance.cpp:41-45 / dataset.cpp:25-27). */
+ * (ValidationError, message as in distance.cpp:41-45 / dataset.cpp:25-27).
+ * Pageable buffers of 16 MB or more are copied through the context's pinned
+ * staging lanes (allocated on first use, freed by knn_b200_destroy). */
 KNN_B200_API int knn_b200_solve(knn_b200_ctx *ctx, const float *host_vectors, uint32_t n, uint32_t d,
                    uint32_t k, int metric, int arith, uint32_t *out_index, float *out_dist,
                    knn_b200_stats *stats);
