@@ -52,7 +52,7 @@ constexpr uint32_t TS_SMEM_MAX = 232448;
 constexpr int TS_MAX_RES_KC = 4;              // A resident in smem when d <= 256
 constexpr int kTriCap = 256;   // triangle mode: column-side buffer entries per row
 constexpr int kTriRank = 4;    // its threshold: the 4th smallest y over the row's sample columns
-constexpr int kTriSampleKpl = 6;  // sample lists: two of 6 per row hold the 6 smallest of the sample
+constexpr int kTriSampleKpl = 4;  // sample lists: two of 4 per row hold the 4 smallest of the sample (6: +1 ms at C2)
 constexpr int kTriStride = 16; // sample: every 16th sorted column (C2: 0.6% of rows to the capture pass;
                                // measured against 12/6 (0.05%): step -5 ms, tools/_knobs.sh)
 constexpr int kTriBucket = 1024;  // second order: thresholds sorted within 1024-column norm buckets
@@ -2036,8 +2036,8 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         const char* se = getenv("KNN_B200_TRI_STRIDE");  // tuning: sample every stride-th column
         const char* re = getenv("KNN_B200_TRI_RANK");    // tuning: threshold = rank-th of 24 sample candidates
         const uint32_t stride = se ? uint32_t(atoi(se)) : uint32_t(kTriStride);
-        const char* ke = getenv("KNN_B200_TRI_SAMPLE_KPL");  // tuning: 6 (default) or 12
-        const uint32_t skpl = ke && atoi(ke) == 12 ? 12u : uint32_t(kTriSampleKpl);
+        const char* ke = getenv("KNN_B200_TRI_SAMPLE_KPL");  // tuning: 4 (default), 6 or 12
+        const uint32_t skpl = ke && atoi(ke) == 12 ? 12u : ke && atoi(ke) == 6 ? 6u : uint32_t(kTriSampleKpl);
         uint32_t trank = re ? uint32_t(atoi(re)) : uint32_t(kTriRank);
         trank = trank < 1 ? 1 : (trank > skpl ? skpl : trank);  // the lists hold the skpl smallest
         const uint32_t sm = (n + stride - 1) / stride, spad = (sm + 255) / 256 * 256;
@@ -2132,7 +2132,9 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         SweepParams ss{xs,     alpha_s, sm,      spad,    skc, 0, n, gts, 0,
                        cand_s, xrows,   npad,    nullptr, nullptr, nullptr, 0, bmin_s};
         ss.e4m3 = f8;
-        e = skpl == 12 ? launch_sweep_pair<12, 256, 8>(ss, n, st) : launch_sweep_pair<kTriSampleKpl, 256, 8>(ss, n, st);
+        e = skpl == 12  ? launch_sweep_pair<12, 256, 8>(ss, n, st)
+            : skpl == 6 ? launch_sweep_pair<6, 256, 8>(ss, n, st)
+                        : launch_sweep_pair<kTriSampleKpl, 256, 8>(ss, n, st);
         if (e != cudaSuccess) return e;
         tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, npad, 2 * skpl, trank, 1.0f / dscale, tc2,
                                                               tl1);
