@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -87,8 +88,9 @@ std::string fmt_value(float v) {
 // chunks and a copy stream; a thread memcpys chunk c into one buffer while
 // the DMA of the other is in flight, so the copy runs at the PCIe rate
 // instead of the driver's pageable path (C2: 1 GB in ~90 ms -> ~20 ms).
-constexpr int kStageThreads = 12;
-constexpr size_t kStageChunk = size_t(4) << 20;
+constexpr int kStageThreads = 16;  // lanes allocated at most; 12 used by default
+constexpr int kStageThreadsDefault = 12;
+constexpr size_t kStageChunkDefault = size_t(4) << 20;
 constexpr size_t kStageMin = size_t(16) << 20;  // smaller copies: plain cudaMemcpyAsync
 struct StageLane {
     void* buf[2] = {nullptr, nullptr};
@@ -107,6 +109,8 @@ struct knn_b200_ctx {
     StageLane stage[kStageThreads];
     cudaEvent_t stage_go = nullptr;
     bool stage_ready = false;
+    int stage_n = kStageThreadsDefault;     // tuning: KNN_B200_STAGE_THREADS
+    size_t stage_chunk = kStageChunkDefault;  // tuning: KNN_B200_STAGE_CHUNK_MB
     std::mutex mu;
 };
 
@@ -114,10 +118,13 @@ namespace {
 
 void stage_init(knn_b200_ctx* ctx) {
     if (ctx->stage_ready) return;
+    if (const char* e = getenv("KNN_B200_STAGE_THREADS")) ctx->stage_n = std::max(1, std::min(atoi(e), kStageThreads));
+    if (const char* e = getenv("KNN_B200_STAGE_CHUNK_MB")) ctx->stage_chunk = size_t(std::max(1, atoi(e))) << 20;
     cuda_check(cudaEventCreateWithFlags(&ctx->stage_go, cudaEventDisableTiming), "stage event");
-    for (auto& l : ctx->stage) {
+    for (int t = 0; t < ctx->stage_n; ++t) {
+        StageLane& l = ctx->stage[t];
         for (int b = 0; b < 2; ++b) {
-            cuda_check(cudaHostAlloc(&l.buf[b], kStageChunk, cudaHostAllocDefault), "cudaHostAlloc staging");
+            cuda_check(cudaHostAlloc(&l.buf[b], ctx->stage_chunk, cudaHostAllocDefault), "cudaHostAlloc staging");
             cuda_check(cudaEventCreateWithFlags(&l.ev[b], cudaEventDisableTiming), "stage event");
         }
         cuda_check(cudaStreamCreateWithFlags(&l.st, cudaStreamNonBlocking), "stage stream");
@@ -155,7 +162,7 @@ bool host_pinned(const void* p) {
 // pageable ones through the staging lanes.  D2H returns with the data in
 // host memory.
 void host_copy(knn_b200_ctx* ctx, void* dst, const void* src, size_t bytes, bool h2d, cudaStream_t s,
-               int threads = kStageThreads) {
+               int threads = 0) {
     const void* host = h2d ? src : dst;
     if (bytes < kStageMin || host_pinned(host)) {
         cuda_check(cudaMemcpyAsync(dst, src, bytes, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s),
@@ -164,7 +171,8 @@ void host_copy(knn_b200_ctx* ctx, void* dst, const void* src, size_t bytes, bool
         return;
     }
     stage_init(ctx);
-    threads = std::max(1, std::min(threads, kStageThreads));
+    const size_t kStageChunk = ctx->stage_chunk;
+    threads = threads > 0 ? std::min(threads, ctx->stage_n) : ctx->stage_n;
     cuda_check(cudaEventRecord(ctx->stage_go, s), "stage event");
     const size_t nchunks = (bytes + kStageChunk - 1) / kStageChunk;
     std::vector<cudaError_t> errs(threads, cudaSuccess);
@@ -548,7 +556,7 @@ int knn_b200_solve_multi(const float* host_vectors, uint32_t n, uint32_t d, uint
                 cudaStream_t s = ctx->stream;
                 cuda_check(cudaEventRecord(ctx->ev[0], s), "event");
                 // the lanes share the host: each stages with its share of the threads
-                const int st_threads = std::max(1, kStageThreads / int(use));
+                const int st_threads = std::max(1, kStageThreadsDefault / int(use));
                 host_copy(ctx, X, host_vectors, vec_bytes, true, s, st_threads);
                 cuda_check(cudaEventRecord(ctx->ev[1], s), "event");
                 solve_rows_core(ctx, X, n, d, k, metric, arith, r0, r1, oi, od, s, ctrs[g]);
