@@ -1,0 +1,35 @@
+"""bench.py's JSON-line contract on the CPU-only leg: the reference arm
+(`--impl reference`) times the reference engine compiled from its own sources
+(oracle/_ref) and prints one line with the keys the driver reads."""
+from __future__ import annotations
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_reference_arm_json_line():
+    if not (ROOT / "oracle" / "_ref").exists():
+        pytest.skip("oracle/_ref not built (make oracle)")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--n", "3000",
+                          "--steps", "1", "--warmup", "3", "--cpu-budget", "1"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference"
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "cpu_baseline"):
+        assert key in d, key
+    assert d["value"] > 0 and d["higher_is_better"] is True
+    assert d["e2e"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    cb = d["cpu_baseline"]
+    assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] == d["value"]
+    assert "workload" in d["config"]
