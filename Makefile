@@ -48,10 +48,27 @@ $(ENGINE_A): $(PKG)/host/engine_b200.cpp include/knn_b200.h
 	$(CXX) $(REF_FLAGS) -I$(REF)/include -Iinclude -c $< -o build/obj/engine_b200.o
 	rm -f $@ && ar rcs $@ build/obj/engine_b200.o
 
+# The same TU for the reference's KNN_DOUBLE_ACCUM build (dist_t = double).
+ENGINE_F64_A := $(PKG)/lib/libknn_b200_engine_f64.a
+$(ENGINE_F64_A): $(PKG)/host/engine_b200.cpp include/knn_b200.h
+	@mkdir -p build/obj $(PKG)/lib
+	$(CXX) $(REF_FLAGS) -DKNN_DOUBLE_ACCUM=1 -I$(REF)/include -Iinclude -c $< -o build/obj/engine_b200_f64.o
+	rm -f $@ && ar rcs $@ build/obj/engine_b200_f64.o
+
 REF_LINK := $(ENGINE_A) oracle/_ref/libtknn_ref_noengine.a -L$(PKG)/lib -lknn_b200 \
             -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib' -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib' -lpthread
 
-ref-bins: oracle/_ref/acceptance_b200 build/test_engine_b200 build/tknn_b200 oracle/_ref/tknn_ref
+REF_LINK_F64 := $(ENGINE_F64_A) oracle/_ref/f64/libtknn_ref_noengine.a -L$(PKG)/lib -lknn_b200 \
+            -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib' -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib' -lpthread
+
+ref-bins: oracle/_ref/acceptance_b200 build/test_engine_b200 build/tknn_b200 oracle/_ref/tknn_ref \
+          oracle/_ref/acceptance_b200_f64 build/test_engine_b200_f64
+
+oracle/_ref/acceptance_b200_f64: $(REF)/tests/acceptance.cpp $(ENGINE_F64_A) $(LIB) oracle
+	$(CXX) $(REF_FLAGS) -DKNN_DOUBLE_ACCUM=1 -I$(REF)/include -o $@ $< $(REF_LINK_F64)
+
+build/test_engine_b200_f64: tests/cpp/test_engine_b200.cpp $(ENGINE_F64_A) $(LIB) oracle
+	$(CXX) $(REF_FLAGS) -DKNN_DOUBLE_ACCUM=1 -I$(REF)/include -Iinclude -o $@ $< $(REF_LINK_F64)
 
 # The reference CLI (tools/main.cpp, unmodified) against the B200 drop-in, and
 # against the reference engine for comparison; CLI11 is the minimal shim in

@@ -122,6 +122,17 @@ KNN_B200_API int knn_b200_solve(knn_b200_ctx *ctx, const float *host_vectors, ui
                    uint32_t k, int metric, int arith, uint32_t *out_index, float *out_dist,
                    knn_b200_stats *stats);
 
+/* The reference's KNN_DOUBLE_ACCUM build (include/knn/types.hpp:9-13:
+ * dist_t = double): coordinates stay float, every step is
+ * acc + double(t) * double(t) with t = float(u - v) (distance.hpp:49-52,
+ * :59-62), and distances are stored and ordered as doubles.  EXACT policy
+ * only (SIMT FP64); results are bit-identical to the reference compiled with
+ * -DKNN_DOUBLE_ACCUM.  Same arguments, validation and errors as
+ * knn_b200_solve, with out_dist as n x min(k, n-1) doubles. */
+KNN_B200_API int knn_b200_solve_f64(knn_b200_ctx *ctx, const float *host_vectors, uint32_t n, uint32_t d,
+                                    uint32_t k, int metric, uint32_t *out_index, double *out_dist,
+                                    knn_b200_stats *stats);
+
 /* Device-resident shard solve: dev_vectors is the full n x d reference set
  * already on ctx's device (e.g. replicated by an NCCL broadcast); computes the
  * lists of query rows [row_begin, row_end) against all n vectors and writes

@@ -32,6 +32,8 @@ METRICS = {"hellinger": 0, "sqeuclidean": 1, "cosine": 2}
 _u32p = ctypes.POINTER(ctypes.c_uint32)
 _f32p = ctypes.POINTER(ctypes.c_float)
 _u64p = ctypes.POINTER(ctypes.c_uint64)
+_f64p = ctypes.POINTER(ctypes.c_double)
+REF_F64_CAPI_PATH = HERE / "_ref" / "f64" / "libtknn_ref_capi.so"
 
 
 def _ptr(a: np.ndarray, t):
@@ -63,7 +65,24 @@ class CRestatement:
         lib.ko_rows_topk.argtypes = [_f32p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                                      ctypes.c_int, _u32p, ctypes.c_uint32, ctypes.c_uint32,
                                      _u32p, _f32p]
+        lib.ko_fold_f64.argtypes = [ctypes.c_int, _f32p, _f32p, ctypes.c_uint32]
+        lib.ko_fold_f64.restype = ctypes.c_double
+        lib.ko_brute_force_f64.argtypes = [_f32p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                           ctypes.c_int, _u32p, _f64p]
         self.lib = lib
+
+    def brute_force_f64(self, x: np.ndarray, k: int, metric):
+        """brute_force_knn of the KNN_DOUBLE_ACCUM build: float64 distances."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        n, d = x.shape
+        cap = min(k, n - 1)
+        idx = np.empty((n, cap), dtype=np.uint32)
+        dist = np.empty((n, cap), dtype=np.float64)
+        rc = self.lib.ko_brute_force_f64(_ptr(x, _f32p), n, d, k, metric_id(metric),
+                                         _ptr(idx, _u32p), _ptr(dist, _f64p))
+        if rc != 0:
+            raise ValueError(f"ko_brute_force_f64 failed with code {rc}")
+        return idx, dist
 
     def splitmix64(self, seed: int, count: int) -> list[int]:
         s = ctypes.c_uint64(seed)
@@ -209,3 +228,29 @@ def normalize_rows(x: np.ndarray) -> np.ndarray:
     nrm = np.sqrt((x64 * x64).sum(axis=1, keepdims=True))
     nrm[nrm == 0] = 1.0
     return (x64 / nrm).astype(np.float32)
+
+
+class ReferenceF64:
+    """The compiled reference in its KNN_DOUBLE_ACCUM build
+    (``_ref/f64/libtknn_ref_capi.so``): brute_force_knn with double distances."""
+
+    def __init__(self, path: Path = REF_F64_CAPI_PATH):
+        if not path.exists():
+            raise FileNotFoundError(f"{path} not built (needs /root/reference at build time)")
+        lib = ctypes.CDLL(str(path))
+        lib.ref_last_error.restype = ctypes.c_char_p
+        lib.ref_brute_force_f64.argtypes = [_f32p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                            ctypes.c_int, _u32p, _f64p]
+        self.lib = lib
+
+    def brute_force(self, x: np.ndarray, k: int, metric):
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        n, d = x.shape
+        cap = min(k, n - 1)
+        idx = np.empty((n, cap), dtype=np.uint32)
+        dist = np.empty((n, cap), dtype=np.float64)
+        rc = self.lib.ref_brute_force_f64(_ptr(x, _f32p), n, d, k, metric_id(metric),
+                                          _ptr(idx, _u32p), _ptr(dist, _f64p))
+        if rc != 0:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return idx, dist

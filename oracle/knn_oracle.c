@@ -14,6 +14,7 @@
  *   - Neighbor order .................. include/knn/heap.hpp:21-24
  *   - NeighborHeap push/sift/drain .... src/heap.cpp:18-64
  *   - brute_force_knn ................. src/oracle.cpp:10-42
+ *   - the KNN_DOUBLE_ACCUM fold and brute force (types.hpp:9-13)
  * plus the SURVEY §8(d)(iii) sampled-row oracle (exact top-k for a subset of
  * query rows, multithreaded over rows), which produces the same lists as
  * brute_force_knn for those rows because the bounded heap keeps the k smallest
@@ -207,6 +208,74 @@ int ko_brute_force(const float *x, uint32_t n, uint32_t d, uint32_t k, int metri
     if (pair_evaluations) *pair_evaluations = pairs;
     free(store);
     free(heaps);
+    return 0;
+}
+
+/* ---- KNN_DOUBLE_ACCUM build (types.hpp:9-13: dist_t = double) --------- */
+/* distance.hpp:49-52 / :59-62 with dist_t = double: t stays a float
+ * (su - sv rounded in single precision); acc + dist_t(t) * dist_t(t) in
+ * double.  Hellinger stages sqrtf once per coordinate (distance.hpp:47). */
+double ko_fold_f64(int metric, const float *u, const float *v, uint32_t d) {
+    double acc = 0.0;
+    switch (metric) {
+    case KO_HELLINGER:
+        for (uint32_t j = 0; j < d; ++j) {
+            const float t = sqrtf(u[j]) - sqrtf(v[j]);
+            acc = acc + (double)t * (double)t;
+        }
+        return acc;
+    case KO_SQEUCLIDEAN:
+        for (uint32_t j = 0; j < d; ++j) {
+            const float t = u[j] - v[j];
+            acc = acc + (double)t * (double)t;
+        }
+        return acc;
+    case KO_COSINE:
+        for (uint32_t j = 0; j < d; ++j) acc = acc + (double)u[j] * (double)v[j];
+        return 1.0 - acc;
+    default:
+        return NAN;
+    }
+}
+
+typedef struct {
+    double distance;
+    uint32_t index;
+} ko_neighbor64;
+
+static int nb64_cmp(const void *pa, const void *pb) {
+    const ko_neighbor64 *a = (const ko_neighbor64 *)pa, *b = (const ko_neighbor64 *)pb;
+    if (a->distance != b->distance) return a->distance < b->distance ? -1 : 1;
+    return a->index < b->index ? -1 : (a->index > b->index);
+}
+
+/* brute_force_knn (oracle.cpp:10-42) in the double build.  Each row's list is
+ * the min(k, n-1) smallest of its n-1 (distance, index) pairs in Neighbor
+ * order (heap.hpp:21-24); the bounded heap keeps exactly those whatever the
+ * push order (acceptance criterion 6), so this selects them by sorting.  The
+ * distance of {x, y} is fold(v_x, v_y) with x > y, as oracle.cpp:27. */
+int ko_brute_force_f64(const float *x, uint32_t n, uint32_t d, uint32_t k, int metric,
+                       uint32_t *out_index, double *out_dist) {
+    if (k < 1 || n < 2 || d < 1) return 2;
+    const uint32_t cap = k < n - 1 ? k : n - 1;
+    ko_neighbor64 *row = (ko_neighbor64 *)malloc(sizeof(ko_neighbor64) * n);
+    if (!row) return 4;
+    for (uint32_t q = 0; q < n; ++q) {
+        uint32_t m = 0;
+        for (uint32_t y = 0; y < n; ++y) {
+            if (y == q) continue;
+            const uint32_t hi = y > q ? y : q, lo = y > q ? q : y;
+            row[m].distance = ko_fold_f64(metric, x + (size_t)hi * d, x + (size_t)lo * d, d);
+            row[m].index = y;
+            ++m;
+        }
+        qsort(row, m, sizeof(ko_neighbor64), nb64_cmp);
+        for (uint32_t j = 0; j < cap; ++j) {
+            out_index[(size_t)q * cap + j] = row[j].index;
+            out_dist[(size_t)q * cap + j] = row[j].distance;
+        }
+    }
+    free(row);
     return 0;
 }
 

@@ -111,6 +111,25 @@ int ref_brute_force(const float* x, std::uint32_t n, std::uint32_t d, std::uint3
     });
 }
 
+#if defined(KNN_DOUBLE_ACCUM)
+// The reference's KNN_DOUBLE_ACCUM build (types.hpp:9-13): brute_force_knn
+// with double distances, returned without narrowing.
+int ref_brute_force_f64(const float* x, std::uint32_t n, std::uint32_t d, std::uint32_t k,
+                        int metric, std::uint32_t* idx, double* dist) {
+    return guarded([&] {
+        const knn::CumulativeDistance& f = metric_by_id(metric);
+        knn::Dataset ds(n, d, std::vector<float>(x, x + std::size_t(n) * d));
+        const knn::OracleResult r = knn::brute_force_knn(ds, f, k);
+        const std::uint32_t cap = std::min(k, n - 1);
+        for (std::size_t i = 0; i < r.lists.size(); ++i)
+            for (std::uint32_t j = 0; j < cap; ++j) {
+                idx[i * cap + j] = r.lists[i].neighbors[j].index;
+                dist[i * cap + j] = r.lists[i].neighbors[j].distance;
+            }
+    });
+}
+#endif
+
 int ref_solve_knn(const float* x, std::uint32_t n, std::uint32_t d, std::uint32_t k,
                   int metric, std::uint32_t n_lanes, std::uint32_t gsize,
                   std::uint32_t* idx, float* dist, std::uint64_t* pairs, double* seconds) {

@@ -470,6 +470,58 @@ int knn_b200_solve(knn_b200_ctx* ctx, const float* host_vectors, uint32_t n, uin
     });
 }
 
+int knn_b200_solve_f64(knn_b200_ctx* ctx, const float* host_vectors, uint32_t n, uint32_t d, uint32_t k,
+                       int metric, uint32_t* out_index, double* out_dist, knn_b200_stats* stats) {
+    return guarded([&] {
+        if (!ctx) fail(KNN_B200_ERR_CONFIG, "null context");
+        check_args(n, d, k, metric, KNN_B200_ARITH_EXACT);
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        const auto t0 = std::chrono::steady_clock::now();
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const uint32_t klist = std::min(k, n - 1);
+        const size_t vec_bytes = size_t(n) * d * sizeof(float);
+        const size_t out_elems = size_t(n) * klist;
+        float* X = static_cast<float*>(ctx->vectors.get(vec_bytes));
+        auto* oi = static_cast<uint32_t*>(ctx->out_index.get(out_elems * sizeof(uint32_t)));
+        auto* od = static_cast<double*>(ctx->out_dist.get(out_elems * sizeof(double)));
+        Counters ctr;
+        cudaStream_t s = ctx->stream;
+        cuda_check(cudaEventRecord(ctx->ev[0], s), "event");
+        host_copy(ctx, X, host_vectors, vec_bytes, true, s);
+        cuda_check(cudaEventRecord(ctx->ev[1], s), "event");
+        validate_device(ctx, X, n, d, metric, s, ctr);
+        const float* Xs = X;
+        if (metric == KNN_B200_METRIC_HELLINGER) {
+            float* staged = static_cast<float*>(ctx->staged.get(vec_bytes));
+            cuda_check(knnb::launch_stage_sqrt(X, staged, uint64_t(n) * d, ctx->sm_count, s), "stage launch");
+            ++ctr.launches;
+            Xs = staged;
+        }
+        const int fold = metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean;
+        ctr.distance_evals += uint64_t(n) * n;
+        cuda_check(cudaEventRecord(ctx->ev[4], s), "event");
+        cuda_check(knnb::launch_exact_f64(fold, Xs, n, d, klist, 0, n, oi, od,
+                                          metric == KNN_B200_METRIC_EUCLIDEAN, s),
+                   "exact f64 sweep launch");
+        cuda_check(cudaEventRecord(ctx->ev[5], s), "event");
+        ++ctr.launches;
+        cuda_check(cudaEventRecord(ctx->ev[2], s), "event");
+        cuda_check(cudaEventSynchronize(ctx->ev[2]), "solve sync");
+        const auto t_d2h = std::chrono::steady_clock::now();
+        host_copy(ctx, out_index, oi, out_elems * sizeof(uint32_t), false, s);
+        host_copy(ctx, out_dist, od, out_elems * sizeof(double), false, s);
+        cuda_check(cudaStreamSynchronize(s), "solve sync");
+        if (stats) {
+            fill_stats(stats, ctr, uint64_t(n) * (n - 1) / 2, 1);
+            stats->h2d_ms = elapsed_ms(ctx->ev[0], ctx->ev[1]);
+            stats->kernel_ms = elapsed_ms(ctx->ev[1], ctx->ev[2]);
+            stats->d2h_ms = float(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_d2h).count());
+            stats->sweep_ms = elapsed_ms(ctx->ev[4], ctx->ev[5]);
+            stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+    });
+}
+
 int knn_b200_generate_device(knn_b200_ctx* ctx, float* dev_out, uint64_t count, uint64_t seed, void* stream) {
     return guarded([&] {
         if (!ctx) fail(KNN_B200_ERR_CONFIG, "null context");

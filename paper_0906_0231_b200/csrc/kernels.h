@@ -32,6 +32,12 @@ size_t exact_scratch_bytes(uint32_t nslots, uint32_t n, uint32_t klist, int sm_c
 
 constexpr uint32_t kExactMaxK = 256;
 
+// EXACT sweep with double accumulation (the reference's KNN_DOUBLE_ACCUM
+// build, exact_f64.cu); output rows row_begin..row_end-1 in slot order.
+cudaError_t launch_exact_f64(int metric, const float* X, uint32_t n, uint32_t d, uint32_t klist,
+                             uint32_t row_begin, uint32_t row_end, uint32_t* out_index, double* out_dist,
+                             int out_sqrt, cudaStream_t stream);
+
 // TENSOR policy (tensor_path.cu)
 struct TensorPathArgs {
     const float* X;  // fp32, sqrt-staged for Hellinger

@@ -345,6 +345,21 @@ class Context:
         raise_for_status(rc)
         return index, distance, st.as_dict()
 
+    def solve_f64(self, x: np.ndarray, k: int, metric: CumulativeDistance):
+        """The reference's KNN_DOUBLE_ACCUM build (types.hpp:9-13): float
+        coordinates, double accumulation and distances (knn_b200_solve_f64,
+        EXACT policy).  Returns float64 distances."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        n, d = x.shape
+        klist = min(k, n - 1) if n >= 2 else 0
+        index = np.empty((n, max(klist, 0)), dtype=np.uint32)
+        distance = np.empty((n, max(klist, 0)), dtype=np.float64)
+        st = _lib.Stats()
+        rc = _lib.load().knn_b200_solve_f64(self._h, x.ctypes.data, n, d, k, metric.metric_id,
+                                            index.ctypes.data, distance.ctypes.data, ctypes.byref(st))
+        raise_for_status(rc)
+        return index, distance, st.as_dict()
+
     def solve_rows_device(self, x_ptr: int, n: int, d: int, k: int, metric: CumulativeDistance,
                           row_begin: int, row_end: int, out_index_ptr: int, out_dist_ptr: int,
                           stream_ptr: int = 0, arith: int = _lib.ARITH_AUTO, want_stats: bool = False):

@@ -16,6 +16,7 @@
 // same bits.
 #include <chrono>
 #include <cstdlib>
+#include <mutex>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -27,8 +28,10 @@
 
 namespace knn {
 
-static_assert(std::is_same_v<dist_t, float>,
-              "the B200 engine computes in float; build without KNN_DOUBLE_ACCUM");
+// dist_t is float in the default build and double with KNN_DOUBLE_ACCUM
+// (types.hpp:9-13); the double build runs knn_b200_solve_f64 (EXACT policy,
+// FP64 accumulation, bit-identical to the reference's double build).
+static_assert(std::is_same_v<dist_t, float> || std::is_same_v<dist_t, double>);
 
 namespace {
 
@@ -66,6 +69,30 @@ int arith_from_env() {
     }
 }
 
+// Default build: float distances, one host thread per GPU (n_lanes).
+int gpu_solve(const Dataset& ds, const EngineOptions& opt, int metric, int arith, std::uint32_t lanes,
+              std::uint32_t* index, float* dist, knn_b200_stats* st) {
+    return knn_b200_solve_multi(ds.values().data(), ds.size(), ds.dim(), opt.k, metric, arith, lanes, index,
+                                dist, st);
+}
+
+// KNN_DOUBLE_ACCUM build: double distances on one process-wide device-0
+// context (lists are lane-independent, so n_lanes only changes where the work
+// runs); the mutex serialises concurrent solve_knn calls.
+[[maybe_unused]] int gpu_solve(const Dataset& ds, const EngineOptions& opt, int metric, int arith,
+                               std::uint32_t, std::uint32_t* index, double* dist, knn_b200_stats* st) {
+    if (arith == KNN_B200_ARITH_TENSOR)
+        throw ConfigError("KNN_DOUBLE_ACCUM builds run the exact policy only (KNN_B200_ARITH=tensor)");
+    static std::mutex mu;
+    static knn_b200_ctx* ctx = nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!ctx) {
+        const int rc = knn_b200_create(0, &ctx);
+        if (rc != KNN_B200_OK) return rc;
+    }
+    return knn_b200_solve_f64(ctx, ds.values().data(), ds.size(), ds.dim(), opt.k, metric, index, dist, st);
+}
+
 }  // namespace
 
 EngineResult solve_knn(const Dataset& ds, const CumulativeDistance& f, const EngineOptions& opt) {
@@ -84,10 +111,9 @@ EngineResult solve_knn(const Dataset& ds, const CumulativeDistance& f, const Eng
     const std::uint32_t n = ds.size();
     const std::uint32_t klist = std::min(opt.k, n - 1);
     std::vector<std::uint32_t> index(std::size_t(n) * klist);
-    std::vector<float> dist(std::size_t(n) * klist);
+    std::vector<dist_t> dist(std::size_t(n) * klist);
     knn_b200_stats st{};
-    const int rc = knn_b200_solve_multi(ds.values().data(), n, ds.dim(), opt.k, metric, arith,
-                                        plan.n_lanes, index.data(), dist.data(), &st);
+    const int rc = gpu_solve(ds, opt, metric, arith, plan.n_lanes, index.data(), dist.data(), &st);
     if (rc != KNN_B200_OK) rethrow_status(rc);
 
     EngineResult result;
