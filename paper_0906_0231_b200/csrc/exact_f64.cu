@@ -11,8 +11,8 @@
 //
 // Arithmetic.  t is a float, so double(t) * double(t) has at most 48
 // significant bits and is exact in double; acc + t*t therefore rounds once,
-// which is exactly what one DFMA does.  The fold below is FSUB (rn), two
-// F2F.F64 widenings and one DFMA per coordinate -- bit-identical to the
+// which is exactly what one DFMA does.  The fold below is FSUB (rn), one
+// F2F.F64.F32 widening and one DFMA per coordinate -- bit-identical to the
 // reference's separately written multiply and add.  The cosine fold
 // (acc + u*v) has the same property (float*float is exact in
 // double).
@@ -23,8 +23,9 @@
 // (order-preserving u64 of the double) << 32 | index, so the unsigned order
 // is the reference's (distance, index) order.  With 16-byte keys a 256-entry
 // list for 64 rows does not fit in shared memory, so k > 128 runs with
-// BM = 32 rows per CTA.  FP64 on B200 runs at half the FP32 FMA rate; this
-// policy is a correctness build, not the throughput path.
+// BM = 32 rows per CTA.  The widening runs on the XU pipe (16/clk/SM), which
+// bounds this kernel below the DFMA rate; this policy is a correctness build,
+// not the throughput path.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -40,6 +41,9 @@ using key128 = unsigned __int128;
 constexpr int F64_BN = 64;  // reference columns per tile (reference c1)
 constexpr int F64_DC = 32;  // coordinates per staged chunk (reference c2)
 constexpr int F64_PAD = 4;
+#ifndef F64_MR
+#define F64_MR 2  // query rows per thread (A/B knob: -DF64_MR=4)
+#endif
 
 __device__ __forceinline__ uint64_t double_to_ordered(double v) {
     const uint64_t b = uint64_t(__double_as_longlong(v + 0.0));  // -0.0 -> +0.0 (compares equal)
@@ -143,9 +147,12 @@ struct F64Params {
     int out_sqrt;
 };
 
-template <int METRIC, int BM, int KCAP>
-__global__ void __launch_bounds__(BM * 4) exact_f64_kernel(const F64Params p) {
-    constexpr int THREADS = BM * 4;  // 16 column groups x BM/4 row groups, 4x4 pairs each
+// MR x 4 pairs per thread: 16 column groups x BM/MR row groups.  MR = 2
+// gives 16 warps per CTA: the FSUB -> F2F.F64 (XU pipe) -> DFMA chains are
+// latency-bound at one CTA per SM, so more warps beat more per-thread ILP.
+template <int METRIC, int BM, int KCAP, int MR>
+__global__ void __launch_bounds__(BM / MR * 16) exact_f64_kernel(const F64Params p) {
+    constexpr int THREADS = BM / MR * 16;
     constexpr int WARPS = THREADS / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     F64Smem<BM, KCAP>& S = *reinterpret_cast<F64Smem<BM, KCAP>*>(smem_raw);
@@ -164,34 +171,59 @@ __global__ void __launch_bounds__(BM * 4) exact_f64_kernel(const F64Params p) {
     }
     __syncthreads();
 
-    for (uint32_t c0 = 0; c0 < n; c0 += F64_BN) {
-        double acc[4][4];
+    // Staging is register-prefetched: the global loads of the next
+    // (tile, coordinate-chunk) step are in flight while this step computes.
+    // Lane = coordinate, one row per warp step; coordinates past d stage as 0
+    // on both sides (a 0 step adds +0.0, leaving the accumulator's bits).
+    constexpr int RPW = F64_BN / WARPS;  // staged rows per warp and side
+    const uint32_t nchunk = (d + F64_DC - 1) / F64_DC;
+    float ra[RPW], rb[RPW];
+    auto prefetch = [&](uint32_t c0, uint32_t j0) {
+        const uint32_t j = j0 + lane;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int m = 0; m < RPW; ++m) {
+            const int rr = warp + m * WARPS;
+            ra[m] = 0.0f;
+            if (rr < BM) {
+                const uint32_t q = S.qrow[rr];
+                if (q != 0xffffffffu && j < d) ra[m] = X[size_t(q) * d + j];
+            }
+            const uint32_t col = c0 + rr;
+            rb[m] = (col < n && j < d) ? X[size_t(col) * d + j] : 0.0f;
+        }
+    };
+    prefetch(0, 0);
+    for (uint32_t c0 = 0; c0 < n; c0 += F64_BN) {
+        double acc[MR][4];
+#pragma unroll
+        for (int i = 0; i < MR; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
 
-        for (uint32_t j0 = 0; j0 < d; j0 += F64_DC) {
-            // Coordinates past d stage as 0 on both sides: a 0 step adds +0.0,
-            // which leaves the accumulator's bits unchanged.
-            const uint32_t j = j0 + lane;
-            for (int rr = warp; rr < F64_BN; rr += WARPS) {
-                if (rr < BM) {
-                    const uint32_t q = S.qrow[rr];
-                    S.a[lane][rr] = (q != 0xffffffffu && j < d) ? X[size_t(q) * d + j] : 0.0f;
-                }
-                const uint32_t col = c0 + rr;
-                S.b[lane][rr] = (col < n && j < d) ? X[size_t(col) * d + j] : 0.0f;
+        for (uint32_t jc = 0; jc < nchunk; ++jc) {
+#pragma unroll
+            for (int m = 0; m < RPW; ++m) {
+                const int rr = warp + m * WARPS;
+                if (rr < BM) S.a[lane][rr] = ra[m];
+                S.b[lane][rr] = rb[m];
             }
             __syncthreads();
+            if (jc + 1 < nchunk) prefetch(c0, (jc + 1) * F64_DC);
+            else if (c0 + F64_BN < n) prefetch(c0 + F64_BN, 0);
 #pragma unroll 4
             for (int jj = 0; jj < F64_DC; ++jj) {
-                const float4 a4 = *reinterpret_cast<const float4*>(&S.a[jj][ty * 4]);
+                float av[MR];
+                if constexpr (MR == 4) {
+                    const float4 a4 = *reinterpret_cast<const float4*>(&S.a[jj][ty * 4]);
+                    av[0] = a4.x; av[1] = a4.y; av[2] = a4.z; av[3] = a4.w;
+                } else {
+                    const float2 a2 = *reinterpret_cast<const float2*>(&S.a[jj][ty * 2]);
+                    av[0] = a2.x; av[1] = a2.y;
+                }
                 const float4 b4 = *reinterpret_cast<const float4*>(&S.b[jj][tx * 4]);
-                const float av[4] = {a4.x, a4.y, a4.z, a4.w};
                 const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                for (int i = 0; i < MR; ++i)
 #pragma unroll
                     for (int c = 0; c < 4; ++c) acc[i][c] = fold_step_f64<METRIC>(bv[c], av[i], acc[i][c]);
             }
@@ -199,8 +231,8 @@ __global__ void __launch_bounds__(BM * 4) exact_f64_kernel(const F64Params p) {
         }
 
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int rr = ty * 4 + i;
+        for (int i = 0; i < MR; ++i) {
+            const int rr = ty * MR + i;
             const uint32_t q = S.qrow[rr];
             if (q == 0xffffffffu) continue;
             const key128 thr = S.thr[rr];
@@ -243,13 +275,15 @@ __global__ void __launch_bounds__(BM * 4) exact_f64_kernel(const F64Params p) {
     }
 }
 
+constexpr int kF64MR = F64_MR;
+
 template <int METRIC, int BM, int KCAP>
 cudaError_t launch_f64_t(const F64Params& p, cudaStream_t stream) {
     const size_t smem = sizeof(F64Smem<BM, KCAP>);
-    auto kern = exact_f64_kernel<METRIC, BM, KCAP>;
+    auto kern = exact_f64_kernel<METRIC, BM, KCAP, kF64MR>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    kern<<<(p.nslots + BM - 1) / BM, BM * 4, smem, stream>>>(p);
+    kern<<<(p.nslots + BM - 1) / BM, BM / kF64MR * 16, smem, stream>>>(p);
     return cudaGetLastError();
 }
 
