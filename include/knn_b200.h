@@ -163,6 +163,13 @@ KNN_B200_API int knn_b200_solve_multi(const float *host_vectors, uint32_t n, uin
                          int metric, int arith, uint32_t n_gpus, uint32_t *out_index,
                          float *out_dist, knn_b200_stats *stats);
 
+/* knn_b200_solve_multi for the KNN_DOUBLE_ACCUM build: the same query-row
+ * shards over min(n_gpus, device count) devices, each running the FP64 EXACT
+ * sweep of knn_b200_solve_f64; out_dist is n x min(k, n-1) doubles. */
+KNN_B200_API int knn_b200_solve_multi_f64(const float *host_vectors, uint32_t n, uint32_t d, uint32_t k,
+                                          int metric, uint32_t n_gpus, uint32_t *out_index, double *out_dist,
+                                          knn_b200_stats *stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -24,6 +24,7 @@ EXPORTS = (
     "knn_b200_destroy",
     "knn_b200_solve",
     "knn_b200_solve_f64",
+    "knn_b200_solve_multi_f64",
     "knn_b200_solve_rows_device",
     "knn_b200_solve_multi",
     "knn_b200_generate_device",
@@ -91,6 +92,9 @@ def load() -> ctypes.CDLL:
         lib.knn_b200_solve_f64.argtypes = [
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
             ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)]
+        lib.knn_b200_solve_multi_f64.argtypes = [
+            ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int,
+            ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)]
         lib.knn_b200_solve_rows_device.argtypes = [
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
             ctypes.c_int, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,

@@ -16,6 +16,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/knn_b200.h"
@@ -349,6 +350,30 @@ void solve_rows_core(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, 
     ++ctr.launches;
 }
 
+// KNN_DOUBLE_ACCUM rows: validation + staging + the FP64 EXACT sweep of query
+// rows [row_begin, row_end), enqueued on `stream`.
+void solve_rows_core_f64(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, uint32_t k, int metric,
+                         uint32_t row_begin, uint32_t row_end, uint32_t* out_index, double* out_dist,
+                         cudaStream_t stream, Counters& ctr) {
+    validate_device(ctx, X, n, d, metric, stream, ctr);
+    const float* Xs = X;
+    if (metric == KNN_B200_METRIC_HELLINGER) {
+        float* staged = static_cast<float*>(ctx->staged.get(size_t(n) * d * sizeof(float)));
+        cuda_check(knnb::launch_stage_sqrt(X, staged, uint64_t(n) * d, ctx->sm_count, stream), "stage launch");
+        ++ctr.launches;
+        Xs = staged;
+    }
+    const int fold = metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean;
+    ctr.arith_used = KNN_B200_ARITH_EXACT;
+    ctr.distance_evals += uint64_t(row_end - row_begin) * n;
+    cuda_check(cudaEventRecord(ctx->ev[4], stream), "event");
+    cuda_check(knnb::launch_exact_f64(fold, Xs, n, d, std::min(k, n - 1), row_begin, row_end, out_index, out_dist,
+                                      metric == KNN_B200_METRIC_EUCLIDEAN, stream),
+               "exact f64 sweep launch");
+    cuda_check(cudaEventRecord(ctx->ev[5], stream), "event");
+    ++ctr.launches;
+}
+
 void fill_stats(knn_b200_stats* st, const Counters& ctr, uint64_t pairs, int ndev) {
     if (!st) return;
     st->pair_evaluations = pairs;
@@ -489,22 +514,7 @@ int knn_b200_solve_f64(knn_b200_ctx* ctx, const float* host_vectors, uint32_t n,
         cuda_check(cudaEventRecord(ctx->ev[0], s), "event");
         host_copy(ctx, X, host_vectors, vec_bytes, true, s);
         cuda_check(cudaEventRecord(ctx->ev[1], s), "event");
-        validate_device(ctx, X, n, d, metric, s, ctr);
-        const float* Xs = X;
-        if (metric == KNN_B200_METRIC_HELLINGER) {
-            float* staged = static_cast<float*>(ctx->staged.get(vec_bytes));
-            cuda_check(knnb::launch_stage_sqrt(X, staged, uint64_t(n) * d, ctx->sm_count, s), "stage launch");
-            ++ctr.launches;
-            Xs = staged;
-        }
-        const int fold = metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean;
-        ctr.distance_evals += uint64_t(n) * n;
-        cuda_check(cudaEventRecord(ctx->ev[4], s), "event");
-        cuda_check(knnb::launch_exact_f64(fold, Xs, n, d, klist, 0, n, oi, od,
-                                          metric == KNN_B200_METRIC_EUCLIDEAN, s),
-                   "exact f64 sweep launch");
-        cuda_check(cudaEventRecord(ctx->ev[5], s), "event");
-        ++ctr.launches;
+        solve_rows_core_f64(ctx, X, n, d, k, metric, 0, n, oi, od, s, ctr);
         cuda_check(cudaEventRecord(ctx->ev[2], s), "event");
         cuda_check(cudaEventSynchronize(ctx->ev[2]), "solve sync");
         const auto t_d2h = std::chrono::steady_clock::now();
@@ -565,10 +575,16 @@ int knn_b200_solve_rows_device(knn_b200_ctx* ctx, const float* dev_vectors, uint
     });
 }
 
-int knn_b200_solve_multi(const float* host_vectors, uint32_t n, uint32_t d, uint32_t k, int metric, int arith,
-                         uint32_t n_gpus, uint32_t* out_index, float* out_dist, knn_b200_stats* stats) {
-    // One process-wide context per device, reused across calls and guarded by
-    // a mutex so concurrent solve_knn calls serialise.
+}  // extern "C"
+
+namespace {
+
+// One process-wide context per device, reused across calls and guarded by a
+// mutex so concurrent solve_knn calls serialise.  DistT =
+// float runs the float policies; double runs the KNN_DOUBLE_ACCUM sweep.
+template <typename DistT>
+int solve_multi_impl(const float* host_vectors, uint32_t n, uint32_t d, uint32_t k, int metric, int arith,
+                     uint32_t n_gpus, uint32_t* out_index, DistT* out_dist, knn_b200_stats* stats) {
     static std::mutex pool_mu;
     static std::vector<knn_b200_ctx*> pool;
     return guarded([&] {
@@ -604,20 +620,24 @@ int knn_b200_solve_multi(const float* host_vectors, uint32_t n, uint32_t d, uint
                 const size_t out_elems = size_t(r1 - r0) * klist;
                 float* X = static_cast<float*>(ctx->vectors.get(vec_bytes));
                 auto* oi = static_cast<uint32_t*>(ctx->out_index.get(std::max<size_t>(out_elems, 1) * 4));
-                auto* od = static_cast<float*>(ctx->out_dist.get(std::max<size_t>(out_elems, 1) * 4));
+                auto* od = static_cast<DistT*>(ctx->out_dist.get(std::max<size_t>(out_elems, 1) * sizeof(DistT)));
                 cudaStream_t s = ctx->stream;
                 cuda_check(cudaEventRecord(ctx->ev[0], s), "event");
                 // the lanes share the host: each stages with its share of the threads
                 const int st_threads = std::max(1, kStageThreadsDefault / int(use));
                 host_copy(ctx, X, host_vectors, vec_bytes, true, s, st_threads);
                 cuda_check(cudaEventRecord(ctx->ev[1], s), "event");
-                solve_rows_core(ctx, X, n, d, k, metric, arith, r0, r1, oi, od, s, ctrs[g]);
+                if constexpr (std::is_same_v<DistT, double>)
+                    solve_rows_core_f64(ctx, X, n, d, k, metric, r0, r1, oi, od, s, ctrs[g]);
+                else
+                    solve_rows_core(ctx, X, n, d, k, metric, arith, r0, r1, oi, od, s, ctrs[g]);
                 cuda_check(cudaEventRecord(ctx->ev[2], s), "event");
                 cuda_check(cudaEventSynchronize(ctx->ev[2]), "solve sync");
                 const auto t_d2h = std::chrono::steady_clock::now();
                 if (out_elems) {
                     host_copy(ctx, out_index + size_t(r0) * klist, oi, out_elems * 4, false, s, st_threads);
-                    host_copy(ctx, out_dist + size_t(r0) * klist, od, out_elems * 4, false, s, st_threads);
+                    host_copy(ctx, out_dist + size_t(r0) * klist, od, out_elems * sizeof(DistT), false, s,
+                              st_threads);
                 }
                 cuda_check(cudaStreamSynchronize(s), "solve sync");
                 hms[g] = elapsed_ms(ctx->ev[0], ctx->ev[1]);
@@ -655,6 +675,21 @@ int knn_b200_solve_multi(const float* host_vectors, uint32_t n, uint32_t d, uint
             stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         }
     });
+}
+
+}  // namespace
+
+extern "C" {
+
+int knn_b200_solve_multi(const float* host_vectors, uint32_t n, uint32_t d, uint32_t k, int metric, int arith,
+                         uint32_t n_gpus, uint32_t* out_index, float* out_dist, knn_b200_stats* stats) {
+    return solve_multi_impl<float>(host_vectors, n, d, k, metric, arith, n_gpus, out_index, out_dist, stats);
+}
+
+int knn_b200_solve_multi_f64(const float* host_vectors, uint32_t n, uint32_t d, uint32_t k, int metric,
+                             uint32_t n_gpus, uint32_t* out_index, double* out_dist, knn_b200_stats* stats) {
+    return solve_multi_impl<double>(host_vectors, n, d, k, metric, KNN_B200_ARITH_EXACT, n_gpus, out_index,
+                                    out_dist, stats);
 }
 
 }  // extern "C"

@@ -16,7 +16,6 @@
 // same bits.
 #include <chrono>
 #include <cstdlib>
-#include <mutex>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -76,21 +75,13 @@ int gpu_solve(const Dataset& ds, const EngineOptions& opt, int metric, int arith
                                 dist, st);
 }
 
-// KNN_DOUBLE_ACCUM build: double distances on one process-wide device-0
-// context (lists are lane-independent, so n_lanes only changes where the work
-// runs); the mutex serialises concurrent solve_knn calls.
+// KNN_DOUBLE_ACCUM build: double distances, the same lanes (FP64 EXACT sweep).
 [[maybe_unused]] int gpu_solve(const Dataset& ds, const EngineOptions& opt, int metric, int arith,
-                               std::uint32_t, std::uint32_t* index, double* dist, knn_b200_stats* st) {
+                               std::uint32_t lanes, std::uint32_t* index, double* dist, knn_b200_stats* st) {
     if (arith == KNN_B200_ARITH_TENSOR)
         throw ConfigError("KNN_DOUBLE_ACCUM builds run the exact policy only (KNN_B200_ARITH=tensor)");
-    static std::mutex mu;
-    static knn_b200_ctx* ctx = nullptr;
-    std::lock_guard<std::mutex> lock(mu);
-    if (!ctx) {
-        const int rc = knn_b200_create(0, &ctx);
-        if (rc != KNN_B200_OK) return rc;
-    }
-    return knn_b200_solve_f64(ctx, ds.values().data(), ds.size(), ds.dim(), opt.k, metric, index, dist, st);
+    return knn_b200_solve_multi_f64(ds.values().data(), ds.size(), ds.dim(), opt.k, metric, lanes, index, dist,
+                                    st);
 }
 
 }  // namespace

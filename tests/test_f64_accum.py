@@ -126,3 +126,23 @@ def test_reference_acceptance_gate_on_dropin_f64():
     p = _run_binary(ROOT / "oracle" / "_ref" / "acceptance_b200_f64", ["--skip", "4", "--skip", "5"], "exact")
     assert p.returncode == 0, p.stdout + p.stderr
     assert p.stdout.count("PASS") == 5, p.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lanes", [1, 2, 8])
+def test_solve_multi_f64_lanes(c_oracle, lanes):
+    """knn_b200_solve_multi_f64 (the double build's n_lanes): min(lanes,
+    devices) row shards, lists independent of the lane count."""
+    import ctypes
+    from paper_0906_0231_b200 import _lib
+    n, d, k = 300, 24, 12
+    x = _instance(n, d, 11)
+    idx = np.empty((n, k), dtype=np.uint32)
+    dist = np.empty((n, k), dtype=np.float64)
+    st = _lib.Stats()
+    rc = _lib.load().knn_b200_solve_multi_f64(x.ctypes.data, n, d, k, 1, lanes, idx.ctypes.data,
+                                               dist.ctypes.data, ctypes.byref(st))
+    assert rc == 0, _lib.last_error()
+    oi, od = c_oracle.brute_force_f64(x, k, "sqeuclidean")
+    _assert_f64_equal(idx, dist, oi, od, f"solve_multi_f64 lanes={lanes}")
+    assert st.pair_evaluations == n * (n - 1) // 2
