@@ -62,7 +62,16 @@ REF_LINK_F64 := $(ENGINE_F64_A) oracle/_ref/f64/libtknn_ref_noengine.a -L$(PKG)/
             -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib' -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib' -lpthread
 
 ref-bins: oracle/_ref/acceptance_b200 build/test_engine_b200 build/tknn_b200 oracle/_ref/tknn_ref \
-          oracle/_ref/acceptance_b200_f64 build/test_engine_b200_f64
+          oracle/_ref/acceptance_b200_f64 build/test_engine_b200_f64 build/tknn_b200_f64 oracle/_ref/f64/tknn_ref
+
+# The reference CLI in its KNN_DOUBLE_ACCUM build: on the double drop-in, and
+# on the reference's double engine for comparison.
+build/tknn_b200_f64: $(REF)/tools/main.cpp tools/cli11_shim/CLI11.hpp $(ENGINE_F64_A) $(LIB) oracle
+	$(CXX) $(REF_FLAGS) -DKNN_DOUBLE_ACCUM=1 -Itools/cli11_shim -I$(REF)/include -o $@ $< $(REF_LINK_F64)
+
+oracle/_ref/f64/tknn_ref: $(REF)/tools/main.cpp tools/cli11_shim/CLI11.hpp oracle
+	$(CXX) $(REF_FLAGS) -DKNN_DOUBLE_ACCUM=1 -Itools/cli11_shim -I$(REF)/include -o $@ $< \
+	    oracle/_ref/f64/libtknn_ref.a -lpthread
 
 oracle/_ref/acceptance_b200_f64: $(REF)/tests/acceptance.cpp $(ENGINE_F64_A) $(LIB) oracle
 	$(CXX) $(REF_FLAGS) -DKNN_DOUBLE_ACCUM=1 -I$(REF)/include -o $@ $< $(REF_LINK_F64)

@@ -131,3 +131,25 @@ def test_reference_acceptance_criterion_5_cli_determinism():
         pytest.skip("acceptance_b200 not built")
     p = subprocess.run([str(acc), "--only", "5", "--cli", str(B200)], capture_output=True, text=True, timeout=600)
     assert p.returncode == 0 and "PASS" in p.stdout, p.stdout + p.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fmt", ["text", "binary"])
+def test_double_accum_cli_matches_reference_double_build(tmp_path, fmt):
+    """main.cpp in the KNN_DOUBLE_ACCUM build: `run` on the double drop-in
+    (build/tknn_b200_f64) writes the same bytes as on the reference's double
+    engine (oracle/_ref/f64/tknn_ref), for every lane count."""
+    b200 = ROOT / "build" / "tknn_b200_f64"
+    ref = ROOT / "oracle" / "_ref" / "f64" / "tknn_ref"
+    if not (b200.exists() and ref.exists()):
+        pytest.skip("double-build CLIs not built")
+    data = tmp_path / "data.knnv"
+    assert cli(f"--mode generate --output {data} --n 150 --d 20 --seed 9")[0] == 0
+    ref_out = tmp_path / "ref.out"
+    rc, log = cli(f"--mode run --input {data} --output {ref_out} --k 12 --format {fmt}", binary=ref)
+    assert rc == 0, log
+    for lanes in ("1", "3"):
+        out = tmp_path / f"b200_{lanes}.out"
+        rc, log = cli(f"--mode run --input {data} --output {out} --k 12 --lanes {lanes} --format {fmt}", binary=b200)
+        assert rc == 0, log
+        assert out.read_bytes() == ref_out.read_bytes()
