@@ -216,9 +216,11 @@ __global__ void __launch_bounds__(BM / MR * 16) exact_f64_kernel(const F64Params
                 if constexpr (MR == 4) {
                     const float4 a4 = *reinterpret_cast<const float4*>(&S.a[jj][ty * 4]);
                     av[0] = a4.x; av[1] = a4.y; av[2] = a4.z; av[3] = a4.w;
-                } else {
+                } else if constexpr (MR == 2) {
                     const float2 a2 = *reinterpret_cast<const float2*>(&S.a[jj][ty * 2]);
                     av[0] = a2.x; av[1] = a2.y;
+                } else {
+                    av[0] = S.a[jj][ty];
                 }
                 const float4 b4 = *reinterpret_cast<const float4*>(&S.b[jj][tx * 4]);
                 const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
@@ -279,11 +281,13 @@ constexpr int kF64MR = F64_MR;
 
 template <int METRIC, int BM, int KCAP>
 cudaError_t launch_f64_t(const F64Params& p, cudaStream_t stream) {
+    // 32-row CTAs (k > 128) keep 16 warps with one row per thread
+    constexpr int MR = BM == 32 ? 1 : kF64MR;
     const size_t smem = sizeof(F64Smem<BM, KCAP>);
-    auto kern = exact_f64_kernel<METRIC, BM, KCAP, kF64MR>;
+    auto kern = exact_f64_kernel<METRIC, BM, KCAP, MR>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    kern<<<(p.nslots + BM - 1) / BM, BM / kF64MR * 16, smem, stream>>>(p);
+    kern<<<(p.nslots + BM - 1) / BM, BM / MR * 16, smem, stream>>>(p);
     return cudaGetLastError();
 }
 
