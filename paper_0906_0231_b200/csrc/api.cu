@@ -157,54 +157,91 @@ bool host_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
-// Copy between a host buffer and device memory, ordered on `s` (it starts
+// One host<->device copy: `dst` and `src` are the host and device sides
+// as the direction says.
+struct CopySeg {
+    void* dst;
+    const void* src;
+    size_t bytes;
+};
+
+// Copy host buffers to or from device memory, ordered on `s` (it starts
 // after the work already queued on s, and work queued on s afterwards sees
 // the data).  Pinned or small host buffers go straight to the DMA engine;
-// pageable ones through the staging lanes.  D2H returns with the data in
-// host memory.
-void host_copy(knn_b200_ctx* ctx, void* dst, const void* src, size_t bytes, bool h2d, cudaStream_t s,
-               int threads = 0) {
-    const void* host = h2d ? src : dst;
-    if (bytes < kStageMin || host_pinned(host)) {
-        cuda_check(cudaMemcpyAsync(dst, src, bytes, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s),
-                   h2d ? "H2D" : "D2H");
-        if (!h2d) cuda_check(cudaStreamSynchronize(s), "D2H sync");
+// pageable ones through the staging lanes, all segments' chunks dealt over
+// the lanes together (the two output arrays share one pipelined pass).  D2H
+// returns with the data in host memory.
+void host_copy_segs(knn_b200_ctx* ctx, const std::vector<CopySeg>& segs, bool h2d, cudaStream_t s,
+                    int threads = 0) {
+    std::vector<CopySeg> staged;
+    bool direct_d2h = false;
+    for (const CopySeg& g : segs) {
+        if (g.bytes == 0) continue;
+        const void* host = h2d ? g.src : g.dst;
+        if (g.bytes < kStageMin || host_pinned(host)) {
+            cuda_check(cudaMemcpyAsync(g.dst, g.src, g.bytes, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s),
+                       h2d ? "H2D" : "D2H");
+            direct_d2h |= !h2d;
+        } else {
+            staged.push_back(g);
+        }
+    }
+    if (staged.empty()) {
+        if (direct_d2h) cuda_check(cudaStreamSynchronize(s), "D2H sync");
         return;
     }
     stage_init(ctx);
-    const size_t kStageChunk = ctx->stage_chunk;
     threads = threads > 0 ? std::min(threads, ctx->stage_n) : ctx->stage_n;
+    size_t total = 0;
+    for (const CopySeg& g : staged) total += g.bytes;
+    // H2D uses the lane buffers whole.  D2H is shorter (C2: 80 MB), so its
+    // chunks shrink until every lane pipelines at least four of them.
+    size_t chunk = ctx->stage_chunk;
+    if (!h2d) {
+        const size_t want = (total / (size_t(threads) * 4) + 4095) / 4096 * 4096;
+        chunk = std::max<size_t>(size_t(256) << 10, std::min(chunk, want));
+    }
+    struct Chunk {
+        char* dst;
+        const char* src;
+        size_t len;
+    };
+    std::vector<Chunk> chunks;
+    for (const CopySeg& g : staged)
+        for (size_t off = 0; off < g.bytes; off += chunk)
+            chunks.push_back({static_cast<char*>(g.dst) + off, static_cast<const char*>(g.src) + off,
+                              std::min(chunk, g.bytes - off)});
+    const size_t nchunks = chunks.size();
     cuda_check(cudaEventRecord(ctx->stage_go, s), "stage event");
-    const size_t nchunks = (bytes + kStageChunk - 1) / kStageChunk;
     std::vector<cudaError_t> errs(threads, cudaSuccess);
     auto work = [&](int t) {
         StageLane& l = ctx->stage[t];
         cudaError_t e = cudaSetDevice(ctx->device);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(l.st, ctx->stage_go, 0);
-        size_t i = 0, prev_off = 0, prev_len = 0;
+        size_t i = 0;
+        const Chunk* prev = nullptr;
         for (size_t c = t; c < nchunks && e == cudaSuccess; c += threads, ++i) {
             const int b = int(i & 1);
-            const size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
+            const Chunk& k = chunks[c];
             if (h2d) {
                 if (i >= 2) e = cudaEventSynchronize(l.ev[b]);  // the DMA that last read buf[b]
                 if (e != cudaSuccess) break;
-                std::memcpy(l.buf[b], static_cast<const char*>(src) + off, len);
-                e = cudaMemcpyAsync(static_cast<char*>(dst) + off, l.buf[b], len, cudaMemcpyHostToDevice, l.st);
+                std::memcpy(l.buf[b], k.src, k.len);
+                e = cudaMemcpyAsync(k.dst, l.buf[b], k.len, cudaMemcpyHostToDevice, l.st);
                 if (e == cudaSuccess) e = cudaEventRecord(l.ev[b], l.st);
             } else {
-                e = cudaMemcpyAsync(l.buf[b], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, l.st);
+                e = cudaMemcpyAsync(l.buf[b], k.src, k.len, cudaMemcpyDeviceToHost, l.st);
                 if (e == cudaSuccess) e = cudaEventRecord(l.ev[b], l.st);
-                if (e == cudaSuccess && i >= 1) {  // the previous chunk out of the other buffer
+                if (e == cudaSuccess && prev) {  // the previous chunk out of the other buffer
                     e = cudaEventSynchronize(l.ev[b ^ 1]);
-                    if (e == cudaSuccess) std::memcpy(static_cast<char*>(dst) + prev_off, l.buf[b ^ 1], prev_len);
+                    if (e == cudaSuccess) std::memcpy(prev->dst, l.buf[b ^ 1], prev->len);
                 }
-                prev_off = off;
-                prev_len = len;
+                prev = &k;
             }
         }
-        if (!h2d && e == cudaSuccess && i >= 1) {
+        if (!h2d && e == cudaSuccess && prev) {
             e = cudaEventSynchronize(l.ev[(i - 1) & 1]);
-            if (e == cudaSuccess) std::memcpy(static_cast<char*>(dst) + prev_off, l.buf[(i - 1) & 1], prev_len);
+            if (e == cudaSuccess) std::memcpy(prev->dst, l.buf[(i - 1) & 1], prev->len);
         }
         if (e == cudaSuccess) e = cudaEventRecord(l.done, l.st);
         errs[t] = e;
@@ -215,6 +252,12 @@ void host_copy(knn_b200_ctx* ctx, void* dst, const void* src, size_t bytes, bool
     for (auto& th : pool) th.join();
     for (auto e : errs) cuda_check(e, h2d ? "staged H2D" : "staged D2H");
     for (int t = 0; t < threads; ++t) cuda_check(cudaStreamWaitEvent(s, ctx->stage[t].done, 0), "stage join");
+    if (direct_d2h) cuda_check(cudaStreamSynchronize(s), "D2H sync");
+}
+
+void host_copy(knn_b200_ctx* ctx, void* dst, const void* src, size_t bytes, bool h2d, cudaStream_t s,
+               int threads = 0) {
+    host_copy_segs(ctx, {CopySeg{dst, src, bytes}}, h2d, s, threads);
 }
 
 const char* metric_name(int metric) {
@@ -481,8 +524,8 @@ int knn_b200_solve(knn_b200_ctx* ctx, const float* host_vectors, uint32_t n, uin
         cuda_check(cudaEventRecord(ctx->ev[2], s), "event");
         cuda_check(cudaEventSynchronize(ctx->ev[2]), "solve sync");
         const auto t_d2h = std::chrono::steady_clock::now();
-        host_copy(ctx, out_index, oi, out_elems * sizeof(uint32_t), false, s);
-        host_copy(ctx, out_dist, od, out_elems * sizeof(float), false, s);
+        host_copy_segs(ctx, {{out_index, oi, out_elems * sizeof(uint32_t)}, {out_dist, od, out_elems * sizeof(float)}},
+                       false, s);
         cuda_check(cudaStreamSynchronize(s), "solve sync");
         if (stats) {
             fill_stats(stats, ctr, uint64_t(n) * (n - 1) / 2, 1);
@@ -518,8 +561,9 @@ int knn_b200_solve_f64(knn_b200_ctx* ctx, const float* host_vectors, uint32_t n,
         cuda_check(cudaEventRecord(ctx->ev[2], s), "event");
         cuda_check(cudaEventSynchronize(ctx->ev[2]), "solve sync");
         const auto t_d2h = std::chrono::steady_clock::now();
-        host_copy(ctx, out_index, oi, out_elems * sizeof(uint32_t), false, s);
-        host_copy(ctx, out_dist, od, out_elems * sizeof(double), false, s);
+        host_copy_segs(ctx,
+                       {{out_index, oi, out_elems * sizeof(uint32_t)}, {out_dist, od, out_elems * sizeof(double)}},
+                       false, s);
         cuda_check(cudaStreamSynchronize(s), "solve sync");
         if (stats) {
             fill_stats(stats, ctr, uint64_t(n) * (n - 1) / 2, 1);
@@ -635,9 +679,10 @@ int solve_multi_impl(const float* host_vectors, uint32_t n, uint32_t d, uint32_t
                 cuda_check(cudaEventSynchronize(ctx->ev[2]), "solve sync");
                 const auto t_d2h = std::chrono::steady_clock::now();
                 if (out_elems) {
-                    host_copy(ctx, out_index + size_t(r0) * klist, oi, out_elems * 4, false, s, st_threads);
-                    host_copy(ctx, out_dist + size_t(r0) * klist, od, out_elems * sizeof(DistT), false, s,
-                              st_threads);
+                    host_copy_segs(ctx,
+                                   {{out_index + size_t(r0) * klist, oi, out_elems * 4},
+                                    {out_dist + size_t(r0) * klist, od, out_elems * sizeof(DistT)}},
+                                   false, s, st_threads);
                 }
                 cuda_check(cudaStreamSynchronize(s), "solve sync");
                 hms[g] = elapsed_ms(ctx->ev[0], ctx->ev[1]);
