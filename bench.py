@@ -311,7 +311,10 @@ def main():
     #      N GPUs: pinned host input -> H2D (rank 0) -> NCCL broadcast ->
     #      shard solve -> D2H of the shard's lists, timed by CUDA events.
     e2e_path = None
+    e2e_pinned_ms = None
     if not launched:
+        import numpy as np
+
         x_np = x.cpu().numpy()  # pageable
         ctx.solve(x_np, k, metric, arith)  # staging buffers allocated outside the timed region
         torch.cuda.synchronize()
@@ -321,6 +324,20 @@ def main():
         e2e_ms = (time.perf_counter() - t_e2e) * 1e3
         e2e_path = "knn_b200_solve (C ABI), pageable host buffers in and out, host clock"
         del x_np
+        # The same call with pinned host buffers (the ABI then DMAs directly):
+        # reported beside the pageable headline, not instead of it.
+        x_pin = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
+        x_pin.copy_(x)
+        idx_pin = torch.empty((n, klist), dtype=torch.int32, pin_memory=True)
+        dist_pin = torch.empty((n, klist), dtype=torch.float32, pin_memory=True)
+        pin_out = (idx_pin.numpy().view(np.uint32), dist_pin.numpy())
+        ctx.solve(x_pin.numpy(), k, metric, arith, out=pin_out)
+        torch.cuda.synchronize()
+        t_pin = time.perf_counter()
+        for _ in range(args.steps):
+            ctx.solve(x_pin.numpy(), k, metric, arith, out=pin_out)
+        e2e_pinned_ms = (time.perf_counter() - t_pin) * 1e3 / args.steps
+        del x_pin, idx_pin, dist_pin, pin_out
     if launched:
         x_host = torch.empty((n, d), dtype=torch.float32, pin_memory=True) if rank == 0 else None
         if rank == 0:
@@ -389,7 +406,8 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms / args.steps,
                 "h2d_bytes_per_step": n * d * 4 if rank == 0 else 0,
                 "d2h_bytes_per_step": n * klist * 8 if not launched else (r1 - r0) * klist * 8,
-                "path": e2e_path},
+                "path": e2e_path,
+                "pinned_ms_per_step": e2e_pinned_ms},
         "gpu_launches": launches,
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes/launch (DRAM, ncu)",

@@ -332,13 +332,23 @@ class Context:
         except Exception:
             pass
 
-    def solve(self, x: np.ndarray, k: int, metric: CumulativeDistance, arith: int = _lib.ARITH_AUTO):
-        """Host arrays in, host arrays out (knn_b200_solve)."""
+    def solve(self, x: np.ndarray, k: int, metric: CumulativeDistance, arith: int = _lib.ARITH_AUTO,
+              out: tuple[np.ndarray, np.ndarray] | None = None):
+        """Host arrays in, host arrays out (knn_b200_solve).  ``out``: optional
+        caller-owned (index uint32, distance float32) arrays of shape
+        n x min(k, n-1), e.g. views of pinned memory."""
         x = np.ascontiguousarray(x, dtype=np.float32)
         n, d = x.shape
         klist = min(k, n - 1) if n >= 2 else 0
-        index = np.empty((n, max(klist, 0)), dtype=np.uint32)
-        distance = np.empty((n, max(klist, 0)), dtype=np.float32)
+        if out is not None:
+            index, distance = out
+            if (index.shape != (n, max(klist, 0)) or distance.shape != index.shape or index.dtype != np.uint32
+                    or distance.dtype != np.float32 or not index.flags.c_contiguous
+                    or not distance.flags.c_contiguous):
+                raise ConfigError("out must be C-contiguous (uint32, float32) arrays of shape n x min(k, n-1)")
+        else:
+            index = np.empty((n, max(klist, 0)), dtype=np.uint32)
+            distance = np.empty((n, max(klist, 0)), dtype=np.float32)
         st = _lib.Stats()
         rc = _lib.load().knn_b200_solve(self._h, x.ctypes.data, n, d, k, metric.metric_id, arith,
                                         index.ctypes.data, distance.ctypes.data, ctypes.byref(st))
