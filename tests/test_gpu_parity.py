@@ -330,3 +330,21 @@ def test_staged_host_copies_match_device_path(ctx):
         assert np.array_equal(idx, di)
         assert np.array_equal(dist.view(np.uint32), dd.view(np.uint32))
         assert st["h2d_ms"] > 0 and st["d2h_ms"] > 0
+
+
+def test_solve_into_caller_owned_pinned_outputs(ctx, c_oracle):
+    """Context.solve(out=...) writes into caller-owned (here pinned) arrays,
+    the ABI's direct-DMA path, with the same bits as its own outputs."""
+    import torch
+    from paper_0906_0231_b200 import ConfigError
+    x = c_oracle.generate(3000, 40, 21)
+    m = metric_obj("sqeuclidean")
+    idx_pin = torch.empty((3000, 10), dtype=torch.int32, pin_memory=True)
+    dist_pin = torch.empty((3000, 10), dtype=torch.float32, pin_memory=True)
+    out = (idx_pin.numpy().view(np.uint32), dist_pin.numpy())
+    i1, d1, _ = ctx.solve(x, 10, m, arith_id("tensor"), out=out)
+    assert i1 is out[0] and d1 is out[1]
+    i0, d0, _ = ctx.solve(x, 10, m, arith_id("tensor"))
+    assert np.array_equal(i0, i1) and np.array_equal(d0.view(np.uint32), d1.view(np.uint32))
+    with pytest.raises(ConfigError):
+        ctx.solve(x, 10, m, arith_id("tensor"), out=(out[0][:, :5], out[1]))
