@@ -626,11 +626,12 @@ namespace {
 // One process-wide context per device, reused across calls and guarded by a
 // mutex so concurrent solve_knn calls serialise.  DistT =
 // float runs the float policies; double runs the KNN_DOUBLE_ACCUM sweep.
+std::mutex pool_mu;                // guards `pool`, shared by both distance types
+std::vector<knn_b200_ctx*> pool;  // one context per device, created on first use
+
 template <typename DistT>
 int solve_multi_impl(const float* host_vectors, uint32_t n, uint32_t d, uint32_t k, int metric, int arith,
                      uint32_t n_gpus, uint32_t* out_index, DistT* out_dist, knn_b200_stats* stats) {
-    static std::mutex pool_mu;
-    static std::vector<knn_b200_ctx*> pool;
     return guarded([&] {
         check_args(n, d, k, metric, arith);
         if (n_gpus < 1) fail(KNN_B200_ERR_CONFIG, "n_lanes must be at least 1");
