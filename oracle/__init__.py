@@ -69,7 +69,23 @@ class CRestatement:
         lib.ko_fold_f64.restype = ctypes.c_double
         lib.ko_brute_force_f64.argtypes = [_f32p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                                            ctypes.c_int, _u32p, _f64p]
+        lib.ko_rows_topk_f64.argtypes = [_f32p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                         ctypes.c_int, _u32p, ctypes.c_uint32, _u32p, _f64p]
         self.lib = lib
+
+    def rows_topk_f64(self, x: np.ndarray, k: int, metric, rows):
+        """The double build's lists for the query rows ``rows`` (single thread)."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        rows = np.ascontiguousarray(rows, dtype=np.uint32)
+        n, d = x.shape
+        cap = min(k, n - 1)
+        idx = np.empty((rows.size, cap), dtype=np.uint32)
+        dist = np.empty((rows.size, cap), dtype=np.float64)
+        rc = self.lib.ko_rows_topk_f64(_ptr(x, _f32p), n, d, k, metric_id(metric), _ptr(rows, _u32p), rows.size,
+                                       _ptr(idx, _u32p), _ptr(dist, _f64p))
+        if rc != 0:
+            raise ValueError(f"ko_rows_topk_f64 failed with code {rc}")
+        return idx, dist
 
     def brute_force_f64(self, x: np.ndarray, k: int, metric):
         """brute_force_knn of the KNN_DOUBLE_ACCUM build: float64 distances."""

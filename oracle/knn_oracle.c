@@ -279,6 +279,34 @@ int ko_brute_force_f64(const float *x, uint32_t n, uint32_t d, uint32_t k, int m
     return 0;
 }
 
+/* The double build's lists for a subset of query rows (same selection as
+ * ko_brute_force_f64, row by row). Outputs are nrows x min(k, n-1). */
+int ko_rows_topk_f64(const float *x, uint32_t n, uint32_t d, uint32_t k, int metric, const uint32_t *rows,
+                     uint32_t nrows, uint32_t *out_index, double *out_dist) {
+    if (k < 1 || n < 2 || d < 1) return 2;
+    const uint32_t cap = k < n - 1 ? k : n - 1;
+    ko_neighbor64 *row = (ko_neighbor64 *)malloc(sizeof(ko_neighbor64) * n);
+    if (!row) return 4;
+    for (uint32_t r = 0; r < nrows; ++r) {
+        const uint32_t q = rows[r];
+        uint32_t m = 0;
+        for (uint32_t y = 0; y < n; ++y) {
+            if (y == q) continue;
+            const uint32_t hi = y > q ? y : q, lo = y > q ? q : y;
+            row[m].distance = ko_fold_f64(metric, x + (size_t)hi * d, x + (size_t)lo * d, d);
+            row[m].index = y;
+            ++m;
+        }
+        qsort(row, m, sizeof(ko_neighbor64), nb64_cmp);
+        for (uint32_t j = 0; j < cap; ++j) {
+            out_index[(size_t)r * cap + j] = row[j].index;
+            out_dist[(size_t)r * cap + j] = row[j].distance;
+        }
+    }
+    free(row);
+    return 0;
+}
+
 /* ---- sampled-row oracle ---------------------------- */
 typedef struct {
     const float *x;

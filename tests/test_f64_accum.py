@@ -94,6 +94,33 @@ def test_solve_f64_bit_exact(c_oracle, case):
     assert st["pair_evaluations"] == n * (n - 1) // 2
 
 
+def test_f64_rows_topk_equals_brute_force(c_oracle):
+    x = _instance(90, 7, 12)
+    rows = np.array([0, 5, 44, 89], dtype=np.uint32)
+    bi, bd = c_oracle.brute_force_f64(x, 9, "hellinger")
+    ri, rd = c_oracle.rows_topk_f64(x, 9, "hellinger", rows)
+    _assert_f64_equal(ri, rd, bi[rows], bd[rows], "rows_topk_f64 vs brute_force_f64")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,d,k,metric", [(65536, 64, 50, "sqeuclidean"), (40000, 300, 129, "cosine")])
+def test_solve_f64_large_sampled_rows(c_oracle, n, d, k, metric):
+    """Many column tiles and list merges per CTA: sampled rows against the
+    double oracle, bit for bit."""
+    from paper_0906_0231_b200 import Context, distance_by_name
+    x = _instance(n, d, 13)
+    if metric == "cosine":
+        x /= np.linalg.norm(x.astype(np.float64), axis=1, keepdims=True).astype(np.float32)
+    ctx = Context(0)
+    try:
+        gi, gd, _ = ctx.solve_f64(x, k, distance_by_name(metric))
+    finally:
+        ctx.close()
+    rows = np.unique(np.concatenate([np.random.default_rng(3).choice(n, 48, replace=False), [0, n - 1]]))
+    oi, od = c_oracle.rows_topk_f64(x, k, metric, rows.astype(np.uint32))
+    _assert_f64_equal(gi[rows], gd[rows], oi, od, f"solve_f64 sampled rows n={n} d={d} k={k} {metric}")
+
+
 @pytest.mark.gpu
 def test_solve_f64_validation_errors():
     from paper_0906_0231_b200 import Context, ValidationError, ConfigError, distance_by_name
