@@ -34,7 +34,7 @@ lib: $(LIB)
 
 build/obj/%.o: $(CSRC)/%.cu $(wildcard $(CSRC)/*.cuh) $(CSRC)/kernels.h include/knn_b200.h
 	@mkdir -p build/obj
-	$(NVCC) $(NVFLAGS) -Iinclude -c $< -o $@
+	$(NVCC) $(NVFLAGS) $(NVFLAGS_EXTRA) -Iinclude -c $< -o $@
 
 $(LIB): $(CU_OBJS)
 	@mkdir -p $(PKG)/lib
