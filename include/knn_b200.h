@@ -20,8 +20,9 @@
  *     3 = ValidationError, 4 = internal/CUDA error.  knn_b200_last_error()
  *     returns the message of the last failure on the calling thread.
  *   - Output rows are ascending by (distance, index), self excluded, of length
- *     min(k, n-1), exactly as NeighborList (include/knn/heap.hpp:62-67,
- *     src/heap.cpp:69).  Results are bit-identical to the reference's
+ *     min(k, n-1) for any k >= 1, exactly as NeighborList
+ *     (include/knn/heap.hpp:62-67, src/heap.cpp:69).  Lists longer than 256
+ *     run the sort-based EXACT path.  Results are bit-identical to the reference's
  *     brute_force_knn for every arithmetic policy.
  *   - There is no CPU fallback: without a usable sm_100 device every compute
  *     entry point fails with KNN_B200_ERR_INTERNAL.
@@ -107,7 +108,10 @@ KNN_B200_API int knn_b200_device_count(int *out_count);
 
 /* A context owns one device's streams and grow-only workspace; reuse it
  * across calls (the reference CLI bench calls solve_knn twice,
- * tools/main.cpp:163-164).  Not thread-safe: one context per host thread. */
+ * tools/main.cpp:163-164).  Calls on one context are serialised by a mutex,
+ * and each call's device work is ordered after the previous call's (an
+ * event on the previous call's stream), so consecutive calls may use
+ * different streams without racing on the workspace. */
 KNN_B200_API int knn_b200_create(int device, knn_b200_ctx **out_ctx);
 KNN_B200_API void knn_b200_destroy(knn_b200_ctx *ctx);
 

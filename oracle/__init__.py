@@ -56,6 +56,7 @@ class CRestatement:
         lib.ko_next_unit_float.argtypes = [_u64p]
         lib.ko_next_unit_float.restype = ctypes.c_float
         lib.ko_generate.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, _f32p]
+        lib.ko_generate_at.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _f32p]
         lib.ko_fold.argtypes = [ctypes.c_int, _f32p, _f32p, ctypes.c_uint32]
         lib.ko_fold.restype = ctypes.c_float
         lib.ko_heap_stream.argtypes = [ctypes.c_uint32, _f32p, _u32p, ctypes.c_uint32, _f32p, _u32p]
@@ -111,6 +112,13 @@ class CRestatement:
     def generate(self, n: int, d: int, seed: int) -> np.ndarray:
         out = np.empty((n, d), dtype=np.float32)
         self.lib.ko_generate(n, d, seed, _ptr(out, _f32p))
+        return out
+
+    def generate_at(self, seed: int, first: int, count: int) -> np.ndarray:
+        """Elements [first, first + count) of generate_dataset's row-major
+        stream (Weyl jump, knn_oracle.c ko_generate_at)."""
+        out = np.empty(count, dtype=np.float32)
+        self.lib.ko_generate_at(seed, first, count, _ptr(out, _f32p))
         return out
 
     def fold(self, metric, u: np.ndarray, v: np.ndarray) -> np.float32:

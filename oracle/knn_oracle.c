@@ -58,6 +58,15 @@ void ko_generate(uint32_t n, uint32_t d, uint64_t seed, float *out) {
     for (size_t i = 0; i < total; ++i) out[i] = ko_next_unit_float(&s);
 }
 
+/* Elements [first, first + count) of the same stream.  next() only adds the
+ * Weyl increment to the state (rng.hpp:13-14), so the state before element i
+ * is seed + i * 0x9e3779b97f4a7c15 (mod 2^64): jump there, then step as
+ * ko_generate does.  Pinned against ko_generate in tests/test_oracle_pin.py. */
+void ko_generate_at(uint64_t seed, uint64_t first, uint64_t count, float *out) {
+    uint64_t s = seed + first * 0x9e3779b97f4a7c15ull;
+    for (uint64_t i = 0; i < count; ++i) out[i] = ko_next_unit_float(&s);
+}
+
 /* ---- distance.hpp:41-65 (+ cosine custom fold), fold 98-105 ----------- */
 float ko_fold(int metric, const float *u, const float *v, uint32_t d) {
     float acc = 0.0f;

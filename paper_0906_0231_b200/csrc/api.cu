@@ -106,6 +106,11 @@ struct knn_b200_ctx {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};  // [0..3] call phases, [4..5] around the sweep kernel
     DevBuf vectors, staged, flags, out_index, out_dist, tensor_ws, exact_ws, capture_ws;
+    // Recorded on the working stream at the end of every call; the next call's
+    // stream waits on it first, so a call on another stream never touches the
+    // workspace while the previous call's kernels are still in flight.
+    cudaEvent_t busy = nullptr;
+    bool busy_recorded = false;
     unsigned long long* host_flags = nullptr;  // pinned
     StageLane stage[kStageThreads];
     cudaEvent_t stage_go = nullptr;
@@ -277,10 +282,9 @@ void check_args(uint32_t n, uint32_t d, uint32_t k, int metric, int arith) {
     if (d < 1) fail(KNN_B200_ERR_CONFIG, "dataset dimension must be at least 1");
     if (metric < 0 || metric > 3) fail(KNN_B200_ERR_CONFIG, "unknown metric id " + std::to_string(metric));
     if (arith < 0 || arith > 2) fail(KNN_B200_ERR_CONFIG, "unknown arithmetic policy " + std::to_string(arith));
-    const uint32_t klist = std::min(k, n - 1);
-    if (klist > knnb::kExactMaxK)
-        fail(KNN_B200_ERR_CONFIG, "min(k, n-1) = " + std::to_string(klist) + " exceeds the supported " +
-                                      std::to_string(knnb::kExactMaxK));
+    // any k: lists longer than the fused kernels hold (kExactMaxK) take the
+    // sort-based EXACT path (exact_bigk.cu), as HeapStore holds min(k, n-1)
+    // for any k (heap.cpp:66-70)
 }
 
 struct Counters {
@@ -329,6 +333,7 @@ void solve_rows_core(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, 
                      int arith, uint32_t row_begin, uint32_t row_end, uint32_t* out_index, float* out_dist,
                      cudaStream_t stream, Counters& ctr) {
     validate_device(ctx, X, n, d, metric, stream, ctr);
+    if (row_end == row_begin) return;  // an empty shard: validated, nothing to compute
     const float* Xs = X;
     if (metric == KNN_B200_METRIC_HELLINGER) {
         float* staged = static_cast<float*>(ctx->staged.get(size_t(n) * d * sizeof(float)));
@@ -339,6 +344,19 @@ void solve_rows_core(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, 
     const uint32_t klist = std::min(k, n - 1);
     const int fold = metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean;
     const int out_sqrt = metric == KNN_B200_METRIC_EUCLIDEAN;
+    if (klist > knnb::kExactMaxK) {  // long lists: sort-based EXACT path
+        ctr.arith_used = KNN_B200_ARITH_EXACT;
+        ctr.distance_evals += uint64_t(row_end - row_begin) * n;
+        void* ws = ctx->exact_ws.get(knnb::exact_bigk_workspace_bytes(row_end - row_begin, n, 0));
+        cuda_check(cudaEventRecord(ctx->ev[4], stream), "event");
+        cuda_check(knnb::launch_exact_bigk(fold, 0, Xs, n, d, klist, row_begin, row_end, out_index, out_dist,
+                                           out_sqrt, ws, ctx->sm_count, stream),
+                   "exact long-list launch");
+        cuda_check(cudaEventRecord(ctx->ev[5], stream), "event");
+        ctr.launches += 3 * ((row_end - row_begin + knnb::exact_bigk_batch_rows(row_end - row_begin, n) - 1) /
+                             knnb::exact_bigk_batch_rows(row_end - row_begin, n));
+        return;
+    }
     const uint32_t kp = knnb::tensor_kp_for(klist);
     // AUTO: the tensor filter pays off once the sweep dominates its fixed
     // prologue; both policies return identical bits.
@@ -399,6 +417,7 @@ void solve_rows_core_f64(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t
                          uint32_t row_begin, uint32_t row_end, uint32_t* out_index, double* out_dist,
                          cudaStream_t stream, Counters& ctr) {
     validate_device(ctx, X, n, d, metric, stream, ctr);
+    if (row_end == row_begin) return;
     const float* Xs = X;
     if (metric == KNN_B200_METRIC_HELLINGER) {
         float* staged = static_cast<float*>(ctx->staged.get(size_t(n) * d * sizeof(float)));
@@ -407,12 +426,20 @@ void solve_rows_core_f64(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t
         Xs = staged;
     }
     const int fold = metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean;
+    const uint32_t klist = std::min(k, n - 1);
     ctr.arith_used = KNN_B200_ARITH_EXACT;
     ctr.distance_evals += uint64_t(row_end - row_begin) * n;
     cuda_check(cudaEventRecord(ctx->ev[4], stream), "event");
-    cuda_check(knnb::launch_exact_f64(fold, Xs, n, d, std::min(k, n - 1), row_begin, row_end, out_index, out_dist,
-                                      metric == KNN_B200_METRIC_EUCLIDEAN, stream),
-               "exact f64 sweep launch");
+    if (klist > knnb::kExactMaxK) {
+        void* ws = ctx->exact_ws.get(knnb::exact_bigk_workspace_bytes(row_end - row_begin, n, 1));
+        cuda_check(knnb::launch_exact_bigk(fold, 1, Xs, n, d, klist, row_begin, row_end, out_index, out_dist,
+                                           metric == KNN_B200_METRIC_EUCLIDEAN, ws, ctx->sm_count, stream),
+                   "exact f64 long-list launch");
+    } else {
+        cuda_check(knnb::launch_exact_f64(fold, Xs, n, d, klist, row_begin, row_end, out_index, out_dist,
+                                          metric == KNN_B200_METRIC_EUCLIDEAN, stream),
+                   "exact f64 sweep launch");
+    }
     cuda_check(cudaEventRecord(ctx->ev[5], stream), "event");
     ++ctr.launches;
 }
@@ -427,6 +454,16 @@ void fill_stats(knn_b200_stats* st, const Counters& ctr, uint64_t pairs, int nde
     st->kernel_launches = ctr.launches;
     st->arith_used = ctr.arith_used;
     st->n_devices = ndev;
+}
+
+// Order a call after the context's previous one (which may have left
+// kernels in flight on another stream) and mark its end on `s`.
+void begin_call(knn_b200_ctx* ctx, cudaStream_t s) {
+    if (ctx->busy_recorded) cuda_check(cudaStreamWaitEvent(s, ctx->busy, 0), "wait for the previous call");
+}
+void end_call(knn_b200_ctx* ctx, cudaStream_t s) {
+    cuda_check(cudaEventRecord(ctx->busy, s), "record call end");
+    ctx->busy_recorded = true;
 }
 
 float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
@@ -476,6 +513,7 @@ int knn_b200_create(int device, knn_b200_ctx** out_ctx) {
         cuda_check(cudaSetDevice(device), "cudaSetDevice");
         cuda_check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
         for (auto& e : ctx->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&ctx->busy, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaMallocHost(&ctx->host_flags, 16 * sizeof(unsigned long long)), "cudaMallocHost");
         *out_ctx = ctx;
     });
@@ -497,6 +535,7 @@ void knn_b200_destroy(knn_b200_ctx* ctx) {
     stage_free(ctx);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    if (ctx->busy) cudaEventDestroy(ctx->busy);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -517,6 +556,7 @@ int knn_b200_solve(knn_b200_ctx* ctx, const float* host_vectors, uint32_t n, uin
         auto* od = static_cast<float*>(ctx->out_dist.get(out_elems * sizeof(float)));
         Counters ctr;
         cudaStream_t s = ctx->stream;
+        begin_call(ctx, s);
         cuda_check(cudaEventRecord(ctx->ev[0], s), "event");
         host_copy(ctx, X, host_vectors, vec_bytes, true, s);
         cuda_check(cudaEventRecord(ctx->ev[1], s), "event");
@@ -526,6 +566,7 @@ int knn_b200_solve(knn_b200_ctx* ctx, const float* host_vectors, uint32_t n, uin
         const auto t_d2h = std::chrono::steady_clock::now();
         host_copy_segs(ctx, {{out_index, oi, out_elems * sizeof(uint32_t)}, {out_dist, od, out_elems * sizeof(float)}},
                        false, s);
+        end_call(ctx, s);
         cuda_check(cudaStreamSynchronize(s), "solve sync");
         if (stats) {
             fill_stats(stats, ctr, uint64_t(n) * (n - 1) / 2, 1);
@@ -554,6 +595,7 @@ int knn_b200_solve_f64(knn_b200_ctx* ctx, const float* host_vectors, uint32_t n,
         auto* od = static_cast<double*>(ctx->out_dist.get(out_elems * sizeof(double)));
         Counters ctr;
         cudaStream_t s = ctx->stream;
+        begin_call(ctx, s);
         cuda_check(cudaEventRecord(ctx->ev[0], s), "event");
         host_copy(ctx, X, host_vectors, vec_bytes, true, s);
         cuda_check(cudaEventRecord(ctx->ev[1], s), "event");
@@ -564,6 +606,7 @@ int knn_b200_solve_f64(knn_b200_ctx* ctx, const float* host_vectors, uint32_t n,
         host_copy_segs(ctx,
                        {{out_index, oi, out_elems * sizeof(uint32_t)}, {out_dist, od, out_elems * sizeof(double)}},
                        false, s);
+        end_call(ctx, s);
         cuda_check(cudaStreamSynchronize(s), "solve sync");
         if (stats) {
             fill_stats(stats, ctr, uint64_t(n) * (n - 1) / 2, 1);
@@ -600,9 +643,11 @@ int knn_b200_solve_rows_device(knn_b200_ctx* ctx, const float* dev_vectors, uint
         cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         Counters ctr;
+        begin_call(ctx, s);
         if (stats) cuda_check(cudaEventRecord(ctx->ev[1], s), "event");
         solve_rows_core(ctx, dev_vectors, n, d, k, metric, arith, row_begin, row_end, dev_out_index,
                         dev_out_dist, s, ctr);
+        end_call(ctx, s);
         if (stats) {
             cuda_check(cudaEventRecord(ctx->ev[2], s), "event");
             cuda_check(cudaStreamSynchronize(s), "solve sync");
@@ -667,6 +712,7 @@ int solve_multi_impl(const float* host_vectors, uint32_t n, uint32_t d, uint32_t
                 auto* oi = static_cast<uint32_t*>(ctx->out_index.get(std::max<size_t>(out_elems, 1) * 4));
                 auto* od = static_cast<DistT*>(ctx->out_dist.get(std::max<size_t>(out_elems, 1) * sizeof(DistT)));
                 cudaStream_t s = ctx->stream;
+                begin_call(ctx, s);
                 cuda_check(cudaEventRecord(ctx->ev[0], s), "event");
                 // the lanes share the host: each stages with its share of the threads
                 const int st_threads = std::max(1, kStageThreadsDefault / int(use));
@@ -685,6 +731,7 @@ int solve_multi_impl(const float* host_vectors, uint32_t n, uint32_t d, uint32_t
                                     {out_dist + size_t(r0) * klist, od, out_elems * sizeof(DistT)}},
                                    false, s, st_threads);
                 }
+                end_call(ctx, s);
                 cuda_check(cudaStreamSynchronize(s), "solve sync");
                 hms[g] = elapsed_ms(ctx->ev[0], ctx->ev[1]);
                 kms[g] = elapsed_ms(ctx->ev[1], ctx->ev[2]);

@@ -30,7 +30,16 @@ cudaError_t launch_exact_fused(int metric, const float* X, uint32_t n, uint32_t 
                                uint32_t scatter_base, void* scratch, int sm_count, cudaStream_t stream);
 size_t exact_scratch_bytes(uint32_t nslots, uint32_t n, uint32_t klist, int sm_count);
 
-constexpr uint32_t kExactMaxK = 256;
+constexpr uint32_t kExactMaxK = 256;  // longest list the fused EXACT kernels keep on chip
+
+// EXACT lists longer than kExactMaxK (exact_bigk.cu): batches of query rows,
+// every distance as a key, a stable segmented radix sort per row, the first
+// klist kept.  f64: the KNN_DOUBLE_ACCUM fold and double distances.
+cudaError_t launch_exact_bigk(int metric, int f64, const float* X, uint32_t n, uint32_t d, uint32_t klist,
+                              uint32_t row_begin, uint32_t row_end, uint32_t* out_index, void* out_dist,
+                              int out_sqrt, void* ws, int sm_count, cudaStream_t stream);
+size_t exact_bigk_workspace_bytes(uint32_t rows, uint32_t n, int f64);
+uint32_t exact_bigk_batch_rows(uint32_t rows, uint32_t n);
 
 // EXACT sweep with double accumulation (the reference's KNN_DOUBLE_ACCUM
 // build, exact_f64.cu); output rows row_begin..row_end-1 in slot order.

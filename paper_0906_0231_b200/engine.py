@@ -398,6 +398,12 @@ def solve_rows_torch(ctx: Context, x, k: int, metric: CumulativeDistance, row_be
         dist = torch.empty((rows, klist), dtype=torch.float32, device=x.device)
     else:
         idx, dist = out
+        for t, dt in ((idx, torch.int32), (dist, torch.float32)):
+            if (t.shape != (rows, klist) or t.dtype != dt or not t.is_contiguous() or t.device != x.device):
+                raise ConfigError(f"out must be contiguous (int32, float32) tensors of shape ({rows}, {klist}) "
+                                  f"on {x.device}")
+    if not (0 <= row_begin <= row_end <= n):
+        raise ConfigError(f"row range [{row_begin}, {row_end}) outside [0, {n})")
     stream = torch.cuda.current_stream(x.device).cuda_stream
     st = ctx.solve_rows_device(x.data_ptr(), n, d, k, metric, row_begin, row_end, idx.data_ptr(),
                                dist.data_ptr(), stream, arith, want_stats)

@@ -23,6 +23,7 @@
 
 #include "knn/engine.hpp"
 #include "knn/errors.hpp"
+#include "knn/rng.hpp"
 #include "knn_b200.h"
 
 namespace knn {
@@ -34,6 +35,60 @@ static_assert(std::is_same_v<dist_t, float> || std::is_same_v<dist_t, double>);
 
 namespace {
 
+// Host restatements of the device folds a custom functor may turn out to be
+// (common.cuh fold_step / fold_finalize; exact_f64.cu for dist_t = double).
+// This TU is compiled with -ffp-contract=off, so each is separately rounded
+// exactly like the device code.
+dist_t device_fold_sqeuclidean(const float* u, const float* v, std::uint32_t d) {
+    dist_t acc = 0;
+    for (std::uint32_t j = 0; j < d; ++j) {
+        const float t = u[j] - v[j];
+        acc = acc + dist_t(t) * dist_t(t);
+    }
+    return acc;
+}
+
+dist_t device_fold_cosine(const float* u, const float* v, std::uint32_t d) {
+    dist_t acc = 0;
+    for (std::uint32_t j = 0; j < d; ++j) acc = acc + dist_t(u[j]) * dist_t(v[j]);
+    return dist_t(1) - acc;
+}
+
+// A custom functor is a host function pointer (distance.hpp:68-77); the GPU
+// cannot call it.  It runs on the GPU only if it IS one of the device folds,
+// bit for bit: the functor is probed on random vectors -- as the reference's
+// registry probes symmetry (distance.cpp:117-136) -- and compared with each
+// restatement above.  Anything else is rejected with ConfigError (no CPU
+// fallback).  The name is not trusted: a "cosine" with another initial value,
+// sign convention or float-rounded product in the double build is rejected.
+bool functor_matches(const CumulativeDistance& f, dist_t (*fold)(const float*, const float*, std::uint32_t)) {
+    if (!f.step) return false;
+    const metrics::Erased m{f.initial, f.step, f.finalize};
+    SplitMix64 rng(0x6b2f7a11d3c05e93ull);
+    constexpr std::uint32_t kMaxDim = 67;
+    float u[kMaxDim], v[kMaxDim];
+    for (std::uint32_t trial = 0; trial < 96; ++trial) {
+        const std::uint32_t d = 1 + trial % kMaxDim;
+        // value ranges: [0,1), signed, and wide magnitudes (rounding-sensitive)
+        for (std::uint32_t j = 0; j < d; ++j) {
+            float a = rng.next_unit_float(), b = rng.next_unit_float();
+            if (trial % 3 == 1) {
+                a = 2.0f * a - 1.0f;
+                b = 2.0f * b - 1.0f;
+            } else if (trial % 3 == 2) {
+                a = (2.0f * a - 1.0f) * float(1u << (j % 17));
+                b = (2.0f * b - 1.0f) * float(1u << ((j * 7) % 17));
+            }
+            u[j] = a;
+            v[j] = b;
+        }
+        const dist_t want = fold(u, v, d);
+        const dist_t got = fold_distance(m, u, v, d);
+        if (std::memcmp(&want, &got, sizeof(dist_t)) != 0) return false;
+    }
+    return true;
+}
+
 int gpu_metric(const CumulativeDistance& f) {
     switch (f.kind) {
     case MetricKind::hellinger:
@@ -41,11 +96,13 @@ int gpu_metric(const CumulativeDistance& f) {
     case MetricKind::sqeuclidean:
         return KNN_B200_METRIC_SQEUCLIDEAN;
     case MetricKind::custom:
-        if (f.name == "cosine") return KNN_B200_METRIC_COSINE;
+        if (functor_matches(f, device_fold_sqeuclidean)) return KNN_B200_METRIC_SQEUCLIDEAN;
+        if (functor_matches(f, device_fold_cosine)) return KNN_B200_METRIC_COSINE;
         break;
     }
     throw ConfigError("distance functor '" + f.name +
-                      "' is a host function pointer and cannot run on the GPU engine");
+                      "' is a host function pointer that matches none of the GPU engine's folds "
+                      "(sqeuclidean, cosine = 1 - sum u*v); it cannot run on the GPU engine");
 }
 
 int arith_from_env() {

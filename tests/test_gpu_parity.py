@@ -348,3 +348,60 @@ def test_solve_into_caller_owned_pinned_outputs(ctx, c_oracle):
     assert np.array_equal(i0, i1) and np.array_equal(d0.view(np.uint32), d1.view(np.uint32))
     with pytest.raises(ConfigError):
         ctx.solve(x, 10, m, arith_id("tensor"), out=(out[0][:, :5], out[1]))
+
+
+@pytest.mark.parametrize("n,d,k,m", [(5000, 40, 1000, "sqeuclidean"), (1300, 17, 5000, "hellinger"),
+                                     (3000, 64, 300, "cosine"), (2500, 33, 257, "euclidean")])
+def test_long_lists_beyond_256(ctx, c_oracle, n, d, k, m):
+    """min(k, n-1) > 256: the reference keeps any k (heap.cpp:66-70); here the
+    sort-based EXACT path (exact_bigk.cu) -- same bits as brute_force_knn."""
+    from oracle import normalize_rows
+    x = c_oracle.generate(n, d, n + k)
+    if m == "cosine":
+        x = normalize_rows(x)
+    om = "sqeuclidean" if m == "euclidean" else m
+    ri, rd, _ = c_oracle.brute_force(x, k, om)
+    if m == "euclidean":
+        rd = np.sqrt(rd)
+    for arith in ("auto", "tensor"):
+        idx, dist, st = ctx.solve(x, k, metric_obj(m), arith_id(arith))
+        assert_lists_bit_equal(idx, dist, ri, rd, f"long lists n={n} k={k} {m} [{arith}]")
+        assert st["arith_used"] == 1
+
+
+def test_long_lists_heavy_ties_and_f64(ctx, c_oracle):
+    """Tie-heavy data (16 distinct points) with k = 400: ties break by index;
+    and the KNN_DOUBLE_ACCUM build's long lists (double keys, stable sort)."""
+    x = np.floor(c_oracle.generate(2000, 2, 12) * 4).astype(np.float32)
+    ri, rd, _ = c_oracle.brute_force(x, 400, "sqeuclidean")
+    idx, dist, _ = ctx.solve(x, 400, metric_obj("sqeuclidean"))
+    assert_lists_bit_equal(idx, dist, ri, rd, "long lists, heavy ties")
+    for xx, k, m in ((x, 400, "sqeuclidean"), (c_oracle.generate(1500, 30, 5), 600, "hellinger")):
+        ri, rd = c_oracle.brute_force_f64(xx, k, m)
+        idx, dist, _ = ctx.solve_f64(xx, k, metric_obj(m))
+        assert np.array_equal(idx, ri), f"f64 long lists {m}: indices"
+        assert np.array_equal(dist.view(np.uint64), rd.view(np.uint64)), f"f64 long lists {m}: distance bits"
+
+
+def test_device_api_empty_shard_and_stream_switch(ctx, c_oracle):
+    """An empty row range is a valid (empty) shard; consecutive calls on
+    different streams reuse the workspace safely (the context orders each
+    call after the previous one)."""
+    import torch
+    from paper_0906_0231_b200 import ConfigError, solve_rows_torch, squared_euclidean
+    x = c_oracle.generate(6000, 24, 3)
+    ri, rd, _ = c_oracle.brute_force(x, 8, "sqeuclidean")
+    xt = torch.from_numpy(x).cuda()
+    i0, d0, _ = solve_rows_torch(ctx, xt, 8, squared_euclidean(), 300, 300)
+    assert i0.shape == (0, 8)
+    outs = []
+    for rep in range(3):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            outs.append(solve_rows_torch(ctx, xt, 8, squared_euclidean(), 0, 6000, arith_id("tensor")))
+    torch.cuda.synchronize()
+    for i, dd, _ in outs:
+        assert_lists_bit_equal(i.cpu().numpy().view(np.uint32), dd.cpu().numpy(), ri, rd, "stream switch")
+    bad = torch.empty((10, 8), dtype=torch.int32, device="cuda")
+    with pytest.raises(ConfigError):
+        solve_rows_torch(ctx, xt, 8, squared_euclidean(), 0, 6000, out=(bad, bad.float()))

@@ -39,6 +39,19 @@ def test_generate_is_row_major_stream(c_oracle):
     assert not np.array_equal(c_oracle.generate(50, 9, 2024), c_oracle.generate(50, 9, 2025))
 
 
+def test_generate_at_jumps_the_same_stream(c_oracle):
+    """generate_at (the Weyl jump the large-offset generator checks use)
+    reproduces slices of the sequential stream: start, middle, end of a
+    20M-element stream, and the reference's own stream when it was built."""
+    full = c_oracle.generate(20_000, 1000, 4).reshape(-1)
+    for first, count in ((0, 1000), (123_457, 5000), (19_999_000, 1000), (7, 1)):
+        assert np.array_equal(c_oracle.generate_at(4, first, count), full[first:first + count])
+    import oracle
+    ref = oracle.reference()
+    if ref is not None:
+        assert np.array_equal(ref.generate(300, 7, 99).reshape(-1), c_oracle.generate_at(99, 0, 2100))
+
+
 def test_distance_kats(c_oracle):
     # test_distance.cpp / SPEC examples
     f = c_oracle.fold
