@@ -38,7 +38,7 @@ build/obj/%.o: $(CSRC)/%.cu $(wildcard $(CSRC)/*.cuh) $(CSRC)/kernels.h include/
 
 $(LIB): $(CU_OBJS)
 	@mkdir -p $(PKG)/lib
-	$(NVCC) $(ARCH) -shared -o $@ $^ -Xlinker --exclude-libs,ALL -lpthread
+	$(NVCC) $(ARCH) -shared -o $@ $^ -Xlinker --exclude-libs,ALL -lnccl -lpthread
 
 oracle:
 	$(MAKE) -C oracle REF=$(REF)
@@ -61,7 +61,7 @@ REF_LINK := $(ENGINE_A) oracle/_ref/libtknn_ref_noengine.a -L$(PKG)/lib -lknn_b2
 REF_LINK_F64 := $(ENGINE_F64_A) oracle/_ref/f64/libtknn_ref_noengine.a -L$(PKG)/lib -lknn_b200 \
             -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib' -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib' -lpthread
 
-ref-bins: oracle/_ref/acceptance_b200 build/test_engine_b200 build/tknn_b200 oracle/_ref/tknn_ref \
+ref-bins: oracle/_ref/acceptance_b200 build/test_engine_b200 build/tknn_b200 oracle/_ref/tknn_ref build/bench_dropin \
           oracle/_ref/acceptance_b200_f64 build/test_engine_b200_f64 build/tknn_b200_f64 oracle/_ref/f64/tknn_ref
 
 # The reference CLI in its KNN_DOUBLE_ACCUM build: on the double drop-in, and
@@ -89,6 +89,10 @@ oracle/_ref/tknn_ref: $(REF)/tools/main.cpp tools/cli11_shim/CLI11.hpp oracle
 	$(CXX) $(REF_FLAGS) -Itools/cli11_shim -I$(REF)/include -o $@ $< oracle/_ref/libtknn_ref.a -lpthread
 
 oracle/_ref/acceptance_b200: $(REF)/tests/acceptance.cpp $(ENGINE_A) $(LIB) oracle
+	$(CXX) $(REF_FLAGS) -I$(REF)/include -o $@ $< $(REF_LINK)
+
+# The C++ drop-in timed end to end (bench.py's e2e.dropin_ms_per_step).
+build/bench_dropin: tools/bench_dropin.cpp $(ENGINE_A) $(LIB) oracle
 	$(CXX) $(REF_FLAGS) -I$(REF)/include -o $@ $< $(REF_LINK)
 
 build/test_engine_b200: tests/cpp/test_engine_b200.cpp $(ENGINE_A) $(LIB) oracle

@@ -14,8 +14,11 @@ pair_evaluations, engine.hpp:28), so
 Inputs are SplitMix64 generate_dataset(n, d, seed) (src/io.cpp:57-62), made on
 the device by knn_b200_generate_device (bit-identical to the host stream).
 Multi-GPU (torchrun, one rank per GPU): rank 0 generates, the reference set is
-replicated by an NCCL broadcast, each rank solves a contiguous query-row
-shard (weak in pairs per GPU only approximately; n is fixed, so "strong").
+replicated by an NCCL broadcast over the engine's own communicator, and the
+ranks solve the whole problem together -- the sharded triangle computes each
+unordered pair once across the ranks and exchanges column-side candidates
+(NCCL all-to-all); each rank ends with a contiguous shard of rows.  n is
+fixed as N grows: "strong" scaling.
 
 `value` is device-resident (inputs already in HBM); `e2e` is the same metric
 through the public API with the host copy of the inputs (rank 0, pinned) and
@@ -124,11 +127,28 @@ def dist_env():
 # --------------------------------------------------------------------------
 # CPU reference arm / cpu_baseline (the ONLY places bench.py runs oracle/)
 
-def cpu_reference_sample(cfg, budget_s: float):
+# The CPU sample: a prefix of n' rows of the same stream (SURVEY §8(d) CPU
+# baseline (ii): n' in {32768, 65536}).  One fixed size per config, used by
+# BOTH the cpu_baseline leg and the --impl reference arm, so the two report
+# the same measurement.
+CPU_SAMPLE_N = {"c1": 16384, "c2": 65536, "c3": 32768, "c4": 65536, "c5": 65536}
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_reference_sample(cfg, nn: int):
     """Time the reference's own solve_knn (oracle/_ref, unmodified library,
-    all host cores as lanes) on a bounded prefix of the workload, or the C
+    all host cores as lanes) once on the prefix of nn rows, or the C
     restatement when the reference was not compiled.  Returns
-    (pairs_per_s, seconds, cores, kind, sample_desc)."""
+    (pairs_per_s, seconds, cores, kind, sample_desc, nn)."""
     import numpy as np
 
     import oracle
@@ -154,15 +174,11 @@ def cpu_reference_sample(cfg, budget_s: float):
         # rows_topk evaluates every ordered pair: report unordered-pair rate
         return 2 * (time.perf_counter() - t0), "port", f"C restatement rows_topk, {cores} threads (x2: no symmetry)"
 
-    nn = 2048
+    nn = min(nn, cfg["n"])
     t, kind, desc = run(nn)
-    # pairs scale as nn^2: grow to about budget_s
-    while t < budget_s / 4 and nn < cfg["n"]:
-        nn = min(cfg["n"], int(nn * min(4.0, math.sqrt(budget_s / max(t, 1e-3)))) // 64 * 64)
-        t, kind, desc = run(nn)
     pairs = nn * (nn - 1) / 2
     sample = (f"prefix n'={nn} of {cfg['label']} (same seed/metric), {desc}; "
-              f"pairs/s = n'(n'-1)/2 / time")
+              f"pairs/s = n'(n'-1)/2 / time; host {cpu_model()}, nproc {cores}")
     return pairs / t, t, cores, kind, sample, nn
 
 
@@ -170,12 +186,12 @@ def run_reference_arm(args, cfg):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    budget = max(5.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
-    # calibrate the sample size once, then time W + K steps of that size
-    rate, t, cores, kind, sample, nn = cpu_reference_sample(cfg, budget)
     import numpy as np
 
     import oracle
+    cores = os.cpu_count() or 1
+    nn = min(CPU_SAMPLE_N.get(args.config, 65536), cfg["n"])
+    kind = "reference" if oracle.reference() is not None else "port"
     ref = oracle.reference()
     co = oracle.c_oracle()
     metric = {"euclidean": "sqeuclidean"}.get(cfg["metric"], cfg["metric"])
@@ -197,6 +213,10 @@ def run_reference_arm(args, cfg):
     pairs = nn * (nn - 1) / 2
     total = sum(times)
     value = pairs * len(times) / total
+    desc = (f"reference solve_knn, {cores} lanes, gsize {64 * max(1, math.ceil(nn / (2 * cores * 64)))}"
+            if ref is not None else f"C restatement rows_topk, {cores} threads (x2: no symmetry)")
+    sample = (f"prefix n'={nn} of {cfg['label']} (same seed/metric), {desc}; pairs/s = n'(n'-1)/2 / time; "
+              f"host {cpu_model()}, nproc {cores}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
@@ -223,7 +243,7 @@ def main():
     ap.add_argument("--arith", default="auto", choices=["auto", "exact", "tensor"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-sample-n", type=int, default=None, help="CPU sample rows (default CPU_SAMPLE_N)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.n:
@@ -235,7 +255,8 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_0906_0231_b200 import Context, _lib, distance_by_name, generate_torch, solve_rows_torch
+    from paper_0906_0231_b200 import (Context, _lib, comm_broadcast_torch, comm_init, comm_unique_id,
+                                      distance_by_name, generate_torch, shard_rows, solve_sharded_torch)
 
     rank, world, local = dist_env()
     launched = "RANK" in os.environ and "MASTER_ADDR" in os.environ  # torchrun (any world size)
@@ -248,8 +269,14 @@ def main():
     metric = distance_by_name(cfg["metric"])
     arith = _lib.ARITH_NAMES[args.arith]
     klist = min(k, n - 1)
-    r0, r1 = n * rank // world, n * (rank + 1) // world
+    r0, r1 = shard_rows(n, rank, world)
     stream = torch.cuda.current_stream(dev)
+    if launched:
+        # the engine's own NCCL communicator (one rank per GPU): rank 0 makes
+        # the id, torch.distributed ships it
+        box = [comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        comm_init(ctx, box[0], rank, world)
 
     # ---- inputs: generated on rank 0's device, replicated by NCCL broadcast
     x = generate_torch(ctx, n, d, cfg["seed"], dev) if rank == 0 else torch.empty((n, d), dtype=torch.float32,
@@ -259,20 +286,20 @@ def main():
         x = (xd / xd.norm(dim=1, keepdim=True).clamp_min(1e-300)).float().contiguous()
         del xd
     if launched:
-        dist.broadcast(x, src=0)  # NCCL broadcast of the reference set
+        comm_broadcast_torch(ctx, x, 0)  # NCCL broadcast of the reference set
     torch.cuda.synchronize()
-    out_idx = torch.empty((r1 - r0, klist), dtype=torch.int32, device=dev)
-    out_dist = torch.empty((r1 - r0, klist), dtype=torch.float32, device=dev)
 
     def barrier():
         if launched:
             dist.barrier(device_ids=[dev.index])
         torch.cuda.synchronize()
 
-    def device_step(want_stats=True):
-        _, _, st = solve_rows_torch(ctx, x, k, metric, r0, r1, arith, out=(out_idx, out_dist),
-                                    want_stats=want_stats)
-        return st
+    def device_step(xx=None, want_stats=True):
+        # one whole solve across the ranks: each rank gets its row shard
+        # (the sharded triangle where eligible)
+        i, dd, st = solve_sharded_torch(ctx, x if xx is None else xx, k, metric, arith, rank, world,
+                                        want_stats=want_stats)
+        return i, dd, st
 
     # ---- warm-up (W >= 3 full steps)
     for _ in range(max(args.warmup, 0)):
@@ -289,7 +316,7 @@ def main():
     launches = 0
     sweep_ms, stats = [], []
     for _ in range(args.steps):
-        st = device_step()
+        _, _, st = device_step()
         launches += st["kernel_launches"]
         sweep_ms.append(st["sweep_ms"])
         stats.append(st)
@@ -338,6 +365,18 @@ def main():
             ctx.solve(x_pin.numpy(), k, metric, arith, out=pin_out)
         e2e_pinned_ms = (time.perf_counter() - t_pin) * 1e3 / args.steps
         del x_pin, idx_pin, dist_pin, pin_out
+        # The C++ drop-in itself (knn::solve_knn from the reference's header,
+        # engine_b200.cpp): pageable Dataset in, EngineResult.lists (one
+        # std::vector per row) out -- what a reference user's call costs.
+        dropin = ROOT / "build" / "bench_dropin"
+        dropin_ms = None
+        if dropin.exists() and not args.n:
+            try:
+                out = subprocess.run([str(dropin), str(n), str(d), str(k), str(cfg["seed"]), str(args.steps), "1"],
+                                     capture_output=True, text=True, timeout=600, check=True).stdout
+                dropin_ms = json.loads(out.strip().splitlines()[-1])["ms_per_step"]
+            except Exception as e:  # reported, never substituted
+                dropin_ms = f"unavailable: {e}"
     if launched:
         x_host = torch.empty((n, d), dtype=torch.float32, pin_memory=True) if rank == 0 else None
         if rank == 0:
@@ -352,8 +391,8 @@ def main():
         for _ in range(args.steps):
             if rank == 0:
                 x_e2e.copy_(x_host, non_blocking=True)
-            dist.broadcast(x_e2e, src=0)
-            solve_rows_torch(ctx, x_e2e, k, metric, r0, r1, arith, out=(out_idx, out_dist))
+            comm_broadcast_torch(ctx, x_e2e, 0)
+            out_idx, out_dist, _ = device_step(x_e2e, want_stats=False)
             idx_host.copy_(out_idx, non_blocking=True)
             dist_host.copy_(out_dist, non_blocking=True)
         e1.record(stream)
@@ -361,17 +400,17 @@ def main():
         t2 = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
         e2e_ms = float(t2.item())
-        e2e_path = "pinned host input, H2D on rank 0, NCCL broadcast, shard solve, D2H; CUDA events, max over ranks"
+        e2e_path = ("pinned host input, H2D on rank 0, NCCL broadcast, sharded solve, D2H of each rank's rows; "
+                    "CUDA events, max over ranks")
     e2e_value = pairs * args.steps / (e2e_ms / 1e3)
 
     # ---- roofline of the dominant kernel (the fused distance + top-k sweep)
     peaks = load_peaks()
     last = stats[-1]
     tensor = last["arith_used"] == _lib.ARITH_TENSOR
-    rows = r1 - r0
     # algorithmic work per launch: 2*d flop per unordered pair;
-    # a shard of `rows` query rows covers rows*(n-1) ordered = half as many pairs
-    alg_flop = rows * (n - 1) / 2 * 2 * d
+    # each of the world ranks covers (about) 1/world of the n(n-1)/2 pairs
+    alg_flop = n * (n - 1) / 2 / world * 2 * d
     sweep_avg_s = statistics.mean(sweep_ms) / 1e3
     achieved = alg_flop / sweep_avg_s / 1e12
     if tensor:
@@ -401,13 +440,18 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f32" if not tensor else "f16->f32 filter, f32 exact rescore",
         "data": "synthetic (SplitMix64 generate_dataset on device)",
         "config": {"workload": cfg["label"], "n": n, "d": d, "k": k, "metric": cfg["metric"],
-                   "seed": cfg["seed"], "arith": args.arith, "parallelism": f"query-row shards x{world}",
+                   "seed": cfg["seed"], "arith": args.arith,
+                   "parallelism": f"sharded triangle x{world} (each pair once across ranks; NCCL all-to-all of "
+                                  f"column-side candidates)" if world > 1 else "one GPU, triangle sweep",
                    "l2": f"inputs {n * d * 4 / 1e9:.2f} GB > 126 MB L2 (no flush needed)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms / args.steps,
                 "h2d_bytes_per_step": n * d * 4 if rank == 0 else 0,
                 "d2h_bytes_per_step": n * klist * 8 if not launched else (r1 - r0) * klist * 8,
                 "path": e2e_path,
-                "pinned_ms_per_step": e2e_pinned_ms},
+                "pinned_ms_per_step": e2e_pinned_ms,
+                "dropin_ms_per_step": dropin_ms if not launched else None,
+                "dropin_path": "build/bench_dropin: C++ knn::solve_knn (reference header, B200 drop-in), "
+                               "pageable Dataset in, EngineResult.lists out, sqeuclidean fold, host clock"},
         "gpu_launches": launches,
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes/launch (DRAM, ncu)",
@@ -422,9 +466,10 @@ def main():
     }
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
-            rate, t_cpu, cores, kind, sample, _ = cpu_reference_sample(cfg, args.cpu_budget)
+            nn = args.cpu_sample_n or CPU_SAMPLE_N.get(args.config, 65536)
+            rate, t_cpu, cores, kind, sample, _ = cpu_reference_sample(cfg, nn)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
-                                    "seconds": t_cpu}
+                                    "seconds": t_cpu, "cpu_model": cpu_model()}
         except Exception as e:  # reported, never substituted
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "error": str(e)}
     if rank == 0:

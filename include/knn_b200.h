@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define KNN_B200_ABI_VERSION 1
+#define KNN_B200_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define KNN_B200_API __attribute__((visibility("default")))
@@ -160,9 +160,11 @@ KNN_B200_API int knn_b200_generate_device(knn_b200_ctx *ctx, float *dev_out, uin
                                           uint64_t seed, void *stream /* NULL = legacy default */);
 
 /* Single-process multi-GPU solve (the reference's n_lanes, engine.cpp:37-56):
- * uses min(n_gpus, device count) devices, one host thread each; query rows are
- * split into contiguous shards, every device holds the full reference set and
- * writes its shard straight into the host outputs.  No merge is needed. */
+ * uses min(n_gpus, device count) devices, one host thread each.  The host
+ * buffer goes to device 0 once and is replicated by an NCCL broadcast
+ * (ncclCommInitAll communicator); each device then runs its rank of the
+ * sharded solve (knn_b200_solve_sharded_device) and writes its contiguous
+ * row shard straight into the host outputs. */
 KNN_B200_API int knn_b200_solve_multi(const float *host_vectors, uint32_t n, uint32_t d, uint32_t k,
                          int metric, int arith, uint32_t n_gpus, uint32_t *out_index,
                          float *out_dist, knn_b200_stats *stats);
@@ -173,6 +175,61 @@ KNN_B200_API int knn_b200_solve_multi(const float *host_vectors, uint32_t n, uin
 KNN_B200_API int knn_b200_solve_multi_f64(const float *host_vectors, uint32_t n, uint32_t d, uint32_t k,
                                           int metric, uint32_t n_gpus, uint32_t *out_index, double *out_dist,
                                           knn_b200_stats *stats);
+
+/* ---- Multi-GPU: the sharded triangle -------
+ *
+ * The reference's lanes (engine.cpp:27-59; schedule.cpp:40-75 boustrophedon
+ * lane_of_row; merge.cpp:10-78 merge_all) as GPUs: every unordered pair is
+ * computed once across all ranks, each rank keeps row-side lists for its own
+ * rows, sends column-side candidates to the rows' owners (NCCL all-to-all)
+ * and merges them; results end in contiguous row shards.  One rank per GPU,
+ * in one process (knn_b200_solve_multi) or one process per GPU (these calls
+ * under torchrun / MPI). */
+
+/* Host-only (no device needed): the sharded triangle's ownership of the
+ * `units` 256-row units of the second column order.  Unit u goes to rank
+ * lane_of_row(u) (schedule.cpp:40-44, boustrophedon over `world` ranks); a
+ * rank's units, ascending, are dealt to its min(count, pairs_max) CTA pairs in
+ * snake order.  out_units (units entries) lists rank 0's units in launch
+ * order, then rank 1's, ...; out_counts (world entries) their counts. */
+KNN_B200_API int knn_b200_tri_unit_plan(uint32_t units, uint32_t world, uint32_t pairs_max, uint32_t *out_units,
+                                        uint32_t *out_counts);
+
+/* 128 opaque bytes (an ncclUniqueId) for knn_b200_comm_init; rank 0 creates
+ * it and ships it to the other ranks out of band. */
+KNN_B200_API int knn_b200_comm_unique_id(void *out_id /* 128 bytes */);
+
+/* Bind an NCCL communicator of `world` ranks to ctx (its device).  Collective:
+ * every rank calls it with the same id. */
+KNN_B200_API int knn_b200_comm_init(knn_b200_ctx *ctx, const void *id, int rank, int world);
+
+/* In-place broadcast of `bytes` device bytes from rank `root` (the reference
+ * set's one replication, north_star (3)). */
+KNN_B200_API int knn_b200_comm_broadcast(knn_b200_ctx *ctx, void *dev_buf, uint64_t bytes, int root,
+                                         void *stream);
+
+/* Collective sharded solve.  dev_vectors: the full n x d set on every rank.
+ * Rank r receives rows [R r, min(R (r + 1), n)), R = ceil(n / world), of the
+ * result in dev_out_index / dev_out_dist ((rows) x min(k, n-1), device).
+ * Without a communicator this is the whole problem (rows [0, n)). */
+KNN_B200_API int knn_b200_solve_sharded_device(knn_b200_ctx *ctx, const float *dev_vectors, uint32_t n,
+                                               uint32_t d, uint32_t k, int metric, int arith,
+                                               uint32_t *dev_out_index, float *dev_out_dist, void *stream,
+                                               knn_b200_stats *stats);
+
+/* Test hook: the sharded triangle's `world` rank programs run one after
+ * another on ctx's device, exchanges as device copies (no NCCL); all n rows
+ * land in dev_out_index / dev_out_dist (n x min(k, n-1)).  Only for problems
+ * that take the triangle (else ConfigError).  rank_ms (optional, world x 4):
+ * per rank [replicated prep, sample slice, sweep + binning, merge + rescore]
+ * in ms; rank_xbytes (optional, world): bytes each rank sends in the
+ * column-side exchange.  stats->reserved = 1 when the logs overflowed and
+ * the solve fell back to the rectangular sweep. */
+KNN_B200_API int knn_b200_debug_solve_sharded_loopback(knn_b200_ctx *ctx, const float *dev_vectors, uint32_t n,
+                                                       uint32_t d, uint32_t k, int metric, int world,
+                                                       uint32_t *dev_out_index, float *dev_out_dist, void *stream,
+                                                       knn_b200_stats *stats, float *rank_ms,
+                                                       uint64_t *rank_xbytes);
 
 #ifdef __cplusplus
 }

@@ -30,7 +30,13 @@ from .engine import (  # noqa: F401
     hellinger,
     make_plan,
     solve_knn,
+    comm_broadcast_torch,
+    comm_init,
+    comm_unique_id,
+    shard_rows,
     solve_rows_torch,
+    solve_sharded_loopback_torch,
+    solve_sharded_torch,
     squared_euclidean,
 )
 

@@ -25,12 +25,18 @@ EXPORTS = (
     "knn_b200_solve",
     "knn_b200_solve_f64",
     "knn_b200_solve_multi_f64",
+    "knn_b200_tri_unit_plan",
+    "knn_b200_comm_unique_id",
+    "knn_b200_comm_init",
+    "knn_b200_comm_broadcast",
+    "knn_b200_solve_sharded_device",
+    "knn_b200_debug_solve_sharded_loopback",
     "knn_b200_solve_rows_device",
     "knn_b200_solve_multi",
     "knn_b200_generate_device",
 )
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 OK, ERR_CONFIG, ERR_VALIDATION, ERR_INTERNAL = 0, 2, 3, 4
 METRIC_HELLINGER, METRIC_SQEUCLIDEAN, METRIC_COSINE, METRIC_EUCLIDEAN = 0, 1, 2, 3
@@ -104,6 +110,19 @@ def load() -> ctypes.CDLL:
             ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)]
         lib.knn_b200_generate_device.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
                                                  ctypes.c_uint64, ctypes.c_void_p]
+        lib.knn_b200_tri_unit_plan.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
+                                               ctypes.c_void_p]
+        lib.knn_b200_comm_unique_id.argtypes = [ctypes.c_void_p]
+        lib.knn_b200_comm_init.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+        lib.knn_b200_comm_broadcast.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int,
+                                                ctypes.c_void_p]
+        lib.knn_b200_solve_sharded_device.argtypes = [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int,
+            ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)]
+        lib.knn_b200_debug_solve_sharded_loopback.argtypes = [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int,
+            ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats),
+            ctypes.c_void_p, ctypes.c_void_p]
         if lib.knn_b200_abi_version() != ABI_VERSION:
             raise RuntimeError(f"{LIB_PATH}: ABI version {lib.knn_b200_abi_version()} != {ABI_VERSION}")
         _lib = lib

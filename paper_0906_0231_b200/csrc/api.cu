@@ -6,10 +6,12 @@
 // merge_all (engine.cpp:27-59) has no counterpart: each query row is owned by
 // exactly one CTA, so its list is final when the sweep ends.
 #include <cuda_runtime.h>
+#include <nccl.h>
 #include <stdint.h>
 
 #include <algorithm>
 #include <chrono>
+#include <map>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -111,6 +113,13 @@ struct knn_b200_ctx {
     // workspace while the previous call's kernels are still in flight.
     cudaEvent_t busy = nullptr;
     bool busy_recorded = false;
+    // sharded triangle (tri_shard.cuh): grow-only buffers by slot, the full
+    // padded result arrays before the reduce-scatter, and the communicator
+    std::map<int, DevBuf> shard_ws;
+    DevBuf full_index, full_dist, shard_index, shard_dist;
+    ncclComm_t comm = nullptr;
+    int comm_rank = 0, comm_world = 1;
+    bool comm_owned = false;
     unsigned long long* host_flags = nullptr;  // pinned
     StageLane stage[kStageThreads];
     cudaEvent_t stage_go = nullptr;
@@ -444,6 +453,131 @@ void solve_rows_core_f64(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t
     ++ctr.launches;
 }
 
+// ---- sharded triangle (tri_shard.cuh) ----------------------
+
+void* shard_alloc(void* c, int slot, size_t bytes) {
+    try {
+        return static_cast<knn_b200_ctx*>(c)->shard_ws[slot].get(bytes);
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+void* capture_alloc(void* c, size_t bytes) {
+    try {
+        return static_cast<knn_b200_ctx*>(c)->capture_ws.get(bytes);
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+// The TENSOR-path arguments of a whole-problem triangle solve whose results
+// land in full n-row arrays out_index / out_dist.
+knnb::TensorPathArgs tri_args(knn_b200_ctx* ctx, const float* Xs, uint32_t n, uint32_t d, uint32_t klist, int metric,
+                              uint32_t* out_index, float* out_dist, cudaStream_t stream) {
+    knnb::TensorPathArgs ta{};
+    ta.X = Xs;
+    ta.n = n;
+    ta.d = d;
+    ta.klist = klist;
+    ta.kp = knnb::tensor_kp_for(klist);
+    ta.row_begin = 0;
+    ta.row_end = n;
+    ta.fold = metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean;
+    ta.out_sqrt = metric == KNN_B200_METRIC_EUCLIDEAN;
+    ta.out_index = out_index;
+    ta.out_dist = out_dist;
+    ta.host_scratch = ctx->host_flags + 4;
+    ta.exact_scratch = ctx->exact_ws.get(std::max<size_t>(16, knnb::exact_scratch_bytes(n, n, klist, ctx->sm_count)));
+    ta.sm_count = ctx->sm_count;
+    ta.stream = stream;
+    ta.ev_sweep0 = ctx->ev[4];
+    ta.ev_sweep1 = ctx->ev[5];
+    ta.alloc2 = capture_alloc;
+    ta.alloc2_ctx = ctx;
+    return ta;
+}
+
+bool tri_selected(uint32_t n, uint32_t d, uint32_t klist, int metric, int arith) {
+    return arith != KNN_B200_ARITH_EXACT && klist <= knnb::kExactMaxK && knnb::tensor_kp_for(klist) != 0 &&
+           knnb::tri_eligible(n, d, klist, metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean);
+}
+
+// Rows of rank `rank` of `world`: [R rank, R (rank + 1)) clipped to n, R = ceil(n / world).
+void shard_rows(uint32_t n, int rank, int world, uint32_t& r0, uint32_t& r1) {
+    const uint32_t R = uint32_t((uint64_t(n) + world - 1) / world);
+    r0 = uint32_t(std::min<uint64_t>(uint64_t(R) * rank, n));
+    r1 = uint32_t(std::min<uint64_t>(uint64_t(r0) + R, n));
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) fail(KNN_B200_ERR_INTERNAL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+// One rank of a sharded solve on an NCCL communicator (world > 1): the whole
+// problem is solved across the ranks, this rank's contiguous shard of rows
+// (shard_rows) lands in out_index / out_dist (device).  Triangle-eligible
+// problems compute each unordered pair once across all ranks
+// (run_tri_nccl + a reduce-scatter of the rows); everything else -- and a
+// triangle whose column-side logs overflow -- solves its row shard directly
+// (rectangular sweep: each pair of the shard against all n).
+void solve_sharded_core(knn_b200_ctx* ctx, ncclComm_t comm, int rank, int world, const float* X, uint32_t n,
+                        uint32_t d, uint32_t k, int metric, int arith, uint32_t* out_index, float* out_dist,
+                        cudaStream_t stream, Counters& ctr) {
+    uint32_t r0, r1;
+    shard_rows(n, rank, world, r0, r1);
+    const uint32_t klist = std::min(k, n - 1);
+    if (!tri_selected(n, d, klist, metric, arith)) {
+        solve_rows_core(ctx, X, n, d, k, metric, arith, r0, r1, out_index, out_dist, stream, ctr);
+        return;
+    }
+    validate_device(ctx, X, n, d, metric, stream, ctr);
+    const float* Xs = X;
+    if (metric == KNN_B200_METRIC_HELLINGER) {
+        float* staged = static_cast<float*>(ctx->staged.get(size_t(n) * d * sizeof(float)));
+        cuda_check(knnb::launch_stage_sqrt(X, staged, uint64_t(n) * d, ctx->sm_count, stream), "stage launch");
+        ++ctr.launches;
+        Xs = staged;
+    }
+    const uint32_t R = uint32_t((uint64_t(n) + world - 1) / world);
+    const size_t full = size_t(R) * world * klist;  // rows padded to world x R for the reduce-scatter
+    auto* fi = static_cast<uint32_t*>(ctx->full_index.get(full * 4));
+    auto* fd = static_cast<float*>(ctx->full_dist.get(full * 4));
+    cuda_check(cudaMemsetAsync(fi, 0, full * 4, stream), "memset");
+    cuda_check(cudaMemsetAsync(fd, 0, full * 4, stream), "memset");
+    knnb::TensorPathArgs ta = tri_args(ctx, Xs, n, d, klist, metric, fi, fd, stream);
+    knnb::TensorPathResult tr;
+    bool overflow = false;
+    cuda_check(knnb::run_tri_nccl(ta, comm, uint32_t(rank), uint32_t(world), shard_alloc, ctx, tr, &overflow),
+               "sharded triangle");
+    ctr.arith_used = KNN_B200_ARITH_TENSOR;
+    ctr.launches += tr.launches;
+    ctr.rescored += tr.rescored;
+    ctr.fallback_rows += tr.fallback_rows;
+    ctr.exact_rows += tr.exact_rows;
+    ctr.distance_evals += uint64_t(n) * (n - 1) / 2 / world;  // about this rank's share of the pairs
+    if (overflow) {  // pathological data: every rank solves its rows with the rectangular sweep
+        solve_rows_core(ctx, X, n, d, k, metric, arith == KNN_B200_ARITH_AUTO ? KNN_B200_ARITH_TENSOR : arith, r0, r1,
+                        out_index, out_dist, stream, ctr);
+        return;
+    }
+    // exchange 3: rows to their contiguous shards.  Every element of the
+    // full arrays is written by exactly one rank and 0 elsewhere; u32 + 0 and
+    // f32 + (+0) are exact (no result is -0.0), so a sum is the gather.
+    const size_t rc = size_t(R) * klist;
+    auto* si = static_cast<uint32_t*>(ctx->shard_index.get(rc * 4 + 4));
+    auto* sd = static_cast<float*>(ctx->shard_dist.get(rc * 4 + 4));
+    nccl_check(ncclGroupStart(), "ncclGroupStart");
+    nccl_check(ncclReduceScatter(fi, si, rc, ncclUint32, ncclSum, comm, stream), "ncclReduceScatter");
+    nccl_check(ncclReduceScatter(fd, sd, rc, ncclFloat32, ncclSum, comm, stream), "ncclReduceScatter");
+    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+    const size_t mine = size_t(r1 - r0) * klist;
+    if (mine) {
+        cuda_check(cudaMemcpyAsync(out_index, si, mine * 4, cudaMemcpyDeviceToDevice, stream), "D2D");
+        cuda_check(cudaMemcpyAsync(out_dist, sd, mine * 4, cudaMemcpyDeviceToDevice, stream), "D2D");
+    }
+}
+
 void fill_stats(knn_b200_stats* st, const Counters& ctr, uint64_t pairs, int ndev) {
     if (!st) return;
     st->pair_evaluations = pairs;
@@ -531,6 +665,12 @@ void knn_b200_destroy(knn_b200_ctx* ctx) {
     ctx->tensor_ws.release();
     ctx->exact_ws.release();
     ctx->capture_ws.release();
+    for (auto& kv : ctx->shard_ws) kv.second.release();
+    ctx->full_index.release();
+    ctx->full_dist.release();
+    ctx->shard_index.release();
+    ctx->shard_dist.release();
+    if (ctx->comm && ctx->comm_owned) ncclCommDestroy(ctx->comm);
     if (ctx->host_flags) cudaFreeHost(ctx->host_flags);
     stage_free(ctx);
     for (auto& e : ctx->ev)
@@ -664,6 +804,135 @@ int knn_b200_solve_rows_device(knn_b200_ctx* ctx, const float* dev_vectors, uint
     });
 }
 
+int knn_b200_tri_unit_plan(uint32_t units, uint32_t world, uint32_t pairs_max, uint32_t* out_units,
+                           uint32_t* out_counts) {
+    return guarded([&] {
+        if (world < 1 || world > knnb::kTriMaxWorld || pairs_max < 1)
+            fail(KNN_B200_ERR_CONFIG, "bad world " + std::to_string(world) + " / pairs " + std::to_string(pairs_max));
+        knnb::tri_unit_plan(units, world, pairs_max, out_units, out_counts);
+    });
+}
+
+int knn_b200_comm_unique_id(void* out_id) {
+    return guarded([&] {
+        ncclUniqueId id;
+        nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(out_id, &id, sizeof(id));
+    });
+}
+
+int knn_b200_comm_init(knn_b200_ctx* ctx, const void* id, int rank, int world) {
+    return guarded([&] {
+        if (!ctx) fail(KNN_B200_ERR_CONFIG, "null context");
+        if (world < 1 || rank < 0 || rank >= world || world > int(knnb::kTriMaxWorld))
+            fail(KNN_B200_ERR_CONFIG, "bad rank " + std::to_string(rank) + " of " + std::to_string(world));
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (ctx->comm && ctx->comm_owned) ncclCommDestroy(ctx->comm);
+        ctx->comm = nullptr;
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof(uid));
+        nccl_check(ncclCommInitRank(&ctx->comm, world, uid, rank), "ncclCommInitRank");
+        ctx->comm_rank = rank;
+        ctx->comm_world = world;
+        ctx->comm_owned = true;
+    });
+}
+
+int knn_b200_comm_broadcast(knn_b200_ctx* ctx, void* dev_buf, uint64_t bytes, int root, void* stream) {
+    return guarded([&] {
+        if (!ctx || !ctx->comm) fail(KNN_B200_ERR_CONFIG, "context has no communicator (knn_b200_comm_init)");
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        nccl_check(ncclBroadcast(dev_buf, dev_buf, bytes, ncclUint8, root, ctx->comm, static_cast<cudaStream_t>(stream)),
+                   "ncclBroadcast");
+    });
+}
+
+int knn_b200_solve_sharded_device(knn_b200_ctx* ctx, const float* dev_vectors, uint32_t n, uint32_t d, uint32_t k,
+                                  int metric, int arith, uint32_t* dev_out_index, float* dev_out_dist, void* stream,
+                                  knn_b200_stats* stats) {
+    return guarded([&] {
+        if (!ctx) fail(KNN_B200_ERR_CONFIG, "null context");
+        check_args(n, d, k, metric, arith);
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        const auto t0 = std::chrono::steady_clock::now();
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        Counters ctr;
+        begin_call(ctx, s);
+        if (stats) cuda_check(cudaEventRecord(ctx->ev[1], s), "event");
+        const int world = ctx->comm ? ctx->comm_world : 1;
+        if (!ctx->comm)
+            solve_rows_core(ctx, dev_vectors, n, d, k, metric, arith, 0, n, dev_out_index, dev_out_dist, s, ctr);
+        else  // (a communicator of one rank runs the same collectives, degenerate)
+            solve_sharded_core(ctx, ctx->comm, ctx->comm_rank, world, dev_vectors, n, d, k, metric, arith,
+                               dev_out_index, dev_out_dist, s, ctr);
+        end_call(ctx, s);
+        if (stats) {
+            cuda_check(cudaEventRecord(ctx->ev[2], s), "event");
+            cuda_check(cudaStreamSynchronize(s), "solve sync");
+            fill_stats(stats, ctr, uint64_t(n) * (n - 1) / 2, world);
+            stats->h2d_ms = 0;
+            stats->d2h_ms = 0;
+            stats->kernel_ms = elapsed_ms(ctx->ev[1], ctx->ev[2]);
+            stats->sweep_ms = elapsed_ms(ctx->ev[4], ctx->ev[5]);
+            stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+    });
+}
+
+int knn_b200_debug_solve_sharded_loopback(knn_b200_ctx* ctx, const float* dev_vectors, uint32_t n, uint32_t d,
+                                          uint32_t k, int metric, int world, uint32_t* dev_out_index,
+                                          float* dev_out_dist, void* stream, knn_b200_stats* stats,
+                                          float* rank_ms, uint64_t* rank_xbytes) {
+    return guarded([&] {
+        if (!ctx) fail(KNN_B200_ERR_CONFIG, "null context");
+        check_args(n, d, k, metric, KNN_B200_ARITH_TENSOR);
+        if (world < 1 || world > int(knnb::kTriMaxWorld)) fail(KNN_B200_ERR_CONFIG, "bad world " + std::to_string(world));
+        const uint32_t klist = std::min(k, n - 1);
+        if (!tri_selected(n, d, klist, metric, KNN_B200_ARITH_TENSOR))
+            fail(KNN_B200_ERR_CONFIG, "problem does not take the triangle sweep (see tri_eligible)");
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        const auto t0 = std::chrono::steady_clock::now();
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        Counters ctr;
+        begin_call(ctx, s);
+        cuda_check(cudaEventRecord(ctx->ev[1], s), "event");
+        validate_device(ctx, dev_vectors, n, d, metric, s, ctr);
+        const float* Xs = dev_vectors;
+        if (metric == KNN_B200_METRIC_HELLINGER) {
+            float* staged = static_cast<float*>(ctx->staged.get(size_t(n) * d * sizeof(float)));
+            cuda_check(knnb::launch_stage_sqrt(dev_vectors, staged, uint64_t(n) * d, ctx->sm_count, s), "stage launch");
+            Xs = staged;
+        }
+        knnb::TensorPathArgs ta = tri_args(ctx, Xs, n, d, klist, metric, dev_out_index, dev_out_dist, s);
+        knnb::TensorPathResult tr;
+        bool overflow = false;
+        cuda_check(knnb::run_tri_loopback(ta, uint32_t(world), shard_alloc, ctx, tr, rank_ms,
+                                          reinterpret_cast<unsigned long long*>(rank_xbytes), &overflow),
+                   "sharded triangle (loopback)");
+        ctr.arith_used = KNN_B200_ARITH_TENSOR;
+        ctr.launches += tr.launches;
+        ctr.rescored += tr.rescored;
+        ctr.fallback_rows += tr.fallback_rows;
+        ctr.exact_rows += tr.exact_rows;
+        if (overflow)
+            solve_rows_core(ctx, dev_vectors, n, d, k, metric, KNN_B200_ARITH_TENSOR, 0, n, dev_out_index,
+                            dev_out_dist, s, ctr);
+        end_call(ctx, s);
+        cuda_check(cudaEventRecord(ctx->ev[2], s), "event");
+        cuda_check(cudaStreamSynchronize(s), "solve sync");
+        if (stats) {
+            fill_stats(stats, ctr, uint64_t(n) * (n - 1) / 2, world);
+            stats->reserved = overflow ? 1 : 0;
+            stats->kernel_ms = elapsed_ms(ctx->ev[1], ctx->ev[2]);
+            stats->sweep_ms = elapsed_ms(ctx->ev[4], ctx->ev[5]);
+            stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+    });
+}
+
 }  // extern "C"
 
 namespace {
@@ -673,6 +942,10 @@ namespace {
 // float runs the float policies; double runs the KNN_DOUBLE_ACCUM sweep.
 std::mutex pool_mu;                // guards `pool`, shared by both distance types
 std::vector<knn_b200_ctx*> pool;  // one context per device, created on first use
+
+// NCCL communicators over devices 0..m-1 for the single-process multi-GPU
+// solve (ncclCommInitAll), created on first use per device count.
+std::map<uint32_t, std::vector<ncclComm_t>> multi_comms;  // guarded by pool_mu
 
 template <typename DistT>
 int solve_multi_impl(const float* host_vectors, uint32_t n, uint32_t d, uint32_t k, int metric, int arith,
@@ -693,19 +966,35 @@ int solve_multi_impl(const float* host_vectors, uint32_t n, uint32_t d, uint32_t
                 pool[g] = c;
             }
         }
+        std::vector<ncclComm_t>* comms = nullptr;
+        if (use > 1) {
+            auto it = multi_comms.find(use);
+            if (it == multi_comms.end()) {
+                std::vector<ncclComm_t> cs(use);
+                std::vector<int> devs(use);
+                for (uint32_t g = 0; g < use; ++g) devs[g] = int(g);
+                nccl_check(ncclCommInitAll(cs.data(), int(use), devs.data()), "ncclCommInitAll");
+                it = multi_comms.emplace(use, std::move(cs)).first;
+            }
+            comms = &it->second;
+        }
         const auto t0 = std::chrono::steady_clock::now();
         const uint32_t klist = std::min(k, n - 1);
         std::vector<KnnError> errs(use, KnnError{0, {}});
         std::vector<Counters> ctrs(use);
         std::vector<float> kms(use, 0.f), hms(use, 0.f), dms(use, 0.f), sms(use, 0.f);
+        // One host thread per GPU (engine.cpp:37-56).  The reference set goes
+        // to device 0 once (pinned staging lanes) and is replicated by one
+        // NCCL broadcast; each device then solves its contiguous shard of rows
+        // (shard_rows) -- float distances through the sharded triangle where
+        // eligible -- and copies it straight into the caller's arrays.
         auto lane = [&](uint32_t g) {
             try {
                 knn_b200_ctx* ctx = pool[g];
                 std::lock_guard<std::mutex> cl(ctx->mu);
                 cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
-                // Contiguous query-row shards; every device holds all n vectors.
-                const uint32_t r0 = uint32_t(uint64_t(n) * g / use);
-                const uint32_t r1 = uint32_t(uint64_t(n) * (g + 1) / use);
+                uint32_t r0, r1;
+                shard_rows(n, int(g), int(use), r0, r1);
                 const size_t vec_bytes = size_t(n) * d * sizeof(float);
                 const size_t out_elems = size_t(r1 - r0) * klist;
                 float* X = static_cast<float*>(ctx->vectors.get(vec_bytes));
@@ -714,18 +1003,22 @@ int solve_multi_impl(const float* host_vectors, uint32_t n, uint32_t d, uint32_t
                 cudaStream_t s = ctx->stream;
                 begin_call(ctx, s);
                 cuda_check(cudaEventRecord(ctx->ev[0], s), "event");
-                // the lanes share the host: each stages with its share of the threads
-                const int st_threads = std::max(1, kStageThreadsDefault / int(use));
-                host_copy(ctx, X, host_vectors, vec_bytes, true, s, st_threads);
+                if (g == 0) host_copy(ctx, X, host_vectors, vec_bytes, true, s);
+                if (comms)
+                    nccl_check(ncclBroadcast(X, X, vec_bytes, ncclUint8, 0, (*comms)[g], s), "ncclBroadcast");
                 cuda_check(cudaEventRecord(ctx->ev[1], s), "event");
                 if constexpr (std::is_same_v<DistT, double>)
                     solve_rows_core_f64(ctx, X, n, d, k, metric, r0, r1, oi, od, s, ctrs[g]);
+                else if (comms)
+                    solve_sharded_core(ctx, (*comms)[g], int(g), int(use), X, n, d, k, metric, arith, oi, od, s,
+                                       ctrs[g]);
                 else
                     solve_rows_core(ctx, X, n, d, k, metric, arith, r0, r1, oi, od, s, ctrs[g]);
                 cuda_check(cudaEventRecord(ctx->ev[2], s), "event");
                 cuda_check(cudaEventSynchronize(ctx->ev[2]), "solve sync");
                 const auto t_d2h = std::chrono::steady_clock::now();
                 if (out_elems) {
+                    const int st_threads = std::max(1, kStageThreadsDefault / int(use));
                     host_copy_segs(ctx,
                                    {{out_index + size_t(r0) * klist, oi, out_elems * 4},
                                     {out_dist + size_t(r0) * klist, od, out_elems * sizeof(DistT)}},

@@ -80,5 +80,24 @@ size_t sym_workspace_bytes(uint32_t n, int sm_count);
 cudaError_t run_sym_sweep(const uint8_t* xh, const float* alpha, const float* bmin, uint32_t n, uint32_t npad,
                           uint32_t kc, uint64_t* cand, void* ws, int sm_count, cudaStream_t st);
 cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r);
+bool tri_eligible(uint32_t n, uint32_t d, uint32_t klist, int fold);
+
+// The triangle sweep sharded over `world` ranks (tri_shard.cuh).
+// alloc(ctx, slot, bytes): grow-only device memory per slot.  a.row_begin = 0,
+// a.row_end = n; a.out_* are full n-row arrays that receive the rank's own
+// rows (loopback: every rank's rows).  *overflow: column-side logs overflowed
+// (the caller redoes the solve without the triangle).
+typedef void* (*ShardAlloc)(void* ctx, int slot, size_t bytes);
+constexpr uint32_t kTriMaxWorld = 64;
+// Unit ownership (host): rank r's units are units[sum(counts[<r]) ...], in the
+// order its CTA pairs take them.
+void tri_unit_plan(uint32_t U, uint32_t world, uint32_t pairs_max, uint32_t* units, uint32_t* counts);
+cudaError_t run_tri_loopback(const TensorPathArgs& a, uint32_t world, ShardAlloc alloc, void* actx,
+                             TensorPathResult& r, float* rank_ms, unsigned long long* xbytes, bool* overflow);
+}  // namespace knnb
+typedef struct ncclComm* ncclComm_t;
+namespace knnb {
+cudaError_t run_tri_nccl(const TensorPathArgs& a, ncclComm_t comm, uint32_t rank, uint32_t world, ShardAlloc alloc,
+                         void* actx, TensorPathResult& r, bool* overflow);
 
 }  // namespace knnb

@@ -33,6 +33,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -119,6 +120,12 @@ struct SweepParams {
     // E4M3 operands (kind::f8f6f4, PAIR kernels; the triangle's sample pass):
     // xh/xa hold E4M3 planes, kc counts 128-element chunks
     int e4m3;
+    // Sharded triangle (TRI): this rank's 256-row units, in the order the
+    // persistent CTA pairs take them (pair p: units[p], units[p + pairs], ...);
+    // row-side lists are stored per local unit (cand row = lu * 256 + r).
+    // Null: every unit 0, 1, ... of [row_begin, row_end).
+    const uint32_t* units;
+    uint32_t nunits;
 };
 
 // Candidate keys from the norm-sorted sweep carry sweep-order column indices;
@@ -187,7 +194,8 @@ tensor_sweep_kernel(const SweepParams p) {
     const bool leader = rank == 0;
     const uint32_t unit0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
     const uint32_t unit_step = PAIR ? gridDim.x / 2 : gridDim.x;
-    const uint32_t nunits = PAIR ? (nrb + 1) / 2 : nrb;
+    const uint32_t nunits = p.units ? p.nunits : (PAIR ? (nrb + 1) / 2 : nrb);
+    auto unit_id = [&](uint32_t lu) { return p.units ? __ldg(p.units + lu) : lu; };
     auto unit_block = [&](uint32_t u) { return PAIR ? 2 * u + rank : u; };
     // TRI: a pair unit's 256 rows are exactly tile u; it sweeps tiles >= u
     auto tri_start = [&](uint32_t u) -> uint32_t { return TRI ? u : 0u; };
@@ -241,7 +249,8 @@ tensor_sweep_kernel(const SweepParams p) {
             uint32_t phase = 0, a_phase = 0;
             for (uint32_t g = g_first; g < ngroups; g += g_step) {
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
-                for (uint32_t u = unit0; u < nunits; u += unit_step) {
+                for (uint32_t lu = unit0; lu < nunits; lu += unit_step) {
+                    const uint32_t u = unit_id(lu);
                     const uint32_t r0 = p.row_begin + unit_block(u) * TS_BM;
                     const uint32_t ts = max(t0, tri_start(u));
                     if (ts >= t1) continue;
@@ -291,7 +300,8 @@ tensor_sweep_kernel(const SweepParams p) {
             uint32_t phase = 0, a_phase = 0;
             for (uint32_t g = g_first; g < ngroups; g += g_step) {
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
-                for (uint32_t u = unit0; u < nunits; u += unit_step) {
+                for (uint32_t lu = unit0; lu < nunits; lu += unit_step) {
+                    const uint32_t u = unit_id(lu);
                     const uint32_t ts = max(t0, tri_start(u));
                     if (ts >= t1) continue;
                     wait(afull_bar, a_phase);
@@ -329,7 +339,8 @@ tensor_sweep_kernel(const SweepParams p) {
             uint32_t phase = 0, a_phase = 0, tcount = 0;
             for (uint32_t g = g_first; g < ngroups; g += g_step) {
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
-                for (uint32_t u = unit0; u < nunits; u += unit_step) {
+                for (uint32_t lu = unit0; lu < nunits; lu += unit_step) {
+                    const uint32_t u = unit_id(lu);
                     const uint32_t ts = max(t0, tri_start(u));
                     if (ts >= t1) continue;
                     if constexpr (ARES) {
@@ -455,14 +466,18 @@ tensor_sweep_kernel(const SweepParams p) {
         };
         for (uint32_t g = g_first; g < ngroups; g += g_step) {
             const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
-            for (uint32_t u = unit0; u < nunits; u += unit_step) {
+            for (uint32_t lu = unit0; lu < nunits; lu += unit_step) {
+                const uint32_t u = unit_id(lu);
                 const uint32_t tsu = tri_start(u), ts = max(t0, tsu);
                 if (ts >= t1) continue;
                 const bool fresh = TRI ? t0 <= tsu : g == 0;  // the unit's first group with work
                 const uint32_t row = p.row_begin + unit_block(u) * TS_BM + rl;
                 const bool valid = row < p.row_end;
                 const float alpha_i = TRI && valid ? p.alpha[row] : kInf;  // column side: this row's norm
-                uint64_t* state = p.cand + (size_t(row - p.row_begin) * NSEG + seg) * KPL;
+                // list slot: the row's offset in the call (or, with a unit list, in this rank's units)
+                const uint32_t lrow = p.units ? lu * (PAIR ? 2 * TS_BM : TS_BM) + (PAIR ? rank * TS_BM : 0) + rl
+                                              : row - p.row_begin;
+                uint64_t* state = p.cand + (size_t(lrow) * NSEG + seg) * KPL;
                 // Columns are ranked by y = fl(beta_j - 2 dot): alpha_i is
                 // constant along a row; the rescore forms A = alpha_i + y in fp64.
                 if constexpr (CAPTURE) {
@@ -866,12 +881,14 @@ __global__ void e4m3_planes_kernel(const uint8_t* __restrict__ xh, uint32_t npad
 // side appends); padding rows get -inf (never admit).
 // tl[j]: the largest of them -- a looser capture threshold for a row whose
 // triangle pass ends with fewer than k candidates (the capture re-checks it).
-__global__ void tri_threshold_kernel(const uint64_t* __restrict__ cand, uint32_t n, uint32_t npad, uint32_t kp,
-                                     uint32_t r, float unscale, float* __restrict__ tc, float* __restrict__ tl) {
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < npad; j += gridDim.x * blockDim.x) {
+// Rows [j0, j1) (sorted order); cand holds their lists from row j0 on.
+__global__ void tri_threshold_kernel(const uint64_t* __restrict__ cand, uint32_t n, uint32_t j0, uint32_t j1,
+                                     uint32_t kp, uint32_t r, float unscale, float* __restrict__ tc,
+                                     float* __restrict__ tl) {
+    for (uint32_t j = j0 + blockIdx.x * blockDim.x + threadIdx.x; j < j1; j += gridDim.x * blockDim.x) {
         float t = -__int_as_float(0x7f800000), l = t;
         if (j < n) {
-            const uint64_t* c = cand + size_t(j) * kp;
+            const uint64_t* c = cand + size_t(j - j0) * kp;
             uint64_t best = kEmptyKey, last = 0;
             for (uint32_t a = 0; a < kp; ++a) {
                 uint32_t below = 0;
@@ -892,10 +909,13 @@ __global__ void tri_threshold_kernel(const uint64_t* __restrict__ cand, uint32_t
 // rescore handles a short fixed-size list.  An overflowed buffer is passed on
 // as a count above kTriSel (no proof).
 constexpr int kTriSel = 32;
+// units (sharded triangle, or null): slot `row` is sorted position
+// units[row / 256] * 256 + row % 256, whose threshold is thr[that position].
 __global__ void __launch_bounds__(256) tri_select_kernel(const uint64_t* __restrict__ buf, const uint32_t* __restrict__ cnt,
                                                           uint32_t cap, uint32_t n, const float* __restrict__ thr,
                                                           uint64_t* __restrict__ out, uint32_t* __restrict__ out_cnt,
-                                                          float* __restrict__ out_bound) {
+                                                          float* __restrict__ out_bound,
+                                                          const uint32_t* __restrict__ units = nullptr) {
     __shared__ __align__(16) uint64_t ks[8][kTriCap + 2];
     const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (row >= n) return;
@@ -928,7 +948,7 @@ __global__ void __launch_bounds__(256) tri_select_kernel(const uint64_t* __restr
         }
     }
     if (lane == 0) {
-        float b = thr[row];
+        float b = thr[units ? units[row >> 8] * 256 + (row & 255) : row];
         if (next != kEmptyKey) {
             const float nb = ordered_to_float(uint32_t(next >> 32));
             b = nb < b ? nb : b;
@@ -1161,7 +1181,8 @@ struct RescoreParams {
     const uint64_t* xbuf;     // [slots][XC] extra candidates (column side of the triangle sweep)
     const uint32_t* xcnt;     // [slots] their counts (> XC: overflowed)
     const float* xbound;      // [slots] y bound of the column side's exclusions
-    const float* xcap;        // [slots] capture threshold (y) for rows left with fewer than k candidates, or null
+    const float* xcap;        // [sorted positions] capture threshold (y) for rows left with fewer than k candidates, or null
+    const uint32_t* units;    // sharded triangle: slot s is sorted position units[s / 256] * 256 + s % 256 (or null)
 };
 
 constexpr double kTcSafety = 4.0;  // tensor-core accumulation error allowance
@@ -1292,9 +1313,12 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t slot = blockIdx.x * 8 + warp;
     if (slot >= p.row_end - p.row_begin) return;
-    // slot: input order, or (p.rowperm) a position in the sorted order
-    const uint32_t qo = p.rowperm ? p.rowperm[slot] : p.row_begin + slot;  // input row
-    const uint32_t q = p.rowperm ? slot : (p.rowpos ? p.rowpos[qo] : qo);  // its sorted position
+    // slot: input order, or (p.rowperm) a position in the sorted order, or
+    // (p.units) a row of this rank's units
+    const uint32_t sp = p.units ? p.units[slot >> 8] * 256 + (slot & 255) : slot;
+    if (p.units && sp >= p.n) return;  // padding rows of the last unit
+    const uint32_t qo = p.rowperm ? p.rowperm[sp] : p.row_begin + slot;  // input row
+    const uint32_t q = p.rowperm ? sp : (p.rowpos ? p.rowpos[qo] : qo);  // its sorted position
     const uint64_t* cand = p.cand + size_t(slot) * KP;
     const float* xq = p.X + size_t(qo) * p.d;
     const bool vec = (p.d % 4 == 0);
@@ -1531,7 +1555,7 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         complete = true;  // every column was offered into a non-full list: the list holds all of them
     } else if (valid < p.klist) {
         complete = false;
-        if (XC > 0 && p.xcap) cap_y = double(p.xcap[slot]);
+        if (XC > 0 && p.xcap) cap_y = double(p.xcap[q]);
     } else {
         const uint64_t kth = keys_s[warp][p.klist - 1];
         const double T = double(ordered_to_float(uint32_t(kth >> 32)));
@@ -1914,7 +1938,99 @@ static cudaError_t launch_rescore(TensorCfg c, const RescoreParams& rp, uint32_t
     return cudaGetLastError();
 }
 
+// Rows without a completeness proof: a second tensor pass captures the whole
+// proven band of each such row (fixed per-row thresholds fb_thr), then an
+// exact rescore; only rows whose band overflows the capture buffer are
+// recomputed by the EXACT kernel.  fb_rows are input rows; results go to
+// a.out_* at row fb_rows[i] - a.row_begin.
+struct CaptureArgs {
+    const uint8_t* xh;  // the first-order (norm-sorted) planes and per-row arrays
+    const float* alpha;
+    const double* rho;
+    const double* xnorm;
+    const unsigned long long* gmax;
+    const unsigned int* maxabs;
+    const float* bmin;
+    const uint32_t* perm;    // sorted position -> input row (null: unsorted)
+    const uint32_t* rowpos;  // input row -> sorted position (null: unsorted)
+    uint32_t n, npad, kc, group_tiles, cap;
+    const uint32_t* fb_rows;
+    const float* fb_thr;
+    unsigned long long* rescored;
+};
+
+static cudaError_t run_capture(const TensorPathArgs& a, const CaptureArgs& c, uint32_t nfb, TensorPathResult& r,
+                               uint32_t& launches) {
+    cudaStream_t st = a.stream;
+    cudaError_t e;
+    const uint32_t mpad = (nfb + TS_BM - 1) / TS_BM * TS_BM;
+    uint8_t* w2 = static_cast<uint8_t*>(a.alloc2(a.alloc2_ctx, capture_workspace_bytes(nfb, a.d, c.cap)));
+    if (!w2) return cudaErrorMemoryAllocation;
+    auto take2 = [&](size_t x) {
+        uint8_t* q = w2;
+        w2 += (x + 255) / 256 * 256;
+        return q;
+    };
+    uint8_t* xa = take2(size_t(c.kc) * mpad * 128);
+    uint32_t* cap_cnt = reinterpret_cast<uint32_t*>(take2(size_t(nfb) * 4 + 8));
+    uint64_t* cap_buf = reinterpret_cast<uint64_t*>(take2(size_t(nfb) * c.cap * 8));
+    uint32_t* fb2_rows = reinterpret_cast<uint32_t*>(take2(size_t(nfb) * 4));
+    uint32_t* fb2_count = cap_cnt + nfb;
+    if ((e = cudaMemsetAsync(cap_cnt, 0, size_t(nfb) * 4 + 8, st)) != cudaSuccess) return e;
+    gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(c.xh, c.npad, c.kc, c.fb_rows, 0, nfb, mpad, c.rowpos, xa);
+    SweepParams cp{c.xh,    c.alpha, c.n,  c.npad,   c.kc,    0,       nfb,   c.group_tiles, 0,
+                   nullptr, xa,      mpad, c.fb_thr, cap_cnt, cap_buf, c.cap, c.bmin};
+    if ((e = launch_capture_sweep(c.kc <= uint32_t(TS_MAX_RES_KC), cp, nfb, st)) != cudaSuccess) return e;
+    if (c.perm) {
+        remap_capture_kernel<<<nfb, 128, 0, st>>>(cap_buf, cap_cnt, nfb, c.cap, c.perm);
+        ++launches;
+    }
+    Rescore2Params r2{a.X,     a.n,   a.d,        a.klist,     a.row_begin, c.fb_rows, nfb,      cap_cnt,
+                      cap_buf, c.cap, a.out_sqrt, a.out_index, a.out_dist,  fb2_count, fb2_rows, c.rescored,
+                      c.fb_thr, c.rowpos, c.alpha, c.rho, c.xnorm, c.gmax, c.maxabs};
+    const size_t smem2 = size_t(4) * c.cap * 8;
+    if (a.fold == kCosine) {
+        cudaFuncSetAttribute(rescore_capture_kernel<kCosine>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+        rescore_capture_kernel<kCosine><<<(nfb + 3) / 4, 128, smem2, st>>>(r2);
+    } else {
+        cudaFuncSetAttribute(rescore_capture_kernel<kSqEuclidean>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem2));
+        rescore_capture_kernel<kSqEuclidean><<<(nfb + 3) / 4, 128, smem2, st>>>(r2);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    launches += 3;
+    if ((e = cudaMemcpyAsync(a.host_scratch, fb2_count, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(static_cast<uint8_t*>(a.host_scratch) + 32, c.rescored, 8, cudaMemcpyDeviceToHost, st)) !=
+        cudaSuccess)
+        return e;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    const uint32_t nfb2 = *static_cast<const uint32_t*>(a.host_scratch);
+    r.rescored = *reinterpret_cast<const unsigned long long*>(static_cast<const uint8_t*>(a.host_scratch) + 32);
+    r.exact_rows = nfb2;
+    if (nfb2) {
+        if ((e = launch_exact_fused(a.fold, a.X, a.n, a.d, a.klist, fb2_rows, 0, nfb2, a.out_index, a.out_dist,
+                                    a.out_sqrt, a.row_begin, a.exact_scratch, a.sm_count, st)) != cudaSuccess)
+            return e;
+        ++launches;
+    }
+    return cudaSuccess;
+}
+
 static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResult& r, bool allow_tri);
+
+// Whole problems that take the triangle sweep (each unordered pair once):
+// sorted columns (not cosine), two 12-entry lists (k <= 11), resident A
+// (d <= 256), and n past the measured crossover (262K: rectangular faster,
+// 524K: triangle faster).  KNN_B200_TRI=0 disables it; KNN_B200_TRI=force
+// drops the size gate (testing: the sharded program at small n, sanitizers).
+bool tri_eligible(uint32_t n, uint32_t d, uint32_t klist, int fold) {
+    const char* te = getenv("KNN_B200_TRI");
+    if (te && strcmp(te, "0") == 0) return false;
+    const bool force = te && strcmp(te, "force") == 0;
+    const TensorCfg cfg = tensor_cfg(klist);
+    return fold != kCosine && sort_selected(0, false) && cfg.kpl == 12 && cfg.nseg == 2 &&
+           (d + 63) / 64 <= uint32_t(TS_MAX_RES_KC) && (force ? n >= 512 : n >= 393216);
+}
 
 cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
     return run_tensor_path_impl(a, r, true);
@@ -2017,9 +2133,7 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
     // pair's own, offering each pair to the row side (register lists) and to
     // the column side (fixed-threshold append buffers), and the rescore merges
     // both with a bound for each.
-    const char* te = getenv("KNN_B200_TRI");
-    const bool tri = allow_tri && !(te && atoi(te) == 0) && sorted && a.row_begin == 0 && a.row_end == n && cfg.kpl == 12 &&
-                     cfg.nseg == 2 && kc <= uint32_t(TS_MAX_RES_KC) && n >= 393216;  // measured crossover: 262K rect, 524K tri
+    const bool tri = allow_tri && a.row_begin == 0 && a.row_end == n && !sym && tri_eligible(n, d, a.klist, a.fold);
     uint64_t* tri_cbuf = nullptr;
     uint32_t* tri_ccnt = nullptr;
     float* tri_tc = nullptr;
@@ -2136,8 +2250,8 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
             : skpl == 6 ? launch_sweep_pair<6, 256, 8>(ss, n, st)
                         : launch_sweep_pair<kTriSampleKpl, 256, 8>(ss, n, st);
         if (e != cudaSuccess) return e;
-        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, npad, 2 * skpl, trank, 1.0f / dscale, tc2,
-                                                              tl1);
+        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, 0, npad, 2 * skpl, trank, 1.0f / dscale,
+                                                              tc2, tl1);
         // second order: thresholds sorted within buckets of the norm order;
         // the triangle sweep runs on a copy of the planes in that order
         tri_order_key_kernel<<<a.sm_count * 4, 256, 0, st>>>(tc2, n, kTriBucket, okey, oidx);
@@ -2227,61 +2341,15 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
     r.rescored = *reinterpret_cast<const unsigned long long*>(static_cast<const uint8_t*>(a.host_scratch) + 32);
     r.fallback_rows = nfb;
     if (nfb) {
-        const uint32_t mpad = (nfb + TS_BM - 1) / TS_BM * TS_BM;
-        const uint32_t cap = kp >= 128 ? 1024 : 512;
-        uint8_t* w2 = static_cast<uint8_t*>(a.alloc2(a.alloc2_ctx, capture_workspace_bytes(nfb, d, cap)));
-        if (!w2) return cudaErrorMemoryAllocation;
-        auto take2 = [&](size_t x) {
-            uint8_t* q = w2;
-            w2 += (x + 255) / 256 * 256;
-            return q;
-        };
-        uint8_t* xa = take2(size_t(kc) * mpad * 128);
-        uint32_t* cap_cnt = reinterpret_cast<uint32_t*>(take2(size_t(nfb) * 4 + 8));
-        uint64_t* cap_buf = reinterpret_cast<uint64_t*>(take2(size_t(nfb) * cap * 8));
-        uint32_t* fb2_rows = reinterpret_cast<uint32_t*>(take2(size_t(nfb) * 4));
-        uint32_t* fb2_count = cap_cnt + nfb;
-        if ((e = cudaMemsetAsync(cap_cnt, 0, size_t(nfb) * 4 + 8, st)) != cudaSuccess) return e;
-        gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xh, npad, kc, fb_rows, 0, nfb, mpad,
-                                                           sorted ? rowpos : nullptr, xa);
-        SweepParams cp{xh,      alpha,  n,    npad,   kc,      0,   nfb, group_tiles, 0,
-                       nullptr, xa,     mpad, fb_thr, cap_cnt, cap_buf, cap, bmin};
-        if ((e = launch_capture_sweep(kc <= uint32_t(TS_MAX_RES_KC), cp, nfb, st)) != cudaSuccess) return e;
-        if (sorted) {
-            remap_capture_kernel<<<nfb, 128, 0, st>>>(cap_buf, cap_cnt, nfb, cap, perm);
-            ++launches;
-        }
-        Rescore2Params r2{a.X,     n,       d,         a.klist,   a.row_begin, fb_rows,   nfb,      cap_cnt,
-                          cap_buf, cap,     a.out_sqrt, a.out_index, a.out_dist, fb2_count, fb2_rows, rescored,
-                          fb_thr,  sorted ? rowpos : nullptr, alpha, rho, xnorm, gmax, maxabs};
-        const size_t smem2 = size_t(4) * cap * 8;
-        if (cosine) {
-            cudaFuncSetAttribute(rescore_capture_kernel<kCosine>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
-            rescore_capture_kernel<kCosine><<<(nfb + 3) / 4, 128, smem2, st>>>(r2);
-        } else {
-            cudaFuncSetAttribute(rescore_capture_kernel<kSqEuclidean>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem2));
-            rescore_capture_kernel<kSqEuclidean><<<(nfb + 3) / 4, 128, smem2, st>>>(r2);
-        }
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        launches += 3;
-        if ((e = cudaMemcpyAsync(a.host_scratch, fb2_count, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
-        if ((e = cudaMemcpyAsync(static_cast<uint8_t*>(a.host_scratch) + 32, rescored, 8, cudaMemcpyDeviceToHost, st)) !=
-            cudaSuccess)
-            return e;
-        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
-        const uint32_t nfb2 = *static_cast<const uint32_t*>(a.host_scratch);
-        r.rescored = *reinterpret_cast<const unsigned long long*>(static_cast<const uint8_t*>(a.host_scratch) + 32);
-        r.exact_rows = nfb2;
-        if (nfb2) {
-            if ((e = launch_exact_fused(a.fold, a.X, n, d, a.klist, fb2_rows, 0, nfb2, a.out_index, a.out_dist,
-                                        a.out_sqrt, a.row_begin, a.exact_scratch, a.sm_count, st)) != cudaSuccess)
-                return e;
-            ++launches;
-        }
+        const CaptureArgs ca{xh,   alpha, rho,   xnorm, gmax,  maxabs,      bmin,    sorted ? perm : nullptr,
+                             sorted ? rowpos : nullptr, n,     npad,  kc,    group_tiles, kp >= 128 ? 1024u : 512u,
+                             fb_rows, fb_thr, rescored};
+        if ((e = run_capture(a, ca, nfb, r, launches)) != cudaSuccess) return e;
     }
     r.launches = launches;
     return cudaSuccess;
 }
 
 }  // namespace knnb
+
+#include "tri_shard.cuh"

@@ -381,6 +381,75 @@ class Context:
         return st.as_dict() if st is not None else None
 
 
+def comm_unique_id() -> bytes:
+    """128 opaque bytes (an ncclUniqueId) for Context.comm_init."""
+    buf = ctypes.create_string_buffer(128)
+    raise_for_status(_lib.load().knn_b200_comm_unique_id(buf))
+    return buf.raw
+
+
+def comm_init(ctx: Context, uid: bytes, rank: int, world: int) -> None:
+    """Bind an NCCL communicator of `world` ranks to ctx (collective)."""
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    raise_for_status(_lib.load().knn_b200_comm_init(ctx._h, buf, rank, world))
+
+
+def comm_broadcast_torch(ctx: Context, t, root: int = 0) -> None:
+    """In-place NCCL broadcast of a CUDA tensor over ctx's communicator."""
+    import torch
+    stream = torch.cuda.current_stream(t.device).cuda_stream
+    raise_for_status(_lib.load().knn_b200_comm_broadcast(ctx._h, t.data_ptr(), t.numel() * t.element_size(), root,
+                                                         stream))
+
+
+def shard_rows(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows of rank `rank` in a sharded solve: [R r, min(R (r+1), n)), R = ceil(n / world)."""
+    rr = -(-n // world)
+    b = min(rr * rank, n)
+    return b, min(b + rr, n)
+
+
+def solve_sharded_torch(ctx: Context, x, k: int, metric: CumulativeDistance, arith: int = _lib.ARITH_AUTO,
+                        rank: int = 0, world: int = 1, want_stats: bool = False):
+    """This rank's contiguous shard of the whole problem's lists
+    (knn_b200_solve_sharded_device, collective over ctx's communicator).
+    Returns (index int32, distance float32, stats)."""
+    import torch
+    if not (x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and x.dim() == 2):
+        raise ConfigError("x must be a contiguous 2-D float32 CUDA tensor")
+    n, d = x.shape
+    klist = min(k, n - 1)
+    b, e = shard_rows(n, rank, world)
+    idx = torch.empty((max(e - b, 1), klist), dtype=torch.int32, device=x.device)
+    dist = torch.empty((max(e - b, 1), klist), dtype=torch.float32, device=x.device)
+    st = _lib.Stats() if want_stats else None
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    raise_for_status(_lib.load().knn_b200_solve_sharded_device(
+        ctx._h, x.data_ptr(), n, d, k, metric.metric_id, arith, idx.data_ptr(), dist.data_ptr(), stream,
+        ctypes.byref(st) if st is not None else None))
+    return idx[: e - b], dist[: e - b], (st.as_dict() if st is not None else None)
+
+
+def solve_sharded_loopback_torch(ctx: Context, x, k: int, metric: CumulativeDistance, world: int):
+    """Test hook: all `world` rank programs of the sharded triangle on x's
+    device, one after another (knn_b200_debug_solve_sharded_loopback).
+    Returns (index, distance, stats, rank_ms (world x 4), sent bytes (world))."""
+    import numpy as np
+    import torch
+    n, d = x.shape
+    klist = min(k, n - 1)
+    idx = torch.empty((n, klist), dtype=torch.int32, device=x.device)
+    dist = torch.empty((n, klist), dtype=torch.float32, device=x.device)
+    st = _lib.Stats()
+    rank_ms = np.zeros((world, 4), dtype=np.float32)
+    xbytes = np.zeros(world, dtype=np.uint64)
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    raise_for_status(_lib.load().knn_b200_debug_solve_sharded_loopback(
+        ctx._h, x.data_ptr(), n, d, k, metric.metric_id, world, idx.data_ptr(), dist.data_ptr(), stream,
+        ctypes.byref(st), rank_ms.ctypes.data, xbytes.ctypes.data))
+    return idx, dist, st.as_dict(), rank_ms, xbytes
+
+
 def solve_rows_torch(ctx: Context, x, k: int, metric: CumulativeDistance, row_begin: int, row_end: int,
                      arith: int = _lib.ARITH_AUTO, out=None, want_stats: bool = False):
     """Rows [row_begin, row_end) of a CUDA float32 tensor ``x`` (n x d) against

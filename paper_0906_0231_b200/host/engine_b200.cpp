@@ -15,6 +15,7 @@
 // KNN_B200_ARITH=auto|exact|tensor, default auto.  All policies return the
 // same bits.
 #include <chrono>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -65,22 +66,32 @@ bool functor_matches(const CumulativeDistance& f, dist_t (*fold)(const float*, c
     if (!f.step) return false;
     const metrics::Erased m{f.initial, f.step, f.finalize};
     SplitMix64 rng(0x6b2f7a11d3c05e93ull);
-    constexpr std::uint32_t kMaxDim = 67;
+    constexpr std::uint32_t kMaxDim = 128;
     float u[kMaxDim], v[kMaxDim];
-    for (std::uint32_t trial = 0; trial < 96; ++trial) {
-        const std::uint32_t d = 1 + trial % kMaxDim;
-        // value ranges: [0,1), signed, and wide magnitudes (rounding-sensitive)
+    for (std::uint32_t trial = 0; trial < 256; ++trial) {
+        const std::uint32_t d = 1 + (trial * 7) % kMaxDim;
+        // value mixes: [0,1) and [-1,1) (the data's range), and full 24-bit
+        // mantissas with exponents spread over 2^-2..2^2 and 2^-5..2^5, whose
+        // partial sums need rounding even in double -- a fold that rounds
+        // differently (another order, sign convention or widening) shows there
         for (std::uint32_t j = 0; j < d; ++j) {
-            float a = rng.next_unit_float(), b = rng.next_unit_float();
-            if (trial % 3 == 1) {
-                a = 2.0f * a - 1.0f;
-                b = 2.0f * b - 1.0f;
-            } else if (trial % 3 == 2) {
-                a = (2.0f * a - 1.0f) * float(1u << (j % 17));
-                b = (2.0f * b - 1.0f) * float(1u << ((j * 7) % 17));
+            float x[2];
+            for (float& a : x) {
+                const std::uint32_t mode = trial % 4;
+                if (mode == 0) {
+                    a = rng.next_unit_float();
+                } else if (mode == 1) {
+                    a = 2.0f * rng.next_unit_float() - 1.0f;
+                } else {
+                    const std::uint64_t r = rng.next();
+                    const int spread = mode == 2 ? 2 : 5;
+                    const float m = float((r >> 40) | (1u << 23)) * 0x1.0p-24f;  // [0.5, 1), 24 bits
+                    const int e = int((r >> 8) % std::uint64_t(2 * spread + 1)) - spread;
+                    a = std::ldexp(m, e) * ((r & 1) ? -1.0f : 1.0f);
+                }
             }
-            u[j] = a;
-            v[j] = b;
+            u[j] = x[0];
+            v[j] = x[1];
         }
         const dist_t want = fold(u, v, d);
         const dist_t got = fold_distance(m, u, v, d);

@@ -27,6 +27,27 @@ def shard_pairs(n: int, begin: int, end: int) -> int:
     return rows * (n - 1) - rows * (rows - 1) // 2
 
 
+def tri_unit_plan(units: int, world: int, pairs_max: int = 74) -> list[list[int]]:
+    """The sharded triangle's unit ownership, from the product's host planner
+    (knn_b200_tri_unit_plan): per rank, its 256-row units in launch order."""
+    import ctypes
+
+    import numpy as np
+
+    from . import _lib
+    from .engine import raise_for_status
+
+    out = np.zeros(max(units, 1), dtype=np.uint32)
+    counts = np.zeros(world, dtype=np.uint32)
+    raise_for_status(_lib.load().knn_b200_tri_unit_plan(units, world, pairs_max, out.ctypes.data,
+                                                        counts.ctypes.data))
+    at, plan = 0, []
+    for c in counts.tolist():
+        plan.append(out[at:at + c].tolist())
+        at += c
+    return plan
+
+
 def replicate(x, src: int = 0):
     """Broadcast the reference set from `src` to every rank (in place)."""
     import torch.distributed as dist

@@ -17,7 +17,7 @@ def test_reference_arm_json_line():
     if not (ROOT / "oracle" / "_ref").exists():
         pytest.skip("oracle/_ref not built (make oracle)")
     out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--n", "3000",
-                          "--steps", "1", "--warmup", "3", "--cpu-budget", "1"],
+                          "--steps", "1", "--warmup", "3"],
                          capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]

@@ -76,3 +76,101 @@ def test_gloo_shards_assemble_the_full_answer(tmp_path, world):
         gd = np.load(tmp_path / f"dist{r}.npy")
         assert np.array_equal(gi, ri)
         assert np.array_equal(gd.view(np.uint32), rd.view(np.uint32))
+
+
+def test_tri_unit_plan_is_boustrophedon_and_snake():
+    """The product's host planner (knn_b200_tri_unit_plan): unit u belongs to
+    lane_of_row(u) (schedule.cpp:40-44), every unit exactly once, and the
+    per-rank work (sum of U - u) balanced like the reference's lanes
+    (test_schedule.cpp:169-185)."""
+    from paper_0906_0231_b200.parallel import tri_unit_plan
+    for units, world, pairs in ((3907, 8, 74), (1563, 2, 74), (38, 3, 2), (5, 8, 74), (62500, 8, 74)):
+        plan = tri_unit_plan(units, world, pairs)
+        flat = sorted(u for r in plan for u in r)
+        assert flat == list(range(units))
+        for r, lst in enumerate(plan):
+            for u in lst:
+                m = u % (2 * world)
+                assert (m if m < world else 2 * world - 1 - m) == r
+        if units >= 2 * world * 8:
+            work = [sum(units - u for u in lst) for lst in plan]
+            assert max(work) / min(work) < 1.01
+            # the snake keeps each CTA pair's share within 1% of the mean
+            for lst in plan:
+                p = min(len(lst), pairs)
+                per = [sum(units - u for u in lst[i::p]) for i in range(p)]
+                if len(lst) >= 4 * p:
+                    assert max(per) / (sum(per) / p) < 1.02
+
+
+def _tri_worker(rank, world, port, n, d, k, unit, out_dir):
+    """One rank of the sharded triangle's protocol, on CPU (gloo): own units
+    from the product planner; each unordered pair of the own rows' triangle
+    computed once (oracle fold standing in for the GPU tile); row-side
+    candidates kept, column-side candidates all-to-all'ed to the rows' owners
+    and merged there -- the reference's lane heaps + merge_row
+    (engine.cpp:27-59, merge.cpp:10-57) with GPUs as lanes."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import c_oracle
+    from paper_0906_0231_b200.parallel import tri_unit_plan
+
+    co = c_oracle()
+    x = co.generate(n, d, 123)
+    units = -(-n // unit)
+    plan = tri_unit_plan(units, world, 3)
+    owner = {u: r for r, lst in enumerate(plan) for u in lst}
+    rows = lambda u: range(u * unit, min((u + 1) * unit, n))  # noqa: E731
+    fold = lambda i, j: float(co.fold("sqeuclidean", x[max(i, j)], x[min(i, j)]))  # noqa: E731
+    cand = {i: [] for u in plan[rank] for i in rows(u)}
+    send = [[] for _ in range(world)]
+    for u in plan[rank]:
+        for i in rows(u):
+            for t in range(u, units):
+                for j in rows(t):
+                    if j == i:
+                        continue
+                    dv = fold(i, j)
+                    cand[i].append((dv, j))                   # row side
+                    if t > u:
+                        send[owner[t]].append((j, dv, i))     # column side -> row j's owner
+    # all-to-all: counts, then (row, dist, index) triples as float64 (exact)
+    sc = torch.tensor([len(s) for s in send], dtype=torch.int64)
+    rcnt = torch.empty(world, dtype=torch.int64)
+    dist.all_to_all_single(rcnt, sc)
+    flat = torch.tensor([v for s in send for e in s for v in e], dtype=torch.float64).reshape(-1)
+    recv = torch.empty(int(rcnt.sum()) * 3, dtype=torch.float64)
+    dist.all_to_all_single(recv, flat, [int(c) * 3 for c in rcnt], [int(c) * 3 for c in sc])
+    for j, dv, i in recv.reshape(-1, 3).tolist():
+        cand[int(j)].append((dv, int(i)))
+    out = {}
+    for i, lst in cand.items():
+        idx = [j for _, j in lst]
+        assert len(idx) == len(set(idx)) == n - 1, f"row {i}: pair coverage broken"  # merge.cpp:22-35
+        best = sorted(lst)[: min(k, n - 1)]
+        out[i] = best
+    np.save(os.path.join(out_dir, f"tri{rank}.npy"),
+            np.array([[i, *[j for _, j in out[i]]] for i in sorted(out)], dtype=np.int64))
+    np.save(os.path.join(out_dir, f"trid{rank}.npy"),
+            np.array([[dv for dv, _ in out[i]] for i in sorted(out)], dtype=np.float32))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_sharded_triangle_protocol(tmp_path):
+    n, d, k, unit, world = 150, 6, 5, 8, 2
+    mp.spawn(_tri_worker, args=(world, _free_port(), n, d, k, unit, str(tmp_path)), nprocs=world, join=True)
+    from oracle import c_oracle
+
+    co = c_oracle()
+    ri, rd, _ = co.brute_force(co.generate(n, d, 123), k, "sqeuclidean")
+    seen = set()
+    for r in range(world):
+        a = np.load(tmp_path / f"tri{r}.npy")
+        dd = np.load(tmp_path / f"trid{r}.npy")
+        for row, dist_row in zip(a, dd):
+            i = int(row[0])
+            seen.add(i)
+            assert np.array_equal(row[1:].astype(np.uint32), ri[i])
+            assert np.array_equal(dist_row.view(np.uint32), rd[i].view(np.uint32))
+    assert seen == set(range(n))
