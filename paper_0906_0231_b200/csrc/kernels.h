@@ -76,9 +76,6 @@ struct TensorPathResult {
 uint32_t tensor_kp_for(uint32_t klist);  // 0 = unsupported
 size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32_t row_end, uint32_t klist,
                               int sm_count);
-size_t sym_workspace_bytes(uint32_t n, int sm_count);
-cudaError_t run_sym_sweep(const uint8_t* xh, const float* alpha, const float* bmin, uint32_t n, uint32_t npad,
-                          uint32_t kc, uint64_t* cand, void* ws, int sm_count, cudaStream_t st);
 cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r);
 bool tri_eligible(uint32_t n, uint32_t d, uint32_t klist, int fold);
 

@@ -57,6 +57,7 @@ constexpr int kTriSampleKpl = 4;  // sample lists: two of 4 per row hold the 4 s
 constexpr int kTriStride = 16; // sample: every 16th sorted column (C2: 0.6% of rows to the capture pass;
                                // measured against 12/6 (0.05%): step -5 ms, tools/_knobs.sh)
 constexpr int kTriBucket = 1024;  // second order: thresholds sorted within 1024-column norm buckets
+constexpr int kLogChunk = 1024;   // column-side pool: entries per chunk
 
 // EW epilogue warps (4 or 8).  With 8, two warps share each TMEM lane
 // quadrant and split every tile's columns in halves; each half keeps its own
@@ -113,10 +114,11 @@ struct SweepParams {
     // to the columns' fixed-threshold buffers (the column side)
     const float* tc;     // [npad] column-side threshold: a row enters column j's buffer iff y' < tc[j]
     const float* tcmax;  // [npad / 32] its maximum per 32-column chunk
-    uint64_t* lkey;      // per epilogue warp: a private append log of column-side candidates,
-    uint32_t* lcol;      //   key (y', row) and column, logcap entries per warp (no atomics in the
-    uint32_t* lcnt;      //   sweep; tri_scatter_kernel bins them by column afterwards)
-    uint32_t logcap;
+    uint64_t* lkey;      // column-side candidates: key (y', row) and column, in a pool of
+    uint32_t* lcol;      //   kLogChunk-entry chunks; each epilogue warp fills its own chunk and
+    uint32_t* lcnt;      //   takes the next free one (one atomic on *lnext) when it is full;
+    uint32_t* lnext;     //   lcnt[c] = entries in chunk c (tri_scatter_kernel bins them by column)
+    uint32_t nchunks;    // pool size; *lnext > nchunks = overflow (the host redoes the call)
     // E4M3 operands (kind::f8f6f4, PAIR kernels; the triangle's sample pass):
     // xh/xa hold E4M3 planes, kc counts 128-element chunks
     int e4m3;
@@ -450,9 +452,8 @@ tensor_sweep_kernel(const SweepParams p) {
             }
         };
         uint32_t tcount = 0;
-        // TRI: this warp's column-side append log (count is warp-uniform)
-        uint32_t wlog_n = 0;
-        const size_t wlog_base = TRI ? size_t(blockIdx.x * EW + ew) * p.logcap : 0;
+        // TRI: this warp's current chunk of the column-side pool (warp-uniform)
+        uint32_t wchunk = 0xffffffffu, wfill = kLogChunk;
         // accumulator release: PAIR peers arrive on the leader's barrier
         const uint32_t tempty_rel0 = PAIR && !leader ? ptx::mapa_shared(tempty_bar(0), 0) : tempty_bar(0);
         auto release_acc = [&](uint32_t b) {
@@ -534,6 +535,15 @@ tensor_sweep_kernel(const SweepParams p) {
                                 const bool ok = cm != 0 && col0 + bpos < p.n;
                                 cm &= cm - 1;
                                 const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+                                if (wfill + __popc(bal) > uint32_t(kLogChunk)) {  // next chunk of the pool
+                                    uint32_t nc = 0;
+                                    if (lane == 0) {
+                                        if (wchunk < p.nchunks) p.lcnt[wchunk] = wfill;
+                                        nc = atomicAdd(p.lnext, 1u);
+                                    }
+                                    wchunk = __shfl_sync(0xffffffffu, nc, 0);
+                                    wfill = 0;
+                                }
                                 if (ok) {
                                     uint32_t t16[16];
 #pragma unroll
@@ -546,13 +556,14 @@ tensor_sweep_kernel(const SweepParams p) {
                                     for (int q = 0; q < 2; ++q) t16[q] = (bpos & 2) ? t16[q + 2] : t16[q];
                                     const uint32_t vb = (bpos & 1) ? t16[1] : t16[0];
                                     const float yv = __fmaf_rn(-2.0f, __uint_as_float(vb), alpha_i);
-                                    const uint32_t slot = wlog_n + __popc(bal & ((1u << lane) - 1u));
-                                    if (slot < p.logcap) {
-                                        p.lkey[wlog_base + slot] = make_key(yv, row);
-                                        p.lcol[wlog_base + slot] = col0 + bpos;
+                                    const size_t slot = size_t(wchunk) * kLogChunk + wfill +
+                                                        __popc(bal & ((1u << lane) - 1u));
+                                    if (wchunk < p.nchunks) {
+                                        p.lkey[slot] = make_key(yv, row);
+                                        p.lcol[slot] = col0 + bpos;
                                     }
                                 }
-                                wlog_n += __popc(bal);
+                                wfill += __popc(bal);
                             }
                         }
                         if (!__any_sync(0xffffffffu, fire_r)) return;
@@ -786,7 +797,7 @@ tensor_sweep_kernel(const SweepParams p) {
             }
         }
         if constexpr (TRI) {
-            if (lane == 0) p.lcnt[blockIdx.x * EW + ew] = wlog_n;
+            if (lane == 0 && wchunk < p.nchunks) p.lcnt[wchunk] = wfill;
         }
     }
     ptx::tc_fence_before();
@@ -988,19 +999,19 @@ __global__ void tri_permute_kernel(const uint32_t* __restrict__ order, uint32_t 
     }
 }
 
-// Bin the sweep's per-warp append logs by column (one block per log); a log
+// Bin the sweep's column-side pool by column (one block per chunk); a pool
 // that overflowed raises *overflow (the host then redoes the call without
 // the triangle).
 __global__ void tri_scatter_kernel(const uint64_t* __restrict__ lkey, const uint32_t* __restrict__ lcol,
-                                   const uint32_t* __restrict__ lcnt, uint32_t logcap, uint32_t* __restrict__ ccnt,
-                                   uint64_t* __restrict__ cbuf, uint32_t ccap, unsigned int* __restrict__ overflow) {
+                                   const uint32_t* __restrict__ lcnt, const uint32_t* __restrict__ lnext,
+                                   uint32_t nchunks, uint32_t* __restrict__ ccnt, uint64_t* __restrict__ cbuf,
+                                   uint32_t ccap, unsigned int* __restrict__ overflow) {
     const uint32_t w = blockIdx.x;
-    uint32_t c = lcnt[w];
-    if (c > logcap) {
-        if (threadIdx.x == 0) atomicOr(overflow, 1u);
-        c = logcap;
-    }
-    const size_t base = size_t(w) * logcap;
+    const uint32_t used = *lnext;
+    if (w == 0 && threadIdx.x == 0 && used > nchunks) atomicOr(overflow, 1u);
+    if (w >= min(used, nchunks)) return;
+    const uint32_t c = lcnt[w];
+    const size_t base = size_t(w) * kLogChunk;
     for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) {
         const uint32_t col = lcol[base + i];
         const uint32_t at = atomicAdd(ccnt + col, 1u);
@@ -1340,26 +1351,6 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         if (i < KT) keys_s[warp][i] = ak[m];
     }
     __syncwarp();
-    if constexpr (NSEG == 3) {
-        // symmetric sweep: the column-side list was seeded with copies of
-        // row-side entries -- keep the first copy of each key (the list
-        // maxima below still count every copy)
-#pragma unroll
-        for (int m = 0; m < PER; ++m) {
-            const int i = lane + 32 * m;
-            if (i >= KP || ak[m] == kEmptyKey) continue;
-            for (int j = 0; j < i; ++j)
-                if (keys_s[warp][j] == ak[m]) {
-                    ak[m] = kEmptyKey;
-                    break;
-                }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int m = 0; m < PER; ++m)
-            if (lane + 32 * m < KP) keys_s[warp][lane + 32 * m] = ak[m];
-        __syncwarp();
-    }
     __syncwarp();
 #pragma unroll
     for (int m = 0; m < PER; ++m)
@@ -1759,15 +1750,6 @@ uint32_t tensor_kp_for(uint32_t klist) {
     return c.kpl * c.nseg;
 }
 
-// Symmetric sweep (sym_path.cu): whole problems with k <= 10 and d <= 256,
-// where each tile serves its rows and its columns.  Opt-in (KNN_B200_SYM=1).
-static bool sym_selected(uint32_t n, uint32_t d, uint32_t klist, uint32_t row_begin, uint32_t row_end) {
-    const char* e = getenv("KNN_B200_SYM");
-    if (!e || atoi(e) == 0) return false;
-    // its lists: two 16-entry row-side segments and one 16-entry column-side list
-    return klist + 1 + 5 <= 16 && row_begin == 0 && row_end == n && d <= 256 && n >= 1024;
-}
-
 size_t capture_workspace_bytes(uint32_t m, uint32_t d, uint32_t cap) {
     const uint32_t mpad = (m + TS_BM - 1) / TS_BM * TS_BM;
     const uint32_t kc = (d + 63) / 64;
@@ -1798,18 +1780,17 @@ __global__ void invert_perm_kernel(const uint32_t* __restrict__ perm, uint32_t n
 }
 
 // Sort the sweep's columns by norm (KNN_B200_SORT=0 disables; cosine norms
-// are all equal already; the symmetric sweep keeps input order).  Query rows
-// stay in input order: the sweep reads them from compact gathered planes.
-static bool sort_selected(int cosine, bool sym) {
+// are all equal already).  Query rows stay in input order: the sweep reads
+// them from compact gathered planes.
+static bool sort_selected(int cosine) {
     const char* e = getenv("KNN_B200_SORT");
-    return !(e && atoi(e) == 0) && !cosine && !sym;
+    return !(e && atoi(e) == 0) && !cosine;
 }
 
 size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32_t row_end, uint32_t klist,
                               int sm_count) {
     const uint32_t rows = row_end - row_begin;
-    const bool sym = sym_selected(n, d, klist, row_begin, row_end);
-    const uint32_t kp = sym ? 48 : tensor_kp_for(klist);
+    const uint32_t kp = tensor_kp_for(klist);
     const uint32_t npad = (n + 255) / 256 * 256;
     const uint32_t kc = (d + 63) / 64;
     size_t b = 0;
@@ -1825,7 +1806,6 @@ size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32
     add(size_t(rows) * kp * 8);    // cand
     add(size_t(rows) * 4);         // fallback rows
     add(size_t(rows) * 4);         // capture thresholds
-    if (sym) add(sym_workspace_bytes(n, sm_count));
     add(sort_workspace_bytes(n));                                 // norm-sorted columns
     add(size_t(kc) * ((rows + 255) / 256 * 256) * 128);          // query rows in input order
     return b;
@@ -1932,7 +1912,6 @@ static cudaError_t launch_rescore(TensorCfg c, const RescoreParams& rp, uint32_t
         break;
     case 32: rescore_kernel<FOLD, 64, 2><<<grid, 256, 0, stream>>>(rp); break;
     case 64: rescore_kernel<FOLD, 64, 1><<<grid, 256, 0, stream>>>(rp); break;
-    case 48: rescore_kernel<FOLD, 48, 3><<<grid, 256, 0, stream>>>(rp); break;  // symmetric: R0 | R1 | C
     default: rescore_kernel<FOLD, 128, 1><<<grid, 256, 0, stream>>>(rp); break;
     }
     return cudaGetLastError();
@@ -2028,7 +2007,7 @@ bool tri_eligible(uint32_t n, uint32_t d, uint32_t klist, int fold) {
     if (te && strcmp(te, "0") == 0) return false;
     const bool force = te && strcmp(te, "force") == 0;
     const TensorCfg cfg = tensor_cfg(klist);
-    return fold != kCosine && sort_selected(0, false) && cfg.kpl == 12 && cfg.nseg == 2 &&
+    return fold != kCosine && sort_selected(0) && cfg.kpl == 12 && cfg.nseg == 2 &&
            (d + 63) / 64 <= uint32_t(TS_MAX_RES_KC) && (force ? n >= 512 : n >= 393216);
 }
 
@@ -2042,9 +2021,8 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
     const uint32_t n = a.n, d = a.d, nrows = a.row_end - a.row_begin;
     const uint32_t npad = (n + 255) / 256 * 256;
     const uint32_t kc = (d + 63) / 64;
-    const bool sym = sym_selected(n, d, a.klist, a.row_begin, a.row_end);
-    const TensorCfg cfg = sym ? TensorCfg{48, 3} : tensor_cfg(a.klist);
-    const uint32_t kp = sym ? 48 : cfg.kpl * cfg.nseg;
+    const TensorCfg cfg = tensor_cfg(a.klist);
+    const uint32_t kp = cfg.kpl * cfg.nseg;
     const int cosine = a.fold == kCosine;
     uint8_t* w = static_cast<uint8_t*>(a.workspace);
     auto take = [&](size_t x) {
@@ -2063,8 +2041,7 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
     uint64_t* cand = reinterpret_cast<uint64_t*>(take(size_t(nrows) * kp * 8));
     uint32_t* fb_rows = reinterpret_cast<uint32_t*>(take(size_t(nrows) * 4));
     float* fb_thr = reinterpret_cast<float*>(take(size_t(nrows) * 4));
-    void* sym_ws = sym ? take(sym_workspace_bytes(n, a.sm_count)) : nullptr;
-    const bool sorted = sort_selected(cosine, sym);
+    const bool sorted = sort_selected(cosine);
     float* skey = reinterpret_cast<float*>(take(size_t(n) * 4));
     float* skey2 = reinterpret_cast<float*>(take(size_t(n) * 4));
     uint32_t* sidx = reinterpret_cast<uint32_t*>(take(size_t(n) * 4));
@@ -2133,7 +2110,7 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
     // pair's own, offering each pair to the row side (register lists) and to
     // the column side (fixed-threshold append buffers), and the rescore merges
     // both with a bound for each.
-    const bool tri = allow_tri && a.row_begin == 0 && a.row_end == n && !sym && tri_eligible(n, d, a.klist, a.fold);
+    const bool tri = allow_tri && a.row_begin == 0 && a.row_end == n && tri_eligible(n, d, a.klist, a.fold);
     uint64_t* tri_cbuf = nullptr;
     uint32_t* tri_ccnt = nullptr;
     float* tri_tc = nullptr;
@@ -2186,16 +2163,18 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         add(size_t(npad) * 8 * 2);            // rho2, xnorm2
         add(size_t(n) * 4);                   // perm2
         add(size_t(npad / 32) * 4);           // bmin2
-        // per-epilogue-warp append logs, 4x the expected column-side volume
-        // (C2: ~63M entries = 1/4 of the capacity; an overflow redoes the call)
+        // the column-side pool: 4x the expected volume (C2: ~63M entries =
+        // 1/4 of the capacity; an overflow redoes the call) plus a partial
+        // chunk per epilogue warp
         const uint32_t npairs = (n + 255) / 256;
         const uint32_t gpairs = npairs < uint32_t(a.sm_count / 2) ? npairs : uint32_t(a.sm_count / 2);
-        const uint32_t nlogs = 2 * gpairs * 8;
-        const char* lce = getenv("KNN_B200_TRI_LOGCAP");  // testing: force the overflow fallback
-        const uint32_t logcap = lce ? uint32_t(atoi(lce)) : uint32_t(uint64_t(4) * n * 64 / nlogs + 4096);
-        add(size_t(nlogs) * logcap * 8);      // log keys
-        add(size_t(nlogs) * logcap * 4);      // log columns
-        add(size_t(nlogs) * 4);               // log counts
+        const uint32_t nwarps = 2 * gpairs * 8;
+        const char* lce = getenv("KNN_B200_TRI_LOGCAP");  // testing: pool entries (forces the overflow fallback)
+        const uint64_t pool = lce ? uint64_t(atoi(lce)) : uint64_t(4) * n * 64 + uint64_t(nwarps) * kLogChunk;
+        const uint32_t nchunks = uint32_t((pool + kLogChunk - 1) / kLogChunk);
+        add(size_t(nchunks) * kLogChunk * 8);  // pool keys
+        add(size_t(nchunks) * kLogChunk * 4);  // pool columns
+        add(size_t(nchunks) * 4 + 4);          // chunk counts + next free chunk
         uint8_t* w3 = static_cast<uint8_t*>(a.alloc2(a.alloc2_ctx, need));
         if (!w3) return cudaErrorMemoryAllocation;
         auto take3 = [&](size_t x) {
@@ -2229,9 +2208,10 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         tri_xnorm = reinterpret_cast<double*>(take3(size_t(npad) * 8));
         tri_perm = reinterpret_cast<uint32_t*>(take3(size_t(n) * 4));
         float* bmin2 = reinterpret_cast<float*>(take3(size_t(npad / 32) * 4));
-        uint64_t* lkey = reinterpret_cast<uint64_t*>(take3(size_t(nlogs) * logcap * 8));
-        uint32_t* lcol = reinterpret_cast<uint32_t*>(take3(size_t(nlogs) * logcap * 4));
-        uint32_t* lcnt = reinterpret_cast<uint32_t*>(take3(size_t(nlogs) * 4));
+        uint64_t* lkey = reinterpret_cast<uint64_t*>(take3(size_t(nchunks) * kLogChunk * 8));
+        uint32_t* lcol = reinterpret_cast<uint32_t*>(take3(size_t(nchunks) * kLogChunk * 4));
+        uint32_t* lcnt = reinterpret_cast<uint32_t*>(take3(size_t(nchunks) * 4 + 4));
+        uint32_t* lnext = lcnt + nchunks;
         iota_stride_kernel<<<a.sm_count, 256, 0, st>>>(srows, sm, stride);
         if (f8) e4m3_planes_kernel<<<a.sm_count * 8, 256, 0, st>>>(xh, npad, kc, skc, x8);
         const uint8_t* xrows = f8 ? x8 : xh;
@@ -2264,17 +2244,15 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         chunk_min_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(tri_alpha, npad / 32, bmin2);
         chunk_max_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(tri_tc, npad / 32, tcmax);
         if ((e = cudaMemsetAsync(tri_ccnt, 0, size_t(npad) * 4, st)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(lnext, 0, 4, st)) != cudaSuccess) return e;
         // the triangle sweep: rows are the (re-ordered) set itself
         SweepParams tp{xq_planes, tri_alpha, n,    npad,    kc, 0, n, group_tiles, dbg ? atoi(dbg) : 0,
                        cand,      xq_planes, npad, nullptr, nullptr, nullptr, 0, bmin2,
-                       tri_tc, tcmax, lkey, lcol, lcnt, logcap};
+                       tri_tc, tcmax, lkey, lcol, lcnt, lnext, nchunks};
         if ((e = launch_sweep_pair<12, 256, 8, true>(tp, n, st)) != cudaSuccess) return e;
-        tri_scatter_kernel<<<nlogs, 256, 0, st>>>(lkey, lcol, lcnt, logcap, tri_ccnt, tri_cbuf, kTriCap,
+        tri_scatter_kernel<<<nchunks, 256, 0, st>>>(lkey, lcol, lcnt, lnext, nchunks, tri_ccnt, tri_cbuf, kTriCap,
                                                   reinterpret_cast<unsigned int*>(scal + 40));
         launches += f8 ? 14 : 13;
-    } else if (sym) {
-        if ((e = run_sym_sweep(xh, alpha, bmin, n, npad, kc, cand, sym_ws, a.sm_count, st)) != cudaSuccess) return e;
-        launches += 3;
     } else {
         // CTA pairs (default; KNN_B200_PAIR=0 disables) need whole 256-row
         // pairs of blocks inside the padded planes.  At C2 they halve the

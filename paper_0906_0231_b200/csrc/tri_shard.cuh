@@ -81,20 +81,19 @@ void tri_unit_plan(uint32_t U, uint32_t G, uint32_t pairs_max, uint32_t* units, 
 
 // ---- kernels -----------------------------------------------------------------
 
-// Count the column-side log entries per owner rank (one block per warp log).
+// Count the column-side pool entries per owner rank (one block per chunk).
 __global__ void tri_bin_count_kernel(const uint32_t* __restrict__ lcol, const uint32_t* __restrict__ lcnt,
-                                     uint32_t logcap, const uint32_t* __restrict__ unit_owner, uint32_t G,
+                                     const uint32_t* __restrict__ lnext, uint32_t nchunks,
+                                     const uint32_t* __restrict__ unit_owner, uint32_t G,
                                      unsigned long long* __restrict__ cnt, unsigned int* __restrict__ overflow) {
     __shared__ uint32_t h[kTriMaxWorld];
+    const uint32_t w = blockIdx.x, used = *lnext;
+    if (w == 0 && threadIdx.x == 0 && used > nchunks) atomicOr(overflow, 1u);
+    if (w >= min(used, nchunks)) return;
     for (uint32_t i = threadIdx.x; i < G; i += blockDim.x) h[i] = 0;
     __syncthreads();
-    const uint32_t w = blockIdx.x;
-    uint32_t c = lcnt[w];
-    if (c > logcap) {
-        if (threadIdx.x == 0) atomicOr(overflow, 1u);
-        c = logcap;
-    }
-    const size_t base = size_t(w) * logcap;
+    const uint32_t c = lcnt[w];
+    const size_t base = size_t(w) * kLogChunk;
     for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) atomicAdd(&h[unit_owner[lcol[base + i] >> 8]], 1u);
     __syncthreads();
     for (uint32_t o = threadIdx.x; o < G; o += blockDim.x)
@@ -119,18 +118,19 @@ __global__ void tri_seg_offsets_kernel(const unsigned long long* __restrict__ cn
 // owner's unit list).  Block-local ranges are reserved with one atomic per
 // owner, entries placed with shared-memory atomics.
 __global__ void tri_bin_place_kernel(const uint64_t* __restrict__ lkey, const uint32_t* __restrict__ lcol,
-                                     const uint32_t* __restrict__ lcnt, uint32_t logcap,
-                                     const uint32_t* __restrict__ unit_owner, const uint32_t* __restrict__ unit_lidx,
-                                     uint32_t G, const unsigned long long* __restrict__ off,
-                                     unsigned long long* __restrict__ cur, uint64_t* __restrict__ skey,
-                                     uint32_t* __restrict__ sslot) {
+                                     const uint32_t* __restrict__ lcnt, const uint32_t* __restrict__ lnext,
+                                     uint32_t nchunks, const uint32_t* __restrict__ unit_owner,
+                                     const uint32_t* __restrict__ unit_lidx, uint32_t G,
+                                     const unsigned long long* __restrict__ off, unsigned long long* __restrict__ cur,
+                                     uint64_t* __restrict__ skey, uint32_t* __restrict__ sslot) {
     __shared__ uint32_t h[kTriMaxWorld];
     __shared__ unsigned long long b[kTriMaxWorld];
+    const uint32_t w = blockIdx.x;
+    if (w >= min(*lnext, nchunks)) return;
     for (uint32_t i = threadIdx.x; i < G; i += blockDim.x) h[i] = 0;
     __syncthreads();
-    const uint32_t w = blockIdx.x;
-    const uint32_t c = min(lcnt[w], logcap);
-    const size_t base = size_t(w) * logcap;
+    const uint32_t c = lcnt[w];
+    const size_t base = size_t(w) * kLogChunk;
     for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) atomicAdd(&h[unit_owner[lcol[base + i] >> 8]], 1u);
     __syncthreads();
     for (uint32_t o = threadIdx.x; o < G; o += blockDim.x) {
@@ -267,10 +267,10 @@ struct TriRank {
     unsigned long long *scnt = nullptr, *soff = nullptr, *scur = nullptr;  // [G]
     uint32_t* fb_rows = nullptr;
     float* fb_thr = nullptr;
-    // logs (scratch, phase B)
+    // column-side pool (scratch, phase B)
     uint64_t* lkey = nullptr;
-    uint32_t *lcol = nullptr, *lcnt = nullptr;
-    uint32_t logcap = 0, nlogs = 0;
+    uint32_t *lcol = nullptr, *lcnt = nullptr, *lnext = nullptr;
+    uint32_t nchunks = 0;
     // send segments (by owner) and received entries
     uint64_t* skey = nullptr;
     uint32_t* sslot = nullptr;
@@ -429,32 +429,21 @@ static cudaError_t tri_sweep(TriShared& S, TriRank& R, const TensorPathArgs& a, 
     cudaStream_t st = a.stream;
     cudaError_t e;
     const uint32_t pairs = std::max<uint32_t>(1, std::min<uint32_t>(R.nu, uint32_t(a.sm_count / 2)));
-    R.nlogs = 2 * pairs * 8;
-    // logs: 4x the expected column-side volume (~64 entries per row, spread
-    // over the triangle's pairs) of the busiest CTA pair's 16 warp logs --
-    // with few units per pair their work differs
-    // with few units per pair their work differs.  A unit's column-side
-    // volume lies between "proportional to its pairs" and "the same for every
-    // unit" (a column's candidates come from rows near it in the norm order,
-    // i.e. from the units just below it): size for the larger of the two.
+    // the column-side pool: 4x this rank's expected volume (~64 entries per
+    // row over the whole triangle).  A unit's share lies between "in
+    // proportion to its pairs" and "the same for every unit" (a column's
+    // candidates come from rows near it in the norm order): take the larger.
+    double share_w = 0;
+    for (uint32_t u : S.units_h[R.rank]) share_w += double(S.U - u);
     const double total = double(S.U) * (S.U + 1) / 2;
-    double busiest = 0;
-    const std::vector<uint32_t>& lst = S.units_h[R.rank];
-    for (uint32_t p0 = 0; p0 < pairs; ++p0) {
-        double w = 0, c = 0;
-        for (size_t i = p0; i < lst.size(); i += pairs) {
-            w += double(S.U - lst[i]);
-            c += 1;
-        }
-        busiest = std::max(busiest, std::max(total > 0 ? w / total : 1.0, c / double(S.U)));
-    }
-    const double per_log = double(S.n) * 64.0 * busiest / 16.0;
-    R.logcap = uint32_t(std::min<double>(4.0 * per_log + 4096.0, double(0xffffffffu / 2)));
-    if (const char* lce = getenv("KNN_B200_TRI_LOGCAP")) R.logcap = uint32_t(atoi(lce));
+    const double share = std::max(total > 0 ? share_w / total : 1.0, double(R.nu) / double(S.U));
+    uint64_t pool = uint64_t(4.0 * double(S.n) * 64.0 * share) + uint64_t(2 * pairs * 8) * kLogChunk;
+    if (const char* lce = getenv("KNN_B200_TRI_LOGCAP")) pool = uint64_t(atoi(lce));
+    R.nchunks = uint32_t((pool + kLogChunk - 1) / kLogChunk);
     auto lay = [&](Carve& c) {
-        R.lkey = c.take<uint64_t>(size_t(R.nlogs) * R.logcap);
-        R.lcol = c.take<uint32_t>(size_t(R.nlogs) * R.logcap);
-        R.lcnt = c.take<uint32_t>(R.nlogs);
+        R.lkey = c.take<uint64_t>(size_t(R.nchunks) * kLogChunk);
+        R.lcol = c.take<uint32_t>(size_t(R.nchunks) * kLogChunk);
+        R.lcnt = c.take<uint32_t>(size_t(R.nchunks) + 1);
     };
     Carve c;
     lay(c);
@@ -462,20 +451,22 @@ static cudaError_t tri_sweep(TriShared& S, TriRank& R, const TensorPathArgs& a, 
     if (!c.base) return cudaErrorMemoryAllocation;
     c.off = 0;
     lay(c);
+    R.lnext = R.lcnt + R.nchunks;
+    if ((e = cudaMemsetAsync(R.lnext, 0, 4, st)) != cudaSuccess) return e;
     if (R.nu == 0) {
         std::fill(R.scnt_h.begin(), R.scnt_h.end(), 0ull);
-        return cudaMemsetAsync(R.lcnt, 0, size_t(R.nlogs) * 4, st);
+        return cudaSuccess;
     }
     const char* dbg = getenv("KNN_B200_DEBUG_SWEEP");
     SweepParams tp{S.xq2, S.tri_alpha, S.n,    S.npad,  S.kc, 0, S.n, S.group_tiles, dbg ? atoi(dbg) : 0,
                    R.cand, S.xq2,      S.npad, nullptr, nullptr, nullptr, 0, S.bmin2,
-                   S.tri_tc, S.tcmax,  R.lkey, R.lcol,  R.lcnt, R.logcap};
+                   S.tri_tc, S.tcmax,  R.lkey, R.lcol,  R.lcnt, R.lnext, R.nchunks};
     tp.units = R.units;
     tp.nunits = R.nu;
     if ((e = launch_sweep_pair<12, 256, 8, true>(tp, R.nslots, st)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(R.scnt, 0, size_t(S.G) * 8, st)) != cudaSuccess) return e;
-    tri_bin_count_kernel<<<R.nlogs, 256, 0, st>>>(R.lcol, R.lcnt, R.logcap, S.unit_owner, S.G, R.scnt,
-                                                  reinterpret_cast<unsigned int*>(R.scal + 40));
+    tri_bin_count_kernel<<<R.nchunks, 256, 0, st>>>(R.lcol, R.lcnt, R.lnext, R.nchunks, S.unit_owner, S.G, R.scnt,
+                                                    reinterpret_cast<unsigned int*>(R.scal + 40));
     tri_seg_offsets_kernel<<<1, 32, 0, st>>>(R.scnt, S.G, R.soff, R.scur);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     unsigned long long* h = static_cast<unsigned long long*>(a.host_scratch);  // 64 B pinned: G <= 8 counts
@@ -511,8 +502,8 @@ static cudaError_t tri_bin(TriShared& S, TriRank& R, const TensorPathArgs& a, Sh
     R.skey = c.take<uint64_t>(total + 1);
     R.sslot = c.take<uint32_t>(total + 1);
     if (R.nu == 0) return cudaSuccess;
-    tri_bin_place_kernel<<<R.nlogs, 256, 0, a.stream>>>(R.lkey, R.lcol, R.lcnt, R.logcap, S.unit_owner, S.unit_lidx,
-                                                        S.G, R.soff, R.scur, R.skey, R.sslot);
+    tri_bin_place_kernel<<<R.nchunks, 256, 0, a.stream>>>(R.lkey, R.lcol, R.lcnt, R.lnext, R.nchunks, S.unit_owner,
+                                                          S.unit_lidx, S.G, R.soff, R.scur, R.skey, R.sslot);
     return cudaGetLastError();
 }
 

@@ -221,26 +221,6 @@ def test_full_size_c2_sampled_rows(ctx, c_oracle, arith, monkeypatch):
         assert st["fallback_rows"] < n // 100
 
 
-@pytest.mark.parametrize("n,d,k,m", [(1100, 33, 1, "sqeuclidean"), (2048, 64, 10, "hellinger"),
-                                     (4096, 256, 10, "euclidean"), (5000, 100, 5, "cosine"),
-                                     (3000, 17, 3, "sqeuclidean"), (1500, 1, 10, "sqeuclidean")])
-def test_symmetric_sweep_opt_in(ctx, c_oracle, monkeypatch, n, d, k, m):
-    """The experimental symmetric sweep (KNN_B200_SYM=1, csrc/sym_path.cu):
-    each upper-triangle tile serves its rows and its columns.  Same bar."""
-    from oracle import normalize_rows
-    monkeypatch.setenv("KNN_B200_SYM", "1")
-    x = c_oracle.generate(n, d, 1234 + n)
-    if m == "cosine":
-        x = normalize_rows(x)
-    om = "sqeuclidean" if m == "euclidean" else m
-    ri, rd, _ = c_oracle.brute_force(x, k, om)
-    if m == "euclidean":
-        rd = np.sqrt(rd)
-    idx, dist, st = ctx.solve(x, k, metric_obj(m), arith_id("tensor"))
-    assert st["kernel_launches"] >= 3
-    assert_lists_bit_equal(idx, dist, ri, rd, f"sym n={n} d={d} k={k} {m}")
-
-
 @pytest.mark.parametrize("n,d,k,m", [(400000, 48, 7, "sqeuclidean"), (393216, 32, 1, "hellinger"),
                                      (450001, 100, 10, "euclidean"), (420000, 33, 3, "sqeuclidean")])
 def test_triangle_sweep_sampled_rows(ctx, c_oracle, n, d, k, m):
