@@ -186,6 +186,14 @@ KNN_B200_API int knn_b200_solve_multi_f64(const float *host_vectors, uint32_t n,
  * in one process (knn_b200_solve_multi) or one process per GPU (these calls
  * under torchrun / MPI). */
 
+/* Test hook: dev_out (m x n fp32) = the tensor core's dot products of the
+ * fp16 rows dev_a_f16 (m x d) and dev_b_f16 (n x d), row-major, computed with
+ * the sweep's own instruction (tcgen05.mma kind::f16, FP32 accumulation in
+ * TMEM).  Measures the accumulation error the TENSOR policy's proof bounds
+ * (DESIGN.md §4). */
+KNN_B200_API int knn_b200_debug_tc_dots(knn_b200_ctx *ctx, const void *dev_a_f16, uint32_t m, const void *dev_b_f16,
+                                        uint32_t n, uint32_t d, float *dev_out, void *stream);
+
 /* Host-only (no device needed): the sharded triangle's ownership of the
  * `units` 256-row units of the second column order.  Unit u goes to rank
  * lane_of_row(u) (schedule.cpp:40-44, boustrophedon over `world` ranks); a

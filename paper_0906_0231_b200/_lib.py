@@ -25,6 +25,7 @@ EXPORTS = (
     "knn_b200_solve",
     "knn_b200_solve_f64",
     "knn_b200_solve_multi_f64",
+    "knn_b200_debug_tc_dots",
     "knn_b200_tri_unit_plan",
     "knn_b200_comm_unique_id",
     "knn_b200_comm_init",
@@ -110,6 +111,8 @@ def load() -> ctypes.CDLL:
             ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)]
         lib.knn_b200_generate_device.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
                                                  ctypes.c_uint64, ctypes.c_void_p]
+        lib.knn_b200_debug_tc_dots.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p,
+                                               ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p]
         lib.knn_b200_tri_unit_plan.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
                                                ctypes.c_void_p]
         lib.knn_b200_comm_unique_id.argtypes = [ctypes.c_void_p]

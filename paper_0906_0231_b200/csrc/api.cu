@@ -337,6 +337,8 @@ void validate_device(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, 
     }
 }
 
+void* shard_alloc(void* c, int slot, size_t bytes);
+
 // Validation + staging + the row-shard sweep, all enqueued on `stream`.
 void solve_rows_core(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, uint32_t k, int metric,
                      int arith, uint32_t row_begin, uint32_t row_end, uint32_t* out_index, float* out_dist,
@@ -401,6 +403,8 @@ void solve_rows_core(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, 
             }
         };
         ta.alloc2_ctx = ctx;
+        ta.shard_alloc = shard_alloc;
+        ta.shard_ctx = ctx;
         knnb::TensorPathResult tr;
         cuda_check(knnb::run_tensor_path(ta, tr), "tensor path");
         ctr.launches += tr.launches;
@@ -801,6 +805,16 @@ int knn_b200_solve_rows_device(knn_b200_ctx* ctx, const float* dev_vectors, uint
             stats->sweep_ms = elapsed_ms(ctx->ev[4], ctx->ev[5]);
             stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         }
+    });
+}
+
+int knn_b200_debug_tc_dots(knn_b200_ctx* ctx, const void* dev_a_f16, uint32_t m, const void* dev_b_f16, uint32_t n,
+                           uint32_t d, float* dev_out, void* stream) {
+    return guarded([&] {
+        if (!ctx) fail(KNN_B200_ERR_CONFIG, "null context");
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        cuda_check(knnb::launch_tc_dots(dev_a_f16, m, dev_b_f16, n, d, dev_out, static_cast<cudaStream_t>(stream)),
+                   "tc dots launch");
     });
 }
 

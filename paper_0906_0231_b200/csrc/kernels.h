@@ -66,6 +66,9 @@ struct TensorPathArgs {
     // host once the number of unproven rows is known
     void* (*alloc2)(void* ctx, size_t bytes);
     void* alloc2_ctx;
+    // grow-only device memory by slot (the threshold triangle; null: not available)
+    void* (*shard_alloc)(void* ctx, int slot, size_t bytes);
+    void* shard_ctx;
 };
 struct TensorPathResult {
     unsigned long long rescored = 0;
@@ -78,6 +81,11 @@ size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32
                               int sm_count);
 cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r);
 bool tri_eligible(uint32_t n, uint32_t d, uint32_t klist, int fold);
+
+// tc_probe.cu: out (m x n, fp32) = the tensor core's dots of fp16 rows
+// (row-major m x d and n x d), with the sweep's MMA instruction.
+cudaError_t launch_tc_dots(const void* a_f16, uint32_t m, const void* b_f16, uint32_t n, uint32_t d, float* out,
+                           cudaStream_t stream);
 
 // The triangle sweep sharded over `world` ranks (tri_shard.cuh).
 // alloc(ctx, slot, bytes): grow-only device memory per slot.  a.row_begin = 0,

@@ -161,12 +161,16 @@ __global__ void remap_capture_kernel(uint64_t* __restrict__ buf, const uint32_t*
 // come from HBM once per group instead of once per row block.  The per-row
 // candidate lists are written to `cand` at the end of each item and read
 // back when the row block's next group starts.
-template <int KPL, int BN, bool ARES, int EW, bool CAPTURE, bool PAIR = false, bool TRI = false>
+// TCAP (with TRI): the threshold triangle -- both sides of every pair go to
+// the pool against fixed per-row thresholds p.tc (no lists); the rows' pool
+// entries are then rescored exactly like the band-capture pass.
+template <int KPL, int BN, bool ARES, int EW, bool CAPTURE, bool PAIR = false, bool TRI = false, bool TCAP = false>
 __global__ void __launch_bounds__(TSLayout<KPL, BN, ARES, EW, PAIR>::THREADS, 1)
 tensor_sweep_kernel(const SweepParams p) {
     using L = TSLayout<KPL, BN, ARES, EW, PAIR>;
-    static_assert(!PAIR || (ARES && !CAPTURE), "CTA pairs: resident A, no capture");
+    static_assert(!PAIR || !CAPTURE, "CTA pairs: no capture");
     static_assert(!TRI || (PAIR && BN == 256 && KPL <= 16), "triangle mode: CTA pairs, 256-column tiles");
+    static_assert(!TCAP || TRI, "threshold mode is a triangle mode");
     constexpr int S = L::STAGES;
     constexpr int NSEG = L::NSEG;
     constexpr int SEG_COLS = BN / NSEG;  // columns of a tile one epilogue warp filters
@@ -306,9 +310,11 @@ tensor_sweep_kernel(const SweepParams p) {
                     const uint32_t u = unit_id(lu);
                     const uint32_t ts = max(t0, tri_start(u));
                     if (ts >= t1) continue;
-                    wait(afull_bar, a_phase);
-                    a_phase ^= 1;
-                    ptx::mbar_arrive_remote_relaxed(lead_afull);
+                    if constexpr (ARES) {
+                        wait(afull_bar, a_phase);
+                        a_phase ^= 1;
+                        ptx::mbar_arrive_remote_relaxed(lead_afull);
+                    }
                     for (uint32_t t = ts; t < t1; ++t)
                         for (uint32_t kc = 0; kc < p.kc; ++kc) {
                             wait(full_bar(stage), phase);
@@ -485,6 +491,8 @@ tensor_sweep_kernel(const SweepParams p) {
                     cap_slot = row - p.row_begin;
                     // fixed threshold: admit y <= cap_thr (strict < against its successor)
                     thr = ListMax{valid ? nextafterf(p.cap_thr[cap_slot], kInf) : -kInf, 0};
+                } else if constexpr (TCAP) {
+                    thr = ListMax{valid ? __ldg(p.tc + row) : -kInf, 0};  // fixed: the row's threshold
                 } else if constexpr (REGLIST) {
 #pragma unroll
                     for (int s = 0; s < KPL; ++s) {
@@ -514,57 +522,83 @@ tensor_sweep_kernel(const SweepParams p) {
                 if (!valid) thr.a = -kInf;  // padding rows admit nothing
                 // After a chunk's vote: the column side's appends (TRI), then the
                 // row side's rare path.
-                auto handle = [&](const uint32_t (&v)[W], uint32_t col0, bool fire_r, bool fire_c, float hc) {
+                // Warp-aggregated appends to the pool: every lane walks its mask
+                // m of the chunk's columns; entry (key, dest) -- the column side:
+                // (y', row) for column col; the threshold triangle's row side:
+                // (col) for this row.  Slots come from a ballot prefix (no
+                // atomics but one per pool chunk); a select tree picks each dot.
+                auto append = [&](uint32_t m, const uint32_t (&v)[W], uint32_t col0, bool rowside) {
+                    while (__any_sync(0xffffffffu, m != 0)) {
+                        const int bpos = m ? __ffs(m) - 1 : 0;
+                        const bool ok = m != 0 && col0 + bpos < p.n;
+                        m &= m - 1;
+                        const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+                        if (wfill + __popc(bal) > uint32_t(kLogChunk)) {  // next chunk of the pool
+                            uint32_t nc = 0;
+                            if (lane == 0) {
+                                if (wchunk < p.nchunks) p.lcnt[wchunk] = wfill;
+                                nc = atomicAdd(p.lnext, 1u);
+                            }
+                            wchunk = __shfl_sync(0xffffffffu, nc, 0);
+                            wfill = 0;
+                        }
+                        if (ok) {
+                            const size_t slot = size_t(wchunk) * kLogChunk + wfill + __popc(bal & ((1u << lane) - 1u));
+                            uint64_t key;
+                            if (rowside) {
+                                key = col0 + bpos;  // the capture rescore reads the index only
+                            } else {
+                                uint32_t t16[16];
+#pragma unroll
+                                for (int q = 0; q < 16; ++q) t16[q] = (bpos & 16) ? v[q + 16] : v[q];
+#pragma unroll
+                                for (int q = 0; q < 8; ++q) t16[q] = (bpos & 8) ? t16[q + 8] : t16[q];
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) t16[q] = (bpos & 4) ? t16[q + 4] : t16[q];
+#pragma unroll
+                                for (int q = 0; q < 2; ++q) t16[q] = (bpos & 2) ? t16[q + 2] : t16[q];
+                                const uint32_t vb = (bpos & 1) ? t16[1] : t16[0];
+                                key = make_key(__fmaf_rn(-2.0f, __uint_as_float(vb), alpha_i), row);
+                            }
+                            if (wchunk < p.nchunks) {
+                                p.lkey[slot] = key;
+                                p.lcol[slot] = rowside ? row : col0 + bpos;
+                            }
+                        }
+                        wfill += __popc(bal);
+                    }
+                };
+                // After a chunk's vote: the column side's appends (TRI), then the
+                // row side's rare path (TCAP: appends as well).
+                auto handle = [&](const uint32_t (&v)[W], uint32_t col0, bool fire_r, bool fire_c, float hc,
+                                  float hr) {
                     constexpr int P = W / 2;  // column pairs
                     float bt[W];              // the chunk's column norms
                     if constexpr (TRI) {
                         if (__any_sync(0xffffffffu, fire_c)) {
                             // admitted columns: dot > hc, a superset of y' < the chunk's
-                            // largest threshold (the rescore filters the few extra), then
-                            // warp-aggregated appends to this warp's private log: slots
-                            // from a ballot prefix, no atomic round trip (a select tree
-                            // picks each dot)
+                            // largest threshold (the rescore filters the few extra)
                             uint32_t cm = 0;
                             if (fire_c) {
 #pragma unroll
                                 for (int j = 0; j < W; ++j)
                                     if (__uint_as_float(v[j]) > hc) cm |= 1u << j;
                             }
-                            while (__any_sync(0xffffffffu, cm != 0)) {
-                                const int bpos = cm ? __ffs(cm) - 1 : 0;
-                                const bool ok = cm != 0 && col0 + bpos < p.n;
-                                cm &= cm - 1;
-                                const uint32_t bal = __ballot_sync(0xffffffffu, ok);
-                                if (wfill + __popc(bal) > uint32_t(kLogChunk)) {  // next chunk of the pool
-                                    uint32_t nc = 0;
-                                    if (lane == 0) {
-                                        if (wchunk < p.nchunks) p.lcnt[wchunk] = wfill;
-                                        nc = atomicAdd(p.lnext, 1u);
-                                    }
-                                    wchunk = __shfl_sync(0xffffffffu, nc, 0);
-                                    wfill = 0;
+                            append(cm, v, col0, false);
+                        }
+                        if constexpr (TCAP) {
+                            // row side against the fixed threshold: dot > hr, a
+                            // superset of y < thr (the capture rescore filters)
+                            if (__any_sync(0xffffffffu, fire_r)) {
+                                uint32_t rm = 0;
+                                if (fire_r) {
+#pragma unroll
+                                    for (int j = 0; j < W; ++j)
+                                        if (__uint_as_float(v[j]) > hr) rm |= 1u << j;
                                 }
-                                if (ok) {
-                                    uint32_t t16[16];
-#pragma unroll
-                                    for (int q = 0; q < 16; ++q) t16[q] = (bpos & 16) ? v[q + 16] : v[q];
-#pragma unroll
-                                    for (int q = 0; q < 8; ++q) t16[q] = (bpos & 8) ? t16[q + 8] : t16[q];
-#pragma unroll
-                                    for (int q = 0; q < 4; ++q) t16[q] = (bpos & 4) ? t16[q + 4] : t16[q];
-#pragma unroll
-                                    for (int q = 0; q < 2; ++q) t16[q] = (bpos & 2) ? t16[q + 2] : t16[q];
-                                    const uint32_t vb = (bpos & 1) ? t16[1] : t16[0];
-                                    const float yv = __fmaf_rn(-2.0f, __uint_as_float(vb), alpha_i);
-                                    const size_t slot = size_t(wchunk) * kLogChunk + wfill +
-                                                        __popc(bal & ((1u << lane) - 1u));
-                                    if (wchunk < p.nchunks) {
-                                        p.lkey[slot] = make_key(yv, row);
-                                        p.lcol[slot] = col0 + bpos;
-                                    }
-                                }
-                                wfill += __popc(bal);
+                                append(rm, v, col0, true);
                             }
+                            return;
                         }
                         if (!__any_sync(0xffffffffu, fire_r)) return;
                     }
@@ -669,7 +703,8 @@ tensor_sweep_kernel(const SweepParams p) {
                         }
                     }
                     const float dmax = vmax(v);
-                    const bool fire_r = dmax > row_bound(__ldg(p.bmin + (col0 >> 5)));
+                    const float hr1 = row_bound(__ldg(p.bmin + (col0 >> 5)));
+                    const bool fire_r = dmax > hr1;
                     bool fire_c = false;
                     float hc = kInf;
                     if constexpr (TRI) {
@@ -679,7 +714,7 @@ tensor_sweep_kernel(const SweepParams p) {
                         }
                     }
                     if (!__any_sync(0xffffffffu, fire_r || fire_c) || p.debug_mode == 4) return;
-                    handle(v, col0, fire_r, fire_c, hc);
+                    handle(v, col0, fire_r, fire_c, hc, hr1);
                 };
                 for (uint32_t t = ts; t < t1; ++t, ++tcount) {
                     const uint32_t b = tcount & 1, use = tcount >> 1;
@@ -776,11 +811,11 @@ tensor_sweep_kernel(const SweepParams p) {
                         const bool ra = da > ha, rb = db > hb;
                         const bool fa = TRI && da > ca, fb = TRI && db > cb;
                         if (!__any_sync(0xffffffffu, ra || rb || fa || fb) || p.debug_mode == 4) continue;
-                        if (__any_sync(0xffffffffu, ra || fa)) handle(va, cbase + c0, ra, fa, ca);
-                        if (__any_sync(0xffffffffu, rb || fb)) handle(vb, cbase + c0 + 32, rb, fb, cb);
+                        if (__any_sync(0xffffffffu, ra || fa)) handle(va, cbase + c0, ra, fa, ca, ha);
+                        if (__any_sync(0xffffffffu, rb || fb)) handle(vb, cbase + c0 + 32, rb, fb, cb, hb);
                     }
                 }
-                if (valid && !CAPTURE) {
+                if (valid && !CAPTURE && !TCAP) {
                     for (int s = 0; s < KPL; ++s) {
                         float a;
                         uint32_t col;
@@ -1624,6 +1659,13 @@ struct Rescore2Params {
     const double* xnorm;
     const unsigned long long* gmax;
     const unsigned int* maxabs;
+    // retry mode (the threshold triangle): a row without a proof goes to
+    // fb2_rows with retry_thr = the threshold that would prove it --
+    // proof_bound of the k-th exact distance among its candidates, or loose[q]
+    // when it has fewer than k -- for a second capture pass (null: no retry,
+    // fb2_rows go to the EXACT kernel)
+    float* retry_thr;
+    const float* loose;
 };
 
 // Exact fold of every captured column of an unproven row (one warp per row);
@@ -1638,11 +1680,21 @@ __global__ void __launch_bounds__(128) rescore_capture_kernel(const Rescore2Para
     if (slot >= p.m) return;
     const uint32_t qo = p.rows[slot];  // input order
     uint64_t* ks = keys2 + size_t(warp) * p.cap;
-    const uint32_t c = p.cnt[slot];
-    if (c > p.cap) {
-        if (lane == 0) p.fb2_rows[atomicAdd(p.fb2_count, 1u)] = qo;
+    const uint32_t q = p.rowpos ? p.rowpos[qo] : qo;
+    const uint32_t cnt_all = p.cnt[slot];
+    const bool over = cnt_all > p.cap;  // lost candidates: no proof from this buffer
+    auto retry = [&](double thr2) {
+        if (lane == 0) {
+            const uint32_t at = atomicAdd(p.fb2_count, 1u);
+            p.fb2_rows[at] = qo;
+            if (p.retry_thr) p.retry_thr[at] = __double2float_ru(thr2);
+        }
+    };
+    if (over && !p.retry_thr) {
+        retry(0);
         return;
     }
+    const uint32_t c = over ? p.cap : cnt_all;
     const float* xq = p.X + size_t(qo) * p.d;
     const bool vec = (p.d % 4 == 0);
     const uint64_t* in = p.buf + size_t(slot) * p.cap;
@@ -1661,8 +1713,8 @@ __global__ void __launch_bounds__(128) rescore_capture_kernel(const Rescore2Para
     for (int o = 16; o; o >>= 1) valid += __shfl_xor_sync(0xffffffffu, valid, o);
     __syncwarp();
     if (lane == 0) atomicAdd(p.rescored, (unsigned long long)valid);
-    if (valid < p.klist) {  // cannot happen for a correct band; stay exact
-        if (lane == 0) p.fb2_rows[atomicAdd(p.fb2_count, 1u)] = qo;
+    if (valid < p.klist) {  // a proven band has >= k; a threshold guessed too low may not
+        retry(p.loose ? double(p.loose[q]) : 0.0);
         return;
     }
     // keys are unique (distinct columns) except the empty self slot: the
@@ -1683,12 +1735,11 @@ __global__ void __launch_bounds__(128) rescore_capture_kernel(const Rescore2Para
     // every true neighbor has y <= proof_bound(kth) - alpha_q: the band is
     // complete when that is inside its threshold (always, for thresholds the
     // rescore derived from a k-th distance; not always for a looser one)
-    const uint32_t q = p.rowpos ? p.rowpos[qo] : qo;
     const double alpha_q = double(p.alpha[q]);
     const double need = proof_bound<FOLD>(p.d, p.maxabs, p.gmax, p.xnorm[q], p.rho[q], alpha_q,
                                           double(ordered_to_float(uint32_t(kth >> 32)))) - alpha_q;
-    if (!(need <= double(p.thr[slot]))) {
-        if (lane == 0) p.fb2_rows[atomicAdd(p.fb2_count, 1u)] = qo;
+    if (over || !(need <= double(p.thr[slot]))) {
+        retry(need);
         return;
     }
     const size_t orow = size_t(qo - p.row_begin);
@@ -1811,11 +1862,12 @@ size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32
     return b;
 }
 
-// CTA-pair sweep (cluster of 2): one pair per two SMs, persistent.
-template <int KPL, int BN, int EW, bool TRI = false>
+// CTA-pair sweep (cluster of 2): one pair per two SMs, persistent.  ARES =
+// false streams the query rows with every reference chunk (d > 256).
+template <int KPL, int BN, int EW, bool TRI = false, bool TCAP = false, bool ARES = true>
 static cudaError_t launch_sweep_pair(const SweepParams& sp, uint32_t nrows, cudaStream_t stream) {
-    using L = TSLayout<KPL, BN, true, EW, true>;
-    auto kern = tensor_sweep_kernel<KPL, BN, true, EW, false, true, TRI>;
+    using L = TSLayout<KPL, BN, ARES, EW, true>;
+    auto kern = tensor_sweep_kernel<KPL, BN, ARES, EW, false, true, TRI, TCAP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::SMEM));
     if (e != cudaSuccess) return e;
     const uint32_t npairs = (nrows + 2 * TS_BM - 1) / (2 * TS_BM);
@@ -2011,7 +2063,18 @@ bool tri_eligible(uint32_t n, uint32_t d, uint32_t klist, int fold) {
            (d + 63) / 64 <= uint32_t(TS_MAX_RES_KC) && (force ? n >= 512 : n >= 393216);
 }
 
+bool tcap_eligible(uint32_t n, uint32_t d, uint32_t klist);
+cudaError_t run_tcap(const TensorPathArgs& a, void* (*alloc)(void*, int, size_t), void* actx, TensorPathResult& r,
+                     bool* overflow);
+
 cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
+    // whole problems with 10 < k <= 128: the threshold triangle (tri_shard.cuh)
+    if (a.row_begin == 0 && a.row_end == a.n && a.shard_alloc && tcap_eligible(a.n, a.d, a.klist)) {
+        bool overflow = false;
+        const cudaError_t e = run_tcap(a, a.shard_alloc, a.shard_ctx, r, &overflow);
+        if (e != cudaSuccess || !overflow) return e;
+        r = TensorPathResult{};  // the pool overflowed (pathological data): the rectangular sweep
+    }
     return run_tensor_path_impl(a, r, true);
 }
 

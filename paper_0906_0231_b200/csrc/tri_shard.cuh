@@ -159,6 +159,59 @@ __global__ void tri_scatter_flat_kernel(const uint64_t* __restrict__ rkey, const
     }
 }
 
+// The threshold triangle's per-row capture thresholds (y space) from the fp16
+// sample lists: T ~ the row's k-th distance is estimated by the rank-r
+// smallest y over the sample columns (r set so that the sample's r-th
+// exceeds the true k-th with high probability), and the threshold admits its
+// proof band twice over: thr = proof_bound(proof_bound(T)) - alpha.  Any
+// value is correct -- the capture rescore proves each row or retries it.
+// loose: the sample lists' largest y (a retry threshold for rows left with
+// fewer than k candidates).
+struct TcapThrArgs {
+    const uint64_t* cand;  // rows [j0, j1): 2 x 16 sample keys each
+    uint32_t n, j0, j1, kp, r, d;
+    const float* alpha;
+    const double* rho;
+    const double* xnorm;
+    const unsigned long long* gmax;
+    const unsigned int* maxabs;
+    float* thr;
+    float* loose;
+};
+
+template <int FOLD>
+__global__ void tcap_threshold_kernel(const TcapThrArgs t) {
+    for (uint32_t j = t.j0 + blockIdx.x * blockDim.x + threadIdx.x; j < t.j1; j += gridDim.x * blockDim.x) {
+        float thr = -__int_as_float(0x7f800000), lo = thr;
+        if (j < t.n) {
+            const uint64_t* c = t.cand + size_t(j - t.j0) * t.kp;
+            uint64_t kth = kEmptyKey, last = 0;
+            for (uint32_t a = 0; a < t.kp; ++a) {
+                uint32_t below = 0;
+                for (uint32_t b = 0; b < t.kp; ++b) below += c[b] < c[a];
+                if (below == t.r - 1) kth = c[a];
+                if (c[a] != kEmptyKey && c[a] > last) last = c[a];
+            }
+            const double al = double(t.alpha[j]);
+            const int e = scale_exponent(*t.maxabs);
+            // A space: s^2 D (sqeuclidean), 2 s^2 D (cosine: 2 s^2 (1 - cos))
+            const double s2 = (FOLD == kCosine ? 2.0 : 1.0) * ldexp(1.0, 2 * e);
+            if (kth == kEmptyKey) {
+                thr = __int_as_float(0x7f800000);  // fewer than r sampled columns: admit everything
+            } else {
+                const double y = double(ordered_to_float(uint32_t(kth >> 32)));
+                const double b1 = proof_bound<FOLD>(t.d, t.maxabs, t.gmax, t.xnorm[j], t.rho[j], al,
+                                                    fmax((al + y) / s2, 0.0));
+                const double b2 = proof_bound<FOLD>(t.d, t.maxabs, t.gmax, t.xnorm[j], t.rho[j], al, b1 / s2);
+                thr = __double2float_ru(b2 - al);
+            }
+            lo = last == 0 ? thr : fmaxf(thr, ordered_to_float(uint32_t(last >> 32)));
+        }
+        t.thr[j] = thr;
+        t.loose[j] = lo;
+    }
+}
+
 // ---- state ----------------------------------------------------------------
 
 // Bump allocation inside one block; base == null only measures.
@@ -182,6 +235,8 @@ static inline int rank_slot(uint32_t rank, int which) { return kSlotRank0 + 4 * 
 // Replicated state: identical on every rank (same input, same kernels).
 struct TriShared {
     uint32_t n = 0, npad = 0, d = 0, kc = 0, U = 0, G = 1, S = 0;  // S: rows per all-gather slice
+    bool tcap = false;    // the threshold triangle (k > 10, any d, cosine too): fp16 sample, 2 x 16 lists
+    bool cosine = false;  // no norm order (every norm is 1): identity permutation
     uint32_t stride = kTriStride, skpl = kTriSampleKpl, trank = kTriRank, sm = 0, spad = 0, skc = 0;
     bool f8 = true;
     float dscale = 1.0f;
@@ -287,8 +342,20 @@ struct TriRank {
 
 // Replicated prep: norm order, fp16 planes + per-row terms, E4M3 planes, the
 // sample columns; unit tables.  Fills S (allocating kSlotShared).
-static cudaError_t tri_prep(TriShared& S, const TensorPathArgs& a, uint32_t G, ShardAllocFn alloc, void* actx) {
+static cudaError_t tri_prep(TriShared& S, const TensorPathArgs& a, uint32_t G, ShardAllocFn alloc, void* actx,
+                            bool tcap = false) {
     const uint32_t n = a.n, d = a.d;
+    S.tcap = tcap;
+    S.cosine = a.fold == kCosine;
+    if (tcap) {
+        // the sample pass estimates each row's k-th distance: fp16 (an E4M3
+        // dot is too coarse for that), 2 x 16-entry lists, the rank-r value
+        // with r ~ k / stride + 2.5 sqrt(k / stride) + 1 (tcap_threshold_kernel)
+        S.f8 = false;
+        S.skpl = 16;
+        const double m = double(a.klist) / S.stride;
+        S.trank = uint32_t(std::min(32.0, std::ceil(m + 2.5 * std::sqrt(m) + 1.0)));
+    }
     S.n = n;
     S.d = d;
     S.npad = (n + 255) / 256 * 256;
@@ -296,11 +363,16 @@ static cudaError_t tri_prep(TriShared& S, const TensorPathArgs& a, uint32_t G, S
     S.U = S.npad / 256;
     S.G = G;
     S.S = (S.U + G - 1) / G * 256;
-    if (const char* se = getenv("KNN_B200_TRI_STRIDE")) S.stride = uint32_t(atoi(se));
-    if (const char* ke = getenv("KNN_B200_TRI_SAMPLE_KPL")) S.skpl = atoi(ke) == 12 ? 12u : atoi(ke) == 6 ? 6u : S.skpl;
-    if (const char* re = getenv("KNN_B200_TRI_RANK")) S.trank = uint32_t(atoi(re));
-    S.trank = S.trank < 1 ? 1 : (S.trank > S.skpl ? S.skpl : S.trank);
-    if (const char* fe = getenv("KNN_B200_TRI_E4M3")) S.f8 = atoi(fe) != 0;
+    if (!tcap) {
+        if (const char* se = getenv("KNN_B200_TRI_STRIDE")) S.stride = uint32_t(atoi(se));
+        if (const char* ke = getenv("KNN_B200_TRI_SAMPLE_KPL"))
+            S.skpl = atoi(ke) == 12 ? 12u : atoi(ke) == 6 ? 6u : S.skpl;
+        if (const char* re = getenv("KNN_B200_TRI_RANK")) S.trank = uint32_t(atoi(re));
+        S.trank = S.trank < 1 ? 1 : (S.trank > S.skpl ? S.skpl : S.trank);
+        if (const char* fe = getenv("KNN_B200_TRI_E4M3")) S.f8 = atoi(fe) != 0;
+    } else if (const char* re = getenv("KNN_B200_TCAP_RANK")) {
+        S.trank = std::max(1u, std::min(2 * S.skpl, uint32_t(atoi(re))));
+    }
     S.skc = S.f8 ? (S.kc + 1) / 2 : S.kc;
     S.sm = (n + S.stride - 1) / S.stride;
     S.spad = (S.sm + 255) / 256 * 256;
@@ -334,16 +406,24 @@ static cudaError_t tri_prep(TriShared& S, const TensorPathArgs& a, uint32_t G, S
     if ((e = cudaMemcpyAsync(S.unit_lidx, lidx.data(), S.U * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(S.scal, 0, 64, st)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(S.muacc, 0, size_t(d) * 8, st)) != cudaSuccess) return e;
-    colsum_kernel<<<a.sm_count * 4, 256, 0, st>>>(a.X, n, d, S.muacc);
-    mu_finalize_kernel<<<(d + 255) / 256, 256, 0, st>>>(S.muacc, n, d, S.mu);
-    maxabs_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, uint64_t(n) * d, d, S.mu, S.maxabs);
-    row_key_kernel<<<(n * 32 + 255) / 256, 256, 0, st>>>(a.X, n, d, S.mu, S.skey, S.sidx);
-    if ((e = cub::DeviceRadixSort::SortPairs(S.stemp, S.stemp_bytes, S.skey, S.skey2, S.sidx, S.perm, int(n), 0, 32,
-                                             st)) != cudaSuccess)
-        return e;
-    invert_perm_kernel<<<a.sm_count * 4, 256, 0, st>>>(S.perm, n, S.rowpos);
+    if (S.cosine) {  // mu = 0, every norm the same: input order
+        if ((e = cudaMemsetAsync(S.mu, 0, size_t(d) * 4, st)) != cudaSuccess) return e;
+        iota_stride_kernel<<<a.sm_count, 256, 0, st>>>(S.perm, n, 1);
+        iota_stride_kernel<<<a.sm_count, 256, 0, st>>>(S.rowpos, n, 1);
+        maxabs_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, uint64_t(n) * d, d, S.mu, S.maxabs);
+    } else {
+        colsum_kernel<<<a.sm_count * 4, 256, 0, st>>>(a.X, n, d, S.muacc);
+        mu_finalize_kernel<<<(d + 255) / 256, 256, 0, st>>>(S.muacc, n, d, S.mu);
+        maxabs_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, uint64_t(n) * d, d, S.mu, S.maxabs);
+        row_key_kernel<<<(n * 32 + 255) / 256, 256, 0, st>>>(a.X, n, d, S.mu, S.skey, S.sidx);
+        if ((e = cub::DeviceRadixSort::SortPairs(S.stemp, S.stemp_bytes, S.skey, S.skey2, S.sidx, S.perm, int(n), 0,
+                                                 32, st)) != cudaSuccess)
+            return e;
+        invert_perm_kernel<<<a.sm_count * 4, 256, 0, st>>>(S.perm, n, S.rowpos);
+    }
     PrepOut po{S.xh, S.alpha, S.rho, S.xnorm, S.gmax};
-    prep_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, n, d, S.npad, S.kc, S.mu, S.maxabs, 0, S.perm, po);
+    prep_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, n, d, S.npad, S.kc, S.mu, S.maxabs, S.cosine ? 1 : 0, S.perm,
+                                                  po);
     chunk_min_kernel<<<(S.npad / 32 * 32 + 255) / 256, 256, 0, st>>>(S.alpha, S.npad / 32, S.bmin);
     iota_stride_kernel<<<a.sm_count, 256, 0, st>>>(S.srows, S.sm, S.stride);
     if (S.f8) e4m3_planes_kernel<<<a.sm_count * 8, 256, 0, st>>>(S.xh, S.npad, S.kc, S.skc, S.x8);
@@ -396,12 +476,23 @@ static cudaError_t tri_sample(TriShared& S, TriRank& R, const TensorPathArgs& a)
     SweepParams ss{S.xs,     S.alpha_s, S.sm,  S.spad, S.skc,   R.s0, std::min(R.s1, S.n), S.gts, 0,
                    R.cand_s, S.f8 ? S.x8 : S.xh, S.npad, nullptr, nullptr, nullptr, 0, S.bmin_s};
     ss.e4m3 = S.f8;
-    cudaError_t e = S.skpl == 12  ? launch_sweep_pair<12, 256, 8>(ss, R.s1 - R.s0, st)
-                    : S.skpl == 6 ? launch_sweep_pair<6, 256, 8>(ss, R.s1 - R.s0, st)
-                                  : launch_sweep_pair<kTriSampleKpl, 256, 8>(ss, R.s1 - R.s0, st);
+    const uint32_t rows = R.s1 - R.s0;
+    const bool ares = S.skc <= uint32_t(TS_MAX_RES_KC);
+    cudaError_t e = S.skpl == 16 ? (ares ? launch_sweep_pair<16, 256, 8>(ss, rows, st)
+                                         : launch_sweep_pair<16, 256, 8, false, false, false>(ss, rows, st))
+                    : S.skpl == 12 ? launch_sweep_pair<12, 256, 8>(ss, rows, st)
+                    : S.skpl == 6  ? launch_sweep_pair<6, 256, 8>(ss, rows, st)
+                                   : launch_sweep_pair<kTriSampleKpl, 256, 8>(ss, rows, st);
     if (e != cudaSuccess) return e;
-    tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(R.cand_s, S.n, R.s0, R.s1, 2 * S.skpl, S.trank,
-                                                          1.0f / S.dscale, S.tc2, S.tl1);
+    if (S.tcap) {
+        const TcapThrArgs ta{R.cand_s, S.n, R.s0, R.s1, 2 * S.skpl, S.trank, S.d, S.alpha, S.rho, S.xnorm,
+                             S.gmax, S.maxabs, S.tc2, S.tl1};
+        if (S.cosine) tcap_threshold_kernel<kCosine><<<a.sm_count * 4, 256, 0, st>>>(ta);
+        else tcap_threshold_kernel<kSqEuclidean><<<a.sm_count * 4, 256, 0, st>>>(ta);
+    } else {
+        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(R.cand_s, S.n, R.s0, R.s1, 2 * S.skpl, S.trank,
+                                                              1.0f / S.dscale, S.tc2, S.tl1);
+    }
     return cudaGetLastError();
 }
 
@@ -753,6 +844,111 @@ cudaError_t run_tri_nccl(const TensorPathArgs& a, ncclComm_t comm, uint32_t rank
     r = R.res;
     r.launches += 26;
     return cudaSuccess;
+}
+
+// ---- the threshold triangle (one GPU) ---------------------------------------
+
+// Whole problems with 10 < min(k, n-1) <= 128 (and past the size crossover):
+// every unordered pair once, both endpoints against fixed thresholds from an
+// fp16 sample pass (no lists), each row's captured candidates rescored
+// exactly with the band-capture proof; rows it cannot prove get a second
+// capture pass with the threshold their candidates imply.
+bool tcap_eligible(uint32_t n, uint32_t d, uint32_t klist) {
+    const char* te = getenv("KNN_B200_TCAP");
+    if (te && strcmp(te, "0") == 0) return false;
+    const bool force = te && strcmp(te, "force") == 0;
+    (void)d;
+    return klist > 10 && klist <= 128 && (force ? n >= 512 : n >= 262144);
+}
+
+static uint32_t tcap_cap(uint32_t klist) { return klist <= 47 ? 512u : 1024u; }
+
+cudaError_t run_tcap(const TensorPathArgs& a, ShardAllocFn alloc, void* actx, TensorPathResult& r, bool* overflow) {
+    cudaStream_t st = a.stream;
+    cudaError_t e;
+    TriShared S;
+    TriRank R;
+    if ((e = tri_prep(S, a, 1, alloc, actx, true)) != cudaSuccess) return e;
+    if ((e = tri_rank_init(S, R, 0, a, alloc, actx)) != cudaSuccess) return e;
+    if ((e = tri_sample(S, R, a)) != cudaSuccess) return e;
+    if ((e = tri_order(S, a)) != cudaSuccess) return e;
+    const uint32_t n = S.n, npad = S.npad, cap = tcap_cap(a.klist);
+    const uint32_t pairs = std::max<uint32_t>(1, std::min<uint32_t>(R.nu, uint32_t(a.sm_count / 2)));
+    // pool: ~ (r x stride) captured entries per row plus the proof band, 2.5x
+    uint64_t pool = uint64_t(2.5 * double(n) * (double(S.trank) * S.stride + 64.0)) + uint64_t(2 * pairs * 8) * kLogChunk;
+    if (const char* lce = getenv("KNN_B200_TRI_LOGCAP")) pool = uint64_t(atoi(lce));
+    const uint32_t nchunks = uint32_t((pool + kLogChunk - 1) / kLogChunk);
+    uint64_t *lkey, *cbuf;
+    uint32_t *lcol, *lcnt, *ccnt, *rowpos2, *fb_rows, *fb_count;
+    float* fb_thr;
+    auto lay = [&](Carve& c) {
+        lkey = c.take<uint64_t>(size_t(nchunks) * kLogChunk);
+        lcol = c.take<uint32_t>(size_t(nchunks) * kLogChunk);
+        lcnt = c.take<uint32_t>(size_t(nchunks) + 1);
+        cbuf = c.take<uint64_t>(size_t(npad) * cap);
+        ccnt = c.take<uint32_t>(npad);
+        rowpos2 = c.take<uint32_t>(n);
+        fb_rows = c.take<uint32_t>(n);
+        fb_thr = c.take<float>(n);
+        fb_count = c.take<uint32_t>(16);
+    };
+    Carve c;
+    lay(c);
+    c.base = static_cast<uint8_t*>(alloc(actx, kSlotScratch, c.off));
+    if (!c.base) return cudaErrorMemoryAllocation;
+    c.off = 0;
+    lay(c);
+    uint32_t* lnext = lcnt + nchunks;
+    if ((e = cudaMemsetAsync(lnext, 0, 4, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(ccnt, 0, size_t(npad) * 4, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(fb_count, 0, 64, st)) != cudaSuccess) return e;
+    const char* dbg = getenv("KNN_B200_DEBUG_SWEEP");
+    SweepParams tp{S.xq2, S.tri_alpha, n,      npad,    S.kc, 0,       n, S.group_tiles, dbg ? atoi(dbg) : 0,
+                   nullptr, S.xq2,     npad,   nullptr, nullptr, nullptr, 0, S.bmin2,
+                   S.tri_tc, S.tcmax,  lkey,   lcol,    lcnt,  lnext,  nchunks};
+    tp.units = R.units;
+    tp.nunits = R.nu;
+    if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
+    e = S.kc <= uint32_t(TS_MAX_RES_KC) ? launch_sweep_pair<2, 256, 8, true, true, true>(tp, R.nslots, st)
+                                        : launch_sweep_pair<2, 256, 8, true, true, false>(tp, R.nslots, st);
+    if (e != cudaSuccess) return e;
+    tri_scatter_kernel<<<nchunks, 256, 0, st>>>(lkey, lcol, lcnt, lnext, nchunks, ccnt, cbuf, cap,
+                                                reinterpret_cast<unsigned int*>(R.scal + 40));
+    if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
+    remap_capture_kernel<<<n, 128, 0, st>>>(cbuf, ccnt, n, cap, S.tri_perm);
+    invert_perm_kernel<<<a.sm_count * 4, 256, 0, st>>>(S.tri_perm, n, rowpos2);
+    unsigned long long* rescored = reinterpret_cast<unsigned long long*>(R.scal + 32);
+    Rescore2Params r2{a.X,  n,   a.d,        a.klist,     0,          S.tri_perm, n,        ccnt,
+                      cbuf, cap, a.out_sqrt, a.out_index, a.out_dist, fb_count,   fb_rows,  rescored,
+                      S.tri_tc, rowpos2, S.tri_alpha, S.tri_rho, S.tri_xnorm, S.gmax, S.maxabs};
+    r2.retry_thr = fb_thr;
+    r2.loose = S.tri_tl;
+    const size_t smem2 = size_t(4) * cap * 8;
+    if (a.fold == kCosine) {
+        cudaFuncSetAttribute(rescore_capture_kernel<kCosine>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+        rescore_capture_kernel<kCosine><<<(n + 3) / 4, 128, smem2, st>>>(r2);
+    } else {
+        cudaFuncSetAttribute(rescore_capture_kernel<kSqEuclidean>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem2));
+        rescore_capture_kernel<kSqEuclidean><<<(n + 3) / 4, 128, smem2, st>>>(r2);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    uint32_t* h = static_cast<uint32_t*>(a.host_scratch);
+    if ((e = cudaMemcpyAsync(h, fb_count, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(h + 2, R.scal + 40, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(h + 4, rescored, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    const uint32_t nretry = h[0];
+    *overflow = h[2] != 0;
+    r.rescored = *reinterpret_cast<const unsigned long long*>(h + 4);
+    r.fallback_rows = nretry;
+    r.launches += 30;
+    if (*overflow || nretry == 0) return cudaSuccess;
+    // second capture pass: the retried rows against their implied thresholds
+    const CaptureArgs ca{S.xh, S.alpha, S.rho, S.xnorm, S.gmax, S.maxabs, S.bmin, S.cosine ? nullptr : S.perm,
+                         S.cosine ? nullptr : S.rowpos, n, npad, S.kc, S.group_tiles, cap, fb_rows, fb_thr,
+                         rescored};
+    return run_capture(a, ca, nretry, r, r.launches);
 }
 
 }  // namespace knnb

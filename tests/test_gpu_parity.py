@@ -385,3 +385,48 @@ def test_device_api_empty_shard_and_stream_switch(ctx, c_oracle):
     bad = torch.empty((10, 8), dtype=torch.int32, device="cuda")
     with pytest.raises(ConfigError):
         solve_rows_torch(ctx, xt, 8, squared_euclidean(), 0, 6000, out=(bad, bad.float()))
+
+
+@pytest.mark.parametrize("n,d,k,m", [(20000, 48, 30, "sqeuclidean"), (9000, 300, 100, "euclidean"),
+                                     (12000, 64, 20, "cosine"), (5000, 20, 64, "hellinger"),
+                                     (3000, 1024, 11, "sqeuclidean")])
+def test_threshold_triangle_forced_all_rows(ctx, c_oracle, monkeypatch, n, d, k, m):
+    """The threshold triangle (k > 10: each pair once, both endpoints against
+    fixed thresholds, capture rescore; KNN_B200_TCAP=force below its size
+    gate), every row against the oracle -- resident (d <= 256) and streamed
+    query rows (d > 256), cosine without the norm order."""
+    import torch
+    from oracle import normalize_rows
+    from paper_0906_0231_b200 import solve_rows_torch
+    monkeypatch.setenv("KNN_B200_TCAP", "force")
+    xh = c_oracle.generate(n, d, n + k)
+    if m == "cosine":
+        xh = normalize_rows(xh)
+    om = "sqeuclidean" if m == "euclidean" else m
+    ri, rd = c_oracle.rows_topk(xh, k, om, np.arange(n, dtype=np.uint32))
+    if m == "euclidean":
+        rd = np.sqrt(rd)
+    x = torch.from_numpy(np.ascontiguousarray(xh)).cuda()
+    idx, dist, st = solve_rows_torch(ctx, x, k, metric_obj(m), 0, n, arith_id("tensor"), want_stats=True)
+    assert_lists_bit_equal(idx.cpu().numpy().view(np.uint32), dist.cpu().numpy(), ri, rd,
+                           f"threshold triangle n={n} d={d} k={k} {m}")
+    assert st["fallback_rows"] < n  # most rows proven by the first pass
+
+
+def test_threshold_triangle_retry_and_overflow_paths(ctx, c_oracle, monkeypatch):
+    """Thresholds forced far too low (every row retried through the second
+    capture pass) and a pool forced to overflow (the rectangular sweep redoes
+    the call): the same bits either way."""
+    import torch
+    from paper_0906_0231_b200 import solve_rows_torch
+    monkeypatch.setenv("KNN_B200_TCAP", "force")
+    n, d, k = 8000, 40, 25
+    xh = c_oracle.generate(n, d, 77)
+    ri, rd = c_oracle.rows_topk(xh, k, "sqeuclidean", np.arange(n, dtype=np.uint32))
+    x = torch.from_numpy(xh).cuda()
+    for env, val in (("KNN_B200_TCAP_RANK", "1"), ("KNN_B200_TRI_LOGCAP", "4096")):
+        monkeypatch.setenv(env, val)
+        idx, dist, st = solve_rows_torch(ctx, x, k, metric_obj("sqeuclidean"), 0, n, arith_id("tensor"),
+                                         want_stats=True)
+        assert_lists_bit_equal(idx.cpu().numpy().view(np.uint32), dist.cpu().numpy(), ri, rd, f"{env}={val}")
+        monkeypatch.delenv(env)
