@@ -502,9 +502,14 @@ knnb::TensorPathArgs tri_args(knn_b200_ctx* ctx, const float* Xs, uint32_t n, ui
     return ta;
 }
 
-bool tri_selected(uint32_t n, uint32_t d, uint32_t klist, int metric, int arith) {
-    return arith != KNN_B200_ARITH_EXACT && klist <= knnb::kExactMaxK && knnb::tensor_kp_for(klist) != 0 &&
-           knnb::tri_eligible(n, d, klist, metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean);
+// Which triangle a whole problem takes: 0 none, 1 the list triangle (k <= 10),
+// 2 the threshold triangle (10 < k <= 128).
+int tri_selected(uint32_t n, uint32_t d, uint32_t klist, int metric, int arith) {
+    if (arith == KNN_B200_ARITH_EXACT || klist > knnb::kExactMaxK) return 0;
+    if (knnb::tensor_kp_for(klist) != 0 &&
+        knnb::tri_eligible(n, d, klist, metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean))
+        return 1;
+    return knnb::tcap_eligible(n, d, klist) ? 2 : 0;
 }
 
 // Rows of rank `rank` of `world`: [R rank, R (rank + 1)) clipped to n, R = ceil(n / world).
@@ -531,7 +536,8 @@ void solve_sharded_core(knn_b200_ctx* ctx, ncclComm_t comm, int rank, int world,
     uint32_t r0, r1;
     shard_rows(n, rank, world, r0, r1);
     const uint32_t klist = std::min(k, n - 1);
-    if (!tri_selected(n, d, klist, metric, arith)) {
+    const int mode = tri_selected(n, d, klist, metric, arith);
+    if (!mode) {
         solve_rows_core(ctx, X, n, d, k, metric, arith, r0, r1, out_index, out_dist, stream, ctr);
         return;
     }
@@ -552,7 +558,8 @@ void solve_sharded_core(knn_b200_ctx* ctx, ncclComm_t comm, int rank, int world,
     knnb::TensorPathArgs ta = tri_args(ctx, Xs, n, d, klist, metric, fi, fd, stream);
     knnb::TensorPathResult tr;
     bool overflow = false;
-    cuda_check(knnb::run_tri_nccl(ta, comm, uint32_t(rank), uint32_t(world), shard_alloc, ctx, tr, &overflow),
+    cuda_check(knnb::run_tri_nccl(ta, comm, uint32_t(rank), uint32_t(world), shard_alloc, ctx, tr, &overflow,
+                                  mode == 2),
                "sharded triangle");
     ctr.arith_used = KNN_B200_ARITH_TENSOR;
     ctr.launches += tr.launches;
@@ -904,8 +911,9 @@ int knn_b200_debug_solve_sharded_loopback(knn_b200_ctx* ctx, const float* dev_ve
         check_args(n, d, k, metric, KNN_B200_ARITH_TENSOR);
         if (world < 1 || world > int(knnb::kTriMaxWorld)) fail(KNN_B200_ERR_CONFIG, "bad world " + std::to_string(world));
         const uint32_t klist = std::min(k, n - 1);
-        if (!tri_selected(n, d, klist, metric, KNN_B200_ARITH_TENSOR))
-            fail(KNN_B200_ERR_CONFIG, "problem does not take the triangle sweep (see tri_eligible)");
+        const int mode = tri_selected(n, d, klist, metric, KNN_B200_ARITH_TENSOR);
+        if (!mode)
+            fail(KNN_B200_ERR_CONFIG, "problem does not take a triangle sweep (see tri_eligible, tcap_eligible)");
         std::lock_guard<std::mutex> lock(ctx->mu);
         const auto t0 = std::chrono::steady_clock::now();
         cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
@@ -924,7 +932,7 @@ int knn_b200_debug_solve_sharded_loopback(knn_b200_ctx* ctx, const float* dev_ve
         knnb::TensorPathResult tr;
         bool overflow = false;
         cuda_check(knnb::run_tri_loopback(ta, uint32_t(world), shard_alloc, ctx, tr, rank_ms,
-                                          reinterpret_cast<unsigned long long*>(rank_xbytes), &overflow),
+                                          reinterpret_cast<unsigned long long*>(rank_xbytes), &overflow, mode == 2),
                    "sharded triangle (loopback)");
         ctr.arith_used = KNN_B200_ARITH_TENSOR;
         ctr.launches += tr.launches;

@@ -97,12 +97,15 @@ constexpr uint32_t kTriMaxWorld = 64;
 // Unit ownership (host): rank r's units are units[sum(counts[<r]) ...], in the
 // order its CTA pairs take them.
 void tri_unit_plan(uint32_t U, uint32_t world, uint32_t pairs_max, uint32_t* units, uint32_t* counts);
+// tcap: the threshold triangle (10 < k <= 128) instead of the list triangle (k <= 10).
+bool tcap_eligible(uint32_t n, uint32_t d, uint32_t klist);
 cudaError_t run_tri_loopback(const TensorPathArgs& a, uint32_t world, ShardAlloc alloc, void* actx,
-                             TensorPathResult& r, float* rank_ms, unsigned long long* xbytes, bool* overflow);
+                             TensorPathResult& r, float* rank_ms, unsigned long long* xbytes, bool* overflow,
+                             bool tcap);
 }  // namespace knnb
 typedef struct ncclComm* ncclComm_t;
 namespace knnb {
 cudaError_t run_tri_nccl(const TensorPathArgs& a, ncclComm_t comm, uint32_t rank, uint32_t world, ShardAlloc alloc,
-                         void* actx, TensorPathResult& r, bool* overflow);
+                         void* actx, TensorPathResult& r, bool* overflow, bool tcap);
 
 }  // namespace knnb

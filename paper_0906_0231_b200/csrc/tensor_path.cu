@@ -544,22 +544,20 @@ tensor_sweep_kernel(const SweepParams p) {
                         }
                         if (ok) {
                             const size_t slot = size_t(wchunk) * kLogChunk + wfill + __popc(bal & ((1u << lane) - 1u));
-                            uint64_t key;
-                            if (rowside) {
-                                key = col0 + bpos;  // the capture rescore reads the index only
-                            } else {
-                                uint32_t t16[16];
+                            uint32_t t16[16];
 #pragma unroll
-                                for (int q = 0; q < 16; ++q) t16[q] = (bpos & 16) ? v[q + 16] : v[q];
+                            for (int q = 0; q < 16; ++q) t16[q] = (bpos & 16) ? v[q + 16] : v[q];
 #pragma unroll
-                                for (int q = 0; q < 8; ++q) t16[q] = (bpos & 8) ? t16[q + 8] : t16[q];
+                            for (int q = 0; q < 8; ++q) t16[q] = (bpos & 8) ? t16[q + 8] : t16[q];
 #pragma unroll
-                                for (int q = 0; q < 4; ++q) t16[q] = (bpos & 4) ? t16[q + 4] : t16[q];
+                            for (int q = 0; q < 4; ++q) t16[q] = (bpos & 4) ? t16[q + 4] : t16[q];
 #pragma unroll
-                                for (int q = 0; q < 2; ++q) t16[q] = (bpos & 2) ? t16[q + 2] : t16[q];
-                                const uint32_t vb = (bpos & 1) ? t16[1] : t16[0];
-                                key = make_key(__fmaf_rn(-2.0f, __uint_as_float(vb), alpha_i), row);
-                            }
+                            for (int q = 0; q < 2; ++q) t16[q] = (bpos & 2) ? t16[q + 2] : t16[q];
+                            const float dot = __uint_as_float((bpos & 1) ? t16[1] : t16[0]);
+                            // key: (y relative to the destination row, the other endpoint)
+                            const uint64_t key =
+                                rowside ? make_key(__fmaf_rn(-2.0f, dot, __ldg(p.alpha + col0 + bpos)), col0 + bpos)
+                                        : make_key(__fmaf_rn(-2.0f, dot, alpha_i), row);
                             if (wchunk < p.nchunks) {
                                 p.lkey[slot] = key;
                                 p.lcol[slot] = rowside ? row : col0 + bpos;
@@ -1668,18 +1666,39 @@ struct Rescore2Params {
     const float* loose;
 };
 
-// Exact fold of every captured column of an unproven row (one warp per row);
-// the captured band contains every true neighbor by construction, so the
-// exact top-k of the buffer is the answer.  Overflowing rows go to the exact
-// kernel.
+// Exact rescore of a captured band (one warp per row): the band holds every
+// column whose approximate y is within the row's threshold, each with that y
+// in its key.  The k + 4 best by approximate y are folded first; their k-th
+// exact distance bounds the true k-th, so only candidates whose approximate
+// A is inside proof_bound of it are folded next (the others cannot be in the
+// top-k).  The band is complete -- the row proven -- when
+// proof_bound(k-th exact) - alpha is inside the capture threshold.
+//
+// Folds run 32 candidates at a time, one per lane, in coordinate order (bit
+// parity): each 32-coordinate chunk of the 32 candidate rows is staged
+// through shared memory with 32 coalesced 128-byte loads (all independent, so
+// the warp keeps 4 KB in flight), then every lane folds its own row from the
+// tile (the query's chunk comes by shuffle).  One lane per candidate with its
+// own strided loads was latency-bound (ncu: 89% long-scoreboard stalls,
+// 9% of DRAM bandwidth at C3).
+constexpr int kBandWarps = 4;
+__device__ __forceinline__ size_t band_smem_per_warp(uint32_t cap) {
+    return size_t(cap) * 16 + size_t(cap) * 2 + 32 * 33 * 4 + 64;
+}
+
 template <int FOLD>
-__global__ void __launch_bounds__(128) rescore_capture_kernel(const Rescore2Params p) {
-    extern __shared__ uint64_t keys2[];  // [4][cap]
+__global__ void __launch_bounds__(32 * kBandWarps) rescore_capture_kernel(const Rescore2Params p) {
+    extern __shared__ __align__(16) uint8_t band_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t slot = blockIdx.x * 4 + warp;
+    const uint32_t slot = blockIdx.x * kBandWarps + warp;
     if (slot >= p.m) return;
+    uint8_t* wbase = band_smem + size_t(warp) * band_smem_per_warp(p.cap);
+    uint64_t* ak = reinterpret_cast<uint64_t*>(wbase);         // approximate keys (y, col)
+    uint64_t* ek = ak + p.cap;                                   // exact keys (distance, col) or empty
+    float* tile = reinterpret_cast<float*>(ek + p.cap);          // [32][33]
+    uint16_t* todo = reinterpret_cast<uint16_t*>(tile + 32 * 33);  // candidate positions of a batch
     const uint32_t qo = p.rows[slot];  // input order
-    uint64_t* ks = keys2 + size_t(warp) * p.cap;
+    if (qo == 0xffffffffu) return;     // a padding slot of a rank's last unit
     const uint32_t q = p.rowpos ? p.rowpos[qo] : qo;
     const uint32_t cnt_all = p.cnt[slot];
     const bool over = cnt_all > p.cap;  // lost candidates: no proof from this buffer
@@ -1695,47 +1714,117 @@ __global__ void __launch_bounds__(128) rescore_capture_kernel(const Rescore2Para
         return;
     }
     const uint32_t c = over ? p.cap : cnt_all;
-    const float* xq = p.X + size_t(qo) * p.d;
-    const bool vec = (p.d % 4 == 0);
     const uint64_t* in = p.buf + size_t(slot) * p.cap;
-    uint32_t valid = 0;
     for (uint32_t i = lane; i < c; i += 32) {
-        const uint32_t col = uint32_t(in[i]);  // input order (remap_kernel)
-        uint64_t key = kEmptyKey;
-        if (col != qo) {
-            const float* xc = p.X + size_t(col) * p.d;
-            const float dist = col > qo ? exact_fold_rows<FOLD>(xc, xq, p.d, vec) : exact_fold_rows<FOLD>(xq, xc, p.d, vec);
-            key = make_key(dist, col);
-            ++valid;
-        }
-        ks[i] = key;
+        const uint64_t key = in[i];
+        ak[i] = uint32_t(key) == qo ? kEmptyKey : key;  // the row itself is not a candidate
+        ek[i] = kEmptyKey;
     }
-    for (int o = 16; o; o >>= 1) valid += __shfl_xor_sync(0xffffffffu, valid, o);
     __syncwarp();
+    const float* xq = p.X + size_t(qo) * p.d;
+    // fold the candidates at positions todo[0, nt) (ak -> ek)
+    auto fold_batch = [&](uint32_t nt) {
+        for (uint32_t g = 0; g < nt; g += 32) {
+            const uint32_t mine = g + lane < nt ? todo[g + lane] : 0xffffu;
+            const uint32_t col = mine != 0xffffu ? uint32_t(ak[mine]) : qo;
+            // lane r's candidate row: lanes load row r's chunk (coalesced);
+            // the next chunk's 32 loads are in flight while this one folds
+            float nxt[32];
+            float qn = 0.0f;
+            auto load_chunk = [&](uint32_t j0) {
+                const uint32_t w = p.d - j0 < 32 ? p.d - j0 : 32;
+#pragma unroll
+                for (int r = 0; r < 32; ++r) {
+                    const uint32_t cr = __shfl_sync(0xffffffffu, col, r);
+                    nxt[r] = uint32_t(lane) < w ? __ldg(p.X + size_t(cr) * p.d + j0 + lane) : 0.0f;
+                }
+                qn = uint32_t(lane) < w ? __ldg(xq + j0 + lane) : 0.0f;
+            };
+            float acc = 0.0f;
+            load_chunk(0);
+            for (uint32_t j0 = 0; j0 < p.d; j0 += 32) {
+                const uint32_t w = p.d - j0 < 32 ? p.d - j0 : 32;
+#pragma unroll
+                for (int r = 0; r < 32; ++r) tile[r * 33 + lane] = nxt[r];
+                const float qv = qn;
+                __syncwarp();
+                if (j0 + 32 < p.d) load_chunk(j0 + 32);
+                for (uint32_t jj = 0; jj < w; ++jj)
+                    acc = fold_step<FOLD>(tile[lane * 33 + jj], __shfl_sync(0xffffffffu, qv, jj), acc);
+                __syncwarp();
+            }
+            if (mine != 0xffffu) ek[mine] = make_key(fold_finalize<FOLD>(acc), col);
+        }
+        __syncwarp();
+    };
+    // the klist-th smallest exact key so far (keys are unique: distinct columns)
+    auto kth_exact = [&]() -> uint64_t {
+        uint64_t kth = kEmptyKey;
+        for (uint32_t i = lane; i < c; i += 32) {
+            const uint64_t mk = ek[i];
+            if (mk == kEmptyKey) continue;
+            uint32_t rank = 0;
+            for (uint32_t j = 0; j < c; ++j) rank += ek[j] < mk;
+            if (rank == p.klist - 1) kth = mk;
+        }
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t other = __shfl_xor_sync(0xffffffffu, kth, o);
+            kth = other < kth ? other : kth;
+        }
+        return kth;
+    };
+    // phase 1: the klist + 4 best by approximate y
+    uint32_t nt = 0;
+    {
+        const uint32_t r1 = p.klist + 4;
+        for (uint32_t i0 = 0; i0 < c; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            bool take = false;
+            if (i < c && ak[i] != kEmptyKey) {
+                uint32_t rank = 0;
+                for (uint32_t j = 0; j < c; ++j) rank += ak[j] < ak[i];
+                take = rank < r1;
+            }
+            const uint32_t b = __ballot_sync(0xffffffffu, take);
+            if (take) todo[nt + __popc(b & ((1u << lane) - 1u))] = uint16_t(i);
+            nt += __popc(b);
+        }
+        __syncwarp();
+        fold_batch(nt);
+    }
+    const double alpha_q = double(p.alpha[q]);
+    const uint64_t kth1 = kth_exact();
+    // phase 2: everything whose approximate A is inside the bound of kth1
+    // (everything left when there is no k-th yet)
+    {
+        double lim = __longlong_as_double(0x7ff0000000000000ll);
+        if (kth1 != kEmptyKey)
+            lim = proof_bound<FOLD>(p.d, p.maxabs, p.gmax, p.xnorm[q], p.rho[q], alpha_q,
+                                    double(ordered_to_float(uint32_t(kth1 >> 32))));
+        nt = 0;
+        for (uint32_t i0 = 0; i0 < c; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const bool take = i < c && ak[i] != kEmptyKey && ek[i] == kEmptyKey &&
+                              alpha_q + double(ordered_to_float(uint32_t(ak[i] >> 32))) <= lim;
+            const uint32_t b = __ballot_sync(0xffffffffu, take);
+            if (take) todo[nt + __popc(b & ((1u << lane) - 1u))] = uint16_t(i);
+            nt += __popc(b);
+        }
+        __syncwarp();
+        if (nt) fold_batch(nt);
+    }
+    uint32_t valid = 0;
+    for (uint32_t i = lane; i < c; i += 32) valid += ek[i] != kEmptyKey;
+    for (int o = 16; o; o >>= 1) valid += __shfl_xor_sync(0xffffffffu, valid, o);
     if (lane == 0) atomicAdd(p.rescored, (unsigned long long)valid);
     if (valid < p.klist) {  // a proven band has >= k; a threshold guessed too low may not
         retry(p.loose ? double(p.loose[q]) : 0.0);
         return;
     }
-    // keys are unique (distinct columns) except the empty self slot: the
-    // rank of an element is the number of smaller keys
-    uint64_t kth = kEmptyKey;
-    for (uint32_t i = lane; i < c; i += 32) {
-        const uint64_t mk = ks[i];
-        if (mk == kEmptyKey) continue;
-        uint32_t rank = 0;
-        for (uint32_t j = 0; j < c; ++j) rank += ks[j] < mk;
-        if (rank == p.klist - 1) kth = mk;
-    }
-    for (int o = 16; o; o >>= 1) {
-        const uint64_t other = __shfl_xor_sync(0xffffffffu, kth, o);
-        kth = other < kth ? other : kth;
-    }
+    const uint64_t kth = kth_exact();
     // the band's k-th exact distance bounds the true k-th from above, so
     // every true neighbor has y <= proof_bound(kth) - alpha_q: the band is
-    // complete when that is inside its threshold (always, for thresholds the
-    // rescore derived from a k-th distance; not always for a looser one)
-    const double alpha_q = double(p.alpha[q]);
+    // complete when that is inside its threshold
     const double need = proof_bound<FOLD>(p.d, p.maxabs, p.gmax, p.xnorm[q], p.rho[q], alpha_q,
                                           double(ordered_to_float(uint32_t(kth >> 32)))) - alpha_q;
     if (over || !(need <= double(p.thr[slot]))) {
@@ -1744,16 +1833,28 @@ __global__ void __launch_bounds__(128) rescore_capture_kernel(const Rescore2Para
     }
     const size_t orow = size_t(qo - p.row_begin);
     for (uint32_t i = lane; i < c; i += 32) {
-        const uint64_t mk = ks[i];
-        if (mk == kEmptyKey) continue;
+        const uint64_t mk = ek[i];
+        if (mk == kEmptyKey || mk > kth) continue;
         uint32_t rank = 0;
-        for (uint32_t j = 0; j < c; ++j) rank += ks[j] < mk;
-        if (rank < p.klist) {
-            const float dv = ordered_to_float(uint32_t(mk >> 32));
-            p.out_index[orow * p.klist + rank] = uint32_t(mk);
-            p.out_dist[orow * p.klist + rank] = p.out_sqrt ? __fsqrt_rn(dv) : dv;
-        }
+        for (uint32_t j = 0; j < c; ++j) rank += ek[j] < mk;
+        const float dv = ordered_to_float(uint32_t(mk >> 32));
+        p.out_index[orow * p.klist + rank] = uint32_t(mk);
+        p.out_dist[orow * p.klist + rank] = p.out_sqrt ? __fsqrt_rn(dv) : dv;
     }
+}
+
+static size_t band_smem_bytes(uint32_t cap) {
+    return kBandWarps * (size_t(cap) * 16 + size_t(cap) * 2 + 32 * 33 * 4 + 64);
+}
+
+template <int FOLD>
+static cudaError_t launch_rescore_capture(const Rescore2Params& r2, uint32_t rows, cudaStream_t st) {
+    const size_t smem = band_smem_bytes(r2.cap);
+    cudaError_t e = cudaFuncSetAttribute(rescore_capture_kernel<FOLD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e != cudaSuccess) return e;
+    rescore_capture_kernel<FOLD><<<(rows + kBandWarps - 1) / kBandWarps, 32 * kBandWarps, smem, st>>>(r2);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -2019,16 +2120,8 @@ static cudaError_t run_capture(const TensorPathArgs& a, const CaptureArgs& c, ui
     Rescore2Params r2{a.X,     a.n,   a.d,        a.klist,     a.row_begin, c.fb_rows, nfb,      cap_cnt,
                       cap_buf, c.cap, a.out_sqrt, a.out_index, a.out_dist,  fb2_count, fb2_rows, c.rescored,
                       c.fb_thr, c.rowpos, c.alpha, c.rho, c.xnorm, c.gmax, c.maxabs};
-    const size_t smem2 = size_t(4) * c.cap * 8;
-    if (a.fold == kCosine) {
-        cudaFuncSetAttribute(rescore_capture_kernel<kCosine>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
-        rescore_capture_kernel<kCosine><<<(nfb + 3) / 4, 128, smem2, st>>>(r2);
-    } else {
-        cudaFuncSetAttribute(rescore_capture_kernel<kSqEuclidean>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem2));
-        rescore_capture_kernel<kSqEuclidean><<<(nfb + 3) / 4, 128, smem2, st>>>(r2);
-    }
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    e = a.fold == kCosine ? launch_rescore_capture<kCosine>(r2, nfb, st) : launch_rescore_capture<kSqEuclidean>(r2, nfb, st);
+    if (e != cudaSuccess) return e;
     launches += 3;
     if ((e = cudaMemcpyAsync(a.host_scratch, fb2_count, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
     if ((e = cudaMemcpyAsync(static_cast<uint8_t*>(a.host_scratch) + 32, c.rescored, 8, cudaMemcpyDeviceToHost, st)) !=
@@ -2047,7 +2140,7 @@ static cudaError_t run_capture(const TensorPathArgs& a, const CaptureArgs& c, ui
     return cudaSuccess;
 }
 
-static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResult& r, bool allow_tri);
+static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResult& r);
 
 // Whole problems that take the triangle sweep (each unordered pair once):
 // sorted columns (not cosine), two 12-entry lists (k <= 11), resident A
@@ -2063,24 +2156,31 @@ bool tri_eligible(uint32_t n, uint32_t d, uint32_t klist, int fold) {
            (d + 63) / 64 <= uint32_t(TS_MAX_RES_KC) && (force ? n >= 512 : n >= 393216);
 }
 
-bool tcap_eligible(uint32_t n, uint32_t d, uint32_t klist);
-cudaError_t run_tcap(const TensorPathArgs& a, void* (*alloc)(void*, int, size_t), void* actx, TensorPathResult& r,
-                     bool* overflow);
 
 cudaError_t run_tensor_path(const TensorPathArgs& a, TensorPathResult& r) {
-    // whole problems with 10 < k <= 128: the threshold triangle (tri_shard.cuh)
-    if (a.row_begin == 0 && a.row_end == a.n && a.shard_alloc && tcap_eligible(a.n, a.d, a.klist)) {
+    const bool whole = a.row_begin == 0 && a.row_end == a.n && a.shard_alloc;
+    // whole problems with k <= 10: the list triangle, run as the one-rank case
+    // of the sharded program (tri_shard.cuh: snake-dealt units, chunk pool)
+    if (whole && tri_eligible(a.n, a.d, a.klist, a.fold)) {
         bool overflow = false;
-        const cudaError_t e = run_tcap(a, a.shard_alloc, a.shard_ctx, r, &overflow);
+        const cudaError_t e =
+            run_tri_loopback(a, 1, a.shard_alloc, a.shard_ctx, r, nullptr, nullptr, &overflow, false);
+        if (e != cudaSuccess || !overflow) return e;
+        r = TensorPathResult{};  // the pool overflowed (pathological data): the rectangular sweep
+        return run_tensor_path_impl(a, r);
+    }
+    // whole problems with 10 < k <= 128: the threshold triangle (tri_shard.cuh)
+    if (whole && tcap_eligible(a.n, a.d, a.klist)) {
+        bool overflow = false;
+        const cudaError_t e =
+            run_tri_loopback(a, 1, a.shard_alloc, a.shard_ctx, r, nullptr, nullptr, &overflow, true);
         if (e != cudaSuccess || !overflow) return e;
         r = TensorPathResult{};  // the pool overflowed (pathological data): the rectangular sweep
     }
-    return run_tensor_path_impl(a, r, true);
+    return run_tensor_path_impl(a, r);
 }
 
-// allow_tri = false: the triangle sweep's append logs overflowed on this
-// input (pathological data); redo the call with the rectangular sweep.
-static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResult& r, bool allow_tri) {
+static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResult& r) {
     const uint32_t n = a.n, d = a.d, nrows = a.row_end - a.row_begin;
     const uint32_t npad = (n + 255) / 256 * 256;
     const uint32_t kc = (d + 63) / 64;
@@ -2166,182 +2266,27 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
     const uint32_t npad_a = sorted ? qpad : npad;
     SweepParams sp{xh,   alpha,  n,       npad,    kc, sr0, sr1, group_tiles, dbg ? atoi(dbg) : 0,
                    cand, xa_rows, npad_a, nullptr, nullptr, nullptr, 0, bmin};
-    // Triangle mode (default for whole problems with k <= 11 and d <= 256;
-    // KNN_B200_TRI=0 disables): each unordered pair is computed once.  A
-    // sample pass (every kTriStride-th sorted column) fixes every row's
-    // column-side threshold; the sweep then covers only tiles >= each row
-    // pair's own, offering each pair to the row side (register lists) and to
-    // the column side (fixed-threshold append buffers), and the rescore merges
-    // both with a bound for each.
-    const bool tri = allow_tri && a.row_begin == 0 && a.row_end == n && tri_eligible(n, d, a.klist, a.fold);
-    uint64_t* tri_cbuf = nullptr;
-    uint32_t* tri_ccnt = nullptr;
-    float* tri_tc = nullptr;
-    float* tri_alpha = nullptr;
-    double* tri_rho = nullptr;
-    double* tri_xnorm = nullptr;
-    uint32_t* tri_perm = nullptr;
-    uint64_t* tri_sel = nullptr;
-    uint32_t* tri_scnt = nullptr;
-    float* tri_sbound = nullptr;
-    float* tri_tl = nullptr;
+    // (whole problems with k <= 10 take the triangle sweep before reaching
+    // here: run_tensor_path -> run_tri_loopback, tri_shard.cuh)
     if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
-    if (tri) {
-        const char* se = getenv("KNN_B200_TRI_STRIDE");  // tuning: sample every stride-th column
-        const char* re = getenv("KNN_B200_TRI_RANK");    // tuning: threshold = rank-th of 24 sample candidates
-        const uint32_t stride = se ? uint32_t(atoi(se)) : uint32_t(kTriStride);
-        const char* ke = getenv("KNN_B200_TRI_SAMPLE_KPL");  // tuning: 4 (default), 6 or 12
-        const uint32_t skpl = ke && atoi(ke) == 12 ? 12u : ke && atoi(ke) == 6 ? 6u : uint32_t(kTriSampleKpl);
-        uint32_t trank = re ? uint32_t(atoi(re)) : uint32_t(kTriRank);
-        trank = trank < 1 ? 1 : (trank > skpl ? skpl : trank);  // the lists hold the skpl smallest
-        const uint32_t sm = (n + stride - 1) / stride, spad = (sm + 255) / 256 * 256;
-        // the sample pass only sets thresholds (any value is correct), so it
-        // runs on E4M3 copies of the planes at twice the fp16 MMA rate
-        const char* fe = getenv("KNN_B200_TRI_E4M3");  // tuning: 0 = fp16 sample pass
-        const bool f8 = !(fe && atoi(fe) == 0);
-        const uint32_t skc = f8 ? (kc + 1) / 2 : kc;
-        size_t need = 0;
-        auto add = [&](size_t x) { need += (x + 255) / 256 * 256; };
-        add(size_t(sm) * 4);                  // sample rows
-        add(size_t(skc) * spad * 128);        // sample planes
-        if (f8) add(size_t(skc) * npad * 128);  // E4M3 planes of every row
-        add(size_t(spad) * 4);                // sample alpha
-        add(size_t(spad / 32) * 4);           // sample bmin
-        add(size_t(n) * 2 * skpl * 8);        // sample lists
-        add(size_t(npad) * 4);                // tc
-        add(size_t(npad / 32) * 4);           // tcmax
-        add(size_t(npad) * kTriCap * 8);      // column-side buffers
-        add(size_t(npad) * 4);                // counts
-        add(size_t(n) * kTriSel * 8);         // selected column-side candidates
-        add(size_t(n) * 4);                   // their counts
-        add(size_t(n) * 4);                   // their bounds
-        size_t otemp = 0;                     // the second order
-        cub::DeviceRadixSort::SortPairs(nullptr, otemp, static_cast<const unsigned long long*>(nullptr),
-                                        static_cast<unsigned long long*>(nullptr), static_cast<const uint32_t*>(nullptr),
-                                        static_cast<uint32_t*>(nullptr), int(n));
-        add(otemp);
-        add(size_t(n) * 8 * 2);               // keys in / out
-        add(size_t(n) * 4 * 2);               // index in / order
-        add(size_t(npad) * 4 * 4);            // alpha2, tc2, tl, tl2
-        add(size_t(npad) * 8 * 2);            // rho2, xnorm2
-        add(size_t(n) * 4);                   // perm2
-        add(size_t(npad / 32) * 4);           // bmin2
-        // the column-side pool: 4x the expected volume (C2: ~63M entries =
-        // 1/4 of the capacity; an overflow redoes the call) plus a partial
-        // chunk per epilogue warp
-        const uint32_t npairs = (n + 255) / 256;
-        const uint32_t gpairs = npairs < uint32_t(a.sm_count / 2) ? npairs : uint32_t(a.sm_count / 2);
-        const uint32_t nwarps = 2 * gpairs * 8;
-        const char* lce = getenv("KNN_B200_TRI_LOGCAP");  // testing: pool entries (forces the overflow fallback)
-        const uint64_t pool = lce ? uint64_t(atoi(lce)) : uint64_t(4) * n * 64 + uint64_t(nwarps) * kLogChunk;
-        const uint32_t nchunks = uint32_t((pool + kLogChunk - 1) / kLogChunk);
-        add(size_t(nchunks) * kLogChunk * 8);  // pool keys
-        add(size_t(nchunks) * kLogChunk * 4);  // pool columns
-        add(size_t(nchunks) * 4 + 4);          // chunk counts + next free chunk
-        uint8_t* w3 = static_cast<uint8_t*>(a.alloc2(a.alloc2_ctx, need));
-        if (!w3) return cudaErrorMemoryAllocation;
-        auto take3 = [&](size_t x) {
-            uint8_t* q = w3;
-            w3 += (x + 255) / 256 * 256;
-            return q;
-        };
-        uint32_t* srows = reinterpret_cast<uint32_t*>(take3(size_t(sm) * 4));
-        uint8_t* xs = take3(size_t(skc) * spad * 128);
-        uint8_t* x8 = f8 ? take3(size_t(skc) * npad * 128) : nullptr;
-        float* alpha_s = reinterpret_cast<float*>(take3(size_t(spad) * 4));
-        float* bmin_s = reinterpret_cast<float*>(take3(size_t(spad / 32) * 4));
-        uint64_t* cand_s = reinterpret_cast<uint64_t*>(take3(size_t(n) * 2 * skpl * 8));
-        tri_tc = reinterpret_cast<float*>(take3(size_t(npad) * 4));
-        float* tcmax = reinterpret_cast<float*>(take3(size_t(npad / 32) * 4));
-        tri_cbuf = reinterpret_cast<uint64_t*>(take3(size_t(npad) * kTriCap * 8));
-        tri_ccnt = reinterpret_cast<uint32_t*>(take3(size_t(npad) * 4));
-        tri_sel = reinterpret_cast<uint64_t*>(take3(size_t(n) * kTriSel * 8));
-        tri_scnt = reinterpret_cast<uint32_t*>(take3(size_t(n) * 4));
-        tri_sbound = reinterpret_cast<float*>(take3(size_t(n) * 4));
-        void* otmp = take3(otemp);
-        auto* okey = reinterpret_cast<unsigned long long*>(take3(size_t(n) * 8));
-        auto* okey2 = reinterpret_cast<unsigned long long*>(take3(size_t(n) * 8));
-        uint32_t* oidx = reinterpret_cast<uint32_t*>(take3(size_t(n) * 4));
-        uint32_t* order = reinterpret_cast<uint32_t*>(take3(size_t(n) * 4));
-        tri_alpha = reinterpret_cast<float*>(take3(size_t(npad) * 4));
-        float* tc2 = reinterpret_cast<float*>(take3(size_t(npad) * 4));
-        float* tl1 = reinterpret_cast<float*>(take3(size_t(npad) * 4));
-        tri_tl = reinterpret_cast<float*>(take3(size_t(npad) * 4));
-        tri_rho = reinterpret_cast<double*>(take3(size_t(npad) * 8));
-        tri_xnorm = reinterpret_cast<double*>(take3(size_t(npad) * 8));
-        tri_perm = reinterpret_cast<uint32_t*>(take3(size_t(n) * 4));
-        float* bmin2 = reinterpret_cast<float*>(take3(size_t(npad / 32) * 4));
-        uint64_t* lkey = reinterpret_cast<uint64_t*>(take3(size_t(nchunks) * kLogChunk * 8));
-        uint32_t* lcol = reinterpret_cast<uint32_t*>(take3(size_t(nchunks) * kLogChunk * 4));
-        uint32_t* lcnt = reinterpret_cast<uint32_t*>(take3(size_t(nchunks) * 4 + 4));
-        uint32_t* lnext = lcnt + nchunks;
-        iota_stride_kernel<<<a.sm_count, 256, 0, st>>>(srows, sm, stride);
-        if (f8) e4m3_planes_kernel<<<a.sm_count * 8, 256, 0, st>>>(xh, npad, kc, skc, x8);
-        const uint8_t* xrows = f8 ? x8 : xh;
-        gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xrows, npad, skc, srows, 0, sm, spad, nullptr, xs);
-        const float dscale = f8 ? kE4m3Scale * kE4m3Scale : 1.0f;  // dots of the E4M3 planes: 2^-16
-        gather_alpha_kernel<<<a.sm_count, 256, 0, st>>>(alpha, srows, sm, spad, dscale, alpha_s);
-        chunk_min_kernel<<<(spad / 32 * 32 + 255) / 256, 256, 0, st>>>(alpha_s, spad / 32, bmin_s);
-        // sample pass: every row (sorted order) against the sample columns
-        uint32_t gts = uint32_t((40ull << 20) / (uint64_t(256) * skc * 128));
-        const uint32_t stiles = spad / 256;
-        gts = gts < 1 ? 1 : (gts > stiles ? stiles : gts);
-        SweepParams ss{xs,     alpha_s, sm,      spad,    skc, 0, n, gts, 0,
-                       cand_s, xrows,   npad,    nullptr, nullptr, nullptr, 0, bmin_s};
-        ss.e4m3 = f8;
-        e = skpl == 12  ? launch_sweep_pair<12, 256, 8>(ss, n, st)
-            : skpl == 6 ? launch_sweep_pair<6, 256, 8>(ss, n, st)
-                        : launch_sweep_pair<kTriSampleKpl, 256, 8>(ss, n, st);
+    // CTA pairs (default; KNN_B200_PAIR=0 disables) need whole 256-row
+    // pairs of blocks inside the padded planes.  At C2 they halve the
+    // L2->SM operand traffic and cut the sweep ~3%.
+    const char* pe = getenv("KNN_B200_PAIR");
+    const bool pair = !(pe && atoi(pe) == 0) && kc <= uint32_t(TS_MAX_RES_KC) && cfg.nseg == 2 &&
+                      (cfg.kpl == 12 || cfg.kpl == 16) && sr0 % 256 == 0 && sr0 + (nrows + 255) / 256 * 256 <= npad_a;
+    if (pair) {
+        e = cfg.kpl == 12 ? launch_sweep_pair<12, 256, 8>(sp, nrows, st)
+                          : launch_sweep_pair<16, 256, 8>(sp, nrows, st);
         if (e != cudaSuccess) return e;
-        tri_threshold_kernel<<<a.sm_count * 4, 256, 0, st>>>(cand_s, n, 0, npad, 2 * skpl, trank, 1.0f / dscale,
-                                                              tc2, tl1);
-        // second order: thresholds sorted within buckets of the norm order;
-        // the triangle sweep runs on a copy of the planes in that order
-        tri_order_key_kernel<<<a.sm_count * 4, 256, 0, st>>>(tc2, n, kTriBucket, okey, oidx);
-        if ((e = cub::DeviceRadixSort::SortPairs(otmp, otemp, okey, okey2, oidx, order, int(n), 0, 64, st)) !=
-            cudaSuccess)
-            return e;
-        tri_permute_kernel<<<a.sm_count * 4, 256, 0, st>>>(order, n, npad, alpha, rho, xnorm, tc2, tl1, perm,
-                                                            tri_alpha, tri_rho, tri_xnorm, tri_tc, tri_tl, tri_perm);
-        gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(xh, npad, kc, order, 0, n, npad, nullptr, xq_planes);
-        chunk_min_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(tri_alpha, npad / 32, bmin2);
-        chunk_max_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(tri_tc, npad / 32, tcmax);
-        if ((e = cudaMemsetAsync(tri_ccnt, 0, size_t(npad) * 4, st)) != cudaSuccess) return e;
-        if ((e = cudaMemsetAsync(lnext, 0, 4, st)) != cudaSuccess) return e;
-        // the triangle sweep: rows are the (re-ordered) set itself
-        SweepParams tp{xq_planes, tri_alpha, n,    npad,    kc, 0, n, group_tiles, dbg ? atoi(dbg) : 0,
-                       cand,      xq_planes, npad, nullptr, nullptr, nullptr, 0, bmin2,
-                       tri_tc, tcmax, lkey, lcol, lcnt, lnext, nchunks};
-        if ((e = launch_sweep_pair<12, 256, 8, true>(tp, n, st)) != cudaSuccess) return e;
-        tri_scatter_kernel<<<nchunks, 256, 0, st>>>(lkey, lcol, lcnt, lnext, nchunks, tri_ccnt, tri_cbuf, kTriCap,
-                                                  reinterpret_cast<unsigned int*>(scal + 40));
-        launches += f8 ? 14 : 13;
-    } else {
-        // CTA pairs (default; KNN_B200_PAIR=0 disables) need whole 256-row
-        // pairs of blocks inside the padded planes.  At C2 they halve the
-        // L2->SM operand traffic and cut the sweep ~3%.
-        const char* pe = getenv("KNN_B200_PAIR");
-        const bool pair = !(pe && atoi(pe) == 0) && kc <= uint32_t(TS_MAX_RES_KC) && cfg.nseg == 2 &&
-                          (cfg.kpl == 12 || cfg.kpl == 16) && sr0 % 256 == 0 && sr0 + (nrows + 255) / 256 * 256 <= npad_a;
-        if (pair) {
-            e = cfg.kpl == 12 ? launch_sweep_pair<12, 256, 8>(sp, nrows, st)
-                              : launch_sweep_pair<16, 256, 8>(sp, nrows, st);
-            if (e != cudaSuccess) return e;
-        } else if ((e = launch_sweep(cfg, kc <= uint32_t(TS_MAX_RES_KC), sp, nrows, st)) != cudaSuccess) {
-            return e;
-        }
-        ++launches;
+    } else if ((e = launch_sweep(cfg, kc <= uint32_t(TS_MAX_RES_KC), sp, nrows, st)) != cudaSuccess) {
+        return e;
     }
+    ++launches;
     if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
     if (sorted) {
-        remap_kernel<<<a.sm_count * 8, 256, 0, st>>>(cand, size_t(nrows) * kp, tri ? tri_perm : perm);
+        remap_kernel<<<a.sm_count * 8, 256, 0, st>>>(cand, size_t(nrows) * kp, perm);
         ++launches;
-    }
-    if (tri) {  // column-side entries: sweep-order row ids -> input rows; keep each row's best kTriSel
-        remap_capture_kernel<<<n, 128, 0, st>>>(tri_cbuf, tri_ccnt, n, kTriCap, tri_perm);
-        tri_select_kernel<<<(n * 32 + 255) / 256, 256, 0, st>>>(tri_cbuf, tri_ccnt, kTriCap, n, tri_tc, tri_sel,
-                                                                 tri_scnt, tri_sbound);
-        launches += 2;
     }
 
     RescoreParams rp{a.X,  n,         d,          a.klist,  kp,       a.row_begin, a.row_end, cand,
@@ -2351,23 +2296,7 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
         const char* fc = getenv("KNN_B200_FORCE_CAPTURE");
         rp.force_capture = fc && atoi(fc) != 0;
     }
-    if (tri) {  // slots are sorted positions; both sides' candidates
-        rp.rowpos = nullptr;
-        rp.rowperm = tri_perm;
-        rp.alpha = tri_alpha;
-        rp.rho = tri_rho;
-        rp.xnorm = tri_xnorm;
-        rp.xbuf = tri_sel;
-        rp.xcnt = tri_scnt;
-        rp.xbound = tri_sbound;
-        rp.xcap = tri_tl;
-        const dim3 grid((nrows + 7) / 8);
-        if (cosine) rescore_kernel<kCosine, 24, 2, kTriSel><<<grid, 256, 0, st>>>(rp);
-        else rescore_kernel<kSqEuclidean, 24, 2, kTriSel><<<grid, 256, 0, st>>>(rp);
-        e = cudaGetLastError();
-    } else {
-        e = cosine ? launch_rescore<kCosine>(cfg, rp, nrows, st) : launch_rescore<kSqEuclidean>(cfg, rp, nrows, st);
-    }
+    e = cosine ? launch_rescore<kCosine>(cfg, rp, nrows, st) : launch_rescore<kSqEuclidean>(cfg, rp, nrows, st);
     if (e != cudaSuccess) return e;
     ++launches;
 
@@ -2377,8 +2306,6 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
     if ((e = cudaMemcpyAsync(a.host_scratch, scal, 64, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
     const uint32_t nfb = *reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(a.host_scratch) + 4);
-    if (tri && *reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(a.host_scratch) + 40) != 0)
-        return run_tensor_path_impl(a, r, false);
     r.rescored = *reinterpret_cast<const unsigned long long*>(static_cast<const uint8_t*>(a.host_scratch) + 32);
     r.fallback_rows = nfb;
     if (nfb) {

@@ -147,6 +147,26 @@ __global__ void tri_bin_place_kernel(const uint64_t* __restrict__ lkey, const ui
     }
 }
 
+// One rank (no exchange): the pool straight into the per-row buffers, the
+// column translated to its slot (unit_lidx: its unit's place in the list).
+__global__ void tri_scatter_local_kernel(const uint64_t* __restrict__ lkey, const uint32_t* __restrict__ lcol,
+                                         const uint32_t* __restrict__ lcnt, const uint32_t* __restrict__ lnext,
+                                         uint32_t nchunks, const uint32_t* __restrict__ unit_lidx,
+                                         uint32_t* __restrict__ ccnt, uint64_t* __restrict__ cbuf, uint32_t ccap,
+                                         unsigned int* __restrict__ overflow) {
+    const uint32_t w = blockIdx.x, used = *lnext;
+    if (w == 0 && threadIdx.x == 0 && used > nchunks) atomicOr(overflow, 1u);
+    if (w >= min(used, nchunks)) return;
+    const uint32_t c = lcnt[w];
+    const size_t base = size_t(w) * kLogChunk;
+    for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) {
+        const uint32_t col = lcol[base + i];
+        const uint32_t s = unit_lidx[col >> 8] * 256 + (col & 255);
+        const uint32_t at = atomicAdd(ccnt + s, 1u);
+        if (at < ccap) cbuf[size_t(s) * ccap + at] = lkey[base + i];
+    }
+}
+
 // Received column-side entries -> the owner's per-row buffers.
 __global__ void tri_scatter_flat_kernel(const uint64_t* __restrict__ rkey, const uint32_t* __restrict__ rslot,
                                         unsigned long long count, uint32_t* __restrict__ ccnt,
@@ -163,13 +183,14 @@ __global__ void tri_scatter_flat_kernel(const uint64_t* __restrict__ rkey, const
 // sample lists: T ~ the row's k-th distance is estimated by the rank-r
 // smallest y over the sample columns (r set so that the sample's r-th
 // exceeds the true k-th with high probability), and the threshold admits its
-// proof band twice over: thr = proof_bound(proof_bound(T)) - alpha.  Any
+// proof band: thr = proof_bound(T) - alpha.  Any
 // value is correct -- the capture rescore proves each row or retries it.
 // loose: the sample lists' largest y (a retry threshold for rows left with
 // fewer than k candidates).
 struct TcapThrArgs {
     const uint64_t* cand;  // rows [j0, j1): 2 x 16 sample keys each
     uint32_t n, j0, j1, kp, r, d;
+    float unscale;         // sample y -> fp16-plane y (1 / 2^-16 for E4M3 operands)
     const float* alpha;
     const double* rho;
     const double* xnorm;
@@ -199,13 +220,12 @@ __global__ void tcap_threshold_kernel(const TcapThrArgs t) {
             if (kth == kEmptyKey) {
                 thr = __int_as_float(0x7f800000);  // fewer than r sampled columns: admit everything
             } else {
-                const double y = double(ordered_to_float(uint32_t(kth >> 32)));
+                const double y = double(ordered_to_float(uint32_t(kth >> 32))) * t.unscale;
                 const double b1 = proof_bound<FOLD>(t.d, t.maxabs, t.gmax, t.xnorm[j], t.rho[j], al,
                                                     fmax((al + y) / s2, 0.0));
-                const double b2 = proof_bound<FOLD>(t.d, t.maxabs, t.gmax, t.xnorm[j], t.rho[j], al, b1 / s2);
-                thr = __double2float_ru(b2 - al);
+                thr = __double2float_ru(b1 - al);
             }
-            lo = last == 0 ? thr : fmaxf(thr, ordered_to_float(uint32_t(last >> 32)));
+            lo = last == 0 ? thr : fmaxf(thr, __fmul_rn(ordered_to_float(uint32_t(last >> 32)), t.unscale));
         }
         t.thr[j] = thr;
         t.loose[j] = lo;
@@ -268,6 +288,7 @@ struct TriShared {
     uint8_t* xq2;  // the triangle's operand planes (second order)
     // unit tables
     uint32_t *unit_owner, *unit_lidx;
+    uint32_t* tri_rowpos;  // input row -> second-order position (threshold triangle)
     std::vector<std::vector<uint32_t>> units_h;
 
     void layout(Carve& c) {
@@ -308,6 +329,7 @@ struct TriShared {
         xq2 = c.take<uint8_t>(size_t(kc) * npad * 128);
         unit_owner = c.take<uint32_t>(U);
         unit_lidx = c.take<uint32_t>(U);
+        tri_rowpos = c.take<uint32_t>(tcap ? n : 1);
     }
 };
 
@@ -348,11 +370,15 @@ static cudaError_t tri_prep(TriShared& S, const TensorPathArgs& a, uint32_t G, S
     S.tcap = tcap;
     S.cosine = a.fold == kCosine;
     if (tcap) {
-        // the sample pass estimates each row's k-th distance: fp16 (an E4M3
-        // dot is too coarse for that), 2 x 16-entry lists, the rank-r value
-        // with r ~ k / stride + 2.5 sqrt(k / stride) + 1 (tcap_threshold_kernel)
-        S.f8 = false;
+        // the sample pass estimates each row's k-th distance: every 16th
+        // (k <= 47) or 32nd column, E4M3 operands (the dot's error is well
+        // inside the gap between the k-th and the r x stride-th neighbour at
+        // C3 and C4), 2 x 16-entry lists, the rank-r value with
+        // r ~ k / stride + 2.5 sqrt(k / stride) + 1 (tcap_threshold_kernel)
         S.skpl = 16;
+        S.stride = a.klist <= 47 ? 16 : 32;  // tuning: KNN_B200_TCAP_STRIDE
+        if (const char* se = getenv("KNN_B200_TCAP_STRIDE")) S.stride = std::max(1, atoi(se));
+        if (const char* fe = getenv("KNN_B200_TCAP_E4M3")) S.f8 = atoi(fe) != 0;
         const double m = double(a.klist) / S.stride;
         S.trank = uint32_t(std::min(32.0, std::ceil(m + 2.5 * std::sqrt(m) + 1.0)));
     }
@@ -447,7 +473,7 @@ static cudaError_t tri_rank_init(TriShared& S, TriRank& R, uint32_t rank, const 
     R.soff_h.assign(S.G, 0);
     auto lay = [&](Carve& c) {
         R.units = c.take<uint32_t>(std::max<uint32_t>(R.nu, 1));
-        R.cand = c.take<uint64_t>(size_t(R.nslots) * 24 + 1);
+        R.cand = c.take<uint64_t>(S.tcap ? 1 : size_t(R.nslots) * 24 + 1);  // the threshold triangle keeps no lists
         R.cand_s = c.take<uint64_t>(size_t(R.s1 - R.s0) * 2 * S.skpl + 1);
         R.scal = c.take<uint8_t>(64);
         R.scnt = c.take<unsigned long long>(S.G);
@@ -485,8 +511,8 @@ static cudaError_t tri_sample(TriShared& S, TriRank& R, const TensorPathArgs& a)
                                    : launch_sweep_pair<kTriSampleKpl, 256, 8>(ss, rows, st);
     if (e != cudaSuccess) return e;
     if (S.tcap) {
-        const TcapThrArgs ta{R.cand_s, S.n, R.s0, R.s1, 2 * S.skpl, S.trank, S.d, S.alpha, S.rho, S.xnorm,
-                             S.gmax, S.maxabs, S.tc2, S.tl1};
+        const TcapThrArgs ta{R.cand_s, S.n,   R.s0,    R.s1,   2 * S.skpl, S.trank, S.d,  1.0f / S.dscale,
+                             S.alpha,  S.rho, S.xnorm, S.gmax, S.maxabs,   S.tc2,   S.tl1};
         if (S.cosine) tcap_threshold_kernel<kCosine><<<a.sm_count * 4, 256, 0, st>>>(ta);
         else tcap_threshold_kernel<kSqEuclidean><<<a.sm_count * 4, 256, 0, st>>>(ta);
     } else {
@@ -510,6 +536,7 @@ static cudaError_t tri_order(TriShared& S, const TensorPathArgs& a) {
     gather_rows_kernel<<<a.sm_count * 4, 256, 0, st>>>(S.xh, npad, S.kc, S.order, 0, n, npad, nullptr, S.xq2);
     chunk_min_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(S.tri_alpha, npad / 32, S.bmin2);
     chunk_max_kernel<<<(npad / 32 * 32 + 255) / 256, 256, 0, st>>>(S.tri_tc, npad / 32, S.tcmax);
+    if (S.tcap) invert_perm_kernel<<<a.sm_count * 4, 256, 0, st>>>(S.tri_perm, n, S.tri_rowpos);
     return cudaGetLastError();
 }
 
@@ -528,7 +555,10 @@ static cudaError_t tri_sweep(TriShared& S, TriRank& R, const TensorPathArgs& a, 
     for (uint32_t u : S.units_h[R.rank]) share_w += double(S.U - u);
     const double total = double(S.U) * (S.U + 1) / 2;
     const double share = std::max(total > 0 ? share_w / total : 1.0, double(R.nu) / double(S.U));
-    uint64_t pool = uint64_t(4.0 * double(S.n) * 64.0 * share) + uint64_t(2 * pairs * 8) * kLogChunk;
+    // the threshold triangle: ~ (r x stride) captured entries per row plus
+    // the proof band (tcap_threshold_kernel; C3 ~ 350, C4 ~ 220 per row), 2.5x
+    const double per_row = S.tcap ? 2.5 * (double(S.trank) * S.stride + 64.0) : 4.0 * 64.0;
+    uint64_t pool = uint64_t(per_row * double(S.n) * share) + uint64_t(2 * pairs * 8) * kLogChunk;
     if (const char* lce = getenv("KNN_B200_TRI_LOGCAP")) pool = uint64_t(atoi(lce));
     R.nchunks = uint32_t((pool + kLogChunk - 1) / kLogChunk);
     auto lay = [&](Carve& c) {
@@ -554,7 +584,18 @@ static cudaError_t tri_sweep(TriShared& S, TriRank& R, const TensorPathArgs& a, 
                    S.tri_tc, S.tcmax,  R.lkey, R.lcol,  R.lcnt, R.lnext, R.nchunks};
     tp.units = R.units;
     tp.nunits = R.nu;
-    if ((e = launch_sweep_pair<12, 256, 8, true>(tp, R.nslots, st)) != cudaSuccess) return e;
+    e = !S.tcap                        ? launch_sweep_pair<12, 256, 8, true>(tp, R.nslots, st)
+        : S.kc <= uint32_t(TS_MAX_RES_KC) ? launch_sweep_pair<2, 256, 8, true, true, true>(tp, R.nslots, st)
+                                           : launch_sweep_pair<2, 256, 8, true, true, false>(tp, R.nslots, st);
+    if (e != cudaSuccess) return e;
+    if (S.G == 1) {  // no exchange: only the pool's overflow matters (phase C scatters it in place)
+        uint32_t* h = static_cast<uint32_t*>(a.host_scratch);
+        if ((e = cudaMemcpyAsync(h, R.lnext, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+        R.overflow = h[0] > R.nchunks;
+        R.scnt_h[0] = 0;
+        return cudaSuccess;
+    }
     if ((e = cudaMemsetAsync(R.scnt, 0, size_t(S.G) * 8, st)) != cudaSuccess) return e;
     tri_bin_count_kernel<<<R.nchunks, 256, 0, st>>>(R.lcol, R.lcnt, R.lnext, R.nchunks, S.unit_owner, S.G, R.scnt,
                                                     reinterpret_cast<unsigned int*>(R.scal + 40));
@@ -617,10 +658,13 @@ static cudaError_t tri_recv_alloc(TriRank& R, unsigned long long count, ShardAll
 // per-row buffers, the best kTriSel of each, and the exact rescore of row
 // side + column side; unproven rows through the capture pass.  Outputs go
 // to a.out_* at the rows' input positions.
+static cudaError_t tcap_finish(TriShared& S, TriRank& R, const TensorPathArgs& a, ShardAllocFn alloc, void* actx);
+
 static cudaError_t tri_finish(TriShared& S, TriRank& R, const TensorPathArgs& a, ShardAllocFn alloc, void* actx) {
     cudaStream_t st = a.stream;
     cudaError_t e;
     if (R.nu == 0) return cudaSuccess;
+    if (S.tcap) return tcap_finish(S, R, a, alloc, actx);
     uint64_t* cbuf;
     uint32_t* ccnt;
     uint64_t* sel;
@@ -635,12 +679,19 @@ static cudaError_t tri_finish(TriShared& S, TriRank& R, const TensorPathArgs& a,
     };
     Carve c;
     lay(c);
-    c.base = static_cast<uint8_t*>(alloc(actx, kSlotScratch, c.off));
+    // one rank scatters its pool directly, so the pool (kSlotScratch) must
+    // outlive this allocation: use the (unused) receive slot instead
+    const int slot = S.G == 1 ? rank_slot(R.rank, 2) : kSlotScratch;
+    c.base = static_cast<uint8_t*>(alloc(actx, slot, c.off));
     if (!c.base) return cudaErrorMemoryAllocation;
     c.off = 0;
     lay(c);
     if ((e = cudaMemsetAsync(ccnt, 0, size_t(R.nslots) * 4, st)) != cudaSuccess) return e;
-    if (R.rcount)
+    if (S.G == 1)
+        tri_scatter_local_kernel<<<R.nchunks, 256, 0, st>>>(R.lkey, R.lcol, R.lcnt, R.lnext, R.nchunks, S.unit_lidx,
+                                                            ccnt, cbuf, kTriCap,
+                                                            reinterpret_cast<unsigned int*>(R.scal + 40));
+    else if (R.rcount)
         tri_scatter_flat_kernel<<<a.sm_count * 8, 256, 0, st>>>(R.rkey, R.rslot, R.rcount, ccnt, cbuf, kTriCap);
     remap_kernel<<<a.sm_count * 8, 256, 0, st>>>(R.cand, size_t(R.nslots) * 24, S.tri_perm);
     remap_capture_kernel<<<R.nslots, 128, 0, st>>>(cbuf, ccnt, R.nslots, kTriCap, S.tri_perm);
@@ -688,7 +739,8 @@ static float ev_ms(cudaEvent_t x, cudaEvent_t y) {
 // world x 4): per rank [replicated prep + order, phase A, phase B, phase C]
 // in ms (CUDA events); exchange volume per rank in xbytes (optional, world).
 cudaError_t run_tri_loopback(const TensorPathArgs& a, uint32_t G, ShardAllocFn alloc, void* actx,
-                             TensorPathResult& r, float* rank_ms, unsigned long long* xbytes, bool* overflow) {
+                             TensorPathResult& r, float* rank_ms, unsigned long long* xbytes, bool* overflow,
+                             bool tcap) {
     cudaStream_t st = a.stream;
     cudaError_t e;
     TriShared S;
@@ -700,10 +752,11 @@ cudaError_t run_tri_loopback(const TensorPathArgs& a, uint32_t G, ShardAllocFn a
         return err;
     };
     cudaEventRecord(ev[0], st);
-    if ((e = tri_prep(S, a, G, alloc, actx)) != cudaSuccess) return done(e);
+    if ((e = tri_prep(S, a, G, alloc, actx, tcap)) != cudaSuccess) return done(e);
     for (uint32_t g = 0; g < G; ++g)
         if ((e = tri_rank_init(S, R[g], g, a, alloc, actx)) != cudaSuccess) return done(e);
     cudaEventRecord(ev[1], st);
+    if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);  // the sweep phase: sample pass + order + triangle
     std::vector<float> ms_a(G), ms_b(G), ms_c(G);
     for (uint32_t g = 0; g < G; ++g) {  // phase A; exchange 1 is implicit (shared tc2/tl1)
         cudaEventRecord(ev[2], st);
@@ -715,12 +768,11 @@ cudaError_t run_tri_loopback(const TensorPathArgs& a, uint32_t G, ShardAllocFn a
     cudaEventRecord(ev[4], st);
     if ((e = tri_order(S, a)) != cudaSuccess) return done(e);
     cudaEventRecord(ev[5], st);
-    if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
     bool ovf = false;
     for (uint32_t g = 0; g < G; ++g) {  // phase B (the logs are per-rank scratch, binned at once)
         cudaEventRecord(ev[2], st);
         if ((e = tri_sweep(S, R[g], a, alloc, actx)) != cudaSuccess) return done(e);
-        if ((e = tri_bin(S, R[g], a, alloc, actx)) != cudaSuccess) return done(e);
+        if (G > 1 && (e = tri_bin(S, R[g], a, alloc, actx)) != cudaSuccess) return done(e);
         cudaEventRecord(ev[3], st);
         cudaEventSynchronize(ev[3]);
         ms_b[g] = ev_ms(ev[2], ev[3]);
@@ -730,7 +782,7 @@ cudaError_t run_tri_loopback(const TensorPathArgs& a, uint32_t G, ShardAllocFn a
     if (overflow) *overflow = ovf;
     if (ovf) return done(cudaSuccess);  // the caller redoes the call without the triangle
     // exchange 2: rank o receives segment [g -> o] of every rank g, in rank order
-    for (uint32_t o = 0; o < G; ++o) {
+    for (uint32_t o = 0; o < G && G > 1; ++o) {
         unsigned long long cnt = 0;
         for (uint32_t g = 0; g < G; ++g) cnt += R[g].scnt_h[o];
         if ((e = tri_recv_alloc(R[o], cnt, alloc, actx)) != cudaSuccess) return done(e);
@@ -784,13 +836,14 @@ static cudaError_t nccl_err(ncclResult_t x) { return x == ncclSuccess ? cudaSucc
 // reduce-scatter then leaves each rank with its contiguous shard.
 // *overflow: some rank's column-side logs overflowed (all ranks agree).
 cudaError_t run_tri_nccl(const TensorPathArgs& a, ncclComm_t comm, uint32_t rank, uint32_t G, ShardAllocFn alloc,
-                         void* actx, TensorPathResult& r, bool* overflow) {
+                         void* actx, TensorPathResult& r, bool* overflow, bool tcap) {
     cudaStream_t st = a.stream;
     cudaError_t e;
     TriShared S;
     TriRank R;
-    if ((e = tri_prep(S, a, G, alloc, actx)) != cudaSuccess) return e;
+    if ((e = tri_prep(S, a, G, alloc, actx, tcap)) != cudaSuccess) return e;
     if ((e = tri_rank_init(S, R, rank, a, alloc, actx)) != cudaSuccess) return e;
+    if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);  // the sweep phase: sample pass + order + triangle
     if ((e = tri_sample(S, R, a)) != cudaSuccess) return e;
     // exchange 1: every rank's threshold slice (S rows) to every rank, in place
     if ((e = nccl_err(ncclGroupStart())) != cudaSuccess) return e;
@@ -798,8 +851,16 @@ cudaError_t run_tri_nccl(const TensorPathArgs& a, ncclComm_t comm, uint32_t rank
     ncclAllGather(S.tl1 + size_t(rank) * S.S, S.tl1, S.S, ncclFloat32, comm, st);
     if ((e = nccl_err(ncclGroupEnd())) != cudaSuccess) return e;
     if ((e = tri_order(S, a)) != cudaSuccess) return e;
-    if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
     if ((e = tri_sweep(S, R, a, alloc, actx)) != cudaSuccess) return e;
+    if (G == 1) {  // one rank: the pool goes straight to the merge (no exchange 2)
+        if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
+        *overflow = R.overflow;
+        if (R.overflow) return cudaSuccess;
+        if ((e = tri_finish(S, R, a, alloc, actx)) != cudaSuccess) return e;
+        r = R.res;
+        r.launches += 20;
+        return cudaSuccess;
+    }
     if ((e = tri_bin(S, R, a, alloc, actx)) != cudaSuccess) return e;
     if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
     // exchange 2a: the G x (G + 1) count matrix (last column: overflow flag)
@@ -861,94 +922,82 @@ bool tcap_eligible(uint32_t n, uint32_t d, uint32_t klist) {
     return klist > 10 && klist <= 128 && (force ? n >= 512 : n >= 262144);
 }
 
-static uint32_t tcap_cap(uint32_t klist) { return klist <= 47 ? 512u : 1024u; }
+static uint32_t tcap_cap(uint32_t klist) {
+    if (const char* e = getenv("KNN_B200_TCAP_CAP")) return uint32_t(std::max(64, std::min(2048, atoi(e))));
+    (void)klist;
+    return 1024u;  // C4 (k = 32): 512 sent 2x more rows to the retry pass
+}
 
-cudaError_t run_tcap(const TensorPathArgs& a, ShardAllocFn alloc, void* actx, TensorPathResult& r, bool* overflow) {
+// Slot s of a rank's rows (second-order position units[s / 256] * 256 +
+// s % 256): its input row (or ~0 for padding) and its capture threshold.
+__global__ void tcap_slots_kernel(const uint32_t* __restrict__ units, uint32_t nslots, uint32_t n,
+                                  const uint32_t* __restrict__ tri_perm, const float* __restrict__ tri_tc,
+                                  uint32_t* __restrict__ rows, float* __restrict__ thr) {
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < nslots; s += gridDim.x * blockDim.x) {
+        const uint32_t pos = units[s >> 8] * 256 + (s & 255);
+        rows[s] = pos < n ? tri_perm[pos] : 0xffffffffu;
+        thr[s] = pos < n ? tri_tc[pos] : 0.0f;
+    }
+}
+
+// Phase C of the threshold triangle: this rank's rows' captured candidates
+// (pool entries (y, other endpoint) -> per-row buffers), the exact capture
+// rescore with its proof, and a second capture pass for the rows it retries.
+static cudaError_t tcap_finish(TriShared& S, TriRank& R, const TensorPathArgs& a, ShardAllocFn alloc, void* actx) {
     cudaStream_t st = a.stream;
     cudaError_t e;
-    TriShared S;
-    TriRank R;
-    if ((e = tri_prep(S, a, 1, alloc, actx, true)) != cudaSuccess) return e;
-    if ((e = tri_rank_init(S, R, 0, a, alloc, actx)) != cudaSuccess) return e;
-    if ((e = tri_sample(S, R, a)) != cudaSuccess) return e;
-    if ((e = tri_order(S, a)) != cudaSuccess) return e;
-    const uint32_t n = S.n, npad = S.npad, cap = tcap_cap(a.klist);
-    const uint32_t pairs = std::max<uint32_t>(1, std::min<uint32_t>(R.nu, uint32_t(a.sm_count / 2)));
-    // pool: ~ (r x stride) captured entries per row plus the proof band, 2.5x
-    uint64_t pool = uint64_t(2.5 * double(n) * (double(S.trank) * S.stride + 64.0)) + uint64_t(2 * pairs * 8) * kLogChunk;
-    if (const char* lce = getenv("KNN_B200_TRI_LOGCAP")) pool = uint64_t(atoi(lce));
-    const uint32_t nchunks = uint32_t((pool + kLogChunk - 1) / kLogChunk);
-    uint64_t *lkey, *cbuf;
-    uint32_t *lcol, *lcnt, *ccnt, *rowpos2, *fb_rows, *fb_count;
-    float* fb_thr;
+    const uint32_t cap = tcap_cap(a.klist);
+    uint64_t* cbuf;
+    uint32_t *ccnt, *rows, *fb_count;
+    float* thr;
     auto lay = [&](Carve& c) {
-        lkey = c.take<uint64_t>(size_t(nchunks) * kLogChunk);
-        lcol = c.take<uint32_t>(size_t(nchunks) * kLogChunk);
-        lcnt = c.take<uint32_t>(size_t(nchunks) + 1);
-        cbuf = c.take<uint64_t>(size_t(npad) * cap);
-        ccnt = c.take<uint32_t>(npad);
-        rowpos2 = c.take<uint32_t>(n);
-        fb_rows = c.take<uint32_t>(n);
-        fb_thr = c.take<float>(n);
+        cbuf = c.take<uint64_t>(size_t(R.nslots) * cap);
+        ccnt = c.take<uint32_t>(R.nslots);
+        rows = c.take<uint32_t>(R.nslots);
+        thr = c.take<float>(R.nslots);
         fb_count = c.take<uint32_t>(16);
     };
     Carve c;
     lay(c);
-    c.base = static_cast<uint8_t*>(alloc(actx, kSlotScratch, c.off));
+    const int slot = S.G == 1 ? rank_slot(R.rank, 2) : kSlotScratch;  // one rank: the pool is still live
+    c.base = static_cast<uint8_t*>(alloc(actx, slot, c.off));
     if (!c.base) return cudaErrorMemoryAllocation;
     c.off = 0;
     lay(c);
-    uint32_t* lnext = lcnt + nchunks;
-    if ((e = cudaMemsetAsync(lnext, 0, 4, st)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(ccnt, 0, size_t(npad) * 4, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(ccnt, 0, size_t(R.nslots) * 4, st)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(fb_count, 0, 64, st)) != cudaSuccess) return e;
-    const char* dbg = getenv("KNN_B200_DEBUG_SWEEP");
-    SweepParams tp{S.xq2, S.tri_alpha, n,      npad,    S.kc, 0,       n, S.group_tiles, dbg ? atoi(dbg) : 0,
-                   nullptr, S.xq2,     npad,   nullptr, nullptr, nullptr, 0, S.bmin2,
-                   S.tri_tc, S.tcmax,  lkey,   lcol,    lcnt,  lnext,  nchunks};
-    tp.units = R.units;
-    tp.nunits = R.nu;
-    if (a.ev_sweep0) cudaEventRecord(a.ev_sweep0, st);
-    e = S.kc <= uint32_t(TS_MAX_RES_KC) ? launch_sweep_pair<2, 256, 8, true, true, true>(tp, R.nslots, st)
-                                        : launch_sweep_pair<2, 256, 8, true, true, false>(tp, R.nslots, st);
-    if (e != cudaSuccess) return e;
-    tri_scatter_kernel<<<nchunks, 256, 0, st>>>(lkey, lcol, lcnt, lnext, nchunks, ccnt, cbuf, cap,
-                                                reinterpret_cast<unsigned int*>(R.scal + 40));
-    if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
-    remap_capture_kernel<<<n, 128, 0, st>>>(cbuf, ccnt, n, cap, S.tri_perm);
-    invert_perm_kernel<<<a.sm_count * 4, 256, 0, st>>>(S.tri_perm, n, rowpos2);
+    if (S.G == 1)
+        tri_scatter_local_kernel<<<R.nchunks, 256, 0, st>>>(R.lkey, R.lcol, R.lcnt, R.lnext, R.nchunks, S.unit_lidx,
+                                                            ccnt, cbuf, cap,
+                                                            reinterpret_cast<unsigned int*>(R.scal + 40));
+    else if (R.rcount)
+        tri_scatter_flat_kernel<<<a.sm_count * 8, 256, 0, st>>>(R.rkey, R.rslot, R.rcount, ccnt, cbuf, cap);
+    remap_capture_kernel<<<R.nslots, 128, 0, st>>>(cbuf, ccnt, R.nslots, cap, S.tri_perm);
+    tcap_slots_kernel<<<a.sm_count * 4, 256, 0, st>>>(R.units, R.nslots, S.n, S.tri_perm, S.tri_tc, rows, thr);
     unsigned long long* rescored = reinterpret_cast<unsigned long long*>(R.scal + 32);
-    Rescore2Params r2{a.X,  n,   a.d,        a.klist,     0,          S.tri_perm, n,        ccnt,
-                      cbuf, cap, a.out_sqrt, a.out_index, a.out_dist, fb_count,   fb_rows,  rescored,
-                      S.tri_tc, rowpos2, S.tri_alpha, S.tri_rho, S.tri_xnorm, S.gmax, S.maxabs};
-    r2.retry_thr = fb_thr;
+    Rescore2Params r2{a.X,  S.n, a.d,        a.klist,     0,          rows,     R.nslots, ccnt,
+                      cbuf, cap, a.out_sqrt, a.out_index, a.out_dist, fb_count, R.fb_rows, rescored,
+                      thr,  S.tri_rowpos, S.tri_alpha, S.tri_rho, S.tri_xnorm, S.gmax, S.maxabs};
+    r2.retry_thr = R.fb_thr;
     r2.loose = S.tri_tl;
-    const size_t smem2 = size_t(4) * cap * 8;
-    if (a.fold == kCosine) {
-        cudaFuncSetAttribute(rescore_capture_kernel<kCosine>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
-        rescore_capture_kernel<kCosine><<<(n + 3) / 4, 128, smem2, st>>>(r2);
-    } else {
-        cudaFuncSetAttribute(rescore_capture_kernel<kSqEuclidean>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem2));
-        rescore_capture_kernel<kSqEuclidean><<<(n + 3) / 4, 128, smem2, st>>>(r2);
-    }
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    e = a.fold == kCosine ? launch_rescore_capture<kCosine>(r2, R.nslots, st)
+                          : launch_rescore_capture<kSqEuclidean>(r2, R.nslots, st);
+    if (e != cudaSuccess) return e;
     uint32_t* h = static_cast<uint32_t*>(a.host_scratch);
     if ((e = cudaMemcpyAsync(h, fb_count, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
-    if ((e = cudaMemcpyAsync(h + 2, R.scal + 40, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
-    if ((e = cudaMemcpyAsync(h + 4, rescored, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(h + 2, rescored, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
     const uint32_t nretry = h[0];
-    *overflow = h[2] != 0;
-    r.rescored = *reinterpret_cast<const unsigned long long*>(h + 4);
-    r.fallback_rows = nretry;
-    r.launches += 30;
-    if (*overflow || nretry == 0) return cudaSuccess;
-    // second capture pass: the retried rows against their implied thresholds
+    R.res.rescored = *reinterpret_cast<const unsigned long long*>(h + 2);
+    R.res.fallback_rows = nretry;
+    R.res.launches += 5;
+    if (nretry == 0) return cudaSuccess;
+    // second capture pass: the retried rows against their implied thresholds,
+    // with room for wider bands (rows that filled their first buffer)
     const CaptureArgs ca{S.xh, S.alpha, S.rho, S.xnorm, S.gmax, S.maxabs, S.bmin, S.cosine ? nullptr : S.perm,
-                         S.cosine ? nullptr : S.rowpos, n, npad, S.kc, S.group_tiles, cap, fb_rows, fb_thr,
-                         rescored};
-    return run_capture(a, ca, nretry, r, r.launches);
+                         S.cosine ? nullptr : S.rowpos, S.n, S.npad, S.kc, S.group_tiles, 2048u, R.fb_rows,
+                         R.fb_thr, rescored};
+    return run_capture(a, ca, nretry, R.res, R.res.launches);
 }
 
 }  // namespace knnb

@@ -136,3 +136,24 @@ def test_solve_multi_nccl_path_one_gpu(c_oracle):
     for lanes in (1, 4):
         r = solve_knn(Dataset.from_array(x), squared_euclidean(), EngineOptions(k=10, n_lanes=lanes))
         assert_lists_bit_equal(r.index[rows], r.distance[rows], ri, rd, f"solve_knn lanes={lanes}")
+
+
+@pytest.mark.parametrize("world,n,d,k,metric", [(2, 20000, 48, 30, "sqeuclidean"), (3, 9000, 300, 100, "euclidean"),
+                                                (8, 12000, 64, 20, "cosine"), (5, 4000, 20, 64, "hellinger")])
+def test_loopback_threshold_triangle_all_rows(ctx, c_oracle, monkeypatch, world, n, d, k, metric):
+    """The threshold triangle (10 < k <= 128) sharded the same way: every
+    pair once across the ranks, both endpoints' candidates binned by owner,
+    the capture rescore at the owner -- every row against the oracle."""
+    import torch
+    from oracle import normalize_rows
+    from paper_0906_0231_b200 import solve_sharded_loopback_torch
+    monkeypatch.setenv("KNN_B200_TCAP", "force")
+    xh = c_oracle.generate(n, d, n + world)
+    if metric == "cosine":
+        xh = normalize_rows(xh)
+    x = torch.from_numpy(np.ascontiguousarray(xh)).cuda()
+    iw, dw, st, rank_ms, xbytes = solve_sharded_loopback_torch(ctx, x, k, _metric(metric), world)
+    assert st["reserved"] == 0
+    ri, rd = _oracle_rows(c_oracle, xh, k, metric, np.arange(n, dtype=np.uint32))
+    assert_lists_bit_equal(iw.cpu().numpy().view(np.uint32), dw.cpu().numpy(), ri, rd,
+                           f"threshold-triangle loopback world={world} n={n} {metric}")
