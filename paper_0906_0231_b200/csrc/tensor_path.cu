@@ -133,10 +133,14 @@ struct SweepParams {
 // Candidate keys from the norm-sorted sweep carry sweep-order column indices;
 // map them to input indices once (the rescores and the reference's
 // (distance, index) tie-break work in input order).
-__global__ void remap_kernel(uint64_t* __restrict__ keys, size_t count, const uint32_t* __restrict__ perm) {
+// (n: the size of perm -- a sharded rank's padding slots hold stale keys
+// from earlier calls, which must not be looked up)
+__global__ void remap_kernel(uint64_t* __restrict__ keys, size_t count, const uint32_t* __restrict__ perm,
+                             uint32_t n) {
     for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += size_t(gridDim.x) * blockDim.x) {
         const uint64_t k = keys[i];
-        if (k != kEmptyKey && uint32_t(k) != kVirtualIdx) keys[i] = (k & 0xffffffff00000000ull) | perm[uint32_t(k)];
+        if (k != kEmptyKey && uint32_t(k) != kVirtualIdx && uint32_t(k) < n)
+            keys[i] = (k & 0xffffffff00000000ull) | perm[uint32_t(k)];
     }
 }
 
@@ -527,7 +531,7 @@ tensor_sweep_kernel(const SweepParams p) {
                 // (y', row) for column col; the threshold triangle's row side:
                 // (col) for this row.  Slots come from a ballot prefix (no
                 // atomics but one per pool chunk); a select tree picks each dot.
-                auto append = [&](uint32_t m, const uint32_t (&v)[W], uint32_t col0, bool rowside) {
+                auto append = [&](uint32_t m, const uint32_t (&v)[W], uint32_t col0, bool rowside, float bm) {
                     while (__any_sync(0xffffffffu, m != 0)) {
                         const int bpos = m ? __ffs(m) - 1 : 0;
                         const bool ok = m != 0 && col0 + bpos < p.n;
@@ -554,10 +558,12 @@ tensor_sweep_kernel(const SweepParams p) {
 #pragma unroll
                             for (int q = 0; q < 2; ++q) t16[q] = (bpos & 2) ? t16[q + 2] : t16[q];
                             const float dot = __uint_as_float((bpos & 1) ? t16[1] : t16[0]);
-                            // key: (y relative to the destination row, the other endpoint)
-                            const uint64_t key =
-                                rowside ? make_key(__fmaf_rn(-2.0f, dot, __ldg(p.alpha + col0 + bpos)), col0 + bpos)
-                                        : make_key(__fmaf_rn(-2.0f, dot, alpha_i), row);
+                            // key: (y relative to the destination row, the other endpoint);
+                            // the row side uses the chunk's smallest norm bm for beta_j: a
+                            // lower bound on y, which is all the capture rescore's ordering
+                            // and skip test need (a smaller A is never skipped wrongly)
+                            const uint64_t key = rowside ? make_key(__fmaf_rn(-2.0f, dot, bm), col0 + bpos)
+                                                         : make_key(__fmaf_rn(-2.0f, dot, alpha_i), row);
                             if (wchunk < p.nchunks) {
                                 p.lkey[slot] = key;
                                 p.lcol[slot] = rowside ? row : col0 + bpos;
@@ -582,7 +588,7 @@ tensor_sweep_kernel(const SweepParams p) {
                                 for (int j = 0; j < W; ++j)
                                     if (__uint_as_float(v[j]) > hc) cm |= 1u << j;
                             }
-                            append(cm, v, col0, false);
+                            append(cm, v, col0, false, 0.0f);
                         }
                         if constexpr (TCAP) {
                             // row side against the fixed threshold: dot > hr, a
@@ -594,7 +600,7 @@ tensor_sweep_kernel(const SweepParams p) {
                                     for (int j = 0; j < W; ++j)
                                         if (__uint_as_float(v[j]) > hr) rm |= 1u << j;
                                 }
-                                append(rm, v, col0, true);
+                                append(rm, v, col0, true, __ldg(p.bmin + (col0 >> 5)));
                             }
                             return;
                         }
@@ -2285,7 +2291,7 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
     ++launches;
     if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
     if (sorted) {
-        remap_kernel<<<a.sm_count * 8, 256, 0, st>>>(cand, size_t(nrows) * kp, perm);
+        remap_kernel<<<a.sm_count * 8, 256, 0, st>>>(cand, size_t(nrows) * kp, perm, n);
         ++launches;
     }
 

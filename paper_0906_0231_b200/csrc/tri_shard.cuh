@@ -371,11 +371,12 @@ static cudaError_t tri_prep(TriShared& S, const TensorPathArgs& a, uint32_t G, S
     S.cosine = a.fold == kCosine;
     if (tcap) {
         // the sample pass estimates each row's k-th distance: every 16th
-        // (k <= 47) or 32nd column, E4M3 operands (the dot's error is well
-        // inside the gap between the k-th and the r x stride-th neighbour at
-        // C3 and C4), 2 x 16-entry lists, the rank-r value with
-        // r ~ k / stride + 2.5 sqrt(k / stride) + 1 (tcap_threshold_kernel)
+        // (k <= 47) or 32nd column, fp16 operands (E4M3 thresholds are
+        // noisier: at C4 twice the rows needed a retry), 2 x 16-entry lists,
+        // the rank-r value with r ~ k / stride + 2.5 sqrt(k / stride) + 1
+        // (tcap_threshold_kernel)
         S.skpl = 16;
+        S.f8 = false;  // tuning: KNN_B200_TCAP_E4M3=1 (C4: 2x the retried rows, sweep +0.5 s)
         S.stride = a.klist <= 47 ? 16 : 32;  // tuning: KNN_B200_TCAP_STRIDE
         if (const char* se = getenv("KNN_B200_TCAP_STRIDE")) S.stride = std::max(1, atoi(se));
         if (const char* fe = getenv("KNN_B200_TCAP_E4M3")) S.f8 = atoi(fe) != 0;
@@ -693,7 +694,7 @@ static cudaError_t tri_finish(TriShared& S, TriRank& R, const TensorPathArgs& a,
                                                             reinterpret_cast<unsigned int*>(R.scal + 40));
     else if (R.rcount)
         tri_scatter_flat_kernel<<<a.sm_count * 8, 256, 0, st>>>(R.rkey, R.rslot, R.rcount, ccnt, cbuf, kTriCap);
-    remap_kernel<<<a.sm_count * 8, 256, 0, st>>>(R.cand, size_t(R.nslots) * 24, S.tri_perm);
+    remap_kernel<<<a.sm_count * 8, 256, 0, st>>>(R.cand, size_t(R.nslots) * 24, S.tri_perm, S.n);
     remap_capture_kernel<<<R.nslots, 128, 0, st>>>(cbuf, ccnt, R.nslots, kTriCap, S.tri_perm);
     tri_select_kernel<<<(R.nslots * 32 + 255) / 256, 256, 0, st>>>(cbuf, ccnt, kTriCap, R.nslots, S.tri_tc, sel, selcnt,
                                                                      selbound, R.units);

@@ -32,10 +32,15 @@ ap.add_argument("--seed", type=int, default=1)
 ap.add_argument("--worlds", default="1,2,4,8")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--nvlink-gbs", type=float, default=300.0)
+ap.add_argument("--metric", default="euclidean")
 a = ap.parse_args()
 ctx = Context(0)
 x = generate_torch(ctx, a.n, a.d, a.seed)
-m = distance_by_name("euclidean")
+if a.metric == "cosine":  # rows L2-normalised in double, stored f32
+    xd = x.double()
+    x = (xd / xd.norm(dim=1, keepdim=True)).float().contiguous()
+    del xd
+m = distance_by_name(a.metric)
 klist = min(a.k, a.n - 1)
 # the sharded runs first, on their own context (its workspace is freed
 # before the single-GPU solve allocates its own: C5 needs both to fit)
