@@ -387,7 +387,15 @@ void solve_rows_core(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, 
         ta.out_sqrt = out_sqrt;
         ta.out_index = out_index;
         ta.out_dist = out_dist;
-        ta.workspace = ctx->tensor_ws.get(knnb::tensor_workspace_bytes(n, d, row_begin, row_end, klist, ctx->sm_count));
+        // the rectangular sweep's workspace, allocated only if that path runs
+        // (whole problems take a triangle, which uses the slot buffers)
+        ta.alloc_ws = [](void* c, size_t bytes) -> void* {
+            try {
+                return static_cast<knn_b200_ctx*>(c)->tensor_ws.get(bytes);
+            } catch (...) {
+                return nullptr;
+            }
+        };
         ta.host_scratch = ctx->host_flags + 4;
         ta.exact_scratch = ctx->exact_ws.get(std::max<size_t>(
             16, knnb::exact_scratch_bytes(row_end - row_begin, n, klist, ctx->sm_count)));

@@ -56,7 +56,8 @@ struct TensorPathArgs {
     int out_sqrt;
     uint32_t* out_index;
     float* out_dist;
-    void* workspace;      // tensor_workspace_bytes()
+    void* workspace;      // tensor_workspace_bytes(), or null: taken from alloc_ws(alloc2_ctx, bytes) on demand
+    void* (*alloc_ws)(void* ctx, size_t bytes);
     void* exact_scratch;  // exact_scratch_bytes(row_end - row_begin, ...) for fallback rows
     void* host_scratch;   // 64 B pinned
     int sm_count;

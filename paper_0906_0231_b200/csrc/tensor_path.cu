@@ -720,11 +720,37 @@ tensor_sweep_kernel(const SweepParams p) {
                     if (!__any_sync(0xffffffffu, fire_r || fire_c) || p.debug_mode == 4) return;
                     handle(v, col0, fire_r, fire_c, hc, hr1);
                 };
+                constexpr int NCH = SEG_COLS / 32;
                 for (uint32_t t = ts; t < t1; ++t, ++tcount) {
                     const uint32_t b = tcount & 1, use = tcount >> 1;
+                    const uint32_t cbase = t * BN + seg0;
+                    // the tile's chunk norms (and column thresholds) are loaded
+                    // before the accumulator wait, so their L2 latency overlaps it
+                    float bmv[NCH], tcm[NCH];
+                    {
+                        const float* bp = p.bmin + (cbase >> 5);
+                        if constexpr (NCH % 4 == 0) {
+#pragma unroll
+                            for (int q = 0; q < NCH / 4; ++q) {
+                                const float4 f = __ldg(reinterpret_cast<const float4*>(bp) + q);
+                                bmv[4 * q] = f.x, bmv[4 * q + 1] = f.y, bmv[4 * q + 2] = f.z, bmv[4 * q + 3] = f.w;
+                            }
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < NCH; ++q) bmv[q] = __ldg(bp + q);
+                        }
+#pragma unroll
+                        for (int q = 0; q < NCH; ++q) tcm[q] = kInf;
+                        if constexpr (TRI) {
+                            if (TRI && t > tsu && valid) {
+                                const float* tp = p.tcmax + (cbase >> 5);
+#pragma unroll
+                                for (int q = 0; q < NCH; ++q) tcm[q] = __ldg(tp + q);
+                            }
+                        }
+                    }
                     wait(tfull_bar(b), use & 1);
                     ptx::tc_fence_after();
-                    const uint32_t cbase = t * BN + seg0;
                     const uint32_t taddr = lane_addr + b * BN + seg0;
                     const bool first = DIRECT && g == 0 && t == 0;
                     const bool cside = TRI && t > tsu;  // tiles above the unit's own: both sides
@@ -748,35 +774,11 @@ tensor_sweep_kernel(const SweepParams p) {
                     // This tile's chunk bounds, once per tile.  A row bound computed
                     // before an insertion earlier in the tile is below the fresh
                     // one (thr only falls), so it admits a superset: still exact.
-                    constexpr int NCH = SEG_COLS / 32;
                     float hr[NCH], hcv[NCH];
-                    {
-                        float bmv[NCH];
-                        const float* bp = p.bmin + (cbase >> 5);
-                        if constexpr (NCH % 4 == 0) {
 #pragma unroll
-                            for (int q = 0; q < NCH / 4; ++q) {
-                                const float4 f = __ldg(reinterpret_cast<const float4*>(bp) + q);
-                                bmv[4 * q] = f.x, bmv[4 * q + 1] = f.y, bmv[4 * q + 2] = f.z, bmv[4 * q + 3] = f.w;
-                            }
-                        } else {
-#pragma unroll
-                            for (int q = 0; q < NCH; ++q) bmv[q] = __ldg(bp + q);
-                        }
-#pragma unroll
-                        for (int q = 0; q < NCH; ++q) {
-                            hr[q] = row_bound(bmv[q]);
-                            hcv[q] = kInf;
-                        }
-                        if constexpr (TRI) {
-                            if (cside) {
-                                const float* tp = p.tcmax + (cbase >> 5);
-#pragma unroll
-                                for (int q = 0; q < NCH; ++q) {
-                                    hcv[q] = valid ? col_bound(__ldg(tp + q)) : kInf;
-                                }
-                            }
-                        }
+                    for (int q = 0; q < NCH; ++q) {
+                        hr[q] = row_bound(bmv[q]);
+                        hcv[q] = TRI && cside && valid ? col_bound(tcm[q]) : kInf;
                     }
                     uint32_t va[32], vb[32];
                     // two chunks per step: both TMEM reads, two independent max
@@ -2194,6 +2196,10 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
     const uint32_t kp = cfg.kpl * cfg.nseg;
     const int cosine = a.fold == kCosine;
     uint8_t* w = static_cast<uint8_t*>(a.workspace);
+    if (!w && a.alloc_ws)
+        w = static_cast<uint8_t*>(
+            a.alloc_ws(a.alloc2_ctx, tensor_workspace_bytes(n, d, a.row_begin, a.row_end, a.klist, a.sm_count)));
+    if (!w) return cudaErrorMemoryAllocation;
     auto take = [&](size_t x) {
         uint8_t* p = w;
         w += (x + 255) / 256 * 256;

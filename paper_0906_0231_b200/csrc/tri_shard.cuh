@@ -548,8 +548,8 @@ static cudaError_t tri_sweep(TriShared& S, TriRank& R, const TensorPathArgs& a, 
     cudaStream_t st = a.stream;
     cudaError_t e;
     const uint32_t pairs = std::max<uint32_t>(1, std::min<uint32_t>(R.nu, uint32_t(a.sm_count / 2)));
-    // the column-side pool: 4x this rank's expected volume (~64 entries per
-    // row over the whole triangle).  A unit's share lies between "in
+    // the column-side pool: 3x this rank's expected volume (~64 entries per
+    // row over the whole triangle; C2 uses 63).  A unit's share lies between "in
     // proportion to its pairs" and "the same for every unit" (a column's
     // candidates come from rows near it in the norm order): take the larger.
     double share_w = 0;
@@ -558,7 +558,7 @@ static cudaError_t tri_sweep(TriShared& S, TriRank& R, const TensorPathArgs& a, 
     const double share = std::max(total > 0 ? share_w / total : 1.0, double(R.nu) / double(S.U));
     // the threshold triangle: ~ (r x stride) captured entries per row plus
     // the proof band (tcap_threshold_kernel; C3 ~ 350, C4 ~ 220 per row), 2.5x
-    const double per_row = S.tcap ? 2.5 * (double(S.trank) * S.stride + 64.0) : 4.0 * 64.0;
+    const double per_row = S.tcap ? 2.5 * (double(S.trank) * S.stride + 64.0) : 3.0 * 64.0;  // C2 uses ~63
     uint64_t pool = uint64_t(per_row * double(S.n) * share) + uint64_t(2 * pairs * 8) * kLogChunk;
     if (const char* lce = getenv("KNN_B200_TRI_LOGCAP")) pool = uint64_t(atoi(lce));
     R.nchunks = uint32_t((pool + kLogChunk - 1) / kLogChunk);
