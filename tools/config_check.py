@@ -1,5 +1,6 @@
 """Full-size config run on the GPU + sampled-row parity against the oracle
-(dev tool; the committed test is tests/test_gpu_parity.py::test_full_configs)."""
+(dev tool; the committed tests are tests/test_gpu_configs.py::test_c1_all_rows,
+test_c3_full_size, test_c4_full_size and test_c5_full_size_one_gpu)."""
 import argparse, sys, time
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
