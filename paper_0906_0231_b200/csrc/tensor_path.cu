@@ -780,38 +780,6 @@ tensor_sweep_kernel(const SweepParams p) {
                         hr[q] = row_bound(bmv[q]);
                         hcv[q] = TRI && cside && valid ? col_bound(tcm[q]) : kInf;
                     }
-                    if constexpr (TCAP && NCH == 4) {
-                        // no lists to hold: all 128 of this warp's columns come out
-                        // of TMEM in one round trip, the accumulator is released at
-                        // once, then the two chunk pairs are filtered
-                        uint32_t va[32], vb[32], vc[32], vd[32];
-                        ptx::tmem_ld_32x32b_x32(taddr, va);
-                        ptx::tmem_ld_32x32b_x32(taddr + 32, vb);
-                        ptx::tmem_ld_32x32b_x32(taddr + 64, vc);
-                        ptx::tmem_ld_32x32b_x32(taddr + 96, vd);
-                        ptx::tmem_wait_ld();
-                        ptx::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) release_acc(b);
-                        if (p.debug_mode == 4) continue;
-                        {
-                            const float da = vmax(va), db = vmax(vb);
-                            const bool ra = da > hr[0], rb = db > hr[1], fa = da > hcv[0], fb = db > hcv[1];
-                            if (__any_sync(0xffffffffu, ra || rb || fa || fb)) {
-                                if (__any_sync(0xffffffffu, ra || fa)) handle(va, cbase, ra, fa, hcv[0], hr[0]);
-                                if (__any_sync(0xffffffffu, rb || fb)) handle(vb, cbase + 32, rb, fb, hcv[1], hr[1]);
-                            }
-                        }
-                        {
-                            const float dc = vmax(vc), dd = vmax(vd);
-                            const bool rc = dc > hr[2], rd = dd > hr[3], fc = dc > hcv[2], fd = dd > hcv[3];
-                            if (__any_sync(0xffffffffu, rc || rd || fc || fd)) {
-                                if (__any_sync(0xffffffffu, rc || fc)) handle(vc, cbase + 64, rc, fc, hcv[2], hr[2]);
-                                if (__any_sync(0xffffffffu, rd || fd)) handle(vd, cbase + 96, rd, fd, hcv[3], hr[3]);
-                            }
-                        }
-                        continue;
-                    }
                     uint32_t va[32], vb[32];
                     // two chunks per step: both TMEM reads, two independent max
                     // trees, one vote; column norms only for chunks that reach

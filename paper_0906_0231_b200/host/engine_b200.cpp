@@ -14,11 +14,13 @@
 // The arithmetic policy is chosen out of band (EngineOptions has no field):
 // KNN_B200_ARITH=auto|exact|tensor, default auto.  All policies return the
 // same bits.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <type_traits>
 #include <vector>
 
@@ -175,17 +177,28 @@ EngineResult solve_knn(const Dataset& ds, const CumulativeDistance& f, const Eng
     const int rc = gpu_solve(ds, opt, metric, arith, plan.n_lanes, index.data(), dist.data(), &st);
     if (rc != KNN_B200_OK) rethrow_status(rc);
 
+    // EngineResult owns one std::vector per row (engine.hpp:25-31): at C2
+    // that is 1M heap allocations, built by a few host threads in parallel
+    // (one thread took ~110 ms of the drop-in's end-to-end time).
     EngineResult result;
     result.lists.resize(n);
-    for (std::uint32_t i = 0; i < n; ++i) {
-        NeighborList& list = result.lists[i];
-        list.query = i;
-        list.neighbors.resize(klist);
-        const std::size_t base = std::size_t(i) * klist;
-        for (std::uint32_t j = 0; j < klist; ++j) {
-            list.neighbors[j] = Neighbor{dist[base + j], index[base + j]};
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const std::uint32_t nthreads = n < 65536 ? 1u : std::min<std::uint32_t>(16u, hw);
+    auto fill = [&](std::uint32_t r0, std::uint32_t r1) {
+        for (std::uint32_t i = r0; i < r1; ++i) {
+            NeighborList& list = result.lists[i];
+            list.query = i;
+            list.neighbors.resize(klist);
+            const std::size_t base = std::size_t(i) * klist;
+            for (std::uint32_t j = 0; j < klist; ++j) list.neighbors[j] = Neighbor{dist[base + j], index[base + j]};
         }
-    }
+    };
+    std::vector<std::thread> pool;
+    for (std::uint32_t t = 1; t < nthreads; ++t)
+        pool.emplace_back(fill, std::uint32_t(std::uint64_t(n) * t / nthreads),
+                          std::uint32_t(std::uint64_t(n) * (t + 1) / nthreads));
+    fill(0, std::uint32_t(std::uint64_t(n) / nthreads));
+    for (auto& th : pool) th.join();
     result.seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     result.plan = plan;
