@@ -62,7 +62,14 @@ typedef enum {
     KNN_B200_METRIC_COSINE = 2,
     /* "Euclidean" of the BASELINE configs: selection on the
      * sqeuclidean fold, reported distance = IEEE sqrtf of it at output. */
-    KNN_B200_METRIC_EUCLIDEAN = 3
+    KNN_B200_METRIC_EUCLIDEAN = 3,
+    /* Custom folds of the reference's registry (distance.hpp:68-77) the
+     * device restates, EXACT policy: manhattan = acc + |u - v|
+     * (test_distance.cpp:134-145); root-of-squares = the sqeuclidean fold
+     * with finalize sqrt, ranked by the finalized distance
+     * (test_distance.cpp:166-178). */
+    KNN_B200_METRIC_MANHATTAN = 4,
+    KNN_B200_METRIC_ROOT_SQUARES = 5
 } knn_b200_metric;
 
 /* Arithmetic policy for Phase 1 (EngineOptions has no field for it; the C++

@@ -27,7 +27,7 @@ HERE = Path(__file__).resolve().parent
 C_ORACLE_PATH = HERE / "libknn_oracle.so"
 REF_CAPI_PATH = HERE / "_ref" / "libtknn_ref_capi.so"
 
-METRICS = {"hellinger": 0, "sqeuclidean": 1, "cosine": 2}
+METRICS = {"hellinger": 0, "sqeuclidean": 1, "cosine": 2, "manhattan": 3, "root_of_squares": 4}
 
 _u32p = ctypes.POINTER(ctypes.c_uint32)
 _f32p = ctypes.POINTER(ctypes.c_float)

@@ -37,7 +37,10 @@
 #include <stdlib.h>
 #include <string.h>
 
-enum { KO_HELLINGER = 0, KO_SQEUCLIDEAN = 1, KO_COSINE = 2 };
+/* KO_MANHATTAN and KO_ROOT_SQUARES restate the custom functors the
+ * reference's own tests register: test_distance.cpp:134-145 (acc +
+ * dist_t(fabs(u - v))) and :166-178 (the sqeuclidean step, finalize sqrt). */
+enum { KO_HELLINGER = 0, KO_SQEUCLIDEAN = 1, KO_COSINE = 2, KO_MANHATTAN = 3, KO_ROOT_SQUARES = 4 };
 
 /* ---- rng.hpp:13-23 ---------------------------------------------------- */
 uint64_t ko_splitmix64_next(uint64_t *state) {
@@ -86,6 +89,15 @@ float ko_fold(int metric, const float *u, const float *v, uint32_t d) {
     case KO_COSINE:
         for (uint32_t j = 0; j < d; ++j) acc = acc + u[j] * v[j];
         return 1.0f - acc;
+    case KO_MANHATTAN:
+        for (uint32_t j = 0; j < d; ++j) acc = acc + fabsf(u[j] - v[j]);
+        return acc;
+    case KO_ROOT_SQUARES:
+        for (uint32_t j = 0; j < d; ++j) {
+            const float t = u[j] - v[j];
+            acc = acc + t * t;
+        }
+        return sqrtf(acc);
     default:
         return NAN;
     }
@@ -242,6 +254,15 @@ double ko_fold_f64(int metric, const float *u, const float *v, uint32_t d) {
     case KO_COSINE:
         for (uint32_t j = 0; j < d; ++j) acc = acc + (double)u[j] * (double)v[j];
         return 1.0 - acc;
+    case KO_MANHATTAN:
+        for (uint32_t j = 0; j < d; ++j) acc = acc + (double)fabsf(u[j] - v[j]);
+        return acc;
+    case KO_ROOT_SQUARES:
+        for (uint32_t j = 0; j < d; ++j) {
+            const float t = u[j] - v[j];
+            acc = acc + (double)t * (double)t;
+        }
+        return sqrt(acc);
     default:
         return NAN;
     }

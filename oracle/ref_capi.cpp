@@ -27,6 +27,8 @@
 #include "knn/distance.hpp"
 #include "knn/engine.hpp"
 #include "knn/errors.hpp"
+#include <cmath>
+
 #include "knn/heap.hpp"
 #include "knn/io.hpp"
 #include "knn/oracle.hpp"
@@ -48,11 +50,41 @@ const knn::CumulativeDistance& cosine_fold() {
     return f;
 }
 
+// The custom functors of the reference's own tests, registered through the
+// reference's registry: test_distance.cpp:134-145 and :166-178.
+const knn::CumulativeDistance& manhattan_fold() {
+    static const knn::CumulativeDistance& f = [] () -> const knn::CumulativeDistance& {
+        knn::CumulativeDistance c;
+        c.name = "manhattan";
+        c.initial = 0;
+        c.step = +[](float u, float v, knn::dist_t acc) { return acc + knn::dist_t(std::fabs(u - v)); };
+        return knn::register_distance(c);
+    }();
+    return f;
+}
+
+const knn::CumulativeDistance& root_squares_fold() {
+    static const knn::CumulativeDistance& f = [] () -> const knn::CumulativeDistance& {
+        knn::CumulativeDistance c;
+        c.name = "root_of_squares";
+        c.initial = 0;
+        c.step = +[](float u, float v, knn::dist_t acc) {
+            const float t = u - v;
+            return acc + knn::dist_t(t) * knn::dist_t(t);
+        };
+        c.finalize = +[](knn::dist_t acc) { return knn::dist_t(std::sqrt(acc)); };
+        return knn::register_distance(c);
+    }();
+    return f;
+}
+
 const knn::CumulativeDistance& metric_by_id(int metric) {
     switch (metric) {
     case 0: return knn::distance_by_name("hellinger");
     case 1: return knn::distance_by_name("sqeuclidean");
     case 2: return cosine_fold();
+    case 3: return manhattan_fold();
+    case 4: return root_squares_fold();
     default: throw knn::ConfigError("unknown metric id " + std::to_string(metric));
     }
 }

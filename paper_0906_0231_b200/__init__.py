@@ -29,6 +29,8 @@ from .engine import (  # noqa: F401
     generate_torch,
     hellinger,
     make_plan,
+    manhattan,
+    root_of_squares,
     solve_knn,
     comm_broadcast_torch,
     comm_init,

@@ -41,6 +41,7 @@ ABI_VERSION = 2
 
 OK, ERR_CONFIG, ERR_VALIDATION, ERR_INTERNAL = 0, 2, 3, 4
 METRIC_HELLINGER, METRIC_SQEUCLIDEAN, METRIC_COSINE, METRIC_EUCLIDEAN = 0, 1, 2, 3
+METRIC_MANHATTAN, METRIC_ROOT_SQUARES = 4, 5
 ARITH_AUTO, ARITH_EXACT, ARITH_TENSOR = 0, 1, 2
 ARITH_NAMES = {"auto": ARITH_AUTO, "exact": ARITH_EXACT, "tensor": ARITH_TENSOR}
 

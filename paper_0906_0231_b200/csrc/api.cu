@@ -280,16 +280,31 @@ const char* metric_name(int metric) {
     case KNN_B200_METRIC_SQEUCLIDEAN: return "sqeuclidean";
     case KNN_B200_METRIC_COSINE: return "cosine";
     case KNN_B200_METRIC_EUCLIDEAN: return "euclidean";
+    case KNN_B200_METRIC_MANHATTAN: return "manhattan";
+    case KNN_B200_METRIC_ROOT_SQUARES: return "root_of_squares";
     default: return "?";
     }
 }
+
+// The device fold of a metric id (kernels: common.cuh).
+int fold_of(int metric) {
+    switch (metric) {
+    case KNN_B200_METRIC_COSINE: return knnb::kCosine;
+    case KNN_B200_METRIC_MANHATTAN: return knnb::kManhattan;
+    case KNN_B200_METRIC_ROOT_SQUARES: return knnb::kRootSquares;
+    default: return knnb::kSqEuclidean;  // sqeuclidean, euclidean, sqrt-staged hellinger
+    }
+}
+
+// Folds the TENSOR filter's completeness proof covers.
+bool tensor_fold(int metric) { return metric <= KNN_B200_METRIC_EUCLIDEAN; }
 
 void check_args(uint32_t n, uint32_t d, uint32_t k, int metric, int arith) {
     // engine.cpp:15 (k), schedule.cpp:12 (n), dataset.cpp:13-19 (n, d)
     if (k < 1) fail(KNN_B200_ERR_CONFIG, "k must be at least 1");
     if (n < 2) fail(KNN_B200_ERR_CONFIG, "n must be at least 2, got " + std::to_string(n));
     if (d < 1) fail(KNN_B200_ERR_CONFIG, "dataset dimension must be at least 1");
-    if (metric < 0 || metric > 3) fail(KNN_B200_ERR_CONFIG, "unknown metric id " + std::to_string(metric));
+    if (metric < 0 || metric > 5) fail(KNN_B200_ERR_CONFIG, "unknown metric id " + std::to_string(metric));
     if (arith < 0 || arith > 2) fail(KNN_B200_ERR_CONFIG, "unknown arithmetic policy " + std::to_string(arith));
     // any k: lists longer than the fused kernels hold (kExactMaxK) take the
     // sort-based EXACT path (exact_bigk.cu), as HeapStore holds min(k, n-1)
@@ -353,7 +368,7 @@ void solve_rows_core(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, 
         Xs = staged;
     }
     const uint32_t klist = std::min(k, n - 1);
-    const int fold = metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean;
+    const int fold = fold_of(metric);
     const int out_sqrt = metric == KNN_B200_METRIC_EUCLIDEAN;
     if (klist > knnb::kExactMaxK) {  // long lists: sort-based EXACT path
         ctr.arith_used = KNN_B200_ARITH_EXACT;
@@ -371,7 +386,10 @@ void solve_rows_core(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t d, 
     const uint32_t kp = knnb::tensor_kp_for(klist);
     // AUTO: the tensor filter pays off once the sweep dominates its fixed
     // prologue; both policies return identical bits.
-    const bool tensor = kp != 0 && (arith == KNN_B200_ARITH_TENSOR || (arith == KNN_B200_ARITH_AUTO && n >= 4096));
+    // (the custom-functor folds run EXACT whatever the policy asks: the
+    // filter's proof covers the sqeuclidean and cosine forms only)
+    const bool tensor = kp != 0 && tensor_fold(metric) &&
+                        (arith == KNN_B200_ARITH_TENSOR || (arith == KNN_B200_ARITH_AUTO && n >= 4096));
     ctr.distance_evals += uint64_t(row_end - row_begin) * n;
     if (tensor) {
         ctr.arith_used = KNN_B200_ARITH_TENSOR;
@@ -446,7 +464,7 @@ void solve_rows_core_f64(knn_b200_ctx* ctx, const float* X, uint32_t n, uint32_t
         ++ctr.launches;
         Xs = staged;
     }
-    const int fold = metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean;
+    const int fold = fold_of(metric);
     const uint32_t klist = std::min(k, n - 1);
     ctr.arith_used = KNN_B200_ARITH_EXACT;
     ctr.distance_evals += uint64_t(row_end - row_begin) * n;
@@ -495,7 +513,7 @@ knnb::TensorPathArgs tri_args(knn_b200_ctx* ctx, const float* Xs, uint32_t n, ui
     ta.kp = knnb::tensor_kp_for(klist);
     ta.row_begin = 0;
     ta.row_end = n;
-    ta.fold = metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean;
+    ta.fold = fold_of(metric);
     ta.out_sqrt = metric == KNN_B200_METRIC_EUCLIDEAN;
     ta.out_index = out_index;
     ta.out_dist = out_dist;
@@ -513,7 +531,7 @@ knnb::TensorPathArgs tri_args(knn_b200_ctx* ctx, const float* Xs, uint32_t n, ui
 // Which triangle a whole problem takes: 0 none, 1 the list triangle (k <= 10),
 // 2 the threshold triangle (10 < k <= 128).
 int tri_selected(uint32_t n, uint32_t d, uint32_t klist, int metric, int arith) {
-    if (arith == KNN_B200_ARITH_EXACT || klist > knnb::kExactMaxK) return 0;
+    if (arith == KNN_B200_ARITH_EXACT || klist > knnb::kExactMaxK || !tensor_fold(metric)) return 0;
     if (knnb::tensor_kp_for(klist) != 0 &&
         knnb::tri_eligible(n, d, klist, metric == KNN_B200_METRIC_COSINE ? knnb::kCosine : knnb::kSqEuclidean))
         return 1;

@@ -6,7 +6,14 @@
 
 namespace knnb {
 
-enum Metric : int { kHellinger = 0, kSqEuclidean = 1, kCosine = 2 };
+// Device folds.  kHellinger and kSqEuclidean are the reference built-ins
+// (Hellinger arrives sqrt-staged and folds like kSqEuclidean); the others
+// restate custom functors of the reference's registry that a drop-in caller
+// may register (distance.hpp:68-77): cosine, manhattan
+// (acc + |u - v|, test_distance.cpp:134-145) and root-of-squares
+// (sqeuclidean with finalize sqrt, test_distance.cpp:166-178).  The last two
+// run on the EXACT policy only.
+enum Metric : int { kHellinger = 0, kSqEuclidean = 1, kCosine = 2, kManhattan = 3, kRootSquares = 4 };
 
 // (distance, index) packed into one u64 whose unsigned order is the
 // reference's Neighbor order (include/knn/heap.hpp:21-24): distance first,
@@ -49,6 +56,8 @@ template <int METRIC>
 __device__ __forceinline__ float fold_step(float u, float v, float acc) {
     if constexpr (METRIC == kCosine) {
         return __fadd_rn(acc, __fmul_rn(u, v));
+    } else if constexpr (METRIC == kManhattan) {
+        return __fadd_rn(acc, fabsf(__fsub_rn(u, v)));
     } else {
         const float t = __fsub_rn(u, v);
         return __fadd_rn(acc, __fmul_rn(t, t));
@@ -59,6 +68,8 @@ template <int METRIC>
 __device__ __forceinline__ float fold_finalize(float acc) {
     if constexpr (METRIC == kCosine) {
         return __fsub_rn(1.0f, acc);
+    } else if constexpr (METRIC == kRootSquares) {
+        return __fsqrt_rn(acc);
     } else {
         return acc;
     }

@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -46,6 +48,7 @@ __device__ __forceinline__ void step_bk(float u, float v, float& a32, double& a6
     if constexpr (F64) {
         // distance.hpp:49-52 with dist_t = double: FSUB, exact widened product, one rounding
         if constexpr (METRIC == kCosine) a64 = __fma_rn(double(u), double(v), a64);
+        else if constexpr (METRIC == kManhattan) a64 = __dadd_rn(a64, double(fabsf(__fsub_rn(u, v))));
         else {
             const double t = double(__fsub_rn(u, v));
             a64 = __fma_rn(t, t, a64);
@@ -111,7 +114,9 @@ __global__ void __launch_bounds__(BK_THREADS) bigk_tile_kernel(const BigkParams 
             if (col >= p.n) continue;
             const size_t at = size_t(s) * p.n + col;
             if constexpr (F64) {
-                const double dist = METRIC == kCosine ? __dsub_rn(1.0, a64[i][c]) : a64[i][c];
+                const double dist = METRIC == kCosine       ? __dsub_rn(1.0, a64[i][c])
+                                    : METRIC == kRootSquares ? __dsqrt_rn(a64[i][c])
+                                                             : a64[i][c];
                 p.keys[at] = col == q ? kEmptyKey : double_to_ordered_bk(dist);
                 p.cols[at] = col;
             } else {
@@ -236,17 +241,24 @@ cudaError_t launch_exact_bigk(int metric, int f64, const float* X, uint32_t n, u
                               int out_sqrt, void* ws, int sm_count, cudaStream_t stream) {
     if (row_end <= row_begin) return cudaSuccess;
     // Hellinger arrives sqrt-staged and folds exactly like sqeuclidean.
-    if (f64)
-        return metric == kCosine
-                   ? run_bigk<kCosine, true>(X, n, d, klist, row_begin, row_end, out_index, out_dist, out_sqrt, ws,
-                                             sm_count, stream)
-                   : run_bigk<kSqEuclidean, true>(X, n, d, klist, row_begin, row_end, out_index, out_dist, out_sqrt,
-                                                  ws, sm_count, stream);
-    return metric == kCosine
-               ? run_bigk<kCosine, false>(X, n, d, klist, row_begin, row_end, out_index, out_dist, out_sqrt, ws,
-                                          sm_count, stream)
-               : run_bigk<kSqEuclidean, false>(X, n, d, klist, row_begin, row_end, out_index, out_dist, out_sqrt, ws,
-                                               sm_count, stream);
+    auto run = [&](auto m, auto f) {
+        return run_bigk<decltype(m)::value, decltype(f)::value>(X, n, d, klist, row_begin, row_end, out_index,
+                                                                 out_dist, out_sqrt, ws, sm_count, stream);
+    };
+    using T = std::true_type;
+    using F = std::false_type;
+    switch (metric) {
+    case kCosine: return f64 ? run(std::integral_constant<int, kCosine>{}, T{}) : run(std::integral_constant<int, kCosine>{}, F{});
+    case kManhattan:
+        return f64 ? run(std::integral_constant<int, kManhattan>{}, T{})
+                   : run(std::integral_constant<int, kManhattan>{}, F{});
+    case kRootSquares:
+        return f64 ? run(std::integral_constant<int, kRootSquares>{}, T{})
+                   : run(std::integral_constant<int, kRootSquares>{}, F{});
+    default:
+        return f64 ? run(std::integral_constant<int, kSqEuclidean>{}, T{})
+                   : run(std::integral_constant<int, kSqEuclidean>{}, F{});
+    }
 }
 
 }  // namespace knnb

@@ -65,6 +65,8 @@ template <int METRIC>
 __device__ __forceinline__ double fold_step_f64(float u, float v, double acc) {
     if constexpr (METRIC == kCosine) {
         return __fma_rn(double(u), double(v), acc);  // product exact: == acc + u*v
+    } else if constexpr (METRIC == kManhattan) {
+        return __dadd_rn(acc, double(fabsf(__fsub_rn(u, v))));  // acc + dist_t(fabs(u - v))
     } else {
         const double t = double(__fsub_rn(u, v));
         return __fma_rn(t, t, acc);  // product exact: == acc + t*t
@@ -74,6 +76,7 @@ __device__ __forceinline__ double fold_step_f64(float u, float v, double acc) {
 template <int METRIC>
 __device__ __forceinline__ double fold_finalize_f64(double acc) {
     if constexpr (METRIC == kCosine) return __dsub_rn(1.0, acc);
+    if constexpr (METRIC == kRootSquares) return __dsqrt_rn(acc);
     return acc;
 }
 
@@ -309,6 +312,8 @@ cudaError_t launch_exact_f64(int metric, const float* X, uint32_t n, uint32_t d,
     const F64Params p{X, n, d, klist, row_begin, row_end - row_begin, out_index, out_dist, out_sqrt};
     // Hellinger arrives sqrt-staged and folds exactly like sqeuclidean.
     if (metric == kCosine) return launch_f64_m<kCosine>(p, stream);
+    if (metric == kManhattan) return launch_f64_m<kManhattan>(p, stream);
+    if (metric == kRootSquares) return launch_f64_m<kRootSquares>(p, stream);
     return launch_f64_m<kSqEuclidean>(p, stream);
 }
 

@@ -335,6 +335,8 @@ cudaError_t launch_exact_fused(int metric, const float* X, uint32_t n, uint32_t 
     // Hellinger arrives sqrt-staged and folds exactly like sqeuclidean.
     switch (metric) {
     case kCosine: return launch_exact_m<kCosine>(p, nch, stream);
+    case kManhattan: return launch_exact_m<kManhattan>(p, nch, stream);
+    case kRootSquares: return launch_exact_m<kRootSquares>(p, nch, stream);
     default: return launch_exact_m<kSqEuclidean>(p, nch, stream);
     }
 }

@@ -152,7 +152,21 @@ def euclidean() -> CumulativeDistance:
     return CumulativeDistance("euclidean", MetricKind.custom, _lib.METRIC_EUCLIDEAN)
 
 
-_REGISTRY = {"hellinger": hellinger, "sqeuclidean": squared_euclidean, "cosine": cosine, "euclidean": euclidean}
+def manhattan() -> CumulativeDistance:
+    """The reference test suite's custom functor: step acc + |u - v|
+    (test_distance.cpp:134-145).  EXACT policy."""
+    return CumulativeDistance("manhattan", MetricKind.custom, _lib.METRIC_MANHATTAN)
+
+
+def root_of_squares() -> CumulativeDistance:
+    """The reference test suite's custom functor: the sqeuclidean step with
+    finalize sqrt, ranked by the finalized distance (test_distance.cpp:166-178).
+    EXACT policy."""
+    return CumulativeDistance("root_of_squares", MetricKind.custom, _lib.METRIC_ROOT_SQUARES)
+
+
+_REGISTRY = {"hellinger": hellinger, "sqeuclidean": squared_euclidean, "cosine": cosine, "euclidean": euclidean,
+             "manhattan": manhattan, "root_of_squares": root_of_squares}
 
 
 def distance_by_name(name: str) -> CumulativeDistance:

@@ -57,6 +57,16 @@ dist_t device_fold_cosine(const float* u, const float* v, std::uint32_t d) {
     return dist_t(1) - acc;
 }
 
+dist_t device_fold_manhattan(const float* u, const float* v, std::uint32_t d) {
+    dist_t acc = 0;
+    for (std::uint32_t j = 0; j < d; ++j) acc = acc + dist_t(std::fabs(u[j] - v[j]));
+    return acc;
+}
+
+dist_t device_fold_root_squares(const float* u, const float* v, std::uint32_t d) {
+    return dist_t(std::sqrt(device_fold_sqeuclidean(u, v, d)));
+}
+
 // A custom functor is a host function pointer (distance.hpp:68-77); the GPU
 // cannot call it.  It runs on the GPU only if it IS one of the device folds,
 // bit for bit: the functor is probed on random vectors -- as the reference's
@@ -111,11 +121,14 @@ int gpu_metric(const CumulativeDistance& f) {
     case MetricKind::custom:
         if (functor_matches(f, device_fold_sqeuclidean)) return KNN_B200_METRIC_SQEUCLIDEAN;
         if (functor_matches(f, device_fold_cosine)) return KNN_B200_METRIC_COSINE;
+        if (functor_matches(f, device_fold_manhattan)) return KNN_B200_METRIC_MANHATTAN;
+        if (functor_matches(f, device_fold_root_squares)) return KNN_B200_METRIC_ROOT_SQUARES;
         break;
     }
     throw ConfigError("distance functor '" + f.name +
                       "' is a host function pointer that matches none of the GPU engine's folds "
-                      "(sqeuclidean, cosine = 1 - sum u*v); it cannot run on the GPU engine");
+                      "(sqeuclidean, cosine = 1 - sum u*v, manhattan = sum |u - v|, sqrt of sqeuclidean); "
+                      "it cannot run on the GPU engine");
 }
 
 int arith_from_env() {

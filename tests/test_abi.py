@@ -117,7 +117,7 @@ def test_engine_option_errors_precede_compute():
 
 def test_distance_registry():
     from paper_0906_0231_b200 import ConfigError, distance_by_name, distance_names
-    assert distance_names() == ["cosine", "euclidean", "hellinger", "sqeuclidean"]
+    assert distance_names() == ["cosine", "euclidean", "hellinger", "manhattan", "root_of_squares", "sqeuclidean"]
     assert distance_by_name("hellinger").nonnegative_domain
     with pytest.raises(ConfigError):
         distance_by_name("l1")

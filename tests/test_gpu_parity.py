@@ -430,3 +430,23 @@ def test_threshold_triangle_retry_and_overflow_paths(ctx, c_oracle, monkeypatch)
                                          want_stats=True)
         assert_lists_bit_equal(idx.cpu().numpy().view(np.uint32), dist.cpu().numpy(), ri, rd, f"{env}={val}")
         monkeypatch.delenv(env)
+
+
+@pytest.mark.parametrize("m", ["manhattan", "root_of_squares"])
+def test_custom_functor_folds(ctx, c_oracle, m):
+    """The reference suite's own custom functors (test_distance.cpp:134-145
+    manhattan, :166-178 sqeuclidean finalized by sqrt) run on the device
+    (EXACT, whatever the policy asked), bit for bit, float and double builds,
+    short and long lists, tie-heavy data."""
+    cases = [(c_oracle.generate(1500, 24, 3), 12), (c_oracle.generate(700, 5, 4), 300),
+             (np.floor(c_oracle.generate(600, 3, 5) * 7) * np.float32(0.37), 30)]
+    for x, k in cases:
+        x = np.ascontiguousarray(x, np.float32)
+        ri, rd, _ = c_oracle.brute_force(x, k, m)
+        for arith in ("auto", "tensor"):
+            idx, dist, st = ctx.solve(x, k, metric_obj(m), arith_id(arith))
+            assert_lists_bit_equal(idx, dist, ri, rd, f"{m} n={x.shape[0]} k={k} [{arith}]")
+            assert st["arith_used"] == 1
+        ri64, rd64 = c_oracle.brute_force_f64(x, k, m)
+        i64, d64, _ = ctx.solve_f64(x, k, metric_obj(m))
+        assert np.array_equal(i64, ri64) and np.array_equal(d64.view(np.uint64), rd64.view(np.uint64)), f"{m} f64"

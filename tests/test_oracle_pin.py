@@ -163,3 +163,23 @@ def test_restatement_matches_compiled_reference(c_oracle):
         # and the reference's own multi-lane engine agrees (engine.hpp:33-36)
         ei, ed, ep, _ = ref.solve_knn(x, k, m, n_lanes=1 + trial % 3)
         assert_lists_bit_equal(ei, ed, ri, rd, f"engine trial {trial} {m}")
+
+
+def test_custom_functor_folds_pinned_to_the_reference(c_oracle):
+    """The oracle's restatements of the reference suite's custom functors
+    equal the compiled reference running the same functors through its own
+    registry (oracle/ref_capi.cpp), float and double builds."""
+    import oracle
+    ref = oracle.reference()
+    if ref is None:
+        pytest.skip("reference not built")
+    for m in ("manhattan", "root_of_squares"):
+        for n, d, k, seed in ((90, 7, 5, 1), (300, 3, 40, 2)):
+            x = c_oracle.generate(n, d, seed)
+            ri, rd, _, _ = ref.brute_force(x, k, m)
+            oi, od, _ = c_oracle.brute_force(x, k, m)
+            assert np.array_equal(ri, oi) and np.array_equal(rd.view(np.uint32), od.view(np.uint32)), m
+            if oracle.REF_F64_CAPI_PATH.exists():
+                ri64, rd64 = oracle.ReferenceF64().brute_force(x, k, m)
+                oi64, od64 = c_oracle.brute_force_f64(x, k, m)
+                assert np.array_equal(ri64, oi64) and np.array_equal(rd64.view(np.uint64), od64.view(np.uint64)), m
