@@ -48,7 +48,8 @@ typedef enum {
     KNN_B200_OK = 0,
     KNN_B200_ERR_CONFIG = 2,     /* knn::ConfigError     (engine.cpp:15-17)  */
     KNN_B200_ERR_VALIDATION = 3, /* knn::ValidationError (distance.cpp:36-59, dataset.cpp:13-29) */
-    KNN_B200_ERR_INTERNAL = 4    /* std::runtime_error / CUDA failure        */
+    KNN_B200_ERR_INTERNAL = 4,   /* std::runtime_error / CUDA failure        */
+    KNN_B200_ERR_IO = 5          /* knn::IoError (io.cpp; CLI exit code 3)   */
 } knn_b200_status;
 
 /* Metric ids.  HELLINGER and SQEUCLIDEAN are the reference built-ins
@@ -157,6 +158,19 @@ KNN_B200_API int knn_b200_solve_rows_device(knn_b200_ctx *ctx, const float *dev_
                                uint32_t d, uint32_t k, int metric, int arith,
                                uint32_t row_begin, uint32_t row_end, uint32_t *dev_out_index,
                                float *dev_out_dist, void *stream, knn_b200_stats *stats);
+
+/* KNNV dataset files (the reference's load_dataset, io.cpp:64-97): magic
+ * "KNNV", u32 version 1, u32 n, u32 d (little endian), then n x d float32.
+ * knn_b200_knnv_header reads and checks the header (host only).
+ * knn_b200_load_knnv_device reads the payload straight into dev_out
+ * (capacity floats, caller-owned) through the context's pinned staging lanes
+ * -- parallel preads overlapping the DMA, no whole-file host copy -- then
+ * checks n >= 2, d >= 1 and every coordinate finite on the device, with the
+ * reference's messages (IoError -> KNN_B200_ERR_IO, the Dataset checks ->
+ * KNN_B200_ERR_VALIDATION). */
+KNN_B200_API int knn_b200_knnv_header(const char *path, uint32_t *out_n, uint32_t *out_d);
+KNN_B200_API int knn_b200_load_knnv_device(knn_b200_ctx *ctx, const char *path, float *dev_out, uint64_t capacity,
+                                           uint32_t *out_n, uint32_t *out_d, void *stream);
 
 /* Synthetic inputs on the device, bit-identical to the reference's
  * generate_dataset (src/io.cpp:57-62, include/knn/rng.hpp:13-23): element i of

@@ -27,7 +27,10 @@ from .engine import (  # noqa: F401
     distance_names,
     euclidean,
     generate_torch,
+    IoError,
     hellinger,
+    knnv_header,
+    load_knnv_torch,
     make_plan,
     manhattan,
     root_of_squares,

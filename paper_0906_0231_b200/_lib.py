@@ -25,6 +25,8 @@ EXPORTS = (
     "knn_b200_solve",
     "knn_b200_solve_f64",
     "knn_b200_solve_multi_f64",
+    "knn_b200_knnv_header",
+    "knn_b200_load_knnv_device",
     "knn_b200_debug_tc_dots",
     "knn_b200_tri_unit_plan",
     "knn_b200_comm_unique_id",
@@ -39,7 +41,7 @@ EXPORTS = (
 
 ABI_VERSION = 2
 
-OK, ERR_CONFIG, ERR_VALIDATION, ERR_INTERNAL = 0, 2, 3, 4
+OK, ERR_CONFIG, ERR_VALIDATION, ERR_INTERNAL, ERR_IO = 0, 2, 3, 4, 5
 METRIC_HELLINGER, METRIC_SQEUCLIDEAN, METRIC_COSINE, METRIC_EUCLIDEAN = 0, 1, 2, 3
 METRIC_MANHATTAN, METRIC_ROOT_SQUARES = 4, 5
 ARITH_AUTO, ARITH_EXACT, ARITH_TENSOR = 0, 1, 2
@@ -112,6 +114,11 @@ def load() -> ctypes.CDLL:
             ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)]
         lib.knn_b200_generate_device.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
                                                  ctypes.c_uint64, ctypes.c_void_p]
+        lib.knn_b200_knnv_header.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint32),
+                                             ctypes.POINTER(ctypes.c_uint32)]
+        lib.knn_b200_load_knnv_device.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_void_p, ctypes.c_uint64,
+                                                  ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
+                                                  ctypes.c_void_p]
         lib.knn_b200_debug_tc_dots.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p,
                                                ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p]
         lib.knn_b200_tri_unit_plan.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,

@@ -6,8 +6,11 @@
 // merge_all (engine.cpp:27-59) has no counterpart: each query row is owned by
 // exactly one CTA, so its list is final when the sweep ends.
 #include <cuda_runtime.h>
+#include <fcntl.h>
 #include <nccl.h>
 #include <stdint.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <chrono>
@@ -273,6 +276,91 @@ void host_copy(knn_b200_ctx* ctx, void* dst, const void* src, size_t bytes, bool
                int threads = 0) {
     host_copy_segs(ctx, {CopySeg{dst, src, bytes}}, h2d, s, threads);
 }
+
+// A file's byte range [off, off + bytes) to device memory, ordered on `s`:
+// the staging lanes pread chunks into their pinned buffers and DMA them, so
+// the read runs in parallel and overlaps the copies (the reference reads the
+// whole file into a std::vector first, io.cpp:35-46).
+void file_to_device(knn_b200_ctx* ctx, int fd, uint64_t off, void* dst, size_t bytes, cudaStream_t s,
+                    const std::string& path) {
+    if (bytes == 0) return;
+    stage_init(ctx);
+    const int threads = ctx->stage_n;
+    const size_t chunk = ctx->stage_chunk;
+    const size_t nchunks = (bytes + chunk - 1) / chunk;
+    cuda_check(cudaEventRecord(ctx->stage_go, s), "stage event");
+    std::vector<cudaError_t> errs(threads, cudaSuccess);
+    std::vector<int> ioerr(threads, 0);
+    auto work = [&](int t) {
+        StageLane& l = ctx->stage[t];
+        cudaError_t e = cudaSetDevice(ctx->device);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(l.st, ctx->stage_go, 0);
+        size_t i = 0;
+        for (size_t c = t; c < nchunks && e == cudaSuccess && !ioerr[t]; c += threads, ++i) {
+            const int b = int(i & 1);
+            const size_t pos = c * chunk, len = std::min(chunk, bytes - pos);
+            if (i >= 2) e = cudaEventSynchronize(l.ev[b]);  // the DMA that last read buf[b]
+            if (e != cudaSuccess) break;
+            size_t got = 0;
+            while (got < len) {
+                const ssize_t r = pread(fd, static_cast<char*>(l.buf[b]) + got, len - got, off_t(off + pos + got));
+                if (r <= 0) {
+                    ioerr[t] = 1;
+                    break;
+                }
+                got += size_t(r);
+            }
+            if (ioerr[t]) break;
+            e = cudaMemcpyAsync(static_cast<char*>(dst) + pos, l.buf[b], len, cudaMemcpyHostToDevice, l.st);
+            if (e == cudaSuccess) e = cudaEventRecord(l.ev[b], l.st);
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(l.done, l.st);
+        errs[t] = e;
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    for (int t = 0; t < threads; ++t) {
+        cuda_check(errs[t], "file staging");
+        if (ioerr[t]) fail(KNN_B200_ERR_IO, "failed to read '" + path + "'");
+    }
+    for (int t = 0; t < threads; ++t) cuda_check(cudaStreamWaitEvent(s, ctx->stage[t].done, 0), "stage join");
+}
+
+// KNNV header (io.cpp:64-88): magic "KNNV", u32 version (kFormatVersion = 1),
+// u32 n, u32 d, little endian, then n x d f32; the reference's messages.
+struct KnnvHeader {
+    uint32_t n, d;
+};
+KnnvHeader read_knnv_header(int fd, const std::string& path) {
+    struct stat sb;
+    if (fstat(fd, &sb) != 0) fail(KNN_B200_ERR_IO, "failed to read '" + path + "'");
+    const uint64_t size = uint64_t(sb.st_size);
+    if (size < 16) fail(KNN_B200_ERR_IO, "'" + path + "' is too short to hold a dataset header");
+    unsigned char h[16];
+    if (pread(fd, h, 16, 0) != 16) fail(KNN_B200_ERR_IO, "failed to read '" + path + "'");
+    if (std::memcmp(h, "KNNV", 4) != 0) fail(KNN_B200_ERR_IO, "'" + path + "' is not a dataset file (bad magic)");
+    auto u32 = [&](int o) {
+        return uint32_t(h[o]) | uint32_t(h[o + 1]) << 8 | uint32_t(h[o + 2]) << 16 | uint32_t(h[o + 3]) << 24;
+    };
+    if (u32(4) != 1)
+        fail(KNN_B200_ERR_IO, "'" + path + "' has unsupported format version " + std::to_string(u32(4)));
+    KnnvHeader hd{u32(8), u32(12)};
+    const uint64_t expect = 16 + uint64_t(hd.n) * hd.d * 4;
+    if (size != expect)
+        fail(KNN_B200_ERR_IO, "'" + path + "' holds " + std::to_string(size) + " bytes but the header implies " +
+                                  std::to_string(expect));
+    return hd;
+}
+
+struct Fd {
+    int fd;
+    explicit Fd(const std::string& path) : fd(open(path.c_str(), O_RDONLY)) {
+        if (fd < 0) fail(KNN_B200_ERR_IO, "cannot open '" + path + "' for reading");
+    }
+    ~Fd() { close(fd); }
+};
 
 const char* metric_name(int metric) {
     switch (metric) {
@@ -838,6 +926,51 @@ int knn_b200_solve_rows_device(knn_b200_ctx* ctx, const float* dev_vectors, uint
             stats->sweep_ms = elapsed_ms(ctx->ev[4], ctx->ev[5]);
             stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         }
+    });
+}
+
+int knn_b200_knnv_header(const char* path, uint32_t* out_n, uint32_t* out_d) {
+    return guarded([&] {
+        const std::string p = path ? path : "";
+        Fd f(p);
+        const KnnvHeader h = read_knnv_header(f.fd, p);
+        *out_n = h.n;
+        *out_d = h.d;
+    });
+}
+
+int knn_b200_load_knnv_device(knn_b200_ctx* ctx, const char* path, float* dev_out, uint64_t capacity,
+                              uint32_t* out_n, uint32_t* out_d, void* stream) {
+    return guarded([&] {
+        if (!ctx) fail(KNN_B200_ERR_CONFIG, "null context");
+        const std::string p = path ? path : "";
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        Fd f(p);
+        const KnnvHeader h = read_knnv_header(f.fd, p);
+        const uint64_t count = uint64_t(h.n) * h.d;
+        // the Dataset constructor's checks (dataset.cpp:13-29), prefixed with
+        // the path as load_dataset does (io.cpp:92-96)
+        if (h.n < 2)
+            fail(KNN_B200_ERR_VALIDATION, "'" + p + "': dataset needs at least 2 vectors, got " + std::to_string(h.n));
+        if (h.d < 1) fail(KNN_B200_ERR_VALIDATION, "'" + p + "': dataset dimension must be at least 1");
+        if (count > capacity)
+            fail(KNN_B200_ERR_CONFIG, "'" + p + "' holds " + std::to_string(count) + " floats, the buffer " +
+                                          std::to_string(capacity));
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        begin_call(ctx, s);
+        file_to_device(ctx, f.fd, 16, dev_out, size_t(count) * 4, s, p);
+        Counters ctr;
+        try {
+            validate_device(ctx, dev_out, h.n, h.d, KNN_B200_METRIC_SQEUCLIDEAN, s, ctr);
+        } catch (const KnnError& e) {
+            end_call(ctx, s);
+            if (e.code == KNN_B200_ERR_VALIDATION) fail(e.code, "'" + p + "': " + e.msg);
+            throw;
+        }
+        end_call(ctx, s);
+        *out_n = h.n;
+        *out_d = h.d;
     });
 }
 

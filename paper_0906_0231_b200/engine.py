@@ -47,6 +47,10 @@ class ValidationError(RuntimeError):
     """Rejected input data, e.g. non-finite or out-of-domain (exit code 3)."""
 
 
+class IoError(RuntimeError):
+    """Unreadable or malformed file (io.cpp; CLI exit code 3)."""
+
+
 class ConsistencyError(RuntimeError):
     """Broken internal invariant; always a bug (exit code 4)."""
 
@@ -63,6 +67,8 @@ def raise_for_status(rc: int) -> None:
         raise ConfigError(msg)
     if rc == _lib.ERR_VALIDATION:
         raise ValidationError(msg)
+    if rc == _lib.ERR_IO:
+        raise IoError(msg)
     raise EngineError(msg)
 
 
@@ -491,6 +497,27 @@ def solve_rows_torch(ctx: Context, x, k: int, metric: CumulativeDistance, row_be
     st = ctx.solve_rows_device(x.data_ptr(), n, d, k, metric, row_begin, row_end, idx.data_ptr(),
                                dist.data_ptr(), stream, arith, want_stats)
     return idx, dist, st
+
+
+def knnv_header(path) -> tuple[int, int]:
+    """(n, d) of a KNNV dataset file, checked like load_dataset (io.cpp:64-88)."""
+    n, d = ctypes.c_uint32(0), ctypes.c_uint32(0)
+    raise_for_status(_lib.load().knn_b200_knnv_header(os.fsencode(path), ctypes.byref(n), ctypes.byref(d)))
+    return n.value, d.value
+
+
+def load_knnv_torch(ctx: Context, path, device=None):
+    """load_dataset (io.cpp:64-97) straight into a CUDA tensor: the payload is
+    read in parallel through pinned staging and checked on the device."""
+    import torch
+
+    n, d = knnv_header(path)
+    x = torch.empty((n, d), dtype=torch.float32, device=device or f"cuda:{ctx.device}")
+    on, od = ctypes.c_uint32(0), ctypes.c_uint32(0)
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    raise_for_status(_lib.load().knn_b200_load_knnv_device(ctx._h, os.fsencode(path), x.data_ptr(), n * d,
+                                                           ctypes.byref(on), ctypes.byref(od), stream))
+    return x
 
 
 def generate_torch(ctx: Context, n: int, d: int, seed: int, device=None):
