@@ -1332,9 +1332,22 @@ __device__ __forceinline__ double proof_bound(uint32_t d, const unsigned int* ma
         const double eacc = ctc * nx * xnmax + 2.0 * (rh * xnmax + rhomax * (nx + rh)) + u * 2.0 * s2 * (fabs(Tp) + 2.0);
         return 2.0 * s2 * (Tp + 2.0 * eref) + 2.0 * eacc;
     }
-    const double rr = rh + rhomax;
-    const double e_all = (ctc + 6.0 * u) * nx * xnmax + (dd + 3.0) * u * (al + alphamax) +
-                         rr * (2.0 * sqrt(s2 * fmax(Tp, 0.0)) + rr);
+    // The bound only has to hold for columns j with D_ref(i, j) <= T, and
+    // those lie near row i: ||s(x_j - mu)|| <= ||x^_i|| + rho_i + s sqrt(T')
+    // =: X0 (triangle inequality), so their quantisation error is
+    // rho_j <= 2^-11 (1 + eps) X0 + sqrt(d) 2^-25 (fp16 rounding, relative in
+    // the normal range, absolute for subnormals), ||x^_j|| <= X0 + rho_j and
+    // alpha_j <= ||x^_j||^2 (1 + (d + 2) u).  Each replaces the dataset-wide
+    // maximum when smaller -- so one outlier row no longer widens every other
+    // row's band.
+    const double sqT = sqrt(s2 * fmax(Tp, 0.0));
+    const double X0 = nx + rh + sqT;
+    const double rho_b = 4.8828125e-04 * (1.0 + 1e-3) * X0 + sqrt(dd) * 2.98023223876953125e-08;
+    const double xn_j = fmin(xnmax, X0 + rho_b);
+    const double rho_j = fmin(rhomax, rho_b);
+    const double al_j = fmin(alphamax, xn_j * xn_j * (1.0 + (dd + 2.0) * u));
+    const double rr = rh + rho_j;
+    const double e_all = (ctc + 6.0 * u) * nx * xn_j + (dd + 3.0) * u * (al + al_j) + rr * (2.0 * sqT + rr);
     return s2 * Tp + 2.0 * e_all;
 }
 
