@@ -128,6 +128,7 @@ struct SweepParams {
     // Null: every unit 0, 1, ... of [row_begin, row_end).
     const uint32_t* units;
     uint32_t nunits;
+    unsigned long long* cta_ns;  // profiling only (KNN_B200_DEBUG_CTA_TIMES): per CTA [start, end] globaltimer
 };
 
 // Candidate keys from the norm-sorted sweep carry sweep-order column indices;
@@ -241,6 +242,11 @@ tensor_sweep_kernel(const SweepParams p) {
         ptx::fence_mbar_init();
     }
     if constexpr (PAIR) {
+        if (p.cta_ns && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            p.cta_ns[2 * blockIdx.x] = t;
+        }
         if (warp == 1) ptx::tmem_alloc_pair(ptx::smem_u32(tmem_slot), L::TMEM_COLS);
         ptx::tc_fence_before();
         ptx::cluster_sync();
@@ -844,6 +850,11 @@ tensor_sweep_kernel(const SweepParams p) {
     ptx::tc_fence_before();
     if constexpr (PAIR) {
         ptx::cluster_sync();  // neither CTA frees TMEM while the pair's MMAs may write it
+        if (p.cta_ns && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            p.cta_ns[2 * blockIdx.x + 1] = t;
+        }
         if (warp == 1) {
             ptx::tc_fence_after();
             ptx::tmem_dealloc_pair(tmem, L::TMEM_COLS);

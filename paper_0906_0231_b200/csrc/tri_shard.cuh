@@ -585,10 +585,32 @@ static cudaError_t tri_sweep(TriShared& S, TriRank& R, const TensorPathArgs& a, 
                    S.tri_tc, S.tcmax,  R.lkey, R.lcol,  R.lcnt, R.lnext, R.nchunks};
     tp.units = R.units;
     tp.nunits = R.nu;
+    // profiling only: per-CTA start/end times of this rank's sweep, appended
+    // to the file the variable names (rank, CTA, start ns, end ns, units)
+    const char* ctaf = getenv("KNN_B200_DEBUG_CTA_TIMES");
+    unsigned long long* cta_ns = nullptr;
+    if (ctaf) {
+        cudaMallocAsync(reinterpret_cast<void**>(&cta_ns), 2 * 8 * 2 * pairs, st);
+        tp.cta_ns = cta_ns;
+    }
     e = !S.tcap                        ? launch_sweep_pair<12, 256, 8, true>(tp, R.nslots, st)
         : S.kc <= uint32_t(TS_MAX_RES_KC) ? launch_sweep_pair<2, 256, 8, true, true, true>(tp, R.nslots, st)
                                            : launch_sweep_pair<2, 256, 8, true, true, false>(tp, R.nslots, st);
     if (e != cudaSuccess) return e;
+    if (cta_ns) {
+        std::vector<unsigned long long> t(4 * pairs);
+        cudaMemcpyAsync(t.data(), cta_ns, t.size() * 8, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        cudaFreeAsync(cta_ns, st);
+        if (FILE* f = fopen(ctaf, "a")) {
+            for (uint32_t c = 0; c < 2 * pairs; ++c) {
+                uint32_t nu = 0;
+                for (size_t i = c / 2; i < S.units_h[R.rank].size(); i += pairs) ++nu;
+                fprintf(f, "%u %u %llu %llu %u\n", R.rank, c, t[2 * c], t[2 * c + 1], nu);
+            }
+            fclose(f);
+        }
+    }
     if (S.G == 1) {  // no exchange: only the pool's overflow matters (phase C scatters it in place)
         uint32_t* h = static_cast<uint32_t*>(a.host_scratch);
         if ((e = cudaMemcpyAsync(h, R.lnext, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
