@@ -27,6 +27,7 @@
 //            overflows are recomputed by the EXACT kernel.
 // Result: bit-identical to brute_force_knn.
 #include <cub/device/device_radix_sort.cuh>
+#include <algorithm>
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
 #include <cuda_runtime.h>
@@ -75,7 +76,7 @@ struct TSLayout {
     static constexpr uint32_t LIST_ROWS = TS_BM * NSEG;                 // list "columns"
     static constexpr bool REGLIST = KPL <= 16;  // lists in registers, no shared-memory list arrays
     static constexpr uint32_t LISTS = REGLIST ? 0 : LIST_ROWS * KPL * 8;
-    static constexpr uint32_t MISC = 256;
+    static constexpr uint32_t MISC = 512;  // barriers, TMEM address, the unit queue
     static constexpr uint32_t AVAIL = TS_SMEM_MAX - 1024 - MISC - LISTS - A_BYTES;
     static constexpr int STAGES_RAW = int(AVAIL / STAGE);
 #ifndef KNN_TS_STAGE_CAP
@@ -89,6 +90,17 @@ struct TSLayout {
     static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
     static constexpr uint32_t STRIDE = LIST_ROWS * 4;  // bytes between entries of one list
 };
+
+// The sweep's bound tests compare raw dots with h = (a - b) / 2 less a slack
+// that covers the rounding of y = fl(beta - 2 dot) and of h itself.  h is
+// formed as bound_half(a, 1) + bound_half(b, -1): each half rounded down by
+// 2^-19 of its magnitude (infinities pass through) -- one FADD per chunk in
+// the sweep, the halves precomputed per column chunk (chunk_min_kernel,
+// chunk_max_kernel) and per row.  A smaller h admits a superset: exact.
+__device__ __forceinline__ float bound_half(float x, float sign) {
+    const float h = x * (0.5f * sign);
+    return fabsf(x) <= 3.402823466e+38f ? h - 1.9073486328125e-06f * fabsf(x) : h;  // finite: less the slack
+}
 
 struct SweepParams {
     const uint8_t* xh;    // swizzled fp16 planes
@@ -108,12 +120,12 @@ struct SweepParams {
     uint32_t* cap_cnt;
     uint64_t* cap_buf;
     uint32_t cap;
-    const float* bmin;  // [npad / 32] smallest column norm of every 32-column chunk
+    const float* bmin;  // [2 npad / 32] smallest column norm of every 32-column chunk, then its bound_half
     // triangle mode (TRI kernels): rows and columns are the same sorted set;
     // a row unit sweeps only tiles >= its own and also offers each of its rows
     // to the columns' fixed-threshold buffers (the column side)
     const float* tc;     // [npad] column-side threshold: a row enters column j's buffer iff y' < tc[j]
-    const float* tcmax;  // [npad / 32] its maximum per 32-column chunk
+    const float* tcmax;  // [2 npad / 32] its maximum per 32-column chunk, then its bound_half(., -1)
     uint64_t* lkey;      // column-side candidates: key (y', row) and column, in a pool of
     uint32_t* lcol;      //   kLogChunk-entry chunks; each epilogue warp fills its own chunk and
     uint32_t* lcnt;      //   takes the next free one (one atomic on *lnext) when it is full;
@@ -129,6 +141,13 @@ struct SweepParams {
     const uint32_t* units;
     uint32_t nunits;
     unsigned long long* cta_ns;  // profiling only (KNN_B200_DEBUG_CTA_TIMES): per CTA [start, end] globaltimer
+    // Dynamic unit queue (TRI; null: the static walk above).  Work items
+    // (local unit lu, column group g) are claimed from qctr[g]; units must be
+    // ascending (a group's units with work are then a prefix).  udone[lu]
+    // counts the epilogue warps that saved the unit's list state, so the pair
+    // taking (lu, g + 1) waits for the one that ran (lu, g).  Zeroed per launch.
+    uint32_t* qctr;
+    uint32_t* udone;
 };
 
 // Candidate keys from the norm-sorted sweep carry sweep-order column indices;
@@ -157,6 +176,85 @@ __global__ void remap_capture_kernel(uint64_t* __restrict__ buf, const uint32_t*
         const uint64_t k = b[i];
         b[i] = (k & 0xffffffff00000000ull) | perm[uint32_t(k)];
     }
+}
+
+// The sweep's work-item walk: this CTA's next item (column group g, local
+// unit lu), false when there is none.  role 0: the queue's claiming producer
+// (leader, warp 0); 1: a consumer in the leader; 2: a consumer in the peer.
+// warp_wide: the whole warp calls this (lane 0 releases the queue slot).
+// Without the queue (dyn false): the static walk -- column groups in order,
+// inside a group units unit0, unit0 + unit_step, ...  Out of line: it runs
+// once per item, and inlined copies in every role measurably slowed the
+// epilogue's hot loop (C2: +7%).
+constexpr int kQN = 4;                 // queue slots
+constexpr uint64_t kQEnd = ~0ull;      // the end-of-work item
+struct ItemWalk {
+    const uint32_t* units;
+    uint32_t* qctr;
+    uint32_t g_first, g_step, ngroups, ntiles, group_tiles, unit0, unit_step, nunits;
+    uint32_t qbar0;  // qfull[kQN], qempty[kQN] mbarriers
+    uint64_t* qitem;
+    bool dyn, tri, pair;
+    uint32_t g = 0, lu = 0, qi = 0;
+    bool started = false;
+};
+
+__device__ __noinline__ bool item_next(ItemWalk& w, int role, bool warp_wide) {
+    auto unit_id = [&](uint32_t lu) { return w.units ? __ldg(w.units + lu) : lu; };
+    if (!w.dyn) {
+        for (;;) {
+            if (!w.started) {
+                w.started = true;
+                w.g = w.g_first;
+                w.lu = w.unit0;
+            } else {
+                w.lu += w.unit_step;
+            }
+            if (w.lu >= w.nunits) {
+                w.g += w.g_step;
+                w.lu = w.unit0;
+            }
+            if (w.g >= w.ngroups) return false;
+            const uint32_t t0 = w.g * w.group_tiles, t1 = min(w.ntiles, t0 + w.group_tiles);
+            if (w.lu < w.nunits && max(t0, w.tri ? unit_id(w.lu) : 0u) < t1) return true;
+        }
+    }
+    const int s = w.qi % kQN;
+    const uint32_t ph = (w.qi / kQN) & 1;
+    const uint32_t qfull = w.qbar0 + 8u * s, qempty = w.qbar0 + 8u * (kQN + s);
+    ++w.qi;
+    if (role == 0) {
+        uint64_t item = kQEnd;
+        while (w.g < w.ngroups) {
+            const uint32_t t1 = min(w.ntiles, (w.g + 1) * w.group_tiles);
+            const uint32_t lu = atomicAdd(w.qctr + w.g, 1u);
+            if (lu < w.nunits && unit_id(lu) < t1) {  // (units ascending: a group's units with work are a prefix)
+                w.lu = lu;
+                item = (uint64_t(w.g) << 32) | lu;
+                break;
+            }
+            ++w.g;  // the group's units are all taken
+        }
+        ptx::mbar_wait_cluster(qempty, ph ^ 1);
+        w.qitem[s] = item;
+        if (w.pair) {
+            ptx::st_shared_cluster_u64(ptx::mapa_shared(ptx::smem_u32(w.qitem + s), 1), item);
+            ptx::mbar_arrive_remote(ptx::mapa_shared(qfull, 1));
+        }
+        ptx::mbar_arrive(qfull);
+        return item != kQEnd;
+    }
+    if (role == 2) ptx::mbar_wait_cluster(qfull, ph);
+    else ptx::mbar_wait(qfull, ph);
+    const uint64_t item = w.qitem[s];
+    if (warp_wide) __syncwarp();
+    if (!warp_wide || (threadIdx.x & 31) == 0) {
+        if (role == 2) ptx::mbar_arrive_remote(ptx::mapa_shared(qempty, 0));
+        else ptx::mbar_arrive(qempty);
+    }
+    w.g = uint32_t(item >> 32);
+    w.lu = uint32_t(item);
+    return item != kQEnd;
 }
 
 // Persistent sweep.  Work item = (column group g, row block rb); every CTA
@@ -223,6 +321,31 @@ tensor_sweep_kernel(const SweepParams p) {
     const uint32_t afull_bar = bar0 + 8u * (2 * S + 4);
     const uint32_t aempty_bar = bar0 + 8u * (2 * S + 5);
     auto wait = [&](uint32_t bar, uint32_t parity) { ptx::mbar_wait(bar, parity); };
+    // The dynamic unit queue (p.qctr): the leader's producer claims items and
+    // publishes them through a QN-slot ring held in both CTAs' shared memory;
+    // every other role (MMA issuer, epilogue warps, the peer's producer and
+    // forwarder) takes the same items in the same order.
+    constexpr int QN = kQN;
+#ifdef KNN_NO_DYN
+    constexpr bool dyn = false;
+#else
+    const bool dyn = TRI && p.qctr != nullptr;
+#endif
+    const uint32_t qbar0 = bar0 + 8u * (2 * S + 7);
+    auto qfull_bar = [&](int s) { return qbar0 + 8u * s; };
+    auto qempty_bar = [&](int s) { return qbar0 + 8u * (QN + s); };
+    uint64_t* qitem = bars + 2 * S + 7 + 2 * QN;
+    auto make_walk = [&]() {
+        ItemWalk w;
+        w.units = p.units;
+        w.qctr = p.qctr;
+        w.g_first = g_first, w.g_step = g_step, w.ngroups = ngroups, w.ntiles = ntiles;
+        w.group_tiles = p.group_tiles, w.unit0 = unit0, w.unit_step = unit_step, w.nunits = nunits;
+        w.qbar0 = qbar0;
+        w.qitem = qitem;
+        w.dyn = dyn, w.tri = TRI, w.pair = PAIR;
+        return w;
+    };
 
     if (warp == 0 && lane == 0) {
         // PAIR: the leader's operand barriers also count the peer's
@@ -239,6 +362,12 @@ tensor_sweep_kernel(const SweepParams p) {
         }
         ptx::mbar_init(afull_bar, fwd);
         ptx::mbar_init(aempty_bar, 1);
+        if (dyn)
+            for (int s = 0; s < QN; ++s) {
+                ptx::mbar_init(qfull_bar(s), 1);
+                // the leader's MMA issuer and epilogue warps, the peer's producer, forwarder and epilogue warps
+                ptx::mbar_init(qempty_bar(s), 1 + EW + (PAIR ? 2 + EW : 0));
+            }
         ptx::fence_mbar_init();
     }
     if constexpr (PAIR) {
@@ -263,13 +392,14 @@ tensor_sweep_kernel(const SweepParams p) {
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0, a_phase = 0;
-            for (uint32_t g = g_first; g < ngroups; g += g_step) {
+            ItemWalk cur = make_walk();
+            while (item_next(cur, leader ? 0 : 2, false)) {
+                const uint32_t g = cur.g, lu = cur.lu;
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
-                for (uint32_t lu = unit0; lu < nunits; lu += unit_step) {
+                {
                     const uint32_t u = unit_id(lu);
                     const uint32_t r0 = p.row_begin + unit_block(u) * TS_BM;
                     const uint32_t ts = max(t0, tri_start(u));
-                    if (ts >= t1) continue;
                     if constexpr (ARES) {  // A stays resident for the item; reload once the MMA released it
                         wait(aempty_bar, a_phase ^ 1);
                         ptx::mbar_arrive_expect_tx(afull_bar, p.kc * TS_A_CHUNK);
@@ -314,27 +444,25 @@ tensor_sweep_kernel(const SweepParams p) {
             const uint32_t lead_afull = ptx::mapa_shared(afull_bar, 0);
             int stage = 0;
             uint32_t phase = 0, a_phase = 0;
-            for (uint32_t g = g_first; g < ngroups; g += g_step) {
+            ItemWalk cur = make_walk();
+            while (item_next(cur, 2, false)) {
+                const uint32_t g = cur.g, lu = cur.lu;
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
-                for (uint32_t lu = unit0; lu < nunits; lu += unit_step) {
-                    const uint32_t u = unit_id(lu);
-                    const uint32_t ts = max(t0, tri_start(u));
-                    if (ts >= t1) continue;
-                    if constexpr (ARES) {
-                        wait(afull_bar, a_phase);
-                        a_phase ^= 1;
-                        ptx::mbar_arrive_remote_relaxed(lead_afull);
-                    }
-                    for (uint32_t t = ts; t < t1; ++t)
-                        for (uint32_t kc = 0; kc < p.kc; ++kc) {
-                            wait(full_bar(stage), phase);
-                            ptx::mbar_arrive_remote_relaxed(lead_full0 + 8u * stage);
-                            if (++stage == S) {
-                                stage = 0;
-                                phase ^= 1;
-                            }
-                        }
+                const uint32_t ts = max(t0, tri_start(unit_id(lu)));
+                if constexpr (ARES) {
+                    wait(afull_bar, a_phase);
+                    a_phase ^= 1;
+                    ptx::mbar_arrive_remote_relaxed(lead_afull);
                 }
+                for (uint32_t t = ts; t < t1; ++t)
+                    for (uint32_t kc = 0; kc < p.kc; ++kc) {
+                        wait(full_bar(stage), phase);
+                        ptx::mbar_arrive_remote_relaxed(lead_full0 + 8u * stage);
+                        if (++stage == S) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
             }
         }
     } else if (warp == 1) {
@@ -355,12 +483,12 @@ tensor_sweep_kernel(const SweepParams p) {
             };
             int stage = 0;
             uint32_t phase = 0, a_phase = 0, tcount = 0;
-            for (uint32_t g = g_first; g < ngroups; g += g_step) {
+            ItemWalk cur = make_walk();
+            while (item_next(cur, 1, false)) {
+                const uint32_t g = cur.g, lu = cur.lu;
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
-                for (uint32_t lu = unit0; lu < nunits; lu += unit_step) {
-                    const uint32_t u = unit_id(lu);
-                    const uint32_t ts = max(t0, tri_start(u));
-                    if (ts >= t1) continue;
+                {
+                    const uint32_t ts = max(t0, tri_start(unit_id(lu)));
                     if constexpr (ARES) {
                         wait(afull_bar, a_phase);
                         a_phase ^= 1;
@@ -481,16 +609,18 @@ tensor_sweep_kernel(const SweepParams p) {
             }
             ptx::mbar_arrive(tempty_bar(b));
         };
-        for (uint32_t g = g_first; g < ngroups; g += g_step) {
+        ItemWalk cur = make_walk();
+        while (item_next(cur, leader ? 1 : 2, true)) {
+            const uint32_t g = cur.g, lu = cur.lu;
             const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
-            for (uint32_t lu = unit0; lu < nunits; lu += unit_step) {
+            {
                 const uint32_t u = unit_id(lu);
                 const uint32_t tsu = tri_start(u), ts = max(t0, tsu);
-                if (ts >= t1) continue;
                 const bool fresh = TRI ? t0 <= tsu : g == 0;  // the unit's first group with work
                 const uint32_t row = p.row_begin + unit_block(u) * TS_BM + rl;
                 const bool valid = row < p.row_end;
                 const float alpha_i = TRI && valid ? p.alpha[row] : kInf;  // column side: this row's norm
+                const float alpha_h = bound_half(alpha_i, 1.0f);              // its half for the column bound
                 // list slot: the row's offset in the call (or, with a unit list, in this rank's units)
                 const uint32_t lrow = p.units ? lu * (PAIR ? 2 * TS_BM : TS_BM) + (PAIR ? rank * TS_BM : 0) + rl
                                               : row - p.row_begin;
@@ -504,9 +634,20 @@ tensor_sweep_kernel(const SweepParams p) {
                 } else if constexpr (TCAP) {
                     thr = ListMax{valid ? __ldg(p.tc + row) : -kInf, 0};  // fixed: the row's threshold
                 } else if constexpr (REGLIST) {
+#ifdef KNN_NO_UDONE
+                    if (false) {
+#else
+                    if (dyn && !fresh) {  // the unit's previous group may have run on another pair: wait for its lists
+#endif
+                        if (lane == 0) {
+                            const uint32_t need = (PAIR ? 2 : 1) * EW * (g - u / p.group_tiles);
+                            while (ptx::ld_acquire_gpu_u32(p.udone + lu) < need) __nanosleep(64);
+                        }
+                        __syncwarp();
+                    }
 #pragma unroll
                     for (int s = 0; s < KPL; ++s) {
-                        uint64_t key = (fresh || !valid) ? kEmptyKey : state[s];
+                        uint64_t key = (fresh || !valid) ? kEmptyKey : __ldcg(state + s);
                         if constexpr (TRI) {
                             if (fresh && valid) key = make_key(__ldg(p.tc + row), kVirtualIdx);
                         }
@@ -580,8 +721,9 @@ tensor_sweep_kernel(const SweepParams p) {
                 };
                 // After a chunk's vote: the column side's appends (TRI), then the
                 // row side's rare path (TCAP: appends as well).
+                // bm_lo (TCAP): a lower bound on the chunk's smallest column norm
                 auto handle = [&](const uint32_t (&v)[W], uint32_t col0, bool fire_r, bool fire_c, float hc,
-                                  float hr) {
+                                  float hr, float bm_lo) {
                     constexpr int P = W / 2;  // column pairs
                     float bt[W];              // the chunk's column norms
                     if constexpr (TRI) {
@@ -606,7 +748,7 @@ tensor_sweep_kernel(const SweepParams p) {
                                     for (int j = 0; j < W; ++j)
                                         if (__uint_as_float(v[j]) > hr) rm |= 1u << j;
                                 }
-                                append(rm, v, col0, true, __ldg(p.bmin + (col0 >> 5)));
+                                append(rm, v, col0, true, bm_lo);
                             }
                             return;
                         }
@@ -724,7 +866,7 @@ tensor_sweep_kernel(const SweepParams p) {
                         }
                     }
                     if (!__any_sync(0xffffffffu, fire_r || fire_c) || p.debug_mode == 4) return;
-                    handle(v, col0, fire_r, fire_c, hc, hr1);
+                    handle(v, col0, fire_r, fire_c, hc, hr1, 0.0f);
                 };
                 constexpr int NCH = SEG_COLS / 32;
                 for (uint32_t t = ts; t < t1; ++t, ++tcount) {
@@ -734,7 +876,8 @@ tensor_sweep_kernel(const SweepParams p) {
                     // before the accumulator wait, so their L2 latency overlaps it
                     float bmv[NCH], tcm[NCH];
                     {
-                        const float* bp = p.bmin + (cbase >> 5);
+                        // (the chunks' bound halves: chunk_min_kernel / chunk_max_kernel)
+                        const float* bp = p.bmin + p.npad / 32 + (cbase >> 5);
                         if constexpr (NCH % 4 == 0) {
 #pragma unroll
                             for (int q = 0; q < NCH / 4; ++q) {
@@ -749,7 +892,7 @@ tensor_sweep_kernel(const SweepParams p) {
                         for (int q = 0; q < NCH; ++q) tcm[q] = kInf;
                         if constexpr (TRI) {
                             if (TRI && t > tsu && valid) {
-                                const float* tp = p.tcmax + (cbase >> 5);
+                                const float* tp = p.tcmax + p.npad / 32 + (cbase >> 5);
 #pragma unroll
                                 for (int q = 0; q < NCH; ++q) tcm[q] = __ldg(tp + q);
                             }
@@ -762,7 +905,7 @@ tensor_sweep_kernel(const SweepParams p) {
                     const bool cside = TRI && t > tsu;  // tiles above the unit's own: both sides
                     // Next tile's column norms into L1 now, so the in-loop
                     // loads of that tile hit L1 instead of paying L2 latency.
-                    if (lane < SEG_COLS / 32 && t + 1 < t1)
+                    if (!TCAP && lane < SEG_COLS / 32 && t + 1 < t1)
                         asm volatile("prefetch.global.L1 [%0];" ::"l"(p.alpha + cbase + BN + lane * 32));
                     if (p.debug_mode && p.debug_mode != 4) {  // pipeline-ceiling experiments
                         uint32_t vd[32];
@@ -780,12 +923,23 @@ tensor_sweep_kernel(const SweepParams p) {
                     // This tile's chunk bounds, once per tile.  A row bound computed
                     // before an insertion earlier in the tile is below the fresh
                     // one (thr only falls), so it admits a superset: still exact.
+                    // h = bound_half(beta_min) + bound_half(thr, -1) (row side),
+                    // bound_half(alpha_i) + bound_half(tc_max, -1) (column side)
                     float hr[NCH], hcv[NCH];
+                    const float thr_h = bound_half(thr.a, -1.0f);
+#ifdef KNN_OLD_BOUNDS
 #pragma unroll
                     for (int q = 0; q < NCH; ++q) {
-                        hr[q] = row_bound(bmv[q]);
-                        hcv[q] = TRI && cside && valid ? col_bound(tcm[q]) : kInf;
+                        hr[q] = row_bound(2.0f * bmv[q]);
+                        hcv[q] = TRI && cside && valid ? col_bound(-2.0f * tcm[q]) : kInf;
                     }
+#else
+#pragma unroll
+                    for (int q = 0; q < NCH; ++q) {
+                        hr[q] = __fadd_rn(bmv[q], thr_h);
+                        hcv[q] = TRI && cside && valid ? __fadd_rn(alpha_h, tcm[q]) : kInf;
+                    }
+#endif
                     uint32_t va[32], vb[32];
                     // two chunks per step: both TMEM reads, two independent max
                     // trees, one vote; column norms only for chunks that reach
@@ -808,7 +962,7 @@ tensor_sweep_kernel(const SweepParams p) {
                                 continue;
                             }
                         }
-                        float ha = hr[0], hb = hr[1], ca = hcv[0], cb = hcv[1];
+                        float ha = hr[0], hb = hr[1], ca = hcv[0], cb = hcv[1], ba = bmv[0], bb = bmv[1];
 #pragma unroll
                         for (int q = 1; q < NCH / 2; ++q) {
                             const bool at = it == q;
@@ -818,13 +972,18 @@ tensor_sweep_kernel(const SweepParams p) {
                                 ca = at ? hcv[2 * q] : ca;
                                 cb = at ? hcv[2 * q + 1] : cb;
                             }
+                            if constexpr (TCAP) {
+                                ba = at ? bmv[2 * q] : ba;
+                                bb = at ? bmv[2 * q + 1] : bb;
+                            }
                         }
                         const float da = vmax(va), db = vmax(vb);
                         const bool ra = da > ha, rb = db > hb;
                         const bool fa = TRI && da > ca, fb = TRI && db > cb;
                         if (!__any_sync(0xffffffffu, ra || rb || fa || fb) || p.debug_mode == 4) continue;
-                        if (__any_sync(0xffffffffu, ra || fa)) handle(va, cbase + c0, ra, fa, ca, ha);
-                        if (__any_sync(0xffffffffu, rb || fb)) handle(vb, cbase + c0 + 32, rb, fb, cb, hb);
+                        // (2 bound_half(beta_min) <= beta_min: the TCAP row side's norm, no load)
+                        if (__any_sync(0xffffffffu, ra || fa)) handle(va, cbase + c0, ra, fa, ca, ha, 2.0f * ba);
+                        if (__any_sync(0xffffffffu, rb || fb)) handle(vb, cbase + c0 + 32, rb, fb, cb, hb, 2.0f * bb);
                     }
                 }
                 if (valid && !CAPTURE && !TCAP) {
@@ -839,6 +998,17 @@ tensor_sweep_kernel(const SweepParams p) {
                             col = my_i[s * L::LIST_ROWS];
                         }
                         state[s] = col == 0xffffffffu ? kEmptyKey : (uint64_t(float_to_ordered(a)) << 32) | col;
+                    }
+                }
+#ifdef KNN_NO_UDONE
+                if (false) {
+#else
+                if (dyn && !TCAP) {  // this warp's part of the unit's lists is saved: count it
+#endif
+                    __syncwarp();
+                    if (lane == 0) {
+                        __threadfence();
+                        atomicAdd(p.udone + lu, 1u);
                     }
                 }
             }
@@ -1076,16 +1246,23 @@ __global__ void chunk_max_kernel(const float* __restrict__ v, uint32_t nchunks, 
     if (warp >= nchunks) return;
     float m = v[size_t(warp) * 32 + lane];
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) out[warp] = m;
+    if (lane == 0) {
+        out[warp] = m;
+        out[nchunks + warp] = bound_half(m, -1.0f);  // the column bound's per-chunk half
+    }
 }
 
-// bmin[c] = smallest alpha of columns [32c, 32c + 32) (the sweep's hot-path bound)
+// bmin[c] = smallest alpha of columns [32c, 32c + 32) (the sweep's hot-path
+// bound), bmin[nchunks + c] = its bound_half (the row bound's per-chunk half)
 __global__ void chunk_min_kernel(const float* __restrict__ alpha, uint32_t nchunks, float* __restrict__ bmin) {
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= nchunks) return;
     float m = alpha[size_t(warp) * 32 + lane];
     for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) bmin[warp] = m;
+    if (lane == 0) {
+        bmin[warp] = m;
+        bmin[nchunks + warp] = bound_half(m, 1.0f);
+    }
 }
 
 __device__ __forceinline__ void atomic_max_pos_double(unsigned long long* addr, double v) {
@@ -1696,6 +1873,10 @@ struct Rescore2Params {
     // fb2_rows go to the EXACT kernel)
     float* retry_thr;
     const float* loose;
+    // two-pass split (null: one pass): rows whose band outgrows the first
+    // pass's shared-memory capacity are listed here for a second pass
+    uint32_t* big;
+    uint32_t* nbig;
 };
 
 // Exact rescore of a captured band (one warp per row): the band holds every
@@ -1718,22 +1899,25 @@ __device__ __forceinline__ size_t band_smem_per_warp(uint32_t cap) {
     return size_t(cap) * 16 + size_t(cap) * 2 + 32 * 33 * 4 + 64;
 }
 
+// One band (slot) with shared-memory room for scap candidates; defer: a band
+// larger than that goes to the second pass's list instead.
 template <int FOLD>
-__global__ void __launch_bounds__(32 * kBandWarps) rescore_capture_kernel(const Rescore2Params p) {
-    extern __shared__ __align__(16) uint8_t band_smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t slot = blockIdx.x * kBandWarps + warp;
-    if (slot >= p.m) return;
-    uint8_t* wbase = band_smem + size_t(warp) * band_smem_per_warp(p.cap);
+__device__ __forceinline__ void band_row(const Rescore2Params& p, uint32_t slot, uint8_t* wbase, uint32_t scap,
+                                         bool defer) {
+    const int lane = threadIdx.x & 31;
     uint64_t* ak = reinterpret_cast<uint64_t*>(wbase);         // approximate keys (y, col)
-    uint64_t* ek = ak + p.cap;                                   // exact keys (distance, col) or empty
-    float* tile = reinterpret_cast<float*>(ek + p.cap);          // [32][33]
+    uint64_t* ek = ak + scap;                                    // exact keys (distance, col) or empty
+    float* tile = reinterpret_cast<float*>(ek + scap);           // [32][33]
     uint16_t* todo = reinterpret_cast<uint16_t*>(tile + 32 * 33);  // candidate positions of a batch
     const uint32_t qo = p.rows[slot];  // input order
     if (qo == 0xffffffffu) return;     // a padding slot of a rank's last unit
     const uint32_t q = p.rowpos ? p.rowpos[qo] : qo;
     const uint32_t cnt_all = p.cnt[slot];
     const bool over = cnt_all > p.cap;  // lost candidates: no proof from this buffer
+    if (defer && min(cnt_all, p.cap) > scap && !(over && !p.retry_thr)) {
+        if (lane == 0) p.big[atomicAdd(p.nbig, 1u)] = slot;
+        return;
+    }
     auto retry = [&](double thr2) {
         if (lane == 0) {
             const uint32_t at = atomicAdd(p.fb2_count, 1u);
@@ -1875,17 +2059,55 @@ __global__ void __launch_bounds__(32 * kBandWarps) rescore_capture_kernel(const 
     }
 }
 
-static size_t band_smem_bytes(uint32_t cap) {
-    return kBandWarps * (size_t(cap) * 16 + size_t(cap) * 2 + 32 * 33 * 4 + 64);
+// pass 0: one warp per slot, room for scap candidates, larger bands listed in
+// p.big; pass 1: the listed slots (grid-stride), room for p.cap; pass 2: one
+// warp per slot, room for p.cap (no split).
+template <int FOLD, int NW>
+__global__ void __launch_bounds__(32 * NW, 1) rescore_capture_kernel(const Rescore2Params p, uint32_t scap, int pass) {
+    extern __shared__ __align__(16) uint8_t band_smem[];
+    const int warp = threadIdx.x >> 5;
+    uint8_t* wbase = band_smem + size_t(warp) * band_smem_per_warp(scap);
+    if (pass == 1) {
+        const uint32_t nb = *p.nbig;
+        for (uint32_t i = blockIdx.x * NW + warp; i < nb; i += gridDim.x * NW) band_row<FOLD>(p, p.big[i], wbase, scap, false);
+        return;
+    }
+    const uint32_t slot = blockIdx.x * NW + warp;
+    if (slot < p.m) band_row<FOLD>(p, slot, wbase, scap, pass == 0);
 }
 
+static size_t band_smem_bytes(uint32_t cap, int warps = kBandWarps) {
+    return warps * (size_t(cap) * 16 + size_t(cap) * 2 + 32 * 33 * 4 + 64);
+}
+
+// expect: the typical band size (0: unknown).  With r2.big set, bands up to
+// ~1.5 expect run 8 warps per block in small shared-memory slices (2-3x the
+// occupancy of slices sized for the capacity); the rest get a second pass.
 template <int FOLD>
-static cudaError_t launch_rescore_capture(const Rescore2Params& r2, uint32_t rows, cudaStream_t st) {
+static cudaError_t launch_rescore_capture(const Rescore2Params& r2, uint32_t rows, cudaStream_t st,
+                                          uint32_t expect = 0) {
+    cudaError_t e;
+    uint32_t scap = (expect * 3 / 2 + 63) / 64 * 64;
+    if (r2.big && expect && scap < r2.cap / 2) {
+        scap = std::max(128u, scap);
+        auto k0 = rescore_capture_kernel<FOLD, 8>;
+        auto k1 = rescore_capture_kernel<FOLD, kBandWarps>;
+        const size_t s0 = band_smem_bytes(scap, 8), s1 = band_smem_bytes(r2.cap);
+        if ((e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s0))) != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s1))) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(r2.nbig, 0, 4, st)) != cudaSuccess) return e;
+        k0<<<(rows + 7) / 8, 256, s0, st>>>(r2, scap, 0);
+        int sms = 148, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        k1<<<std::min<uint32_t>((rows + kBandWarps - 1) / kBandWarps, uint32_t(sms) * 2), 32 * kBandWarps, s1, st>>>(
+            r2, r2.cap, 1);
+        return cudaGetLastError();
+    }
+    auto k = rescore_capture_kernel<FOLD, kBandWarps>;
     const size_t smem = band_smem_bytes(r2.cap);
-    cudaError_t e = cudaFuncSetAttribute(rescore_capture_kernel<FOLD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem));
-    if (e != cudaSuccess) return e;
-    rescore_capture_kernel<FOLD><<<(rows + kBandWarps - 1) / kBandWarps, 32 * kBandWarps, smem, st>>>(r2);
+    if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) != cudaSuccess) return e;
+    k<<<(rows + kBandWarps - 1) / kBandWarps, 32 * kBandWarps, smem, st>>>(r2, r2.cap, 2);
     return cudaGetLastError();
 }
 
@@ -1981,7 +2203,7 @@ size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32
     auto add = [&](size_t x) { b += (x + 255) / 256 * 256; };
     add(size_t(kc) * npad * 128);  // xh
     add(size_t(npad) * 4);         // alpha
-    add(size_t(npad / 32) * 4);    // bmin
+    add(size_t(npad / 32) * 8);    // bmin + bound halves
     add(size_t(npad) * 8);         // rho
     add(size_t(npad) * 8);         // xnorm
     add(size_t(d) * 8);            // mu acc
@@ -2231,7 +2453,7 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
     };
     uint8_t* xh = take(size_t(kc) * npad * 128);
     float* alpha = reinterpret_cast<float*>(take(size_t(npad) * 4));
-    float* bmin = reinterpret_cast<float*>(take(size_t(npad / 32) * 4));
+    float* bmin = reinterpret_cast<float*>(take(size_t(npad / 32) * 8));  // + bound halves
     double* rho = reinterpret_cast<double*>(take(size_t(npad) * 8));
     double* xnorm = reinterpret_cast<double*>(take(size_t(npad) * 8));
     double* muacc = reinterpret_cast<double*>(take(size_t(d) * 8));

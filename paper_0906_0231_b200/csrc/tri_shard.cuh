@@ -47,13 +47,22 @@ static inline uint32_t tri_lane_of_unit(uint32_t u, uint32_t world) {
     return r < world ? r : 2 * world - 1 - r;
 }
 
-// Per-rank unit lists.  Units go to ranks in boustrophedon order; a rank's
-// units ascending (work U - u descending) are then dealt to the launch's CTA
-// pairs in snake order, so pair p's strided walk (p, p + P, ...) takes
-// alternately heavier and lighter units.
+// The sweep's dynamic unit queue (default; KNN_B200_TRI_DYN=0: the static walk).
+static bool tri_dyn_enabled() {
+    const char* e = getenv("KNN_B200_TRI_DYN");
+    return !(e && atoi(e) == 0);
+}
+
+// Per-rank unit lists.  Units go to ranks in boustrophedon order.  With the
+// dynamic queue a rank's units stay ascending (work U - u descending): CTA
+// pairs claim them heaviest first, and the units of a column group with work
+// are a prefix.  Without it they are dealt to the launch's CTA pairs in snake
+// order, so pair p's strided walk (p, p + P, ...) takes alternately heavier
+// and lighter units.
 static std::vector<std::vector<uint32_t>> tri_unit_lists(uint32_t U, uint32_t G, uint32_t pairs_max) {
     std::vector<std::vector<uint32_t>> asc(G), out(G);
     for (uint32_t u = 0; u < U; ++u) asc[tri_lane_of_unit(u, G)].push_back(u);
+    if (tri_dyn_enabled()) return asc;
     for (uint32_t r = 0; r < G; ++r) {
         const std::vector<uint32_t>& a = asc[r];
         const uint32_t m = uint32_t(a.size());
@@ -294,7 +303,7 @@ struct TriShared {
     void layout(Carve& c) {
         xh = c.take<uint8_t>(size_t(kc) * npad * 128);
         alpha = c.take<float>(npad);
-        bmin = c.take<float>(npad / 32);
+        bmin = c.take<float>(2 * (npad / 32));  // + bound halves
         rho = c.take<double>(npad);
         xnorm = c.take<double>(npad);
         muacc = c.take<double>(d);
@@ -310,7 +319,7 @@ struct TriShared {
         xs = c.take<uint8_t>(size_t(skc) * spad * 128);
         x8 = f8 ? c.take<uint8_t>(size_t(skc) * npad * 128) : nullptr;
         alpha_s = c.take<float>(spad);
-        bmin_s = c.take<float>(spad / 32);
+        bmin_s = c.take<float>(2 * (spad / 32));
         tc2 = c.take<float>(size_t(G) * S);
         tl1 = c.take<float>(size_t(G) * S);
         okey = c.take<unsigned long long>(n);
@@ -321,8 +330,8 @@ struct TriShared {
         tri_alpha = c.take<float>(npad);
         tri_tc = c.take<float>(npad);
         tri_tl = c.take<float>(npad);
-        bmin2 = c.take<float>(npad / 32);
-        tcmax = c.take<float>(npad / 32);
+        bmin2 = c.take<float>(2 * (npad / 32));
+        tcmax = c.take<float>(2 * (npad / 32));
         tri_rho = c.take<double>(npad);
         tri_xnorm = c.take<double>(npad);
         tri_perm = c.take<uint32_t>(n);
@@ -382,6 +391,11 @@ static cudaError_t tri_prep(TriShared& S, const TensorPathArgs& a, uint32_t G, S
         if (const char* fe = getenv("KNN_B200_TCAP_E4M3")) S.f8 = atoi(fe) != 0;
         const double m = double(a.klist) / S.stride;
         S.trank = uint32_t(std::min(32.0, std::ceil(m + 2.5 * std::sqrt(m) + 1.0)));
+        // each half's list must hold the rank-r value: the shortest list that
+        // does (C4: r = 7 -> 8 entries, C3: r = 9 -> 12; fewer insertions and
+        // registers than 16)
+        S.skpl = S.trank <= 8 ? 8u : S.trank <= 12 ? 12u : 16u;
+        if (const char* ke = getenv("KNN_B200_TCAP_SAMPLE_KPL")) S.skpl = atoi(ke) == 16 ? 16u : S.skpl;
     }
     S.n = n;
     S.d = d;
@@ -505,9 +519,13 @@ static cudaError_t tri_sample(TriShared& S, TriRank& R, const TensorPathArgs& a)
     ss.e4m3 = S.f8;
     const uint32_t rows = R.s1 - R.s0;
     const bool ares = S.skc <= uint32_t(TS_MAX_RES_KC);
-    cudaError_t e = S.skpl == 16 ? (ares ? launch_sweep_pair<16, 256, 8>(ss, rows, st)
-                                         : launch_sweep_pair<16, 256, 8, false, false, false>(ss, rows, st))
-                    : S.skpl == 12 ? launch_sweep_pair<12, 256, 8>(ss, rows, st)
+    // (d > 256: the query rows stream with every reference chunk, ARES = false)
+    cudaError_t e = S.skpl == 16  ? (ares ? launch_sweep_pair<16, 256, 8>(ss, rows, st)
+                                          : launch_sweep_pair<16, 256, 8, false, false, false>(ss, rows, st))
+                    : S.skpl == 12 ? (ares ? launch_sweep_pair<12, 256, 8>(ss, rows, st)
+                                           : launch_sweep_pair<12, 256, 8, false, false, false>(ss, rows, st))
+                    : S.skpl == 8  ? (ares ? launch_sweep_pair<8, 256, 8>(ss, rows, st)
+                                           : launch_sweep_pair<8, 256, 8, false, false, false>(ss, rows, st))
                     : S.skpl == 6  ? launch_sweep_pair<6, 256, 8>(ss, rows, st)
                                    : launch_sweep_pair<kTriSampleKpl, 256, 8>(ss, rows, st);
     if (e != cudaSuccess) return e;
@@ -562,10 +580,16 @@ static cudaError_t tri_sweep(TriShared& S, TriRank& R, const TensorPathArgs& a, 
     uint64_t pool = uint64_t(per_row * double(S.n) * share) + uint64_t(2 * pairs * 8) * kLogChunk;
     if (const char* lce = getenv("KNN_B200_TRI_LOGCAP")) pool = uint64_t(atoi(lce));
     R.nchunks = uint32_t((pool + kLogChunk - 1) / kLogChunk);
+    // the dynamic queue's claim counters (one per column group) and per-unit
+    // list-state counters
+    const uint32_t ngroups = ((S.n + 255) / 256 + S.group_tiles - 1) / S.group_tiles;
+    const bool dyn = tri_dyn_enabled();
+    uint32_t* qctr = nullptr;
     auto lay = [&](Carve& c) {
         R.lkey = c.take<uint64_t>(size_t(R.nchunks) * kLogChunk);
         R.lcol = c.take<uint32_t>(size_t(R.nchunks) * kLogChunk);
         R.lcnt = c.take<uint32_t>(size_t(R.nchunks) + 1);
+        qctr = c.take<uint32_t>(size_t(ngroups) + R.nu + 1);
     };
     Carve c;
     lay(c);
@@ -585,6 +609,11 @@ static cudaError_t tri_sweep(TriShared& S, TriRank& R, const TensorPathArgs& a, 
                    S.tri_tc, S.tcmax,  R.lkey, R.lcol,  R.lcnt, R.lnext, R.nchunks};
     tp.units = R.units;
     tp.nunits = R.nu;
+    if (dyn) {
+        if ((e = cudaMemsetAsync(qctr, 0, (size_t(ngroups) + R.nu) * 4, st)) != cudaSuccess) return e;
+        tp.qctr = qctr;
+        tp.udone = qctr + ngroups;
+    }
     // profiling only: per-CTA start/end times of this rank's sweep, appended
     // to the file the variable names (rank, CTA, start ns, end ns, units)
     const char* ctaf = getenv("KNN_B200_DEBUG_CTA_TIMES");
@@ -604,8 +633,8 @@ static cudaError_t tri_sweep(TriShared& S, TriRank& R, const TensorPathArgs& a, 
         cudaFreeAsync(cta_ns, st);
         if (FILE* f = fopen(ctaf, "a")) {
             for (uint32_t c = 0; c < 2 * pairs; ++c) {
-                uint32_t nu = 0;
-                for (size_t i = c / 2; i < S.units_h[R.rank].size(); i += pairs) ++nu;
+                uint32_t nu = 0;  // (the static walk's units; the dynamic queue's are not recorded)
+                for (size_t i = c / 2; !dyn && i < S.units_h[R.rank].size(); i += pairs) ++nu;
                 fprintf(f, "%u %u %llu %llu %u\n", R.rank, c, t[2 * c], t[2 * c + 1], nu);
             }
             fclose(f);
@@ -804,6 +833,16 @@ cudaError_t run_tri_loopback(const TensorPathArgs& a, uint32_t G, ShardAllocFn a
     if (a.ev_sweep1) cudaEventRecord(a.ev_sweep1, st);
     if (overflow) *overflow = ovf;
     if (ovf) return done(cudaSuccess);  // the caller redoes the call without the triangle
+    if (getenv("KNN_B200_DEBUG_SWEEP_ONLY")) {  // profiling only: phase timings up to the sweep, no results
+        if (rank_ms)
+            for (uint32_t g = 0; g < G; ++g) {
+                rank_ms[4 * g + 0] = ev_ms(ev[0], ev[1]) + ev_ms(ev[4], ev[5]);
+                rank_ms[4 * g + 1] = ms_a[g];
+                rank_ms[4 * g + 2] = ms_b[g];
+                rank_ms[4 * g + 3] = 0;
+            }
+        return done(cudaSuccess);
+    }
     // exchange 2: rank o receives segment [g -> o] of every rank g, in rank order
     for (uint32_t o = 0; o < G && G > 1; ++o) {
         unsigned long long cnt = 0;
@@ -971,14 +1010,15 @@ static cudaError_t tcap_finish(TriShared& S, TriRank& R, const TensorPathArgs& a
     cudaError_t e;
     const uint32_t cap = tcap_cap(a.klist);
     uint64_t* cbuf;
-    uint32_t *ccnt, *rows, *fb_count;
+    uint32_t *ccnt, *rows, *fb_count, *big;
     float* thr;
     auto lay = [&](Carve& c) {
         cbuf = c.take<uint64_t>(size_t(R.nslots) * cap);
         ccnt = c.take<uint32_t>(R.nslots);
         rows = c.take<uint32_t>(R.nslots);
         thr = c.take<float>(R.nslots);
-        fb_count = c.take<uint32_t>(16);
+        fb_count = c.take<uint32_t>(16);  // [0]: retried rows, [8]: second-pass bands
+        big = c.take<uint32_t>(R.nslots);
     };
     Carve c;
     lay(c);
@@ -1003,8 +1043,12 @@ static cudaError_t tcap_finish(TriShared& S, TriRank& R, const TensorPathArgs& a
                       thr,  S.tri_rowpos, S.tri_alpha, S.tri_rho, S.tri_xnorm, S.gmax, S.maxabs};
     r2.retry_thr = R.fb_thr;
     r2.loose = S.tri_tl;
-    e = a.fold == kCosine ? launch_rescore_capture<kCosine>(r2, R.nslots, st)
-                          : launch_rescore_capture<kSqEuclidean>(r2, R.nslots, st);
+    r2.big = big;
+    r2.nbig = fb_count + 8;
+    // the typical band: the sample's rank-r window plus the proof band (~64)
+    const uint32_t expect = S.trank * S.stride + 64;
+    e = a.fold == kCosine ? launch_rescore_capture<kCosine>(r2, R.nslots, st, expect)
+                          : launch_rescore_capture<kSqEuclidean>(r2, R.nslots, st, expect);
     if (e != cudaSuccess) return e;
     uint32_t* h = static_cast<uint32_t*>(a.host_scratch);
     if ((e = cudaMemcpyAsync(h, fb_count, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;

@@ -78,29 +78,42 @@ def test_gloo_shards_assemble_the_full_answer(tmp_path, world):
         assert np.array_equal(gd.view(np.uint32), rd.view(np.uint32))
 
 
-def test_tri_unit_plan_is_boustrophedon_and_snake():
+def test_tri_unit_plan_is_boustrophedon_and_heaviest_first():
     """The product's host planner (knn_b200_tri_unit_plan): unit u belongs to
-    lane_of_row(u) (schedule.cpp:40-44), every unit exactly once, and the
-    per-rank work (sum of U - u) balanced like the reference's lanes
-    (test_schedule.cpp:169-185)."""
+    lane_of_row(u) (schedule.cpp:40-44), every unit exactly once, the per-rank
+    work (sum of U - u) balanced like the reference's lanes
+    (test_schedule.cpp:169-185), and each rank's units ascending -- heaviest
+    first for the sweep's dynamic queue, and a column group's units with work
+    a prefix of the list."""
     from paper_0906_0231_b200.parallel import tri_unit_plan
     for units, world, pairs in ((3907, 8, 74), (1563, 2, 74), (38, 3, 2), (5, 8, 74), (62500, 8, 74)):
         plan = tri_unit_plan(units, world, pairs)
         flat = sorted(u for r in plan for u in r)
         assert flat == list(range(units))
         for r, lst in enumerate(plan):
+            assert lst == sorted(lst)
             for u in lst:
                 m = u % (2 * world)
                 assert (m if m < world else 2 * world - 1 - m) == r
         if units >= 2 * world * 8:
             work = [sum(units - u for u in lst) for lst in plan]
             assert max(work) / min(work) < 1.01
-            # the snake keeps each CTA pair's share within 1% of the mean
-            for lst in plan:
-                p = min(len(lst), pairs)
-                per = [sum(units - u for u in lst[i::p]) for i in range(p)]
-                if len(lst) >= 4 * p:
-                    assert max(per) / (sum(per) / p) < 1.02
+
+
+def test_tri_unit_plan_static_walk_is_snake(monkeypatch):
+    """KNN_B200_TRI_DYN=0 (the static walk): each rank's units are dealt to
+    the CTA pairs in snake order, keeping each pair's share within 2% of the
+    mean."""
+    from paper_0906_0231_b200.parallel import tri_unit_plan
+    monkeypatch.setenv("KNN_B200_TRI_DYN", "0")
+    for units, world, pairs in ((3907, 1, 74), (1563, 2, 74), (62500, 8, 74)):
+        plan = tri_unit_plan(units, world, pairs)
+        assert sorted(u for r in plan for u in r) == list(range(units))
+        for lst in plan:
+            p = min(len(lst), pairs)
+            per = [sum(units - u for u in lst[i::p]) for i in range(p)]
+            if len(lst) >= 4 * p:
+                assert max(per) / (sum(per) / p) < 1.02
 
 
 def _tri_worker(rank, world, port, n, d, k, unit, out_dir):

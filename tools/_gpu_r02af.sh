@@ -1,0 +1,9 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests/test_gpu_configs.py tests/test_gpu_shard.py -x -q -rfE -k "c3 or c4 or gaussian or outlier or equal_norms or loopback or forced or pool" > gpurun_out/r02af_tests.log 2>&1; echo tests rc=$?; tail -2 gpurun_out/r02af_tests.log
+echo "== C2" > gpurun_out/r02af_ab.txt
+bash tools/ab_multi.sh "base new nodyn" --n 1000000 --d 256 --k 10 --seed 1 --reps 3 >> gpurun_out/r02af_ab.txt 2>&1
+echo "== C4" >> gpurun_out/r02af_ab.txt
+bash tools/ab_multi.sh "base new" --n 4000000 --d 128 --k 32 --metric cosine --seed 3 --reps 2 >> gpurun_out/r02af_ab.txt 2>&1
+echo "== C3" >> gpurun_out/r02af_ab.txt
+bash tools/ab_multi.sh "base new" --n 1000000 --d 1024 --k 100 --seed 2 --reps 2 >> gpurun_out/r02af_ab.txt 2>&1
+timeout 600 python tools/shard_emulate.py --worlds 1,8 --reps 2 > gpurun_out/r02af_shard_c2.jsonl 2>&1; echo emu rc=$?
