@@ -178,14 +178,11 @@ __global__ void remap_capture_kernel(uint64_t* __restrict__ buf, const uint32_t*
     }
 }
 
-// The sweep's work-item walk: this CTA's next item (column group g, local
-// unit lu), false when there is none.  role 0: the queue's claiming producer
-// (leader, warp 0); 1: a consumer in the leader; 2: a consumer in the peer.
-// warp_wide: the whole warp calls this (lane 0 releases the queue slot).
-// Without the queue (dyn false): the static walk -- column groups in order,
-// inside a group units unit0, unit0 + unit_step, ...  Out of line: it runs
-// once per item, and inlined copies in every role measurably slowed the
-// epilogue's hot loop (C2: +7%).
+// The dynamic unit queue's item walk (DYN sweeps): this CTA's next item
+// (column group g, local unit lu), false when the queue is drained.  role 0:
+// the claiming producer (leader, warp 0); 1: a consumer in the leader; 2: a
+// consumer in the peer.  warp_wide: the whole warp calls this (lane 0
+// releases the queue slot).  Out of line: it runs once per item.
 constexpr int kQN = 4;                 // queue slots
 constexpr uint64_t kQEnd = ~0ull;      // the end-of-work item
 struct ItemWalk {
@@ -201,24 +198,6 @@ struct ItemWalk {
 
 __device__ __noinline__ bool item_next(ItemWalk& w, int role, bool warp_wide) {
     auto unit_id = [&](uint32_t lu) { return w.units ? __ldg(w.units + lu) : lu; };
-    if (!w.dyn) {
-        for (;;) {
-            if (!w.started) {
-                w.started = true;
-                w.g = w.g_first;
-                w.lu = w.unit0;
-            } else {
-                w.lu += w.unit_step;
-            }
-            if (w.lu >= w.nunits) {
-                w.g += w.g_step;
-                w.lu = w.unit0;
-            }
-            if (w.g >= w.ngroups) return false;
-            const uint32_t t0 = w.g * w.group_tiles, t1 = min(w.ntiles, t0 + w.group_tiles);
-            if (w.lu < w.nunits && max(t0, w.tri ? unit_id(w.lu) : 0u) < t1) return true;
-        }
-    }
     const int s = w.qi % kQN;
     const uint32_t ph = (w.qi / kQN) & 1;
     const uint32_t qfull = w.qbar0 + 8u * s, qempty = w.qbar0 + 8u * (kQN + s);
@@ -267,7 +246,12 @@ __device__ __noinline__ bool item_next(ItemWalk& w, int role, bool warp_wide) {
 // TCAP (with TRI): the threshold triangle -- both sides of every pair go to
 // the pool against fixed per-row thresholds p.tc (no lists); the rows' pool
 // entries are then rescored exactly like the band-capture pass.
-template <int KPL, int BN, bool ARES, int EW, bool CAPTURE, bool PAIR = false, bool TRI = false, bool TCAP = false>
+// DYN (with TRI): the work items come from the dynamic unit queue (p.qctr);
+// otherwise from the static walk.  Separate instantiations: the static walk's
+// inlined loop is what the single-GPU list triangle runs (the queue's code in
+// the same kernel cost C2 ~8% even when unused).
+template <int KPL, int BN, bool ARES, int EW, bool CAPTURE, bool PAIR = false, bool TRI = false, bool TCAP = false,
+          bool DYN = false>
 __global__ void __launch_bounds__(TSLayout<KPL, BN, ARES, EW, PAIR>::THREADS, 1)
 tensor_sweep_kernel(const SweepParams p) {
     using L = TSLayout<KPL, BN, ARES, EW, PAIR>;
@@ -326,15 +310,37 @@ tensor_sweep_kernel(const SweepParams p) {
     // every other role (MMA issuer, epilogue warps, the peer's producer and
     // forwarder) takes the same items in the same order.
     constexpr int QN = kQN;
-#ifdef KNN_NO_DYN
-    constexpr bool dyn = false;
-#else
-    const bool dyn = TRI && p.qctr != nullptr;
-#endif
+    static_assert(!DYN || TRI, "the unit queue serves the triangle sweeps");
+    constexpr bool dyn = DYN;
     const uint32_t qbar0 = bar0 + 8u * (2 * S + 7);
     auto qfull_bar = [&](int s) { return qbar0 + 8u * s; };
     auto qempty_bar = [&](int s) { return qbar0 + 8u * (QN + s); };
     uint64_t* qitem = bars + 2 * S + 7 + 2 * QN;
+    // This CTA's next work item: the queue (DYN: item_next, out of line) or
+    // the static walk, inlined -- column groups in order; inside a group,
+    // units unit0, unit0 + unit_step, ... that have tiles in the group.
+    auto next = [&](ItemWalk& w, int role, bool warp_wide) -> bool {
+        if constexpr (DYN) {
+            return item_next(w, role, warp_wide);
+        } else {
+            for (;;) {
+                if (!w.started) {
+                    w.started = true;
+                    w.g = g_first;
+                    w.lu = unit0;
+                } else {
+                    w.lu += unit_step;
+                }
+                if (w.lu >= nunits) {
+                    w.g += g_step;
+                    w.lu = unit0;
+                }
+                if (w.g >= ngroups) return false;
+                const uint32_t t0 = w.g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
+                if (w.lu < nunits && max(t0, tri_start(unit_id(w.lu))) < t1) return true;
+            }
+        }
+    };
     auto make_walk = [&]() {
         ItemWalk w;
         w.units = p.units;
@@ -393,7 +399,7 @@ tensor_sweep_kernel(const SweepParams p) {
             int stage = 0;
             uint32_t phase = 0, a_phase = 0;
             ItemWalk cur = make_walk();
-            while (item_next(cur, leader ? 0 : 2, false)) {
+            while (next(cur, leader ? 0 : 2, false)) {
                 const uint32_t g = cur.g, lu = cur.lu;
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
                 {
@@ -445,7 +451,7 @@ tensor_sweep_kernel(const SweepParams p) {
             int stage = 0;
             uint32_t phase = 0, a_phase = 0;
             ItemWalk cur = make_walk();
-            while (item_next(cur, 2, false)) {
+            while (next(cur, 2, false)) {
                 const uint32_t g = cur.g, lu = cur.lu;
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
                 const uint32_t ts = max(t0, tri_start(unit_id(lu)));
@@ -484,7 +490,7 @@ tensor_sweep_kernel(const SweepParams p) {
             int stage = 0;
             uint32_t phase = 0, a_phase = 0, tcount = 0;
             ItemWalk cur = make_walk();
-            while (item_next(cur, 1, false)) {
+            while (next(cur, 1, false)) {
                 const uint32_t g = cur.g, lu = cur.lu;
                 const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
                 {
@@ -610,7 +616,7 @@ tensor_sweep_kernel(const SweepParams p) {
             ptx::mbar_arrive(tempty_bar(b));
         };
         ItemWalk cur = make_walk();
-        while (item_next(cur, leader ? 1 : 2, true)) {
+        while (next(cur, leader ? 1 : 2, true)) {
             const uint32_t g = cur.g, lu = cur.lu;
             const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
             {
@@ -634,11 +640,7 @@ tensor_sweep_kernel(const SweepParams p) {
                 } else if constexpr (TCAP) {
                     thr = ListMax{valid ? __ldg(p.tc + row) : -kInf, 0};  // fixed: the row's threshold
                 } else if constexpr (REGLIST) {
-#ifdef KNN_NO_UDONE
-                    if (false) {
-#else
                     if (dyn && !fresh) {  // the unit's previous group may have run on another pair: wait for its lists
-#endif
                         if (lane == 0) {
                             const uint32_t need = (PAIR ? 2 : 1) * EW * (g - u / p.group_tiles);
                             while (ptx::ld_acquire_gpu_u32(p.udone + lu) < need) __nanosleep(64);
@@ -1000,11 +1002,7 @@ tensor_sweep_kernel(const SweepParams p) {
                         state[s] = col == 0xffffffffu ? kEmptyKey : (uint64_t(float_to_ordered(a)) << 32) | col;
                     }
                 }
-#ifdef KNN_NO_UDONE
-                if (false) {
-#else
                 if (dyn && !TCAP) {  // this warp's part of the unit's lists is saved: count it
-#endif
                     __syncwarp();
                     if (lane == 0) {
                         __threadfence();
@@ -1896,19 +1894,43 @@ struct Rescore2Params {
 // 9% of DRAM bandwidth at C3).
 constexpr int kBandWarps = 4;
 __device__ __forceinline__ size_t band_smem_per_warp(uint32_t cap) {
-    return size_t(cap) * 16 + size_t(cap) * 2 + 32 * 33 * 4 + 64;
+    return size_t(cap) * 16 + 32 * 33 * 4 + 64;
 }
 
-// One band (slot) with shared-memory room for scap candidates; defer: a band
-// larger than that goes to the second pass's list instead.
+// Ascending bitonic sort of s[0, n) (n a power of two) by one warp.
+__device__ __forceinline__ void warp_bitonic_sort(uint64_t* s, uint32_t n, int lane) {
+    for (uint32_t k = 2; k <= n; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t t = lane; t < n / 2; t += 32) {  // every lane one compare-exchange
+                const uint32_t i = (t / j) * 2 * j + (t % j), l = i + j;
+                const uint64_t a = s[i], b = s[l];
+                if ((a > b) == ((i & k) == 0)) {
+                    s[i] = b;
+                    s[l] = a;
+                }
+            }
+            __syncwarp();
+        }
+}
+
+__device__ __forceinline__ uint32_t pow2_at_least(uint32_t x) { return x <= 1 ? 1 : 1u << (32 - __clz(x - 1)); }
+
+// One band (slot) with shared-memory room for scap (a power of two)
+// candidates; defer: a band larger than that goes to the second pass's list.
+//
+// The band's approximate keys are sorted once (a warp bitonic sort in shared
+// memory); phase 1 folds the first klist + 4, phase 2 the prefix that follows
+// while alpha + y stays inside the proof bound of phase 1's k-th exact
+// distance -- the same sets as selecting by rank and by bound over the
+// unsorted band.  The folded exact keys are sorted for the k-th distance and
+// the output order.
 template <int FOLD>
 __device__ __forceinline__ void band_row(const Rescore2Params& p, uint32_t slot, uint8_t* wbase, uint32_t scap,
                                          bool defer) {
     const int lane = threadIdx.x & 31;
-    uint64_t* ak = reinterpret_cast<uint64_t*>(wbase);         // approximate keys (y, col)
-    uint64_t* ek = ak + scap;                                    // exact keys (distance, col) or empty
-    float* tile = reinterpret_cast<float*>(ek + scap);           // [32][33]
-    uint16_t* todo = reinterpret_cast<uint16_t*>(tile + 32 * 33);  // candidate positions of a batch
+    uint64_t* ak = reinterpret_cast<uint64_t*>(wbase);  // approximate keys (y, col), sorted
+    uint64_t* ek = ak + scap;                             // exact keys (distance, col) of folded positions
+    float* tile = reinterpret_cast<float*>(ek + scap);    // [32][33]
     const uint32_t qo = p.rows[slot];  // input order
     if (qo == 0xffffffffu) return;     // a padding slot of a rank's last unit
     const uint32_t q = p.rowpos ? p.rowpos[qo] : qo;
@@ -1930,19 +1952,24 @@ __device__ __forceinline__ void band_row(const Rescore2Params& p, uint32_t slot,
         return;
     }
     const uint32_t c = over ? p.cap : cnt_all;
+    const uint32_t na = max(pow2_at_least(c), 2u);
     const uint64_t* in = p.buf + size_t(slot) * p.cap;
-    for (uint32_t i = lane; i < c; i += 32) {
-        const uint64_t key = in[i];
-        ak[i] = uint32_t(key) == qo ? kEmptyKey : key;  // the row itself is not a candidate
-        ek[i] = kEmptyKey;
+    uint32_t nv = 0;  // non-empty candidates
+    for (uint32_t i = lane; i < na; i += 32) {
+        uint64_t key = i < c ? in[i] : kEmptyKey;
+        if (uint32_t(key) == qo) key = kEmptyKey;  // the row itself is not a candidate
+        ak[i] = key;
+        nv += key != kEmptyKey;
     }
+    for (int o = 16; o; o >>= 1) nv += __shfl_xor_sync(0xffffffffu, nv, o);
     __syncwarp();
+    warp_bitonic_sort(ak, na, lane);
     const float* xq = p.X + size_t(qo) * p.d;
-    // fold the candidates at positions todo[0, nt) (ak -> ek)
-    auto fold_batch = [&](uint32_t nt) {
-        for (uint32_t g = 0; g < nt; g += 32) {
-            const uint32_t mine = g + lane < nt ? todo[g + lane] : 0xffffu;
-            const uint32_t col = mine != 0xffffu ? uint32_t(ak[mine]) : qo;
+    // fold the candidates at sorted positions [lo, hi) (ak -> ek, same positions)
+    auto fold_range = [&](uint32_t lo, uint32_t hi) {
+        for (uint32_t g = lo; g < hi; g += 32) {
+            const bool mine = g + lane < hi;
+            const uint32_t col = mine ? uint32_t(ak[g + lane]) : qo;
             // lane r's candidate row: lanes load row r's chunk (coalesced);
             // the next chunk's 32 loads are in flight while this one folds
             float nxt[32];
@@ -1969,75 +1996,53 @@ __device__ __forceinline__ void band_row(const Rescore2Params& p, uint32_t slot,
                     acc = fold_step<FOLD>(tile[lane * 33 + jj], __shfl_sync(0xffffffffu, qv, jj), acc);
                 __syncwarp();
             }
-            if (mine != 0xffffu) ek[mine] = make_key(fold_finalize<FOLD>(acc), col);
+            if (mine) ek[g + lane] = make_key(fold_finalize<FOLD>(acc), col);
         }
         __syncwarp();
     };
-    // the klist-th smallest exact key so far (keys are unique: distinct columns)
-    auto kth_exact = [&]() -> uint64_t {
-        uint64_t kth = kEmptyKey;
-        for (uint32_t i = lane; i < c; i += 32) {
-            const uint64_t mk = ek[i];
-            if (mk == kEmptyKey) continue;
-            uint32_t rank = 0;
-            for (uint32_t j = 0; j < c; ++j) rank += ek[j] < mk;
-            if (rank == p.klist - 1) kth = mk;
-        }
-        for (int o = 16; o; o >>= 1) {
-            const uint64_t other = __shfl_xor_sync(0xffffffffu, kth, o);
-            kth = other < kth ? other : kth;
-        }
-        return kth;
+    // sort ek[0, m) (padding with empty keys up to a power of two)
+    auto sort_exact = [&](uint32_t m) {
+        const uint32_t ne = max(pow2_at_least(m), 2u);
+        for (uint32_t i = m + lane; i < ne; i += 32) ek[i] = kEmptyKey;
+        __syncwarp();
+        warp_bitonic_sort(ek, ne, lane);
     };
     // phase 1: the klist + 4 best by approximate y
-    uint32_t nt = 0;
-    {
-        const uint32_t r1 = p.klist + 4;
-        for (uint32_t i0 = 0; i0 < c; i0 += 32) {
-            const uint32_t i = i0 + lane;
-            bool take = false;
-            if (i < c && ak[i] != kEmptyKey) {
-                uint32_t rank = 0;
-                for (uint32_t j = 0; j < c; ++j) rank += ak[j] < ak[i];
-                take = rank < r1;
-            }
-            const uint32_t b = __ballot_sync(0xffffffffu, take);
-            if (take) todo[nt + __popc(b & ((1u << lane) - 1u))] = uint16_t(i);
-            nt += __popc(b);
-        }
-        __syncwarp();
-        fold_batch(nt);
-    }
+    const uint32_t p1 = min(p.klist + 4, nv);
+    fold_range(0, p1);
+    sort_exact(p1);
     const double alpha_q = double(p.alpha[q]);
-    const uint64_t kth1 = kth_exact();
-    // phase 2: everything whose approximate A is inside the bound of kth1
-    // (everything left when there is no k-th yet)
-    {
-        double lim = __longlong_as_double(0x7ff0000000000000ll);
-        if (kth1 != kEmptyKey)
-            lim = proof_bound<FOLD>(p.d, p.maxabs, p.gmax, p.xnorm[q], p.rho[q], alpha_q,
-                                    double(ordered_to_float(uint32_t(kth1 >> 32))));
-        nt = 0;
-        for (uint32_t i0 = 0; i0 < c; i0 += 32) {
+    // phase 2: the following candidates whose approximate A is inside the
+    // bound of phase 1's k-th exact distance (all of them without a k-th)
+    uint32_t p2 = nv;
+    if (p1 >= p.klist) {
+        const uint64_t kth1 = ek[p.klist - 1];
+        const double lim = proof_bound<FOLD>(p.d, p.maxabs, p.gmax, p.xnorm[q], p.rho[q], alpha_q,
+                                             double(ordered_to_float(uint32_t(kth1 >> 32))));
+        // first position (>= p1) whose alpha + y exceeds lim: y ascends along ak
+        uint32_t cut = nv;
+        for (uint32_t i0 = p1; i0 < nv; i0 += 32) {
             const uint32_t i = i0 + lane;
-            const bool take = i < c && ak[i] != kEmptyKey && ek[i] == kEmptyKey &&
-                              alpha_q + double(ordered_to_float(uint32_t(ak[i] >> 32))) <= lim;
-            const uint32_t b = __ballot_sync(0xffffffffu, take);
-            if (take) todo[nt + __popc(b & ((1u << lane) - 1u))] = uint16_t(i);
-            nt += __popc(b);
+            const bool outside = i < nv && !(alpha_q + double(ordered_to_float(uint32_t(ak[i] >> 32))) <= lim);
+            const uint32_t b = __ballot_sync(0xffffffffu, outside);
+            if (b) {
+                cut = i0 + __ffs(b) - 1;
+                break;
+            }
         }
-        __syncwarp();
-        if (nt) fold_batch(nt);
+        p2 = cut;
     }
-    uint32_t valid = 0;
-    for (uint32_t i = lane; i < c; i += 32) valid += ek[i] != kEmptyKey;
-    for (int o = 16; o; o >>= 1) valid += __shfl_xor_sync(0xffffffffu, valid, o);
+    if (p2 > p1) {
+        fold_range(p1, p2);
+        sort_exact(p2);
+    }
+    const uint32_t valid = p2;  // every folded candidate has an exact key
     if (lane == 0) atomicAdd(p.rescored, (unsigned long long)valid);
     if (valid < p.klist) {  // a proven band has >= k; a threshold guessed too low may not
         retry(p.loose ? double(p.loose[q]) : 0.0);
         return;
     }
-    const uint64_t kth = kth_exact();
+    const uint64_t kth = ek[p.klist - 1];
     // the band's k-th exact distance bounds the true k-th from above, so
     // every true neighbor has y <= proof_bound(kth) - alpha_q: the band is
     // complete when that is inside its threshold
@@ -2048,14 +2053,11 @@ __device__ __forceinline__ void band_row(const Rescore2Params& p, uint32_t slot,
         return;
     }
     const size_t orow = size_t(qo - p.row_begin);
-    for (uint32_t i = lane; i < c; i += 32) {
-        const uint64_t mk = ek[i];
-        if (mk == kEmptyKey || mk > kth) continue;
-        uint32_t rank = 0;
-        for (uint32_t j = 0; j < c; ++j) rank += ek[j] < mk;
+    for (uint32_t r = lane; r < p.klist; r += 32) {
+        const uint64_t mk = ek[r];
         const float dv = ordered_to_float(uint32_t(mk >> 32));
-        p.out_index[orow * p.klist + rank] = uint32_t(mk);
-        p.out_dist[orow * p.klist + rank] = p.out_sqrt ? __fsqrt_rn(dv) : dv;
+        p.out_index[orow * p.klist + r] = uint32_t(mk);
+        p.out_dist[orow * p.klist + r] = p.out_sqrt ? __fsqrt_rn(dv) : dv;
     }
 }
 
@@ -2063,7 +2065,7 @@ __device__ __forceinline__ void band_row(const Rescore2Params& p, uint32_t slot,
 // p.big; pass 1: the listed slots (grid-stride), room for p.cap; pass 2: one
 // warp per slot, room for p.cap (no split).
 template <int FOLD, int NW>
-__global__ void __launch_bounds__(32 * NW, 1) rescore_capture_kernel(const Rescore2Params p, uint32_t scap, int pass) {
+__global__ void __launch_bounds__(32 * NW, 16 / NW) rescore_capture_kernel(const Rescore2Params p, uint32_t scap, int pass) {
     extern __shared__ __align__(16) uint8_t band_smem[];
     const int warp = threadIdx.x >> 5;
     uint8_t* wbase = band_smem + size_t(warp) * band_smem_per_warp(scap);
@@ -2077,26 +2079,35 @@ __global__ void __launch_bounds__(32 * NW, 1) rescore_capture_kernel(const Resco
 }
 
 static size_t band_smem_bytes(uint32_t cap, int warps = kBandWarps) {
-    return warps * (size_t(cap) * 16 + size_t(cap) * 2 + 32 * 33 * 4 + 64);
+    return warps * (size_t(cap) * 16 + 32 * 33 * 4 + 64);
 }
 
 // expect: the typical band size (0: unknown).  With r2.big set, bands up to
-// ~1.5 expect run 8 warps per block in small shared-memory slices (2-3x the
-// occupancy of slices sized for the capacity); the rest get a second pass.
+// ~1.25 expect (rounded up to a power of two) run in small shared-memory
+// slices (2x the occupancy of slices sized for the capacity); the rest get a
+// second pass.  r2.cap must be a power of two.
 template <int FOLD>
 static cudaError_t launch_rescore_capture(const Rescore2Params& r2, uint32_t rows, cudaStream_t st,
                                           uint32_t expect = 0) {
     cudaError_t e;
-    uint32_t scap = (expect * 3 / 2 + 63) / 64 * 64;
-    if (r2.big && expect && scap < r2.cap / 2) {
-        scap = std::max(128u, scap);
-        auto k0 = rescore_capture_kernel<FOLD, 8>;
+    // (band slices hold a power of two: the bitonic sorts' size)
+    uint32_t scap = 128;
+    while (scap < expect + expect / 4) scap *= 2;
+    if (r2.big && expect && scap < r2.cap) {
+        // 8 or 4 warps per block, whichever keeps more warps per SM resident
+        // (227 KB of shared memory; ~128 registers a thread: 2 blocks of 8, 4 of 4)
+        const size_t per_warp = band_smem_bytes(scap, 1);
+        const uint32_t w8 = 8 * std::min<uint32_t>(2, uint32_t((227u << 10) / (8 * per_warp)));
+        const uint32_t w4 = 4 * std::min<uint32_t>(4, uint32_t((227u << 10) / (4 * per_warp)));
+        const bool eight = w8 >= w4;
+        auto k0 = eight ? rescore_capture_kernel<FOLD, 8> : rescore_capture_kernel<FOLD, 4>;
         auto k1 = rescore_capture_kernel<FOLD, kBandWarps>;
-        const size_t s0 = band_smem_bytes(scap, 8), s1 = band_smem_bytes(r2.cap);
+        const int nw0 = eight ? 8 : 4;
+        const size_t s0 = band_smem_bytes(scap, nw0), s1 = band_smem_bytes(r2.cap);
         if ((e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s0))) != cudaSuccess) return e;
         if ((e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s1))) != cudaSuccess) return e;
         if ((e = cudaMemsetAsync(r2.nbig, 0, 4, st)) != cudaSuccess) return e;
-        k0<<<(rows + 7) / 8, 256, s0, st>>>(r2, scap, 0);
+        k0<<<(rows + nw0 - 1) / nw0, 32 * nw0, s0, st>>>(r2, scap, 0);
         int sms = 148, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2219,10 +2230,10 @@ size_t tensor_workspace_bytes(uint32_t n, uint32_t d, uint32_t row_begin, uint32
 
 // CTA-pair sweep (cluster of 2): one pair per two SMs, persistent.  ARES =
 // false streams the query rows with every reference chunk (d > 256).
-template <int KPL, int BN, int EW, bool TRI = false, bool TCAP = false, bool ARES = true>
+template <int KPL, int BN, int EW, bool TRI = false, bool TCAP = false, bool ARES = true, bool DYN = false>
 static cudaError_t launch_sweep_pair(const SweepParams& sp, uint32_t nrows, cudaStream_t stream) {
     using L = TSLayout<KPL, BN, ARES, EW, true>;
-    auto kern = tensor_sweep_kernel<KPL, BN, ARES, EW, false, true, TRI, TCAP>;
+    auto kern = tensor_sweep_kernel<KPL, BN, ARES, EW, false, true, TRI, TCAP, DYN>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::SMEM));
     if (e != cudaSuccess) return e;
     const uint32_t npairs = (nrows + 2 * TS_BM - 1) / (2 * TS_BM);

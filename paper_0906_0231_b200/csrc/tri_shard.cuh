@@ -47,10 +47,17 @@ static inline uint32_t tri_lane_of_unit(uint32_t u, uint32_t world) {
     return r < world ? r : 2 * world - 1 - r;
 }
 
-// The sweep's dynamic unit queue (default; KNN_B200_TRI_DYN=0: the static walk).
-static bool tri_dyn_enabled() {
-    const char* e = getenv("KNN_B200_TRI_DYN");
-    return !(e && atoi(e) == 0);
+// Whether the triangle sweep takes its units from the dynamic queue
+// (KNN_B200_TRI_DYN=0: never; =1: always).  Default, for resident query rows
+// (d <= 256): the threshold triangle always (C4: -14%), the list triangle
+// when sharded -- with ~6 units per CTA pair at 8 ranks the static walk left
+// pairs idle (C2 w8: 43 -> 39 ms) -- but not on one GPU, where its 53 units
+// per pair balance and the static walk's kernel measured faster.  Streamed
+// query rows (d > 256, C3) keep the static walk: its CTA pairs sweep each
+// column group in step, which the queue's staggered items lose (C3: +4%).
+static bool tri_use_dyn(bool tcap, uint32_t G, uint32_t kc) {
+    if (const char* e = getenv("KNN_B200_TRI_DYN")) return atoi(e) != 0;
+    return kc <= uint32_t(TS_MAX_RES_KC) && (tcap || G > 1);
 }
 
 // Per-rank unit lists.  Units go to ranks in boustrophedon order.  With the
@@ -59,10 +66,10 @@ static bool tri_dyn_enabled() {
 // are a prefix.  Without it they are dealt to the launch's CTA pairs in snake
 // order, so pair p's strided walk (p, p + P, ...) takes alternately heavier
 // and lighter units.
-static std::vector<std::vector<uint32_t>> tri_unit_lists(uint32_t U, uint32_t G, uint32_t pairs_max) {
+static std::vector<std::vector<uint32_t>> tri_unit_lists(uint32_t U, uint32_t G, uint32_t pairs_max, bool dyn) {
     std::vector<std::vector<uint32_t>> asc(G), out(G);
     for (uint32_t u = 0; u < U; ++u) asc[tri_lane_of_unit(u, G)].push_back(u);
-    if (tri_dyn_enabled()) return asc;
+    if (dyn) return asc;
     for (uint32_t r = 0; r < G; ++r) {
         const std::vector<uint32_t>& a = asc[r];
         const uint32_t m = uint32_t(a.size());
@@ -80,7 +87,7 @@ static std::vector<std::vector<uint32_t>> tri_unit_lists(uint32_t U, uint32_t G,
 
 // Host-side plan, flattened (the C ABI's knn_b200_tri_unit_plan).
 void tri_unit_plan(uint32_t U, uint32_t G, uint32_t pairs_max, uint32_t* units, uint32_t* counts) {
-    const auto lists = tri_unit_lists(U, G, pairs_max);
+    const auto lists = tri_unit_lists(U, G, pairs_max, tri_use_dyn(false, G, 1));  // the list triangle's plan
     uint32_t at = 0;
     for (uint32_t r = 0; r < G; ++r) {
         counts[r] = uint32_t(lists[r].size());
@@ -266,6 +273,7 @@ struct TriShared {
     uint32_t n = 0, npad = 0, d = 0, kc = 0, U = 0, G = 1, S = 0;  // S: rows per all-gather slice
     bool tcap = false;    // the threshold triangle (k > 10, any d, cosine too): fp16 sample, 2 x 16 lists
     bool cosine = false;  // no norm order (every norm is 1): identity permutation
+    bool dyn = false;     // the sweep takes units from the dynamic queue (tri_use_dyn)
     uint32_t stride = kTriStride, skpl = kTriSampleKpl, trank = kTriRank, sm = 0, spad = 0, skc = 0;
     bool f8 = true;
     float dscale = 1.0f;
@@ -434,7 +442,8 @@ static cudaError_t tri_prep(TriShared& S, const TensorPathArgs& a, uint32_t G, S
     S.layout(c);
     S.maxabs = reinterpret_cast<unsigned int*>(S.scal);
     S.gmax = reinterpret_cast<unsigned long long*>(S.scal + 8);
-    S.units_h = tri_unit_lists(S.U, G, uint32_t(a.sm_count / 2));
+    S.dyn = tri_use_dyn(tcap, G, S.kc);
+    S.units_h = tri_unit_lists(S.U, G, uint32_t(a.sm_count / 2), S.dyn);
     std::vector<uint32_t> owner(S.U), lidx(S.U);
     for (uint32_t r = 0; r < G; ++r)
         for (uint32_t i = 0; i < S.units_h[r].size(); ++i) {
@@ -559,6 +568,14 @@ static cudaError_t tri_order(TriShared& S, const TensorPathArgs& a) {
     return cudaGetLastError();
 }
 
+// The threshold triangle with 16 epilogue warps (4 per TMEM lane quadrant,
+// 64 columns each per tile) instead of 8: twice the warps to hide the
+// filter's latency; it keeps no lists, so 112 registers suffice.
+static bool tcap_ew16() {
+    const char* e = getenv("KNN_B200_TCAP_EW");
+    return e && atoi(e) == 16;
+}
+
 // Phase B: the triangle sweep of this rank's units; column-side entries
 // counted by owner (R.scnt_h, host) -- the caller then sizes the send
 // buffers and calls tri_bin.
@@ -583,7 +600,7 @@ static cudaError_t tri_sweep(TriShared& S, TriRank& R, const TensorPathArgs& a, 
     // the dynamic queue's claim counters (one per column group) and per-unit
     // list-state counters
     const uint32_t ngroups = ((S.n + 255) / 256 + S.group_tiles - 1) / S.group_tiles;
-    const bool dyn = tri_dyn_enabled();
+    const bool dyn = S.dyn;
     uint32_t* qctr = nullptr;
     auto lay = [&](Carve& c) {
         R.lkey = c.take<uint64_t>(size_t(R.nchunks) * kLogChunk);
@@ -622,9 +639,15 @@ static cudaError_t tri_sweep(TriShared& S, TriRank& R, const TensorPathArgs& a, 
         cudaMallocAsync(reinterpret_cast<void**>(&cta_ns), 2 * 8 * 2 * pairs, st);
         tp.cta_ns = cta_ns;
     }
-    e = !S.tcap                        ? launch_sweep_pair<12, 256, 8, true>(tp, R.nslots, st)
-        : S.kc <= uint32_t(TS_MAX_RES_KC) ? launch_sweep_pair<2, 256, 8, true, true, true>(tp, R.nslots, st)
-                                           : launch_sweep_pair<2, 256, 8, true, true, false>(tp, R.nslots, st);
+    const bool ares = S.kc <= uint32_t(TS_MAX_RES_KC);
+    if (!S.tcap) e = dyn ? launch_sweep_pair<12, 256, 8, true, false, true, true>(tp, R.nslots, st)
+                         : launch_sweep_pair<12, 256, 8, true, false, true, false>(tp, R.nslots, st);
+    else if (ares && tcap_ew16()) e = dyn ? launch_sweep_pair<2, 256, 16, true, true, true, true>(tp, R.nslots, st)
+                                          : launch_sweep_pair<2, 256, 16, true, true, true, false>(tp, R.nslots, st);
+    else if (ares) e = dyn ? launch_sweep_pair<2, 256, 8, true, true, true, true>(tp, R.nslots, st)
+                           : launch_sweep_pair<2, 256, 8, true, true, true, false>(tp, R.nslots, st);
+    else e = dyn ? launch_sweep_pair<2, 256, 8, true, true, false, true>(tp, R.nslots, st)
+                 : launch_sweep_pair<2, 256, 8, true, true, false, false>(tp, R.nslots, st);
     if (e != cudaSuccess) return e;
     if (cta_ns) {
         std::vector<unsigned long long> t(4 * pairs);
