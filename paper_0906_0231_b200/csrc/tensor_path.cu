@@ -321,7 +321,23 @@ tensor_sweep_kernel(const SweepParams p) {
     // units unit0, unit0 + unit_step, ... that have tiles in the group.
     auto next = [&](ItemWalk& w, int role, bool warp_wide) -> bool {
         if constexpr (DYN) {
-            return item_next(w, role, warp_wide);
+            if (role == 0) return item_next(w, 0, false);  // the claimer: out of line
+            // consumers, inline: a call here costs the epilogue's hot loop
+            // registers (C2: +8% instructions from rematerialised addresses)
+            const int s = w.qi % kQN;
+            const uint32_t ph = (w.qi / kQN) & 1;
+            ++w.qi;
+            if (role == 2) ptx::mbar_wait_cluster(qfull_bar(s), ph);
+            else ptx::mbar_wait(qfull_bar(s), ph);
+            const uint64_t item = qitem[s];
+            if (warp_wide) __syncwarp();
+            if (!warp_wide || lane == 0) {
+                if (role == 2) ptx::mbar_arrive_remote(ptx::mapa_shared(qempty_bar(s), 0));
+                else ptx::mbar_arrive(qempty_bar(s));
+            }
+            w.g = uint32_t(item >> 32);
+            w.lu = uint32_t(item);
+            return item != kQEnd;
         } else {
             for (;;) {
                 if (!w.started) {
@@ -1039,24 +1055,6 @@ tensor_sweep_kernel(const SweepParams p) {
 // ---------------------------------------------------------------------------
 // prep kernels
 
-// Sort key for the norm-sorted order: ||x - mu||^2 (any order is correct; this
-// one makes every 32-column chunk's norms nearly equal, so the sweep's
-// hot-path bound, which uses the chunk's smallest norm, is nearly exact).
-__global__ void row_key_kernel(const float* __restrict__ X, uint32_t n, uint32_t d, const float* __restrict__ mu,
-                               float* __restrict__ key, uint32_t* __restrict__ idx) {
-    const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (row >= n) return;
-    float s = 0.0f;
-    for (uint32_t k = lane; k < d; k += 32) {
-        const float v = X[size_t(row) * d + k] - mu[k];
-        s += v * v;
-    }
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) {
-        key[row] = s;
-        idx[row] = row;
-    }
-}
 
 // ---- triangle mode helpers --------------------------------------------------
 
@@ -1271,13 +1269,25 @@ __device__ __forceinline__ void atomic_max_pos_double(unsigned long long* addr, 
 // Column sums in double -> mu (any mu is correct: distances are translation
 // invariant; mu only shrinks the magnitudes the fp16 filter sees).
 __global__ void colsum_kernel(const float* __restrict__ X, uint32_t n, uint32_t d, double* __restrict__ acc) {
+    // a block's row range, one thread per column; 8 independent partial sums
+    // keep 8 loads in flight per thread (the loop was latency-bound at 1/4
+    // of HBM bandwidth)
     const uint32_t rows_per = (n + gridDim.x - 1) / gridDim.x;
     const uint32_t ra = blockIdx.x * rows_per;
     const uint32_t rb = min(n, ra + rows_per);
     for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) {
-        double s = 0;
-        for (uint32_t r = ra; r < rb; ++r) s += X[size_t(r) * d + j];
-        atomicAdd(acc + j, s);
+        double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint32_t r = ra;
+        for (; r + 8 <= rb; r += 8) {
+            float v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = __ldg(X + size_t(r + q) * d + j);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s[q] += v[q];
+        }
+        for (; r < rb; ++r) s[0] += __ldg(X + size_t(r) * d + j);
+        const double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+        if (ra < rb) atomicAdd(acc + j, t);
     }
 }
 
@@ -1286,14 +1296,42 @@ __global__ void mu_finalize_kernel(const double* __restrict__ acc, uint32_t n, u
         mu[j] = float(acc[j] / double(n));
 }
 
-__global__ void maxabs_kernel(const float* __restrict__ X, uint64_t count, uint32_t d, const float* __restrict__ mu,
-                              unsigned int* __restrict__ out) {
+
+// One pass over X (one warp per row): the largest |x - mu| (one atomic per
+// block; it sets the fp16 scale) and, with key != null, each row's
+// ||x - mu||^2 -- the norm order's sort key (any order is correct; this one
+// makes every 32-column chunk's norms nearly equal, so the sweep's hot-path
+// bound, which uses the chunk's smallest norm, is nearly exact).
+__global__ void __launch_bounds__(256) center_stats_kernel(const float* __restrict__ X, uint32_t n, uint32_t d,
+                                                           const float* __restrict__ mu, unsigned int* __restrict__ out,
+                                                           float* __restrict__ key, uint32_t* __restrict__ idx) {
+    __shared__ float wmax[8];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     float m = 0.0f;
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride)
-        m = fmaxf(m, fabsf(__fsub_rn(X[i], mu[i % d])));
+    for (uint32_t row = blockIdx.x * 8 + w; row < n; row += gridDim.x * 8) {
+        const float* xr = X + size_t(row) * d;
+        float sq = 0.0f;
+        for (uint32_t k = lane; k < d; k += 32) {
+            const float v = __fsub_rn(__ldg(xr + k), __ldg(mu + k));
+            m = fmaxf(m, fabsf(v));
+            sq = __fadd_rn(sq, __fmul_rn(v, v));
+        }
+        if (key) {
+            for (int o = 16; o; o >>= 1) sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
+            if (lane == 0) {
+                key[row] = sq;
+                idx[row] = row;
+            }
+        }
+    }
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+    if (lane == 0) wmax[w] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float b = 0.0f;
+        for (int i = 0; i < 8; ++i) b = fmaxf(b, wmax[i]);
+        atomicMax(out, __float_as_uint(b));
+    }
 }
 
 // Power-of-two scale with |s x| <= 65504 (fp16 max), capped at 2^40.
@@ -2500,9 +2538,8 @@ static cudaError_t run_tensor_path_impl(const TensorPathArgs& a, TensorPathResul
     } else {
         if ((e = cudaMemsetAsync(mu, 0, size_t(d) * 4, st)) != cudaSuccess) return e;
     }
-    maxabs_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, uint64_t(n) * d, d, mu, maxabs);
+    center_stats_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, n, d, mu, maxabs, sorted ? skey : nullptr, sidx);
     if (sorted) {
-        row_key_kernel<<<(n * 32 + 255) / 256, 256, 0, st>>>(a.X, n, d, mu, skey, sidx);
         if ((e = cub::DeviceRadixSort::SortPairs(stemp, stemp_bytes, skey, skey2, sidx, perm, int(n), 0, 32, st)) !=
             cudaSuccess)
             return e;

@@ -49,15 +49,18 @@ static inline uint32_t tri_lane_of_unit(uint32_t u, uint32_t world) {
 
 // Whether the triangle sweep takes its units from the dynamic queue
 // (KNN_B200_TRI_DYN=0: never; =1: always).  Default, for resident query rows
-// (d <= 256): the threshold triangle always (C4: -14%), the list triangle
-// when sharded -- with ~6 units per CTA pair at 8 ranks the static walk left
-// pairs idle (C2 w8: 43 -> 39 ms) -- but not on one GPU, where its 53 units
-// per pair balance and the static walk's kernel measured faster.  Streamed
-// query rows (d > 256, C3) keep the static walk: its CTA pairs sweep each
-// column group in step, which the queue's staggered items lose (C3: +4%).
-static bool tri_use_dyn(bool tcap, uint32_t G, uint32_t kc) {
+// (d <= 256): the threshold triangle always (C4: -14%); the list triangle
+// only when a rank has fewer than 16 units per CTA pair -- C2 at 8 ranks has
+// 6.6, and the static walk left pairs idle (43 -> 39 ms with the queue) --
+// since with many units per pair the static walk balances (C2 on one GPU:
+// 53 per pair, within 2%) and its CTA pairs sweep each column group in step:
+// the same sweep with the queue's staggered items measured 8% slower per
+// tile.  Streamed query rows (d > 256, C3) keep the static walk for the same
+// reason (C3: +4% with the queue).
+static bool tri_use_dyn(bool tcap, uint32_t G, uint32_t kc, uint32_t U, uint32_t pairs) {
     if (const char* e = getenv("KNN_B200_TRI_DYN")) return atoi(e) != 0;
-    return kc <= uint32_t(TS_MAX_RES_KC) && (tcap || G > 1);
+    if (kc > uint32_t(TS_MAX_RES_KC)) return false;
+    return tcap || (G > 1 && U < 16ull * G * std::max<uint32_t>(1, pairs));
 }
 
 // Per-rank unit lists.  Units go to ranks in boustrophedon order.  With the
@@ -87,7 +90,7 @@ static std::vector<std::vector<uint32_t>> tri_unit_lists(uint32_t U, uint32_t G,
 
 // Host-side plan, flattened (the C ABI's knn_b200_tri_unit_plan).
 void tri_unit_plan(uint32_t U, uint32_t G, uint32_t pairs_max, uint32_t* units, uint32_t* counts) {
-    const auto lists = tri_unit_lists(U, G, pairs_max, tri_use_dyn(false, G, 1));  // the list triangle's plan
+    const auto lists = tri_unit_lists(U, G, pairs_max, tri_use_dyn(false, G, 1, U, pairs_max));  // the list triangle's
     uint32_t at = 0;
     for (uint32_t r = 0; r < G; ++r) {
         counts[r] = uint32_t(lists[r].size());
@@ -442,7 +445,7 @@ static cudaError_t tri_prep(TriShared& S, const TensorPathArgs& a, uint32_t G, S
     S.layout(c);
     S.maxabs = reinterpret_cast<unsigned int*>(S.scal);
     S.gmax = reinterpret_cast<unsigned long long*>(S.scal + 8);
-    S.dyn = tri_use_dyn(tcap, G, S.kc);
+    S.dyn = tri_use_dyn(tcap, G, S.kc, S.U, uint32_t(a.sm_count / 2));
     S.units_h = tri_unit_lists(S.U, G, uint32_t(a.sm_count / 2), S.dyn);
     std::vector<uint32_t> owner(S.U), lidx(S.U);
     for (uint32_t r = 0; r < G; ++r)
@@ -460,12 +463,11 @@ static cudaError_t tri_prep(TriShared& S, const TensorPathArgs& a, uint32_t G, S
         if ((e = cudaMemsetAsync(S.mu, 0, size_t(d) * 4, st)) != cudaSuccess) return e;
         iota_stride_kernel<<<a.sm_count, 256, 0, st>>>(S.perm, n, 1);
         iota_stride_kernel<<<a.sm_count, 256, 0, st>>>(S.rowpos, n, 1);
-        maxabs_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, uint64_t(n) * d, d, S.mu, S.maxabs);
+        center_stats_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, n, d, S.mu, S.maxabs, nullptr, nullptr);
     } else {
         colsum_kernel<<<a.sm_count * 4, 256, 0, st>>>(a.X, n, d, S.muacc);
         mu_finalize_kernel<<<(d + 255) / 256, 256, 0, st>>>(S.muacc, n, d, S.mu);
-        maxabs_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, uint64_t(n) * d, d, S.mu, S.maxabs);
-        row_key_kernel<<<(n * 32 + 255) / 256, 256, 0, st>>>(a.X, n, d, S.mu, S.skey, S.sidx);
+        center_stats_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, n, d, S.mu, S.maxabs, S.skey, S.sidx);
         if ((e = cub::DeviceRadixSort::SortPairs(S.stemp, S.stemp_bytes, S.skey, S.skey2, S.sidx, S.perm, int(n), 0,
                                                  32, st)) != cudaSuccess)
             return e;

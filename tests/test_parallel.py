@@ -78,26 +78,37 @@ def test_gloo_shards_assemble_the_full_answer(tmp_path, world):
         assert np.array_equal(gd.view(np.uint32), rd.view(np.uint32))
 
 
-def test_tri_unit_plan_is_boustrophedon_and_heaviest_first():
+def test_tri_unit_plan_is_boustrophedon_and_balanced():
     """The product's host planner (knn_b200_tri_unit_plan): unit u belongs to
-    lane_of_row(u) (schedule.cpp:40-44), every unit exactly once, the per-rank
-    work (sum of U - u) balanced like the reference's lanes
-    (test_schedule.cpp:169-185), and each rank's units ascending -- heaviest
-    first for the sweep's dynamic queue, and a column group's units with work
-    a prefix of the list."""
+    lane_of_row(u) (schedule.cpp:40-44), every unit exactly once, and the
+    per-rank work (sum of U - u) balanced like the reference's lanes
+    (test_schedule.cpp:169-185).  With fewer than 16 units per CTA pair and
+    rank the sweep takes units from its dynamic queue: each rank's list is
+    ascending (heaviest first; a column group's units with work are a
+    prefix).  Otherwise the static walk's snake keeps each CTA pair's share
+    within 2% of the mean."""
     from paper_0906_0231_b200.parallel import tri_unit_plan
-    for units, world, pairs in ((3907, 8, 74), (1563, 2, 74), (38, 3, 2), (5, 8, 74), (62500, 8, 74)):
+    for units, world, pairs in ((3907, 8, 74), (1563, 2, 74), (38, 3, 2), (5, 8, 74), (62500, 8, 74), (3907, 1, 74),
+                                (3907, 2, 74)):
         plan = tri_unit_plan(units, world, pairs)
         flat = sorted(u for r in plan for u in r)
         assert flat == list(range(units))
+        queue = world > 1 and units < 16 * world * pairs
         for r, lst in enumerate(plan):
-            assert lst == sorted(lst)
+            if queue:
+                assert lst == sorted(lst)
             for u in lst:
                 m = u % (2 * world)
                 assert (m if m < world else 2 * world - 1 - m) == r
         if units >= 2 * world * 8:
             work = [sum(units - u for u in lst) for lst in plan]
             assert max(work) / min(work) < 1.01
+        if not queue:
+            for lst in plan:
+                p = min(len(lst), pairs)
+                per = [sum(units - u for u in lst[i::p]) for i in range(p)]
+                if len(lst) >= 4 * p:
+                    assert max(per) / (sum(per) / p) < 1.02
 
 
 def test_tri_unit_plan_static_walk_is_snake(monkeypatch):
