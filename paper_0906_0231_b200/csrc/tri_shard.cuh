@@ -49,48 +49,87 @@ static inline uint32_t tri_lane_of_unit(uint32_t u, uint32_t world) {
 
 // Whether the triangle sweep takes its units from the dynamic queue
 // (KNN_B200_TRI_DYN=0: never; =1: always).  Default, for resident query rows
-// (d <= 256): the threshold triangle always (C4: -14%); the list triangle
-// only when a rank has fewer than 16 units per CTA pair -- C2 at 8 ranks has
-// 6.6, and the static walk left pairs idle (43 -> 39 ms with the queue) --
-// since with many units per pair the static walk balances (C2 on one GPU:
-// 53 per pair, within 2%) and its CTA pairs sweep each column group in step:
-// the same sweep with the queue's staggered items measured 8% slower per
-// tile.  Streamed query rows (d > 256, C3) keep the static walk for the same
-// reason (C3: +4% with the queue).
-static bool tri_use_dyn(bool tcap, uint32_t G, uint32_t kc, uint32_t U, uint32_t pairs) {
+// (d <= 256): the threshold triangle (C4: -14%), whose items carry no list
+// state between column groups.  The list triangle keeps the static walk at
+// any world size: its CTA pairs sweep each column group in step, so the
+// group's tiles stay L2-resident.  Measured at C2, 8 emulated ranks (6.6
+// units per pair): (unit, group) items from the queue made pairs wait on
+// another pair's list state and lost that residency (sweep +3%); whole-unit
+// claims for the lightest 20% of the tiles after a static head, +8%
+// (profiles/r02at_*).  Streamed query rows (d > 256, C3) keep it for the
+// same reason (C3: +4% with the queue).
+static bool tri_use_dyn(bool tcap, uint32_t kc) {
     if (const char* e = getenv("KNN_B200_TRI_DYN")) return atoi(e) != 0;
-    if (kc > uint32_t(TS_MAX_RES_KC)) return false;
-    return tcap || (G > 1 && U < 16ull * G * std::max<uint32_t>(1, pairs));
+    return tcap && kc <= uint32_t(TS_MAX_RES_KC);
+}
+
+// Estimated sweep cost of unit u (relative units): its U - u tiles, weighted
+// up for the lowest-norm units -- rows near the centroid lie inside many
+// columns' thresholds ("hubs") and append column-side candidates on most of
+// their tiles.  The shape was fitted to the per-pair sweep times of C2 at 8
+// emulated ranks under the plain tile-count deal
+// (profiles/r02aq_cta_static.txt: decay over ~0.4% of the rows); the weight
+// was then measured: 0 / 0.45 / 0.9 -> C2 at 8 ranks 37.4 / 35.5 / 35.0 ms,
+// at 4 ranks 68.1 / 66.2 / 65.8 ms (profiles/r02au_*).  Only the deal
+// depends on it, never the results.
+static double tri_unit_cost(uint32_t u, uint32_t U) {
+    static const double hub = [] {  // tuning: KNN_B200_TRI_HUB = the weight in percent (0: tiles only)
+        const char* e = getenv("KNN_B200_TRI_HUB");
+        return e ? std::max(0, atoi(e)) / 100.0 : 0.9;
+    }();
+    const double tau = std::max(1.0, 0.004 * U);
+    return double(U - u) * (1.0 + hub * std::exp(-double(u) / tau));
+}
+
+// The static walk's deal of a rank's units a (ascending u: cost descending)
+// to P CTA pairs: pair p walks positions p, p + P, ...  Round r hands the P
+// next-heaviest units to the pairs in ascending order of their cost so far
+// (LPT per round, equal unit counts: the snake deal when cost = tiles); the
+// pairs that take a unit in a partial last round are then labelled 0, 1, ...
+static void lpt_deal(const std::vector<uint32_t>& a, uint32_t U, uint32_t pairs_max, uint32_t* out) {
+    const uint32_t m = uint32_t(a.size());
+    const uint32_t P = std::max<uint32_t>(1, std::min(m, pairs_max));
+    const uint32_t rounds = (m + P - 1) / P;
+    std::vector<double> load(P, 0.0);
+    std::vector<std::vector<uint32_t>> got(P);
+    std::vector<uint32_t> order(P);
+    for (uint32_t r = 0; r < rounds; ++r) {
+        for (uint32_t q = 0; q < P; ++q) order[q] = q;
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return load[x] < load[y]; });
+        const uint32_t i0 = r * P, cnt = std::min(P, m - i0);
+        for (uint32_t q = 0; q < cnt; ++q) {
+            got[order[q]].push_back(a[i0 + q]);
+            load[order[q]] += tri_unit_cost(a[i0 + q], U);
+        }
+    }
+    std::vector<uint32_t> label;
+    for (uint32_t q = 0; q < P; ++q)
+        if (got[q].size() == rounds) label.push_back(q);
+    for (uint32_t q = 0; q < P; ++q)
+        if (got[q].size() != rounds) label.push_back(q);
+    for (uint32_t l = 0; l < P; ++l)
+        for (uint32_t k = 0; k < got[label[l]].size(); ++k) out[k * P + l] = got[label[l]][k];
 }
 
 // Per-rank unit lists.  Units go to ranks in boustrophedon order.  With the
 // dynamic queue a rank's units stay ascending (work U - u descending): CTA
 // pairs claim them heaviest first, and the units of a column group with work
-// are a prefix.  Without it they are dealt to the launch's CTA pairs in snake
-// order, so pair p's strided walk (p, p + P, ...) takes alternately heavier
-// and lighter units.
+// are a prefix.  Without it they are dealt to the launch's CTA pairs by
+// lpt_deal.
 static std::vector<std::vector<uint32_t>> tri_unit_lists(uint32_t U, uint32_t G, uint32_t pairs_max, bool dyn) {
     std::vector<std::vector<uint32_t>> asc(G), out(G);
     for (uint32_t u = 0; u < U; ++u) asc[tri_lane_of_unit(u, G)].push_back(u);
     if (dyn) return asc;
     for (uint32_t r = 0; r < G; ++r) {
-        const std::vector<uint32_t>& a = asc[r];
-        const uint32_t m = uint32_t(a.size());
-        const uint32_t P = std::max<uint32_t>(1, std::min(m, pairs_max));
-        out[r].resize(m);
-        for (uint32_t i = 0; i < m; ++i) {
-            const uint32_t round = i / P, pos = i % P;
-            const bool full = (round + 1) * P <= m;
-            const uint32_t src = (round & 1) && full ? round * P + (P - 1 - pos) : i;
-            out[r][i] = a[src];
-        }
+        out[r].resize(asc[r].size());
+        lpt_deal(asc[r], U, pairs_max, out[r].data());
     }
     return out;
 }
 
 // Host-side plan, flattened (the C ABI's knn_b200_tri_unit_plan).
 void tri_unit_plan(uint32_t U, uint32_t G, uint32_t pairs_max, uint32_t* units, uint32_t* counts) {
-    const auto lists = tri_unit_lists(U, G, pairs_max, tri_use_dyn(false, G, 1, U, pairs_max));  // the list triangle's
+    const auto lists = tri_unit_lists(U, G, pairs_max, tri_use_dyn(false, 1));  // the list triangle's
     uint32_t at = 0;
     for (uint32_t r = 0; r < G; ++r) {
         counts[r] = uint32_t(lists[r].size());
@@ -434,7 +473,9 @@ static cudaError_t tri_prep(TriShared& S, const TensorPathArgs& a, uint32_t G, S
                                     static_cast<unsigned long long*>(nullptr), static_cast<const uint32_t*>(nullptr),
                                     static_cast<uint32_t*>(nullptr), int(n));
     const uint64_t tile_bytes = uint64_t(256) * S.kc * 128;
-    S.group_tiles = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>((40ull << 20) / tile_bytes, S.U)));
+    uint64_t group_bytes = 40ull << 20;  // a column group's fp16 tiles, sized to stay L2-resident
+    if (const char* ge = getenv("KNN_B200_TRI_GROUP_MB")) group_bytes = uint64_t(std::max(1, atoi(ge))) << 20;
+    S.group_tiles = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(group_bytes / tile_bytes, S.U)));
     S.gts = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>((40ull << 20) / (uint64_t(256) * S.skc * 128),
                                                                 S.spad / 256)));
     Carve c;
@@ -445,7 +486,7 @@ static cudaError_t tri_prep(TriShared& S, const TensorPathArgs& a, uint32_t G, S
     S.layout(c);
     S.maxabs = reinterpret_cast<unsigned int*>(S.scal);
     S.gmax = reinterpret_cast<unsigned long long*>(S.scal + 8);
-    S.dyn = tri_use_dyn(tcap, G, S.kc, S.U, uint32_t(a.sm_count / 2));
+    S.dyn = tri_use_dyn(tcap, S.kc);
     S.units_h = tri_unit_lists(S.U, G, uint32_t(a.sm_count / 2), S.dyn);
     std::vector<uint32_t> owner(S.U), lidx(S.U);
     for (uint32_t r = 0; r < G; ++r)
@@ -463,11 +504,12 @@ static cudaError_t tri_prep(TriShared& S, const TensorPathArgs& a, uint32_t G, S
         if ((e = cudaMemsetAsync(S.mu, 0, size_t(d) * 4, st)) != cudaSuccess) return e;
         iota_stride_kernel<<<a.sm_count, 256, 0, st>>>(S.perm, n, 1);
         iota_stride_kernel<<<a.sm_count, 256, 0, st>>>(S.rowpos, n, 1);
-        center_stats_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, n, d, S.mu, S.maxabs, nullptr, nullptr);
+        center_stats_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, n, d, S.mu, S.maxabs, nullptr, nullptr,
+                                                            vec4_rows(a.X, d));
     } else {
-        colsum_kernel<<<a.sm_count * 4, 256, 0, st>>>(a.X, n, d, S.muacc);
-        mu_finalize_kernel<<<(d + 255) / 256, 256, 0, st>>>(S.muacc, n, d, S.mu);
-        center_stats_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, n, d, S.mu, S.maxabs, S.skey, S.sidx);
+        launch_colmean(a.X, n, d, S.muacc, S.mu, a.sm_count, st);
+        center_stats_kernel<<<a.sm_count * 8, 256, 0, st>>>(a.X, n, d, S.mu, S.maxabs, S.skey, S.sidx,
+                                                            vec4_rows(a.X, d));
         if ((e = cub::DeviceRadixSort::SortPairs(S.stemp, S.stemp_bytes, S.skey, S.skey2, S.sidx, S.perm, int(n), 0,
                                                  32, st)) != cudaSuccess)
             return e;
