@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+TAG=r02ax
+timeout 600 python bench.py --impl reference > gpurun_out/${TAG}_bench_reference_c2.jsonl 2> gpurun_out/${TAG}_ref.err; echo ref rc=$?
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 500 --csv --log-file gpurun_out/${TAG}_launches_c2.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/${TAG}_ncu_l.log 2>&1; echo ncu launches rc=$?
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:tensor_sweep_kernel --launch-skip 1 -c 1 -o gpurun_out/${TAG}_tri_c2 python tools/profile_solve.py --n 1000000 --reps 1 > gpurun_out/${TAG}_ncu_full.log 2>&1; echo ncu full rc=$?
