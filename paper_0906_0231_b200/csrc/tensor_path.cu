@@ -28,6 +28,7 @@
 // Result: bit-identical to brute_force_knn.
 #include <cub/device/device_radix_sort.cuh>
 #include <algorithm>
+#include <type_traits>
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
 #include <cuda_runtime.h>
@@ -491,58 +492,68 @@ tensor_sweep_kernel(const SweepParams p) {
         // ---------------- MMA issuer (one lane; PAIR: the leader's) ----------------
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_f16_f32(PAIR ? 2 * TS_BM : TS_BM, BN);
-            auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
-                if constexpr (PAIR) {
-                    if (p.e4m3) ptx::mma_e4m3_ss_pair(d, a, b, idesc, acc);
-                    else ptx::mma_f16_ss_pair(d, a, b, idesc, acc);
-                } else {
-                    ptx::mma_f16_ss(d, a, b, idesc, acc);
-                }
-            };
-            auto commit = [&](uint32_t bar) {
-                if constexpr (PAIR) ptx::mma_commit_pair(bar);
-                else ptx::mma_commit(bar);
-            };
-            int stage = 0;
-            uint32_t phase = 0, a_phase = 0, tcount = 0;
-            ItemWalk cur = make_walk();
-            while (next(cur, 1, false)) {
-                const uint32_t g = cur.g, lu = cur.lu;
-                const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
-                {
-                    const uint32_t ts = max(t0, tri_start(unit_id(lu)));
-                    if constexpr (ARES) {
-                        wait(afull_bar, a_phase);
-                        a_phase ^= 1;
+            // The operand kind is a template argument of the issue loop, not a
+            // runtime select per MMA: a select compiles to a predicated
+            // UTCQMMA + UTCHMMA pair per MMA, and the predicated-off one still
+            // occupies the tcgen05 pipe (C2 sweep: tensor pipe 64% busy with
+            // the tcgen05 pipe at 88%; cuBLAS: 96% / 96%, profiles/r02ba_*).
+            auto issue = [&](auto f8) {
+                [[maybe_unused]] constexpr bool F8 = decltype(f8)::value;
+                auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+                    if constexpr (PAIR) {
+                        if constexpr (F8) ptx::mma_e4m3_ss_pair(d, a, b, idesc, acc);
+                        else ptx::mma_f16_ss_pair(d, a, b, idesc, acc);
+                    } else {
+                        ptx::mma_f16_ss(d, a, b, idesc, acc);
                     }
-                    for (uint32_t t = ts; t < t1; ++t, ++tcount) {
-                        const uint32_t b = tcount & 1, use = tcount >> 1;
-                        wait(tempty_bar(b), (use & 1) ^ 1);
-                        ptx::tc_fence_after();
-                        const uint32_t d_tmem = tmem + b * BN;
-                        for (uint32_t kc = 0; kc < p.kc; ++kc) {
-                            wait(full_bar(stage), phase);
-                            ptx::tc_fence_after();
-                            const uint8_t* bsm = stage_smem + stage * L::STAGE;
-                            const uint8_t* asm_ = ARES ? a_smem + kc * TS_A_CHUNK : bsm + L::B_CHUNK;
-                            const uint32_t a_addr = ptx::smem_u32(asm_);
-                            const uint32_t b_addr = ptx::smem_u32(bsm);
-#pragma unroll
-                            for (uint32_t k = 0; k < 4; ++k) {  // UMMA_K = 16 fp16 = 32 B inside the swizzle atom
-                                mma(d_tmem, ptx::sw128_kmajor_desc(a_addr + 32 * k),
-                                    ptx::sw128_kmajor_desc(b_addr + 32 * k), (kc | k) != 0);
-                            }
-                            commit(empty_bar(stage));
-                            if (++stage == S) {
-                                stage = 0;
-                                phase ^= 1;
-                            }
+                };
+                auto commit = [&](uint32_t bar) {
+                    if constexpr (PAIR) ptx::mma_commit_pair(bar);
+                    else ptx::mma_commit(bar);
+                };
+                int stage = 0;
+                uint32_t phase = 0, a_phase = 0, tcount = 0;
+                ItemWalk cur = make_walk();
+                while (next(cur, 1, false)) {
+                    const uint32_t g = cur.g, lu = cur.lu;
+                    const uint32_t t0 = g * p.group_tiles, t1 = min(ntiles, t0 + p.group_tiles);
+                    {
+                        const uint32_t ts = max(t0, tri_start(unit_id(lu)));
+                        if constexpr (ARES) {
+                            wait(afull_bar, a_phase);
+                            a_phase ^= 1;
                         }
-                        commit(tfull_bar(b));
+                        for (uint32_t t = ts; t < t1; ++t, ++tcount) {
+                            const uint32_t b = tcount & 1, use = tcount >> 1;
+                            wait(tempty_bar(b), (use & 1) ^ 1);
+                            ptx::tc_fence_after();
+                            const uint32_t d_tmem = tmem + b * BN;
+                            for (uint32_t kc = 0; kc < p.kc; ++kc) {
+                                wait(full_bar(stage), phase);
+                                ptx::tc_fence_after();
+                                const uint8_t* bsm = stage_smem + stage * L::STAGE;
+                                const uint8_t* asm_ = ARES ? a_smem + kc * TS_A_CHUNK : bsm + L::B_CHUNK;
+                                const uint32_t a_addr = ptx::smem_u32(asm_);
+                                const uint32_t b_addr = ptx::smem_u32(bsm);
+    #pragma unroll
+                                for (uint32_t k = 0; k < 4; ++k) {  // UMMA_K = 16 fp16 = 32 B inside the swizzle atom
+                                    mma(d_tmem, ptx::sw128_kmajor_desc(a_addr + 32 * k),
+                                        ptx::sw128_kmajor_desc(b_addr + 32 * k), (kc | k) != 0);
+                                }
+                                commit(empty_bar(stage));
+                                if (++stage == S) {
+                                    stage = 0;
+                                    phase ^= 1;
+                                }
+                            }
+                            commit(tfull_bar(b));
+                        }
+                        if constexpr (ARES) commit(aempty_bar);  // A may be replaced once these MMAs retire
                     }
-                    if constexpr (ARES) commit(aempty_bar);  // A may be replaced once these MMAs retire
                 }
-            }
+            };
+            if (PAIR && p.e4m3) issue(std::true_type{});
+            else issue(std::false_type{});
         }
     } else {
         // ---------------- epilogue: one thread per (query row, column segment) ----------------
