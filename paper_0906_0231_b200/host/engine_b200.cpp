@@ -19,6 +19,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <memory>
 #include <string>
 #include <thread>
 #include <type_traits>
@@ -184,34 +186,58 @@ EngineResult solve_knn(const Dataset& ds, const CumulativeDistance& f, const Eng
 
     const std::uint32_t n = ds.size();
     const std::uint32_t klist = std::min(opt.k, n - 1);
-    std::vector<std::uint32_t> index(std::size_t(n) * klist);
-    std::vector<dist_t> dist(std::size_t(n) * klist);
+    // caller-owned outputs of the C ABI: not zero-filled (every element is written)
+    std::unique_ptr<std::uint32_t[]> index(new std::uint32_t[std::size_t(n) * klist]);
+    std::unique_ptr<dist_t[]> dist(new dist_t[std::size_t(n) * klist]);
     knn_b200_stats st{};
-    const int rc = gpu_solve(ds, opt, metric, arith, plan.n_lanes, index.data(), dist.data(), &st);
-    if (rc != KNN_B200_OK) rethrow_status(rc);
 
     // EngineResult owns one std::vector per row (engine.hpp:25-31): at C2
-    // that is 1M heap allocations, built by a few host threads in parallel
-    // (one thread took ~110 ms of the drop-in's end-to-end time).
-    EngineResult result;
-    result.lists.resize(n);
+    // that is 1M heap allocations.  The GPU call blocks its thread for the
+    // whole solve (H2D, sweeps, D2H), so it runs on a helper thread while this
+    // one and a few more allocate the rows; only the copy of the values is
+    // left for after it returns (C2: 49 ms of the drop-in's time before).
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     const std::uint32_t nthreads = n < 65536 ? 1u : std::min<std::uint32_t>(16u, hw);
-    auto fill = [&](std::uint32_t r0, std::uint32_t r1) {
-        for (std::uint32_t i = r0; i < r1; ++i) {
-            NeighborList& list = result.lists[i];
-            list.query = i;
-            list.neighbors.resize(klist);
-            const std::size_t base = std::size_t(i) * klist;
-            for (std::uint32_t j = 0; j < klist; ++j) list.neighbors[j] = Neighbor{dist[base + j], index[base + j]};
-        }
+    auto parallel_rows = [&](auto&& body) {
+        std::vector<std::thread> pool;
+        for (std::uint32_t t = 1; t < nthreads; ++t)
+            pool.emplace_back(body, std::uint32_t(std::uint64_t(n) * t / nthreads),
+                              std::uint32_t(std::uint64_t(n) * (t + 1) / nthreads));
+        body(0u, std::uint32_t(std::uint64_t(n) / nthreads));
+        for (auto& th : pool) th.join();
     };
-    std::vector<std::thread> pool;
-    for (std::uint32_t t = 1; t < nthreads; ++t)
-        pool.emplace_back(fill, std::uint32_t(std::uint64_t(n) * t / nthreads),
-                          std::uint32_t(std::uint64_t(n) * (t + 1) / nthreads));
-    fill(0, std::uint32_t(std::uint64_t(n) / nthreads));
-    for (auto& th : pool) th.join();
+    int rc = KNN_B200_ERR_INTERNAL;
+    std::exception_ptr solve_error;
+    std::thread solver([&] {
+        try {
+            rc = gpu_solve(ds, opt, metric, arith, plan.n_lanes, index.get(), dist.get(), &st);
+        } catch (...) {
+            solve_error = std::current_exception();
+        }
+    });
+    EngineResult result;
+    try {
+        result.lists.resize(n);
+        parallel_rows([&](std::uint32_t r0, std::uint32_t r1) {
+            for (std::uint32_t i = r0; i < r1; ++i) {
+                result.lists[i].query = i;
+                result.lists[i].neighbors.resize(klist);
+            }
+        });
+    } catch (...) {
+        solver.join();
+        throw;
+    }
+    solver.join();
+    if (solve_error) std::rethrow_exception(solve_error);
+    if (rc != KNN_B200_OK) rethrow_status(rc);
+    parallel_rows([&](std::uint32_t r0, std::uint32_t r1) {
+        for (std::uint32_t i = r0; i < r1; ++i) {
+            Neighbor* out = result.lists[i].neighbors.data();
+            const std::size_t base = std::size_t(i) * klist;
+            for (std::uint32_t j = 0; j < klist; ++j) out[j] = Neighbor{dist[base + j], index[base + j]};
+        }
+    });
     result.seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     result.plan = plan;
