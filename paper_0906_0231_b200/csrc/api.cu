@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
 #include <map>
 #include <cstdio>
 #include <cstdlib>
@@ -1162,6 +1163,9 @@ int solve_multi_impl(const float* host_vectors, uint32_t n, uint32_t d, uint32_t
         const auto t0 = std::chrono::steady_clock::now();
         const uint32_t klist = std::min(k, n - 1);
         std::vector<KnnError> errs(use, KnnError{0, {}});
+        std::mutex watch_mu;
+        std::condition_variable watch_cv;
+        bool failed = false, finished = false;
         std::vector<Counters> ctrs(use);
         std::vector<float> kms(use, 0.f), hms(use, 0.f), dms(use, 0.f), sms(use, 0.f);
         // One host thread per GPU (engine.cpp:37-56).  The reference set goes
@@ -1216,11 +1220,42 @@ int solve_multi_impl(const float* host_vectors, uint32_t n, uint32_t d, uint32_t
             } catch (const std::exception& e) {
                 errs[g] = KnnError{KNN_B200_ERR_INTERNAL, e.what()};
             }
+            if (errs[g].code) {  // wake the watchdog: the other lanes may be waiting on this one in a collective
+                std::lock_guard<std::mutex> wl(watch_mu);
+                failed = true;
+                watch_cv.notify_all();
+            }
         };
+        // The lanes' collectives wait for every rank: a lane that fails (an
+        // allocation, a CUDA error) would leave the others spinning in NCCL
+        // kernels.  The watchdog aborts the communicators on the first lane
+        // error, which ends those kernels; the lanes then return errors, are
+        // joined, and the first error is rethrown (engine.cpp:53-56).  The
+        // aborted communicators are dropped; the next call makes new ones.
+        std::thread watchdog;
+        bool aborted = false;
+        if (comms)
+            watchdog = std::thread([&] {
+                std::unique_lock<std::mutex> wl(watch_mu);
+                watch_cv.wait(wl, [&] { return failed || finished; });
+                if (failed) {
+                    for (ncclComm_t c : *comms) ncclCommAbort(c);
+                    aborted = true;
+                }
+            });
         std::vector<std::thread> threads;
         for (uint32_t g = 1; g < use; ++g) threads.emplace_back(lane, g);
         lane(0);
         for (auto& t : threads) t.join();
+        if (watchdog.joinable()) {
+            {
+                std::lock_guard<std::mutex> wl(watch_mu);
+                finished = true;
+                watch_cv.notify_all();
+            }
+            watchdog.join();
+        }
+        if (aborted) multi_comms.erase(use);
         // engine.cpp:53-56: rethrow the first lane error after joining.
         for (const auto& e : errs)
             if (e.code) throw e;
