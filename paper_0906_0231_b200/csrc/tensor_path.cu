@@ -28,6 +28,7 @@
 // Result: bit-identical to brute_force_knn.
 #include <cub/device/device_radix_sort.cuh>
 #include <algorithm>
+#include <cstdio>
 #include <type_traits>
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
@@ -2545,6 +2546,8 @@ static cudaError_t run_capture(const TensorPathArgs& a, const CaptureArgs& c, ui
     const uint32_t nfb2 = *static_cast<const uint32_t*>(a.host_scratch);
     r.rescored = *reinterpret_cast<const unsigned long long*>(static_cast<const uint8_t*>(a.host_scratch) + 32);
     r.exact_rows = nfb2;
+    if (getenv("KNN_B200_DEBUG_FB"))  // profiling only
+        fprintf(stderr, "[run_capture] %u rows captured, %u to the EXACT kernel\n", nfb, nfb2);
     if (nfb2) {
         if ((e = launch_exact_fused(a.fold, a.X, a.n, a.d, a.klist, fb2_rows, 0, nfb2, a.out_index, a.out_dist,
                                     a.out_sqrt, a.row_begin, a.exact_scratch, a.sm_count, st)) != cudaSuccess)

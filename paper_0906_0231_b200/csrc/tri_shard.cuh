@@ -37,14 +37,24 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <vector>
 
 namespace knnb {
 
-// schedule.cpp:40-44: r = Y mod 2L; r < L ? r : 2L - 1 - r
+// schedule.cpp:40-44: r = Y mod 2L; r < L ? r : 2L - 1 - r -- rotated by
+// one rank per block of 2L units.  Each rank still takes one unit pair
+// (l, 2L - 1 - l) of every block, so the tile counts balance exactly as in
+// the reference; the rotation mixes the units' positions inside the second
+// column order's 4-unit buckets (sorted by threshold, §3.3), whose first and
+// last units hold the rows that need the capture pass.  Without it, at 8
+// ranks every such unit fell to ranks 0, 3, 4 and 7 (C3: 1.4k retried rows
+// each, none on the others; C5: 233 ms of capture against 24 ms).
 static inline uint32_t tri_lane_of_unit(uint32_t u, uint32_t world) {
     const uint32_t r = u % (2 * world);
-    return r < world ? r : 2 * world - 1 - r;
+    const uint32_t l = r < world ? r : 2 * world - 1 - r;
+    return (l + u / (2 * world)) % world;
 }
 
 // Whether the triangle sweep takes its units from the dynamic queue
@@ -838,9 +848,15 @@ static cudaError_t tri_finish(TriShared& S, TriRank& R, const TensorPathArgs& a,
     R.res.fallback_rows = nfb;
     R.res.launches += 6;
     if (nfb) {
+        const auto tr0 = std::chrono::steady_clock::now();
         const CaptureArgs ca{S.xh,    S.alpha,  S.rho, S.xnorm, S.gmax,        S.maxabs, S.bmin, S.perm, S.rowpos,
                              S.n,     S.npad,   S.kc,  S.group_tiles, 512u, R.fb_rows, R.fb_thr, rescored};
         if ((e = run_capture(a, ca, nfb, R.res, R.res.launches)) != cudaSuccess) return e;
+        if (getenv("KNN_B200_DEBUG_FB")) {  // profiling only: per-rank capture rows and time
+            cudaStreamSynchronize(st);
+            fprintf(stderr, "[tri_finish] rank %u capture %u rows, %.2f ms\n", R.rank, nfb,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr0).count());
+        }
     }
     return cudaSuccess;
 }
@@ -1125,13 +1141,25 @@ static cudaError_t tcap_finish(TriShared& S, TriRank& R, const TensorPathArgs& a
     R.res.rescored = *reinterpret_cast<const unsigned long long*>(h + 2);
     R.res.fallback_rows = nretry;
     R.res.launches += 5;
-    if (nretry == 0) return cudaSuccess;
+    // profiling only: per-rank retried rows and the retry pass's time
+    const bool dbg_fb = getenv("KNN_B200_DEBUG_FB") != nullptr;
+    const auto tr0 = std::chrono::steady_clock::now();
+    if (nretry == 0) {
+        if (dbg_fb) fprintf(stderr, "[tcap_finish] rank %u retried 0\n", R.rank);
+        return cudaSuccess;
+    }
     // second capture pass: the retried rows against their implied thresholds,
     // with room for wider bands (rows that filled their first buffer)
     const CaptureArgs ca{S.xh, S.alpha, S.rho, S.xnorm, S.gmax, S.maxabs, S.bmin, S.cosine ? nullptr : S.perm,
                          S.cosine ? nullptr : S.rowpos, S.n, S.npad, S.kc, S.group_tiles, 2048u, R.fb_rows,
                          R.fb_thr, rescored};
-    return run_capture(a, ca, nretry, R.res, R.res.launches);
+    e = run_capture(a, ca, nretry, R.res, R.res.launches);
+    if (dbg_fb) {
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "[tcap_finish] rank %u retried %u, retry pass %.2f ms\n", R.rank, nretry,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr0).count());
+    }
+    return e;
 }
 
 }  // namespace knnb

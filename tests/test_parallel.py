@@ -87,7 +87,8 @@ def _unit_cost(u, units):
 
 def test_tri_unit_plan_is_boustrophedon_and_balanced():
     """The product's host planner (knn_b200_tri_unit_plan): unit u belongs to
-    lane_of_row(u) (schedule.cpp:40-44), every unit exactly once, and the
+    lane_of_row(u) (schedule.cpp:40-44) rotated by one rank per block of
+    2 * world units, every unit exactly once, and the
     per-rank work (sum of U - u) balanced like the reference's lanes
     (test_schedule.cpp:169-185).  The list triangle's static walk deals each
     rank's units to its CTA pairs (pair p: positions p, p + P, ...) by
@@ -104,7 +105,7 @@ def test_tri_unit_plan_is_boustrophedon_and_balanced():
         for r, lst in enumerate(plan):
             for u in lst:
                 m = u % (2 * world)
-                assert (m if m < world else 2 * world - 1 - m) == r
+                assert ((m if m < world else 2 * world - 1 - m) + u // (2 * world)) % world == r
         if units >= 2 * world * 8:
             work = [sum(units - u for u in lst) for lst in plan]
             assert max(work) / min(work) < 1.01

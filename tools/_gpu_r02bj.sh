@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+TAG=r02bj
+timeout 900 python -m pytest tests/test_gpu_shard.py -q -rfE -x > gpurun_out/${TAG}_pytest_shard.log 2>&1; echo tests rc=$?; tail -1 gpurun_out/${TAG}_pytest_shard.log
+KNN_B200_DEBUG_FB=1 timeout 900 python tools/shard_emulate.py --worlds 1,2,4,8 --reps 3 > gpurun_out/${TAG}_shard_c2.jsonl 2> gpurun_out/${TAG}_c2_fb.txt; echo c2 rc=$?
+KNN_B200_DEBUG_FB=1 timeout 900 python tools/shard_emulate.py --n 1000000 --d 1024 --k 100 --seed 2 --worlds 8 --reps 2 > gpurun_out/${TAG}_shard_c3.jsonl 2> gpurun_out/${TAG}_c3_fb.txt; echo c3 rc=$?
+KNN_B200_DEBUG_FB=1 timeout 900 python tools/shard_emulate.py --n 4000000 --d 128 --k 32 --metric cosine --seed 3 --worlds 2,4,8 --reps 2 > gpurun_out/${TAG}_shard_c4.jsonl 2> gpurun_out/${TAG}_c4_fb.txt; echo c4 rc=$?
