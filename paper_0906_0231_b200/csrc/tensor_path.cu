@@ -2042,9 +2042,28 @@ struct Rescore2Params {
 // tile (the query's chunk comes by shuffle).  One lane per candidate with its
 // own strided loads was latency-bound (ncu: 89% long-scoreboard stalls,
 // 9% of DRAM bandwidth at C3).
+//
+// When rows are 16-byte aligned (d % 4 == 0, the common case) the chunks move
+// with cp.async (16 bytes a lane, 8 per lane per chunk) into a kBandStages
+// ring in XOR-swizzled layout: row r's 16-byte group g sits at g ^ (r & 7), so
+// each lane reads its row with conflict-free LDS.128 and the query chunk is a
+// broadcast LDS.128 -- no register staging, no per-element shuffles, and
+// kBandStages - 1 chunks (8 KB) in flight per warp.  The register-staged
+// version issued ~4x the instructions per coordinate and was issue- and
+// latency-bound (ncu at C3: issue slots 57% busy at 14 warps per SM, DRAM
+// 32% of peak, 167 ms; profiles/r02bm_c3_rescore.csv).
 constexpr int kBandWarps = 4;
+#ifndef KNN_BAND_STAGES
+#define KNN_BAND_STAGES 3
+#endif
+constexpr int kBandStages = KNN_BAND_STAGES;
+constexpr uint32_t kBandStageFloats = 32 * 32 + 32;  // 32 candidate rows + the query, 32 coordinates each
+__host__ __device__ __forceinline__ size_t band_stage_bytes() {
+    const size_t ring = size_t(kBandStages) * kBandStageFloats * 4, tile = 32 * 33 * 4;
+    return ring > tile ? ring : tile;
+}
 __device__ __forceinline__ size_t band_smem_per_warp(uint32_t cap) {
-    return size_t(cap) * 16 + 32 * 33 * 4 + 64;
+    return size_t(cap) * 16 + band_stage_bytes() + 64;
 }
 
 // Ascending bitonic sort of s[0, n) (n a power of two) by one warp.
@@ -2074,7 +2093,7 @@ __device__ __forceinline__ uint32_t pow2_at_least(uint32_t x) { return x <= 1 ? 
 // distance -- the same sets as selecting by rank and by bound over the
 // unsorted band.  The folded exact keys are sorted for the k-th distance and
 // the output order.
-template <int FOLD>
+template <int FOLD, bool VEC>
 __device__ __forceinline__ void band_row(const Rescore2Params& p, uint32_t slot, uint8_t* wbase, uint32_t scap,
                                          bool defer) {
     const int lane = threadIdx.x & 31;
@@ -2117,6 +2136,71 @@ __device__ __forceinline__ void band_row(const Rescore2Params& p, uint32_t slot,
     const float* xq = p.X + size_t(qo) * p.d;
     // fold the candidates at sorted positions [lo, hi) (ak -> ek, same positions)
     auto fold_range = [&](uint32_t lo, uint32_t hi) {
+        if constexpr (VEC) {
+            float* ring = reinterpret_cast<float*>(ek + scap);
+            const uint32_t nch = (p.d + 31) / 32, grp = lane & 7;
+            for (uint32_t g0 = lo; g0 < hi; g0 += 32) {
+                const uint32_t nrow = min(hi - g0, 32u);
+                // lane copies 16-byte group grp of rows lane/8 + 4i, i < 8
+                const float* src[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const uint32_t r = uint32_t(i) * 4 + (lane >> 3);
+                    src[i] = p.X + size_t(r < nrow ? uint32_t(ak[g0 + r]) : qo) * p.d + grp * 4;
+                }
+                auto issue = [&](uint32_t c) {
+                    if (c < nch) {
+                        float* st = ring + (c % kBandStages) * kBandStageFloats;
+                        const uint32_t j0 = c * 32;
+                        const bool gin = j0 + grp * 4 < p.d;  // d % 4 == 0: a group is wholly in or out
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const uint32_t r = uint32_t(i) * 4 + (lane >> 3);
+                            const bool on = gin && r < nrow;
+                            ptx::cp_async16(st + r * 32 + ((grp ^ (r & 7)) << 2), on ? src[i] + j0 : p.X, on ? 16u : 0u);
+                        }
+                        if (lane < 8) ptx::cp_async16(st + 1024 + grp * 4, gin ? xq + j0 + grp * 4 : p.X, gin ? 16u : 0u);
+                    }
+                    ptx::cp_async_commit();  // (empty groups keep the count uniform)
+                };
+#pragma unroll
+                for (int c = 0; c < kBandStages - 1; ++c) issue(uint32_t(c));
+                float acc = 0.0f;
+                for (uint32_t c = 0; c < nch; ++c) {
+                    issue(c + kBandStages - 1);
+                    ptx::cp_async_wait<kBandStages - 1>();  // chunk c has landed (this lane's copies)
+                    __syncwarp();                      // ... and every lane's
+                    const float* st = ring + (c % kBandStages) * kBandStageFloats;
+                    const float* row = st + lane * 32;
+                    const float* qc = st + 1024;
+                    const uint32_t ng = min(p.d - c * 32, 32u) >> 2;
+                    if (ng == 8) {
+#pragma unroll
+                        for (uint32_t g = 0; g < 8; ++g) {
+                            const float4 v = *reinterpret_cast<const float4*>(row + ((g ^ (lane & 7)) << 2));
+                            const float4 q4 = *reinterpret_cast<const float4*>(qc + g * 4);
+                            acc = fold_step<FOLD>(v.x, q4.x, acc);
+                            acc = fold_step<FOLD>(v.y, q4.y, acc);
+                            acc = fold_step<FOLD>(v.z, q4.z, acc);
+                            acc = fold_step<FOLD>(v.w, q4.w, acc);
+                        }
+                    } else {
+                        for (uint32_t g = 0; g < ng; ++g) {
+                            const float4 v = *reinterpret_cast<const float4*>(row + ((g ^ (lane & 7)) << 2));
+                            const float4 q4 = *reinterpret_cast<const float4*>(qc + g * 4);
+                            acc = fold_step<FOLD>(v.x, q4.x, acc);
+                            acc = fold_step<FOLD>(v.y, q4.y, acc);
+                            acc = fold_step<FOLD>(v.z, q4.z, acc);
+                            acc = fold_step<FOLD>(v.w, q4.w, acc);
+                        }
+                    }
+                    __syncwarp();  // the stage is rewritten by the next iteration's issue
+                }
+                if (uint32_t(lane) < nrow)
+                    ek[g0 + lane] = make_key(fold_finalize<FOLD>(acc), uint32_t(ak[g0 + lane]));
+            }
+            __syncwarp();
+        } else {
         for (uint32_t g = lo; g < hi; g += 32) {
             const bool mine = g + lane < hi;
             const uint32_t col = mine ? uint32_t(ak[g + lane]) : qo;
@@ -2149,6 +2233,7 @@ __device__ __forceinline__ void band_row(const Rescore2Params& p, uint32_t slot,
             if (mine) ek[g + lane] = make_key(fold_finalize<FOLD>(acc), col);
         }
         __syncwarp();
+        }
     };
     // sort ek[0, m) (padding with empty keys up to a power of two)
     auto sort_exact = [&](uint32_t m) {
@@ -2214,31 +2299,31 @@ __device__ __forceinline__ void band_row(const Rescore2Params& p, uint32_t slot,
 // pass 0: one warp per slot, room for scap candidates, larger bands listed in
 // p.big; pass 1: the listed slots (grid-stride), room for p.cap; pass 2: one
 // warp per slot, room for p.cap (no split).
-template <int FOLD, int NW>
+template <int FOLD, int NW, bool VEC>
 __global__ void __launch_bounds__(32 * NW, 16 / NW) rescore_capture_kernel(const Rescore2Params p, uint32_t scap, int pass) {
     extern __shared__ __align__(16) uint8_t band_smem[];
     const int warp = threadIdx.x >> 5;
     uint8_t* wbase = band_smem + size_t(warp) * band_smem_per_warp(scap);
     if (pass == 1) {
         const uint32_t nb = *p.nbig;
-        for (uint32_t i = blockIdx.x * NW + warp; i < nb; i += gridDim.x * NW) band_row<FOLD>(p, p.big[i], wbase, scap, false);
+        for (uint32_t i = blockIdx.x * NW + warp; i < nb; i += gridDim.x * NW) band_row<FOLD, VEC>(p, p.big[i], wbase, scap, false);
         return;
     }
     const uint32_t slot = blockIdx.x * NW + warp;
-    if (slot < p.m) band_row<FOLD>(p, slot, wbase, scap, pass == 0);
+    if (slot < p.m) band_row<FOLD, VEC>(p, slot, wbase, scap, pass == 0);
 }
 
 static size_t band_smem_bytes(uint32_t cap, int warps = kBandWarps) {
-    return warps * (size_t(cap) * 16 + 32 * 33 * 4 + 64);
+    return warps * (size_t(cap) * 16 + band_stage_bytes() + 64);
 }
 
 // expect: the typical band size (0: unknown).  With r2.big set, bands up to
 // ~1.25 expect (rounded up to a power of two) run in small shared-memory
 // slices (2x the occupancy of slices sized for the capacity); the rest get a
 // second pass.  r2.cap must be a power of two.
-template <int FOLD>
-static cudaError_t launch_rescore_capture(const Rescore2Params& r2, uint32_t rows, cudaStream_t st,
-                                          uint32_t expect = 0) {
+template <int FOLD, bool VEC>
+static cudaError_t launch_rescore_capture_v(const Rescore2Params& r2, uint32_t rows, cudaStream_t st,
+                                            uint32_t expect) {
     cudaError_t e;
     // (band slices hold a power of two: the bitonic sorts' size)
     uint32_t scap = 128;
@@ -2250,8 +2335,8 @@ static cudaError_t launch_rescore_capture(const Rescore2Params& r2, uint32_t row
         const uint32_t w8 = 8 * std::min<uint32_t>(2, uint32_t((227u << 10) / (8 * per_warp)));
         const uint32_t w4 = 4 * std::min<uint32_t>(4, uint32_t((227u << 10) / (4 * per_warp)));
         const bool eight = w8 >= w4;
-        auto k0 = eight ? rescore_capture_kernel<FOLD, 8> : rescore_capture_kernel<FOLD, 4>;
-        auto k1 = rescore_capture_kernel<FOLD, kBandWarps>;
+        auto k0 = eight ? rescore_capture_kernel<FOLD, 8, VEC> : rescore_capture_kernel<FOLD, 4, VEC>;
+        auto k1 = rescore_capture_kernel<FOLD, kBandWarps, VEC>;
         const int nw0 = eight ? 8 : 4;
         const size_t s0 = band_smem_bytes(scap, nw0), s1 = band_smem_bytes(r2.cap);
         if ((e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s0))) != cudaSuccess) return e;
@@ -2265,11 +2350,21 @@ static cudaError_t launch_rescore_capture(const Rescore2Params& r2, uint32_t row
             r2, r2.cap, 1);
         return cudaGetLastError();
     }
-    auto k = rescore_capture_kernel<FOLD, kBandWarps>;
+    auto k = rescore_capture_kernel<FOLD, kBandWarps, VEC>;
     const size_t smem = band_smem_bytes(r2.cap);
     if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) != cudaSuccess) return e;
     k<<<(rows + kBandWarps - 1) / kBandWarps, 32 * kBandWarps, smem, st>>>(r2, r2.cap, 2);
     return cudaGetLastError();
+}
+
+template <int FOLD>
+static cudaError_t launch_rescore_capture(const Rescore2Params& r2, uint32_t rows, cudaStream_t st,
+                                          uint32_t expect = 0) {
+    // 16-byte aligned rows: the cp.async ring (KNN_B200_BAND_VEC=0: the register-staged fold)
+    const char* ev = getenv("KNN_B200_BAND_VEC");
+    const bool vec = r2.d % 4 == 0 && reinterpret_cast<uintptr_t>(r2.X) % 16 == 0 && !(ev && atoi(ev) == 0);
+    return vec ? launch_rescore_capture_v<FOLD, true>(r2, rows, st, expect)
+               : launch_rescore_capture_v<FOLD, false>(r2, rows, st, expect);
 }
 
 // ---------------------------------------------------------------------------

@@ -389,12 +389,14 @@ def test_device_api_empty_shard_and_stream_switch(ctx, c_oracle):
 
 @pytest.mark.parametrize("n,d,k,m", [(20000, 48, 30, "sqeuclidean"), (9000, 300, 100, "euclidean"),
                                      (12000, 64, 20, "cosine"), (5000, 20, 64, "hellinger"),
-                                     (3000, 1024, 11, "sqeuclidean")])
+                                     (3000, 1024, 11, "sqeuclidean"), (6000, 37, 24, "sqeuclidean")])
 def test_threshold_triangle_forced_all_rows(ctx, c_oracle, monkeypatch, n, d, k, m):
     """The threshold triangle (k > 10: each pair once, both endpoints against
     fixed thresholds, capture rescore; KNN_B200_TCAP=force below its size
     gate), every row against the oracle -- resident (d <= 256) and streamed
-    query rows (d > 256), cosine without the norm order."""
+    query rows (d > 256), cosine without the norm order; the band rescore's
+    cp.async ring with whole and partial 32-coordinate chunks (d % 4 == 0)
+    and its register-staged fold (d = 37)."""
     import torch
     from oracle import normalize_rows
     from paper_0906_0231_b200 import solve_rows_torch
