@@ -2048,13 +2048,15 @@ struct Rescore2Params {
 // ring in XOR-swizzled layout: row r's 16-byte group g sits at g ^ (r & 7), so
 // each lane reads its row with conflict-free LDS.128 and the query chunk is a
 // broadcast LDS.128 -- no register staging, no per-element shuffles, and
-// kBandStages - 1 chunks (8 KB) in flight per warp.  The register-staged
-// version issued ~4x the instructions per coordinate and was issue- and
+// kBandStages - 1 chunks in flight per warp.  The register-staged version
+// issued ~4x the instructions per coordinate and was issue- and
 // latency-bound (ncu at C3: issue slots 57% busy at 14 warps per SM, DRAM
-// 32% of peak, 167 ms; profiles/r02bm_c3_rescore.csv).
+// 32% of peak, 167 ms; profiles/r02bm_c3_rescore.csv).  Two stages beat three
+// and four (C3 step 1.03 against 1.06 s; profiles/r02bs_configs.txt): the
+// smaller ring leaves room for more warps, which also hide the sorts.
 constexpr int kBandWarps = 4;
 #ifndef KNN_BAND_STAGES
-#define KNN_BAND_STAGES 3
+#define KNN_BAND_STAGES 2
 #endif
 constexpr int kBandStages = KNN_BAND_STAGES;
 constexpr uint32_t kBandStageFloats = 32 * 32 + 32;  // 32 candidate rows + the query, 32 coordinates each
@@ -2334,7 +2336,7 @@ static cudaError_t launch_rescore_capture_v(const Rescore2Params& r2, uint32_t r
         const size_t per_warp = band_smem_bytes(scap, 1);
         const uint32_t w8 = 8 * std::min<uint32_t>(2, uint32_t((227u << 10) / (8 * per_warp)));
         const uint32_t w4 = 4 * std::min<uint32_t>(4, uint32_t((227u << 10) / (4 * per_warp)));
-        const bool eight = w8 >= w4;
+        const bool eight = w8 > w4;  // a tie goes to 4-warp blocks: a finished block frees its slices sooner
         auto k0 = eight ? rescore_capture_kernel<FOLD, 8, VEC> : rescore_capture_kernel<FOLD, 4, VEC>;
         auto k1 = rescore_capture_kernel<FOLD, kBandWarps, VEC>;
         const int nw0 = eight ? 8 : 4;
