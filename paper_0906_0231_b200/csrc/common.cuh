@@ -64,6 +64,55 @@ __device__ __forceinline__ float fold_step(float u, float v, float acc) {
     }
 }
 
+// Packed element-wise sub/mul (sm_100 FADD2 / FMUL2): each element is the
+// same IEEE round-to-nearest operation as __fsub_rn / __fmul_rn, two per
+// instruction.  The accumulating adds stay scalar and in fold order, so the
+// folds below are bit-identical to fold_step with a third fewer instructions.
+__device__ __forceinline__ void sub2_rn(float a0, float a1, float b0, float b1, float& r0, float& r1) {
+    asm("{\n\t.reg .b64 x, y, r;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %5};\n\t"
+        "sub.rn.f32x2 r, x, y;\n\tmov.b64 {%0, %1}, r;\n\t}"
+        : "=f"(r0), "=f"(r1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ void mul2_rn(float a0, float a1, float b0, float b1, float& r0, float& r1) {
+    asm("{\n\t.reg .b64 x, y, r;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %5};\n\t"
+        "mul.rn.f32x2 r, x, y;\n\tmov.b64 {%0, %1}, r;\n\t}"
+        : "=f"(r0), "=f"(r1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+// The fold's per-coordinate term (u, v) -> t for two coordinates at once.
+template <int METRIC>
+__device__ __forceinline__ void fold_terms2(float u0, float u1, float v0, float v1, float& t0, float& t1) {
+    if constexpr (METRIC == kCosine) {
+        mul2_rn(u0, u1, v0, v1, t0, t1);
+    } else if constexpr (METRIC == kManhattan) {
+        sub2_rn(u0, u1, v0, v1, t0, t1);
+        t0 = fabsf(t0);
+        t1 = fabsf(t1);
+    } else {
+        sub2_rn(u0, u1, v0, v1, t0, t1);
+        mul2_rn(t0, t1, t0, t1, t0, t1);
+    }
+}
+
+// Two independent folds one step each: acc0 += term(u0, v0), acc1 += term(u1, v1).
+template <int METRIC>
+__device__ __forceinline__ void fold_step2(float u0, float u1, float v0, float v1, float& acc0, float& acc1) {
+    float t0, t1;
+    fold_terms2<METRIC>(u0, u1, v0, v1, t0, t1);
+    acc0 = __fadd_rn(acc0, t0);
+    acc1 = __fadd_rn(acc1, t1);
+}
+
+// One fold, two consecutive coordinates (j, j + 1): the adds in order.
+template <int METRIC>
+__device__ __forceinline__ float fold_step_x2(float u0, float u1, float v0, float v1, float acc) {
+    float t0, t1;
+    fold_terms2<METRIC>(u0, u1, v0, v1, t0, t1);
+    return __fadd_rn(__fadd_rn(acc, t0), t1);
+}
+
 template <int METRIC>
 __device__ __forceinline__ float fold_finalize(float acc) {
     if constexpr (METRIC == kCosine) {

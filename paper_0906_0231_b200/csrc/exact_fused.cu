@@ -166,7 +166,8 @@ __global__ void __launch_bounds__(EX_THREADS) exact_fused_kernel(const ExactPara
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) acc[i][c] = fold_step<METRIC>(bv[c], av[i], acc[i][c]);
+                    for (int c = 0; c < 4; c += 2)  // packed terms for columns c, c + 1 (FADD2/FMUL2)
+                        fold_step2<METRIC>(bv[c], bv[c + 1], av[i], av[i], acc[i][c], acc[i][c + 1]);
             }
             __syncthreads();
         }

@@ -1595,18 +1595,14 @@ __device__ __forceinline__ float exact_fold_rows(const float* __restrict__ a, co
             }
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
-                acc = fold_step<FOLD>(x[t].x, y[t].x, acc);
-                acc = fold_step<FOLD>(x[t].y, y[t].y, acc);
-                acc = fold_step<FOLD>(x[t].z, y[t].z, acc);
-                acc = fold_step<FOLD>(x[t].w, y[t].w, acc);
+                acc = fold_step_x2<FOLD>(x[t].x, x[t].y, y[t].x, y[t].y, acc);
+                acc = fold_step_x2<FOLD>(x[t].z, x[t].w, y[t].z, y[t].w, acc);
             }
         }
         for (; j < d4; ++j) {
             const float4 x = __ldg(a4 + j), y = __ldg(b4 + j);
-            acc = fold_step<FOLD>(x.x, y.x, acc);
-            acc = fold_step<FOLD>(x.y, y.y, acc);
-            acc = fold_step<FOLD>(x.z, y.z, acc);
-            acc = fold_step<FOLD>(x.w, y.w, acc);
+            acc = fold_step_x2<FOLD>(x.x, x.y, y.x, y.y, acc);
+            acc = fold_step_x2<FOLD>(x.z, x.w, y.z, y.w, acc);
         }
     } else {
         for (uint32_t j = 0; j < d; ++j) acc = fold_step<FOLD>(__ldg(a + j), __ldg(b + j), acc);
@@ -1637,10 +1633,8 @@ __device__ __forceinline__ float exact_fold_staged(const float* __restrict__ c, 
         for (int t = 0; t < 8; ++t) {
             if (j + t < d4) {
                 const float4 y = q4[j + t];
-                acc = fold_step<FOLD>(cur[t].x, y.x, acc);
-                acc = fold_step<FOLD>(cur[t].y, y.y, acc);
-                acc = fold_step<FOLD>(cur[t].z, y.z, acc);
-                acc = fold_step<FOLD>(cur[t].w, y.w, acc);
+                acc = fold_step_x2<FOLD>(cur[t].x, cur[t].y, y.x, y.y, acc);
+                acc = fold_step_x2<FOLD>(cur[t].z, cur[t].w, y.z, y.w, acc);
             }
         }
 #pragma unroll
@@ -2181,19 +2175,15 @@ __device__ __forceinline__ void band_row(const Rescore2Params& p, uint32_t slot,
                         for (uint32_t g = 0; g < 8; ++g) {
                             const float4 v = *reinterpret_cast<const float4*>(row + ((g ^ (lane & 7)) << 2));
                             const float4 q4 = *reinterpret_cast<const float4*>(qc + g * 4);
-                            acc = fold_step<FOLD>(v.x, q4.x, acc);
-                            acc = fold_step<FOLD>(v.y, q4.y, acc);
-                            acc = fold_step<FOLD>(v.z, q4.z, acc);
-                            acc = fold_step<FOLD>(v.w, q4.w, acc);
+                            acc = fold_step_x2<FOLD>(v.x, v.y, q4.x, q4.y, acc);
+                            acc = fold_step_x2<FOLD>(v.z, v.w, q4.z, q4.w, acc);
                         }
                     } else {
                         for (uint32_t g = 0; g < ng; ++g) {
                             const float4 v = *reinterpret_cast<const float4*>(row + ((g ^ (lane & 7)) << 2));
                             const float4 q4 = *reinterpret_cast<const float4*>(qc + g * 4);
-                            acc = fold_step<FOLD>(v.x, q4.x, acc);
-                            acc = fold_step<FOLD>(v.y, q4.y, acc);
-                            acc = fold_step<FOLD>(v.z, q4.z, acc);
-                            acc = fold_step<FOLD>(v.w, q4.w, acc);
+                            acc = fold_step_x2<FOLD>(v.x, v.y, q4.x, q4.y, acc);
+                            acc = fold_step_x2<FOLD>(v.z, v.w, q4.z, q4.w, acc);
                         }
                     }
                     __syncwarp();  // the stage is rewritten by the next iteration's issue

@@ -100,6 +100,9 @@ def test_edge_shapes(ctx, c_oracle, arith):
         (c_oracle.generate(129, 1000, 6), 7, "sqeuclidean"),                # d not a chunk multiple
         (c_oracle.generate(257, 31, 6), 256, "hellinger"),                  # klist = 256 (max)
         (-c_oracle.generate(100, 9, 2), 3, "sqeuclidean"),                  # negative coordinates
+        # subnormal terms and sums (the packed FADD2/FMUL2 fold terms must not flush them)
+        (c_oracle.generate(200, 16, 7) * np.float32(1e-19), 5, "sqeuclidean"),
+        (c_oracle.generate(150, 40, 8) * np.float32(3e-20), 9, "sqeuclidean"),
     ]
     for x, k, m in cases:
         x = np.ascontiguousarray(x, np.float32)
