@@ -1808,26 +1808,24 @@ __global__ void __launch_bounds__(256) rescore_kernel(const RescoreParams p) {
         }
         return warp_min_key(kth);
     };
-    // Phase 1: the k + 4 best candidates by approximate distance, picked by
-    // k + 4 rounds of a warp-wide minimum (keys are unique: distinct columns).
+    // Phase 1: the k + 4 best candidates by approximate distance -- those
+    // with fewer than k + 4 smaller keys (keys are unique: distinct columns).
+    // Every lane ranks its own keys against the row's keys in shared memory:
+    // independent compares, where k + 4 rounds of a warp-wide minimum were a
+    // chain of k + 4 dependent shuffle reductions.
     const uint32_t r1 = p.klist + 4 < uint32_t(KT) ? p.klist + 4 : uint32_t(KT);
     bool sel[PER];
+    {
+        uint32_t rk[PER];
 #pragma unroll
-    for (int m = 0; m < PER; ++m) sel[m] = false;
-    for (uint32_t r = 0; r < r1; ++r) {
-        uint64_t mn = kEmptyKey;
-        int mm = -1;
+        for (int m = 0; m < PER; ++m) rk[m] = 0;
+        for (int j = 0; j < KT; ++j) {
+            const uint64_t o = keys_s[warp][j];
 #pragma unroll
-        for (int m = 0; m < PER; ++m)
-            if (!sel[m] && ak[m] < mn) {
-                mn = ak[m];
-                mm = m;
-            }
-        const uint64_t wmin = warp_min_key(mn);
-        if (wmin == kEmptyKey) break;
+            for (int m = 0; m < PER; ++m) rk[m] += o < ak[m];
+        }
 #pragma unroll
-        for (int m = 0; m < PER; ++m)
-            if (m == mm && mn == wmin) sel[m] = true;
+        for (int m = 0; m < PER; ++m) sel[m] = lane + 32 * m < KT && ak[m] != kEmptyKey && rk[m] < r1;
     }
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
