@@ -624,10 +624,12 @@ static cudaError_t tri_order(TriShared& S, const TensorPathArgs& a) {
 
 // The threshold triangle with 16 epilogue warps (4 per TMEM lane quadrant,
 // 64 columns each per tile) instead of 8: twice the warps to hide the
-// filter's latency; it keeps no lists, so 112 registers suffice.
+// filter's latency; it keeps no lists, so 112 registers suffice.  The
+// default for resident query rows: C4 2.363-2.365 s against 2.375-2.384 s
+// with 8, C3 level (profiles/r02cd_ew.txt).  KNN_B200_TCAP_EW=8: 8 warps.
 static bool tcap_ew16() {
     const char* e = getenv("KNN_B200_TCAP_EW");
-    return e && atoi(e) == 16;
+    return !(e && atoi(e) == 8);
 }
 
 // Phase B: the triangle sweep of this rank's units; column-side entries

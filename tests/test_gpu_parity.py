@@ -418,6 +418,22 @@ def test_threshold_triangle_forced_all_rows(ctx, c_oracle, monkeypatch, n, d, k,
     assert st["fallback_rows"] < n  # most rows proven by the first pass
 
 
+@pytest.mark.parametrize("ew", ["8", "16"])
+def test_threshold_triangle_epilogue_widths(ctx, c_oracle, monkeypatch, ew):
+    """The threshold triangle with 8 and 16 epilogue warps (KNN_B200_TCAP_EW;
+    16 is the default for resident query rows): the same bits."""
+    import torch
+    from paper_0906_0231_b200 import solve_rows_torch
+    monkeypatch.setenv("KNN_B200_TCAP", "force")
+    monkeypatch.setenv("KNN_B200_TCAP_EW", ew)
+    n, d, k = 12000, 96, 24
+    xh = c_oracle.generate(n, d, 91)
+    ri, rd = c_oracle.rows_topk(xh, k, "sqeuclidean", np.arange(n, dtype=np.uint32))
+    idx, dist, _ = solve_rows_torch(ctx, torch.from_numpy(xh).cuda(), k, metric_obj("sqeuclidean"), 0, n,
+                                    arith_id("tensor"), want_stats=True)
+    assert_lists_bit_equal(idx.cpu().numpy().view(np.uint32), dist.cpu().numpy(), ri, rd, f"TCAP_EW={ew}")
+
+
 def test_threshold_triangle_retry_and_overflow_paths(ctx, c_oracle, monkeypatch):
     """Thresholds forced far too low (every row retried through the second
     capture pass) and a pool forced to overflow (the rectangular sweep redoes
