@@ -58,19 +58,21 @@ static inline uint32_t tri_lane_of_unit(uint32_t u, uint32_t world) {
 }
 
 // Whether the triangle sweep takes its units from the dynamic queue
-// (KNN_B200_TRI_DYN=0: never; =1: always).  Default, for resident query rows
-// (d <= 256): the threshold triangle (C4: -14%), whose items carry no list
-// state between column groups.  The list triangle keeps the static walk at
-// any world size: its CTA pairs sweep each column group in step, so the
-// group's tiles stay L2-resident.  Measured at C2, 8 emulated ranks (6.6
-// units per pair): (unit, group) items from the queue made pairs wait on
-// another pair's list state and lost that residency (sweep +3%); whole-unit
-// claims for the lightest 20% of the tiles after a static head, +8%
-// (profiles/r02at_*).  Streamed query rows (d > 256, C3) keep it for the
-// same reason (C3: +4% with the queue).
+// (KNN_B200_TRI_DYN=0: never; =1: always).  Default: the threshold triangle
+// (C4: -14%), whose items carry no list state between column groups --
+// resident and streamed query rows alike (C3, d = 1024: sweep 893 -> 830 ms
+// on the last build, profiles/r02cf_knobs.txt, r02cg_knobs.txt; it measured
+// +4% before the band rescore and the epilogue changes).  The list triangle
+// keeps the static walk at any world size: its CTA pairs sweep each column
+// group in step, so the group's tiles stay L2-resident.  Measured at C2, 8
+// emulated ranks (6.6 units per pair): (unit, group) items from the queue
+// made pairs wait on another pair's list state and lost that residency
+// (sweep +3%); whole-unit claims for the lightest 20% of the tiles after a
+// static head, +8% (profiles/r02at_*).
 static bool tri_use_dyn(bool tcap, uint32_t kc) {
+    (void)kc;
     if (const char* e = getenv("KNN_B200_TRI_DYN")) return atoi(e) != 0;
-    return tcap && kc <= uint32_t(TS_MAX_RES_KC);
+    return tcap;
 }
 
 // Estimated sweep cost of unit u (relative units): its U - u tiles, weighted

@@ -434,6 +434,22 @@ def test_threshold_triangle_epilogue_widths(ctx, c_oracle, monkeypatch, ew):
     assert_lists_bit_equal(idx.cpu().numpy().view(np.uint32), dist.cpu().numpy(), ri, rd, f"TCAP_EW={ew}")
 
 
+@pytest.mark.parametrize("dyn", ["0", "1"])
+def test_threshold_triangle_walks_streamed_rows(ctx, c_oracle, monkeypatch, dyn):
+    """Streamed query rows (d > 256) under the static walk and the unit
+    queue (KNN_B200_TRI_DYN; the queue is the default): the same bits."""
+    import torch
+    from paper_0906_0231_b200 import solve_rows_torch
+    monkeypatch.setenv("KNN_B200_TCAP", "force")
+    monkeypatch.setenv("KNN_B200_TRI_DYN", dyn)
+    n, d, k = 7000, 320, 40
+    xh = c_oracle.generate(n, d, 93)
+    ri, rd = c_oracle.rows_topk(xh, k, "sqeuclidean", np.arange(n, dtype=np.uint32))
+    idx, dist, _ = solve_rows_torch(ctx, torch.from_numpy(xh).cuda(), k, metric_obj("sqeuclidean"), 0, n,
+                                    arith_id("tensor"), want_stats=True)
+    assert_lists_bit_equal(idx.cpu().numpy().view(np.uint32), dist.cpu().numpy(), ri, rd, f"TRI_DYN={dyn}")
+
+
 def test_threshold_triangle_retry_and_overflow_paths(ctx, c_oracle, monkeypatch):
     """Thresholds forced far too low (every row retried through the second
     capture pass) and a pool forced to overflow (the rectangular sweep redoes
